@@ -1,0 +1,28 @@
+"""Named workload configurations.
+
+C1..C5 are BASELINE.json configs[0..4]; P0..P3 are the tiny
+parity configurations of SURVEY.md §8(c) that exercise nesting (C1 has admissible
+blocks on the leaf level only).  q is the per-face refinement: sphere n = 8 q^2,
+cube n = 12 q^2.  eta1 = 1 (directions), eta2 = 10 (admissibility) as BASELINE.json
+states.
+"""
+
+CONFIGS = {
+    # tiny parity configs (tests only)
+    "P0": dict(mesh="sphere", q=8, kappa=0.0, m=3, leaf=16, eta1=1.0, eta2=10.0, eps=1e-4),
+    "P1": dict(mesh="sphere", q=8, kappa=4.0, m=3, leaf=8, eta1=1.0, eta2=10.0, eps=1e-4),
+    "P2": dict(mesh="sphere", q=16, kappa=8.0, m=3, leaf=16, eta1=1.0, eta2=10.0, eps=1e-4),
+    "P3": dict(mesh="cube", q=8, kappa=5.0, m=3, leaf=16, eta1=1.0, eta2=10.0, eps=1e-4),
+    # BASELINE.json configs
+    "C1": dict(mesh="sphere", q=8, kappa=4.0, m=3, leaf=16, eta1=1.0, eta2=10.0, eps=1e-4),
+    "C2": dict(mesh="sphere", q=32, kappa=16.0, m=4, leaf=32, eta1=1.0, eta2=10.0, eps=1e-4),
+    "C3": dict(mesh="sphere", q=64, kappa=32.0, m=4, leaf=32, eta1=1.0, eta2=10.0, eps=1e-5),
+    "C4": dict(mesh="sphere", q=128, kappa=64.0, m=5, leaf=64, eta1=1.0, eta2=10.0, eps=1e-6),
+    "C5": dict(mesh="cube", q=128, kappa=115.0, m=5, leaf=64, eta1=1.0, eta2=10.0, eps=1e-6),
+}
+
+
+def get_config(name):
+    cfg = dict(CONFIGS[name])
+    cfg["name"] = name
+    return cfg
