@@ -1,0 +1,169 @@
+/*
+ * dh2.h — C ABI of libdh2.so: B200-native hybrid recompression of directional
+ * H^2-matrices (DH^2), arXiv 1809.04384 (the paper's text is PAPER.md).
+ *
+ * Citations are PAPER.md line numbers (P:<line>) plus the section/equation.
+ *
+ * Problem (Eq. helmholtz/matrix): Galerkin matrix of the Helmholtz single
+ * layer potential g(x,y) = exp(i kappa |x-y|)/(4 pi |x-y|) with piecewise-constant
+ * basis functions on a flat triangle mesh.  dh2_build_interp builds
+ * the DH^2 approximation of its far field by directional Chebyshev interpolation
+ * (Eq. 4, Eq. 10/11, Def. 2.7); dh2_recompress
+ * replaces the interpolation bases by orthogonal, nested, adaptively truncated
+ * ones (§3.2) and projects the couplings.  The
+ * nearfield (inadmissible leaves) is out of scope: it is untouched by the
+ * recompression and is only counted in dh2_storage.
+ *
+ * Conventions (all functions):
+ *   - return int: 0 = DH2_OK, < 0 = error code below; no C++ exception crosses the ABI;
+ *     dh2_last_error(ctx) returns a message for the last failing call on ctx
+ *     (dh2_last_error(NULL) for failures before a context exists).
+ *   - complex values are interleaved (re, im) float64; matrices are column-major.
+ *   - vectors x, y are in the ORIGINAL triangle order; the cluster permutation is internal.
+ *   - input buffers are copied during the call; the caller keeps ownership and may
+ *     free them after return.  Output buffers are caller-owned.
+ *   - a context owns all its device memory and is not thread-safe; distinct
+ *     contexts are independent.  All work is issued on the context's stream
+ *     (dh2_set_stream) and every API call synchronises that stream before return
+ *     unless stated otherwise.
+ *   - there is no CPU fallback: without a CUDA device every compute call fails
+ *     with DH2_ECUDA.
+ */
+#ifndef DH2_H
+#define DH2_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    DH2_OK = 0,
+    DH2_EINVAL = -1,    /* bad parameter, bad mesh index, triangle area <= 0, size mismatch */
+    DH2_ENOMEM = -2,    /* the device memory plan does not fit (checked before any launch) */
+    DH2_ECUDA = -3,     /* CUDA runtime error or no device */
+    DH2_ENCCL = -4,     /* reserved: multi-GPU transport error */
+    DH2_ESTATE = -5,    /* call order: recompress before build, RECOMP matvec before recompress */
+    DH2_EMISMATCH = -6, /* reserved: ranks passed different arguments */
+    DH2_ENOTIMPL = -7   /* configuration outside what this build supports (e.g. k > 64) */
+};
+
+/* recompression error-control modes (reading Q12 of DESIGN.md) */
+enum {
+    DH2_FROB_BLOCKREL = 0,   /* w_b = 1/||G_b||_F, k_tc = min{k : sum_{i>k} s_i^2 <= eps^2} (default) */
+    DH2_FROB_CLUSTERREL = 1, /* w_b = 1, k_tc = min{k : sum_{i>k} s_i^2 <= eps^2 sum_i s_i^2} */
+    DH2_SPEC_BLOCKREL = 2    /* w_b = 1/||G_b||_F, k_tc = min{k : s_{k+1} <= eps} */
+};
+
+/* which matrix: the interpolation DH^2 (V, E, S) or the recompressed one (Q, F, S~) */
+enum { DH2_ORIG = 0, DH2_RECOMP = 1 };
+
+/* matvec flags */
+enum { DH2_HOST_PTRS = 0, DH2_DEVICE_PTRS = 1 };
+
+typedef struct dh2_ctx dh2_ctx; /* opaque; owns all device memory */
+
+/* Triangle mesh.  xyz: nv*3 float64 row-major vertex coordinates;
+ * tri: nt*3 int64 0-based vertex indices.  DoF i = triangle i. */
+typedef struct {
+    int64_t nv, nt;
+    const double* xyz;
+    const int64_t* tri;
+} dh2_mesh;
+
+/* Parameters (BASELINE.json configs).
+ *   kappa     wave number >= 0 (Eq. helmholtz)
+ *   m         Chebyshev order per axis, k = m^3; this build supports 1 <= m <= 4
+ *   leaf_size clusters are split while #t > leaf_size
+ *   eta1      direction parameter of Eq. 3a / Remark 2.4
+ *   eta2      admissibility parameter of Eq. 3b/3c
+ *   quad      triangle quadrature points for V (must be 7: Radon's degree-5 rule) */
+typedef struct {
+    double kappa;
+    int32_t m;
+    int32_t leaf_size;
+    double eta1, eta2;
+    int32_t quad;
+} dh2_params;
+
+/* Device selection and multi-GPU description (world > 1 is reserved; pass NULL for
+ * device 0).  device = CUDA ordinal, or DH2_DEVICE_NONE: build the host structures
+ * only (cluster tree, directions, blocks, pairs — no device memory, no kernels); such a
+ * context supports dh2_export of host arrays and dh2_storage(DH2_ORIG) and fails every
+ * compute call with DH2_ESTATE.  It exists so structure parity can be checked without
+ * a GPU; it is not a compute fallback. */
+enum { DH2_DEVICE_NONE = -1 };
+typedef struct {
+    int32_t rank, world;
+    const void* nccl_uid;
+    int32_t device;
+} dh2_dist;
+
+/* Build the interpolation DH^2 matrix (§2).  Host: cluster tree (Def. 2.1, median
+ * split on the longest axis of the tight box), directions D_l (Remark 2.4) and sd_l
+ * (P:323-330), block tree (Def. 2.5, Eq. 3), row/column pair closure.  Device
+ * (sm_100a kernels): quadrature points, Chebyshev grids, leaf bases V_tc,
+ * transfer factors E_{t'c} (Eq. 10, Kronecker-factored), couplings S_b.
+ * On success *out receives a new context; on failure *out is NULL. */
+int dh2_build_interp(const dh2_mesh* mesh, const dh2_params* params, const dh2_dist* dist, dh2_ctx** out);
+
+/* Re-run only the device set-up kernels of dh2_build_interp on the resident
+ * structure (used to time the device part of the whole path). */
+int dh2_setup_device(dh2_ctx* ctx);
+
+/* Hybrid recompression (§3.2; Lemma Projections) with
+ * accuracy eps >= 0 and error-control mode.  Phases: basis weights (Eq. 18),
+ * block weights, total weights row/col (Eq. 17), truncation row/col (Eq. 19),
+ * projection S~_b = C_tc S_b C'_sc^*.  May be called repeatedly (it recomputes
+ * from the interpolation matrix). */
+int dh2_recompress(dh2_ctx* ctx, double eps, int32_t mode);
+
+/* Far-field matrix-vector product y = G_far x of the ORIG or RECOMP matrix.
+ * x, y: n complex (2n float64) in original triangle order; host pointers
+ * (flags = DH2_HOST_PTRS, copied through the context's stream) or device
+ * pointers (DH2_DEVICE_PTRS, no copies).  Nearfield is not included. */
+int dh2_matvec(dh2_ctx* ctx, int32_t which, const double* x, double* y, int32_t flags);
+
+/* Storage report, 16 B per complex coefficient, 1 KB = 1024 B.
+ * basis = leaf matrices + transfers of the row and the column basis;
+ * matrix = basis + couplings + nearfield (nearfield counted from block sizes). */
+typedef struct {
+    int64_t n;
+    double row_basis_bytes, col_basis_bytes, coupling_bytes, nearfield_bytes;
+    double kb_per_dof_basis, kb_per_dof_matrix;
+    int32_t max_rank;
+    double mean_rank;
+} dh2_storage_report;
+int dh2_storage(const dh2_ctx* ctx, int32_t which, dh2_storage_report* out);
+
+/* Set the CUDA stream (cudaStream_t) all work of ctx is issued on; NULL = the
+ * context's own stream.  The caller keeps ownership of the stream. */
+int dh2_set_stream(dh2_ctx* ctx, void* cuda_stream);
+
+/* Profiling: when enabled, every kernel class is bracketed by CUDA events on the
+ * context's stream; dh2_get_stats then reports per-class device time. */
+int dh2_set_profiling(dh2_ctx* ctx, int32_t enable);
+
+/* Statistics as a JSON document (two-call pattern: buf = NULL returns the size in
+ * *len).  Keys: n, structure counts, per kernel class {launches, ms, flops, bytes},
+ * certified E_row, E_col, ||G_far||_F^2 (after recompress), kernel launch count. */
+int dh2_get_stats(const dh2_ctx* ctx, char* buf, int64_t* len);
+
+/* Introspection for parity tests (two-call pattern): copy the named array into
+ * buf (nbytes = size of buf; buf = NULL returns the size in *nbytes).  Names and
+ * layouts are listed in DESIGN.md §"Export names" (structure arrays, offsets,
+ * and the device pools V, E, S, R, omega, Zhat_row/col, rank_row/col,
+ * sigma_row/col, Q_row/col, F_row/col, C_row/col, St). */
+int dh2_export(const dh2_ctx* ctx, const char* name, void* buf, int64_t* nbytes);
+
+/* Release all memory of ctx (NULL is a no-op). */
+int dh2_destroy(dh2_ctx* ctx);
+
+/* Message of the last failing call on ctx (or of the last failure without a context). */
+const char* dh2_last_error(const dh2_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DH2_H */

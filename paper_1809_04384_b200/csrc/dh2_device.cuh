@@ -1,0 +1,224 @@
+// Device-side building blocks for the DH^2 recompression kernels (sm_100a).
+// Complex float64 is double2 (re, im); all matrices are column-major.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dh2 {
+
+constexpr int MMAX = 5;  // maximal Chebyshev order per axis supported by the grid tables
+
+struct GridD {
+    double mid[3];
+    double half[3];
+    double nodes[3][MMAX];
+    int flat[3];
+};
+
+// ------------------------------------------------------------------ complex helpers
+__device__ __forceinline__ double2 cmk(double r, double i) { return make_double2(r, i); }
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return cmk(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return cmk(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) { return cmk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+__device__ __forceinline__ double2 cconj(double2 a) { return cmk(a.x, -a.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return cmk(a.x * s, a.y * s); }
+__device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
+// acc += a * b
+__device__ __forceinline__ void cfma(double2& acc, double2 a, double2 b) {
+    acc.x = fma(a.x, b.x, acc.x);
+    acc.x = fma(-a.y, b.y, acc.x);
+    acc.y = fma(a.x, b.y, acc.y);
+    acc.y = fma(a.y, b.x, acc.y);
+}
+// acc += conj(a) * b
+__device__ __forceinline__ void cfma_cj(double2& acc, double2 a, double2 b) {
+    acc.x = fma(a.x, b.x, acc.x);
+    acc.x = fma(a.y, b.y, acc.x);
+    acc.y = fma(a.x, b.y, acc.y);
+    acc.y = fma(-a.y, b.x, acc.y);
+}
+// acc += a * conj(b)
+__device__ __forceinline__ void cfma_bj(double2& acc, double2 a, double2 b) {
+    acc.x = fma(a.x, b.x, acc.x);
+    acc.x = fma(a.y, b.y, acc.x);
+    acc.y = fma(a.y, b.x, acc.y);
+    acc.y = fma(-a.x, b.y, acc.y);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double2 warp_sum2(double2 v) {
+    v.x = warp_sum(v.x);
+    v.y = warp_sum(v.y);
+    return v;
+}
+
+// Lagrange basis of the Chebyshev points of the first kind on one axis, evaluated at x
+// (P:245-248): L_j(xhat) = prod_{i != j} (xhat - z_i)/(z_j - z_i), xhat = (x - mid)/half.
+// A collapsed (flat) axis has L_j = delta_{j0} (DESIGN reading Q7).
+__device__ __forceinline__ void lagrange_axis(const GridD& g, int a, int m, const double* z, const double* inv_den,
+                                              double x, double* L) {
+    if (g.flat[a]) {
+        for (int j = 0; j < m; ++j) L[j] = (j == 0) ? 1.0 : 0.0;
+        return;
+    }
+    double xh = (x - g.mid[a]) / g.half[a];
+    for (int j = 0; j < m; ++j) {
+        double v = inv_den[j];
+        for (int i = 0; i < m; ++i)
+            if (i != j) v *= (xh - z[i]);
+        L[j] = v;
+    }
+}
+
+// ------------------------------------------------------------------ CTA-cooperative kernels
+
+// In-place X <- X * E or X <- X * E^* for the Kronecker-structured transfer matrix
+// E = Ez (x) Ey (x) Ex, nu = jx + m jy + m^2 jz (Eq. 10 with separable phase); X occupies
+// rows [0, rows) of the column-major smem matrix X (leading dimension ld).  Ef holds the
+// three m x m factors, Ef[a*m*m + jp*m + j] = E_a[j', j].  Each thread owns whole fibres.
+__device__ inline void kron_apply(double2* X, int ld, int rows, int m, const double2* Ef, bool adjoint) {
+    const int k = m * m * m;
+    const int m2 = m * m;
+    for (int a = 0; a < 3; ++a) {
+        const int stride = a == 0 ? 1 : (a == 1 ? m : m2);
+        const double2* F = Ef + a * m2;
+        const int nfib = rows * m2;
+        for (int f = threadIdx.x; f < nfib; f += blockDim.x) {
+            int i = f % rows;
+            int r = f / rows;  // index among the m^2 fibres of a row
+            // base nu with the a-th digit zero
+            int lowmask = stride;  // digits below a
+            int lo = r % lowmask;
+            int hi = r / lowmask;
+            int base = lo + hi * stride * m;
+            double2 in[MMAX], out[MMAX];
+            for (int j = 0; j < m; ++j) in[j] = X[i + (size_t)(base + j * stride) * ld];
+            for (int j = 0; j < m; ++j) {
+                double2 acc = cmk(0.0, 0.0);
+                if (!adjoint) {
+                    for (int jp = 0; jp < m; ++jp) cfma(acc, in[jp], F[jp * m + j]);  // sum_j' X[j'] E[j', j]
+                } else {
+                    for (int jp = 0; jp < m; ++jp) cfma_bj(acc, in[jp], F[j * m + jp]);  // sum_j' X[j'] conj(E[j, j'])
+                }
+                out[j] = acc;
+            }
+            for (int j = 0; j < m; ++j) X[i + (size_t)(base + j * stride) * ld] = out[j];
+        }
+        (void)k;
+        __syncthreads();
+    }
+}
+
+// Householder QR (R factor only) of the M x N column-major smem matrix A in place
+// ("skinny QR factorization").  On return the upper trapezoid of
+// A[0:min(M,N), :] is R; entries below the diagonal hold Householder vectors and must be
+// read as zero.  H_j = I - tau u u^*, u = x - beta e1, beta = -e^{i arg x0} |x|.
+__device__ inline void cta_qr(double2* A, int lda, int M, int N, double2* sh /* >= 2 */) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int K = min(M, N);
+    __syncthreads();
+    for (int j = 0; j < K; ++j) {
+        double2* colj = A + (size_t)j * lda;
+        if (warp == 0) {
+            double s = 0.0;
+            for (int i = j + 1 + lane; i < M; i += 32) s += cabs2(colj[i]);
+            s = warp_sum(s);
+            if (lane == 0) {
+                double2 alpha = colj[j];
+                double tau = 0.0;
+                double2 beta = alpha;
+                if (s > 0.0) {
+                    double aa = sqrt(cabs2(alpha));
+                    double xn = sqrt(s + aa * aa);
+                    double2 ph = aa > 0.0 ? cscale(alpha, 1.0 / aa) : cmk(1.0, 0.0);
+                    beta = cscale(ph, -xn);
+                    colj[j] = cscale(ph, aa + xn);  // u0 = alpha - beta
+                    tau = 1.0 / (xn * (xn + aa));   // 2 / (u^* u)
+                }
+                sh[0] = beta;
+                sh[1] = cmk(tau, 0.0);
+            }
+        }
+        __syncthreads();
+        const double tau = sh[1].x;
+        if (tau != 0.0) {
+            for (int c = j + 1 + warp; c < N; c += nw) {
+                double2* colc = A + (size_t)c * lda;
+                double2 w = cmk(0.0, 0.0);
+                for (int i = j + lane; i < M; i += 32) cfma_cj(w, colj[i], colc[i]);
+                w = warp_sum2(w);
+                w = cscale(w, tau);
+                for (int i = j + lane; i < M; i += 32) {
+                    double2 u = colj[i];
+                    colc[i] = csub(colc[i], cmul(u, w));
+                }
+            }
+        }
+        __syncthreads();
+        if (tid == 0) colj[j] = sh[0];
+        __syncthreads();
+    }
+}
+
+// One-sided (Hestenes) Jacobi on the columns of the m x n smem matrix W (column-major,
+// leading dimension ld): on return the columns are mutually orthogonal, W = U diag(s) J^*
+// with J unitary, so the non-zero columns normalised are left singular vectors.
+// Round-robin (circle) ordering, one warp per column pair.  Returns the number of sweeps.
+__device__ inline int cta_jacobi(double2* W, int ld, int m, int n, int* flag) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    if (n <= 1) return 0;
+    const int np = n + (n & 1);
+    const double tol = fmax((double)m, 1.0) * 2.220446049250313e-16;
+    int sweep = 0;
+    for (; sweep < 60; ++sweep) {
+        __syncthreads();
+        if (tid == 0) *flag = 0;
+        __syncthreads();
+        for (int r = 0; r < np - 1; ++r) {
+            for (int pi = warp; pi < np / 2; pi += nw) {
+                int i0 = pi, i1 = np - 1 - pi;
+                int p = i0 == 0 ? 0 : 1 + (i0 - 1 + r) % (np - 1);
+                int q = i1 == 0 ? 0 : 1 + (i1 - 1 + r) % (np - 1);
+                if (p >= n || q >= n) continue;
+                double2* cp = W + (size_t)p * ld;
+                double2* cq = W + (size_t)q * ld;
+                double al = 0.0, be = 0.0;
+                double2 ga = cmk(0.0, 0.0);
+                for (int i = lane; i < m; i += 32) {
+                    double2 a = cp[i], b = cq[i];
+                    al += cabs2(a);
+                    be += cabs2(b);
+                    cfma_cj(ga, a, b);
+                }
+                al = warp_sum(al);
+                be = warp_sum(be);
+                ga = warp_sum2(ga);
+                double g = sqrt(cabs2(ga));
+                if (g > tol * sqrt(al * be) && al > 0.0 && be > 0.0) {
+                    double zeta = (be - al) / (2.0 * g);
+                    double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                    double c = 1.0 / sqrt(1.0 + t * t);
+                    double s = c * t;
+                    double2 e = cmk(ga.x / g, -ga.y / g);  // e^{-i phi}, gamma = g e^{i phi}
+                    for (int i = lane; i < m; i += 32) {
+                        double2 a = cp[i];
+                        double2 b = cmul(e, cq[i]);
+                        cp[i] = csub(cscale(a, c), cscale(b, s));
+                        cq[i] = cadd(cscale(a, s), cscale(b, c));
+                    }
+                    if (lane == 0) *flag = 1;
+                }
+            }
+            __syncthreads();
+        }
+        if (*flag == 0) break;
+    }
+    __syncthreads();
+    return sweep;
+}
+
+}  // namespace dh2

@@ -1,0 +1,285 @@
+// Host structures of the DH^2 matrix — see dh2_host.h.  Every formula cites PAPER.md.
+#include "dh2_host.h"
+
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <stdexcept>
+
+namespace dh2 {
+
+static inline double norm3(double a, double b, double c) { return std::sqrt((a * a + b * b) + c * c); }
+
+void validate_mesh(const double* xyz, int64_t nv, const int64_t* tri, int64_t nt) {
+    if (nv < 3 || nt < 1 || !xyz || !tri) throw std::invalid_argument("empty mesh");
+    for (int64_t i = 0; i < nt; ++i) {
+        for (int j = 0; j < 3; ++j)
+            if (tri[3 * i + j] < 0 || tri[3 * i + j] >= nv) throw std::invalid_argument("triangle index out of range");
+        const double* a = xyz + 3 * tri[3 * i];
+        const double* b = xyz + 3 * tri[3 * i + 1];
+        const double* c = xyz + 3 * tri[3 * i + 2];
+        double e1[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+        double e2[3] = {c[0] - a[0], c[1] - a[1], c[2] - a[2]};
+        double cr0 = e1[1] * e2[2] - e1[2] * e2[1];
+        double cr1 = e1[2] * e2[0] - e1[0] * e2[2];
+        double cr2 = e1[0] * e2[1] - e1[1] * e2[0];
+        if (!(norm3(cr0, cr1, cr2) > 0.0)) throw std::invalid_argument("triangle with area <= 0");
+    }
+}
+
+// Cluster tree: median split along the longest axis of the tight box (DESIGN
+// reading R-cluster), ties of the axis to the lowest axis, of the centroid to the triangle
+// index; the first child receives ceil(#t/2); split while #t > leaf; BFS numbering.
+void Structure::build_tree(const double* xyz, const int64_t* tri, int64_t nt) {
+    ClusterTree& T = ct;
+    T.n = nt;
+    std::vector<double> cen(3 * nt);
+    for (int64_t i = 0; i < nt; ++i)
+        for (int a = 0; a < 3; ++a)
+            cen[3 * i + a] = ((xyz[3 * tri[3 * i] + a] + xyz[3 * tri[3 * i + 1] + a]) + xyz[3 * tri[3 * i + 2] + a]) / 3.0;
+    T.perm.resize(nt);
+    std::iota(T.perm.begin(), T.perm.end(), 0);
+    T.begin = {0};
+    T.end = {nt};
+    T.level = {0};
+    T.parent = {-1};
+    T.child0 = {-1};
+    T.child1 = {-1};
+    for (size_t t = 0; t < T.begin.size(); ++t) {
+        int64_t b = T.begin[t], e = T.end[t];
+        double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (int64_t p = b; p < e; ++p)
+            for (int v = 0; v < 3; ++v)
+                for (int a = 0; a < 3; ++a) {
+                    double x = xyz[3 * tri[3 * T.perm[p] + v] + a];
+                    lo[a] = std::min(lo[a], x);
+                    hi[a] = std::max(hi[a], x);
+                }
+        for (int a = 0; a < 3; ++a) {
+            T.lo.push_back(lo[a]);
+            T.hi.push_back(hi[a]);
+        }
+        int64_t cnt = e - b;
+        if (cnt > p.leaf) {
+            double ext[3] = {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]};
+            int axis = 0;
+            for (int a = 1; a < 3; ++a)
+                if (ext[a] > ext[axis]) axis = a;
+            std::sort(T.perm.begin() + b, T.perm.begin() + e, [&](int64_t i, int64_t j) {
+                double ki = cen[3 * i + axis], kj = cen[3 * j + axis];
+                return ki < kj || (ki == kj && i < j);
+            });
+            int64_t half = (cnt + 1) / 2;
+            int64_t c0 = (int64_t)T.begin.size();
+            int64_t rng[2][2] = {{b, b + half}, {b + half, e}};
+            for (auto& r : rng) {
+                T.begin.push_back(r[0]);
+                T.end.push_back(r[1]);
+                T.level.push_back(T.level[t] + 1);
+                T.parent.push_back((int64_t)t);
+                T.child0.push_back(-1);
+                T.child1.push_back(-1);
+            }
+            T.child0[t] = c0;
+            T.child1[t] = c0 + 1;
+        }
+    }
+    int64_t nc = (int64_t)T.begin.size();
+    T.depth = 0;
+    for (int64_t t = 0; t < nc; ++t) T.depth = std::max<int>(T.depth, (int)T.level[t]);
+    T.levels.assign(T.depth + 1, {});
+    T.diam.resize(nc);
+    T.mid.resize(3 * nc);
+    for (int64_t t = 0; t < nc; ++t) {
+        T.levels[T.level[t]].push_back(t);
+        double e0 = T.hi[3 * t] - T.lo[3 * t], e1 = T.hi[3 * t + 1] - T.lo[3 * t + 1], e2 = T.hi[3 * t + 2] - T.lo[3 * t + 2];
+        T.diam[t] = norm3(e0, e1, e2);  // diam(B_t)
+        for (int a = 0; a < 3; ++a) T.mid[3 * t + a] = 0.5 * (T.lo[3 * t + a] + T.hi[3 * t + a]);
+    }
+}
+
+// Remark 2.4: D_l = {0} if kappa d_l <= eta1; else m = ceil(sqrt2 kappa d_l/eta1) and
+// the 6 m^2 normalised centres of the squares of the faces of [-1,1]^3 (DESIGN reading Q2),
+// faces -x,+x,-y,+y,-z,+z, centres (2i+1-m)/m on the two remaining axes in increasing order.
+const std::vector<double>& Structure::D(int l) {
+    if (dirs_ready[l]) return dirs[l];
+    std::vector<double>& out = dirs[l];
+    int md = mdir[l];
+    if (md == 0) {
+        out = {0.0, 0.0, 0.0};
+    } else {
+        out.reserve((size_t)18 * md * md);
+        for (int a = 0; a < 3; ++a) {
+            int u = a == 0 ? 1 : 0, w = a == 2 ? 1 : 2;
+            for (int sgn = -1; sgn <= 1; sgn += 2)
+                for (int iu = 0; iu < md; ++iu)
+                    for (int iv = 0; iv < md; ++iv) {
+                        double q[3];
+                        q[a] = (double)sgn;
+                        q[u] = (double)(2 * iu + 1 - md) / md;
+                        q[w] = (double)(2 * iv + 1 - md) / md;
+                        double nr = norm3(q[0], q[1], q[2]);
+                        out.push_back(q[0] / nr);
+                        out.push_back(q[1] / nr);
+                        out.push_back(q[2] / nr);
+                    }
+        }
+    }
+    dirs_ready[l] = 1;
+    return out;
+}
+
+// Best approximation of y in D_l with the symmetric tie rule (DESIGN reading Q4):
+// candidates |y-c|^2 <= min + 1e-12, maximise s<c,w>, s = sign<y,w>, w = (1,sqrt2,sqrt3)/sqrt6.
+int64_t Structure::nearest(int l, const double y[3]) {
+    const std::vector<double>& Dl = D(l);
+    int64_t nd = (int64_t)Dl.size() / 3;
+    if (nd == 1) return 0;
+    static const double wr[3] = {1.0, std::sqrt(2.0), std::sqrt(3.0)};
+    const double wn = norm3(wr[0], wr[1], wr[2]);
+    const double w[3] = {wr[0] / wn, wr[1] / wn, wr[2] / wn};
+    double mn = INFINITY;
+    for (int64_t c = 0; c < nd; ++c) {
+        double d0 = y[0] - Dl[3 * c], d1 = y[1] - Dl[3 * c + 1], d2 = y[2] - Dl[3 * c + 2];
+        double dd = (d0 * d0 + d1 * d1) + d2 * d2;
+        if (dd < mn) mn = dd;
+    }
+    const double thr = mn + 1e-12;
+    const double yw = (y[0] * w[0] + y[1] * w[1]) + y[2] * w[2];
+    const double s = yw >= 0.0 ? 1.0 : -1.0;
+    int64_t best = -1;
+    double bscore = -INFINITY;
+    for (int64_t c = 0; c < nd; ++c) {
+        double d0 = y[0] - Dl[3 * c], d1 = y[1] - Dl[3 * c + 1], d2 = y[2] - Dl[3 * c + 2];
+        double dd = (d0 * d0 + d1 * d1) + d2 * d2;
+        if (dd <= thr) {
+            double sc = s * ((Dl[3 * c] * w[0] + Dl[3 * c + 1] * w[1]) + Dl[3 * c + 2] * w[2]);
+            if (best < 0 || sc > bscore) {
+                best = c;
+                bscore = sc;
+            }
+        }
+    }
+    return best;
+}
+
+// sd_l(c) = nearest direction of D_{l+1} to c.
+int64_t Structure::sd(int l, int64_t c) {
+    std::vector<int64_t>& cache = sd_cache[l];
+    if ((int64_t)cache.size() <= c) cache.resize(D(l).size() / 3, -1);
+    if (cache[c] < 0) {
+        const std::vector<double>& Dl = D(l);
+        double y[3] = {Dl[3 * c], Dl[3 * c + 1], Dl[3 * c + 2]};
+        cache[c] = nearest(l + 1, y);
+    }
+    return cache[c];
+}
+
+// Minimal block tree (Def. 2.5): level-synchronous recursion from (root, root);
+// admissible (Eq. 3b, 3c) -> L+ with c_ts; else children if both have some; else L-.
+void Structure::build_blocks() {
+    ClusterTree& T = ct;
+    std::vector<std::pair<int64_t, int64_t>> front = {{0, 0}};
+    int lvl = 0;
+    while (!front.empty()) {
+        std::vector<std::pair<int64_t, int64_t>> next;
+        std::vector<Block> adm;
+        for (auto& ts : front) {
+            int64_t t = ts.first, s = ts.second;
+            double g[3];
+            for (int a = 0; a < 3; ++a)
+                g[a] = std::max(0.0, std::max(T.lo[3 * t + a] - T.hi[3 * s + a], T.lo[3 * s + a] - T.hi[3 * t + a]));
+            double dist = norm3(g[0], g[1], g[2]);
+            double dmax = std::max(T.diam[t], T.diam[s]);
+            bool ok = (dmax <= p.eta2 * dist) && (p.kappa * (dmax * dmax) <= p.eta2 * dist);
+            if (ok) {
+                adm.push_back({t, s, -1});
+            } else if (!T.is_leaf(t) && !T.is_leaf(s)) {
+                int64_t tc[2] = {T.child0[t], T.child1[t]}, sc[2] = {T.child0[s], T.child1[s]};
+                for (int i = 0; i < 2; ++i)
+                    for (int j = 0; j < 2; ++j) next.push_back({tc[i], sc[j]});
+            } else {
+                near.push_back({t, s});
+            }
+        }
+        if (!adm.empty()) {
+            D(lvl);
+#pragma omp parallel for schedule(dynamic, 64)
+            for (int64_t i = 0; i < (int64_t)adm.size(); ++i) {
+                int64_t t = adm[i].t, s = adm[i].s;
+                double dv[3];
+                for (int a = 0; a < 3; ++a) dv[a] = T.mid[3 * t + a] - T.mid[3 * s + a];
+                double nr = norm3(dv[0], dv[1], dv[2]);
+                double y[3] = {dv[0] / nr, dv[1] / nr, dv[2] / nr};
+                adm[i].c = nearest(lvl, y);
+            }
+            blocks.insert(blocks.end(), adm.begin(), adm.end());
+        }
+        front.swap(next);
+        ++lvl;
+    }
+    std::sort(blocks.begin(), blocks.end(), [](const Block& a, const Block& b) { return a.t < b.t || (a.t == b.t && a.s < b.s); });
+    std::sort(near.begin(), near.end());
+}
+
+// Active pairs: (t, c_b) of every admissible block plus the closure (t', sd_t(c)).
+std::vector<std::vector<Pair>> Structure::closure(bool row) {
+    ClusterTree& T = ct;
+    std::vector<std::vector<Pair>> pairs(T.depth + 1);
+    for (auto& b : blocks) {
+        int64_t t = row ? b.t : b.s;
+        pairs[T.level[t]].push_back({t, b.c});
+    }
+    for (int l = 0; l <= T.depth; ++l) {
+        auto& v = pairs[l];
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+        if (l == T.depth) break;
+        for (auto& pr : v) {
+            if (T.is_leaf(pr.t)) continue;
+            int64_t c2 = sd(l, pr.c);
+            pairs[l + 1].push_back({T.child0[pr.t], c2});
+            pairs[l + 1].push_back({T.child1[pr.t], c2});
+        }
+    }
+    return pairs;
+}
+
+void Structure::build(const double* xyz, int64_t nv, const int64_t* tri, int64_t nt, const Params& prm) {
+    (void)nv;
+    p = prm;
+    k = p.m * p.m * p.m;
+    build_tree(xyz, tri, nt);
+    int L = ct.depth;
+    d_level.assign(L + 1, 0.0);
+    mdir.assign(L + 1, 0);
+    for (int l = 0; l <= L; ++l) {
+        double d = 0.0;
+        for (int64_t t : ct.levels[l]) d = std::max(d, ct.diam[t]);
+        d_level[l] = d;
+        if (p.kappa * d <= p.eta1)
+            mdir[l] = 0;
+        else
+            mdir[l] = (int)std::ceil(((std::sqrt(2.0) * p.kappa) * d) / p.eta1);
+    }
+    dirs.assign(L + 1, {});
+    dirs_ready.assign(L + 1, 0);
+    sd_cache.assign(L + 1, {});
+    build_blocks();
+    row_pairs = closure(true);
+    col_pairs = closure(false);
+    basis_pairs.assign(L + 1, {});
+    for (int l = 0; l <= L; ++l) {
+        auto& v = basis_pairs[l];
+        v = row_pairs[l];
+        v.insert(v.end(), col_pairs[l].begin(), col_pairs[l].end());
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+        if (!v.empty() && first_level < 0) first_level = l;
+    }
+    // make sure every level that hosts pairs has its direction set materialised
+    for (int l = 0; l <= L; ++l)
+        if (!basis_pairs[l].empty()) D(l);
+}
+
+}  // namespace dh2

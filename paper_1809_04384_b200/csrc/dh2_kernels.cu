@@ -1,0 +1,764 @@
+// sm_100a kernels of the DH^2 set-up and hybrid recompression.
+// Every kernel cites the PAPER.md passage (P:<line>) it implements.
+#include <cmath>
+#include <cstdio>
+
+#include "dh2_kernels.cuh"
+
+namespace dh2 {
+
+__device__ double g_cheb[2 * MMAX];  // z_j and 1/prod_{i!=j}(z_j - z_i) of the current order
+
+static inline int odd_ld(int r) { return (r | 1); }
+
+// ============================================================== set-up (§2)
+
+// Chebyshev points of the first kind z_j = cos(pi (2j+1)/(2m)) (Q6) and the
+// barycentric denominators of the 1-D Lagrange polynomials.
+__global__ void k_cheb(int m) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        for (int j = 0; j < m; ++j) g_cheb[j] = cos(M_PI * (2 * j + 1) / (2.0 * m));
+        for (int j = 0; j < m; ++j) {
+            double d = 1.0;
+            for (int i = 0; i < m; ++i)
+                if (i != j) d *= (g_cheb[j] - g_cheb[i]);
+            g_cheb[MMAX + j] = 1.0 / d;
+        }
+    }
+}
+
+// Quadrature points of Radon's 7-point degree-5 rule on every triangle, in cluster order
+// (v_{tc,i nu} integrals; DESIGN reading Q11).  qp = (x, y, z, |tau| w_q).
+__global__ void k_quad(PlanD P) {
+    const double s15 = sqrt(15.0);
+    const double A = (6.0 - s15) / 21.0, B = (6.0 + s15) / 21.0;
+    const double WA = (155.0 - s15) / 1200.0, WB = (155.0 + s15) / 1200.0;
+    int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= P.n * 7) return;
+    int p = idx / 7, q = idx % 7;
+    int64_t tr = P.perm[p];
+    const double* v0 = P.xyz + 3 * P.tri[3 * tr];
+    const double* v1 = P.xyz + 3 * P.tri[3 * tr + 1];
+    const double* v2 = P.xyz + 3 * P.tri[3 * tr + 2];
+    double l0, l1, l2, w;
+    switch (q) {
+        case 0: l0 = l1 = l2 = 1.0 / 3.0; w = 9.0 / 40.0; break;
+        case 1: l0 = A; l1 = A; l2 = 1.0 - 2.0 * A; w = WA; break;
+        case 2: l0 = A; l1 = 1.0 - 2.0 * A; l2 = A; w = WA; break;
+        case 3: l0 = 1.0 - 2.0 * A; l1 = A; l2 = A; w = WA; break;
+        case 4: l0 = B; l1 = B; l2 = 1.0 - 2.0 * B; w = WB; break;
+        case 5: l0 = B; l1 = 1.0 - 2.0 * B; l2 = B; w = WB; break;
+        default: l0 = 1.0 - 2.0 * B; l1 = B; l2 = B; w = WB; break;
+    }
+    double e1[3], e2[3], x[3];
+    for (int a = 0; a < 3; ++a) {
+        e1[a] = v1[a] - v0[a];
+        e2[a] = v2[a] - v0[a];
+        x[a] = l0 * v0[a] + l1 * v1[a] + l2 * v2[a];
+    }
+    double c0 = e1[1] * e2[2] - e1[2] * e2[1], c1 = e1[2] * e2[0] - e1[0] * e2[2], c2 = e1[0] * e2[1] - e1[1] * e2[0];
+    double area = 0.5 * sqrt(c0 * c0 + c1 * c1 + c2 * c2);
+    P.qp[idx] = make_double4(x[0], x[1], x[2], area * w);
+}
+
+// Tensor Chebyshev grid on the tight box of every cluster: xi = mid + half z,
+// a collapsed axis (hi-lo <= 1e-12 diam) keeps one node at mid (DESIGN reading Q7).
+__global__ void k_grid(PlanD P) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= P.nclusters) return;
+    GridD g;
+    double ext[3];
+    for (int a = 0; a < 3; ++a) ext[a] = P.c_hi[3 * t + a] - P.c_lo[3 * t + a];
+    double diam = sqrt((ext[0] * ext[0] + ext[1] * ext[1]) + ext[2] * ext[2]);
+    for (int a = 0; a < 3; ++a) {
+        g.mid[a] = 0.5 * (P.c_lo[3 * t + a] + P.c_hi[3 * t + a]);
+        g.half[a] = 0.5 * ext[a];
+        g.flat[a] = ext[a] <= 1e-12 * diam;
+        for (int j = 0; j < MMAX; ++j)
+            g.nodes[a][j] = (j < P.m) ? (g.flat[a] ? g.mid[a] : g.mid[a] + g.half[a] * g_cheb[j]) : 0.0;
+    }
+    P.grid[t] = g;
+}
+
+// Leaf bases V_tc[i,nu] = sum_q |tau_i| w_q exp(i kappa <x_iq, c>) L_{t,nu}(x_iq)
+// (modified Lagrange polynomials P:270-275).  One CTA per leaf basis pair.
+__global__ void k_leafV(PlanD P, const int* bps) {
+    extern __shared__ double2 sm[];
+    const int bp = bps[blockIdx.x];
+    const int t = P.bp_t[bp];
+    const int nt = P.c_size[t];
+    const int64_t b0 = P.c_begin[t];
+    const int m = P.m, k = P.k;
+    __shared__ GridD g;
+    __shared__ double cheb[2 * MMAX];
+    if (threadIdx.x == 0) g = P.grid[t];
+    if (threadIdx.x < 2 * MMAX) cheb[threadIdx.x] = g_cheb[threadIdx.x];
+    __syncthreads();
+    const double* c = P.dirs + 3 * P.bp_dir[bp];
+    double2* ph = sm;                              // nt*7
+    double* L = reinterpret_cast<double*>(sm + nt * 7);  // nt*7*3*m
+    for (int idx = threadIdx.x; idx < nt * 7; idx += blockDim.x) {
+        double4 q = P.qp[b0 * 7 + idx];
+        double arg = P.kappa * ((q.x * c[0] + q.y * c[1]) + q.z * c[2]);
+        double s, co;
+        sincos(arg, &s, &co);
+        ph[idx] = cmk(q.w * co, q.w * s);
+        double xs[3] = {q.x, q.y, q.z};
+        for (int a = 0; a < 3; ++a) lagrange_axis(g, a, m, cheb, cheb + MMAX, xs[a], L + (idx * 3 + a) * m);
+    }
+    __syncthreads();
+    double2* V = P.V + P.bp_V_off[bp];
+    for (int idx = threadIdx.x; idx < nt * k; idx += blockDim.x) {
+        int i = idx % nt, nu = idx / nt;
+        int jx = nu % m, jy = (nu / m) % m, jz = nu / (m * m);
+        double2 acc = cmk(0.0, 0.0);
+        for (int q = 0; q < 7; ++q) {
+            const double* Lq = L + ((i * 7 + q) * 3) * m;
+            double l = Lq[jx] * Lq[m + jy] * Lq[2 * m + jz];
+            double2 p = ph[i * 7 + q];
+            acc.x = fma(p.x, l, acc.x);
+            acc.y = fma(p.y, l, acc.y);
+        }
+        V[(size_t)nu * nt + i] = acc;
+    }
+}
+
+// Transfer factors of E_{t'c} (Eq. 10): with c' = sd_t(c) the entry
+// exp(i kappa <xi_{t'nu'}, c - c'>) L_{t,nu}(xi_{t'nu'}) factorises over the axes,
+// E = Ez (x) Ey (x) Ex with E_a[j',j] = exp(i kappa xi'_{a,j'} (c-c')_a) L_{t,a,j}(xi'_{a,j'}).
+__global__ void k_E(PlanD P, const int* bps, int nbps) {
+    const int m = P.m, m2 = m * m;
+    int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    int per = 2 * 3 * m2;
+    if (idx >= nbps * per) return;
+    int ib = idx / per, r = idx % per;
+    int ci = r / (3 * m2);
+    int a = (r / m2) % 3;
+    int jp = (r % m2) / m, j = r % m;
+    int bp = bps[ib];
+    int t = P.bp_t[bp];
+    int cbp = ci == 0 ? P.bp_child0[bp] : P.bp_child1[bp];
+    int tc = P.bp_t[cbp];
+    const GridD& gp = P.grid[t];
+    const GridD& gc = P.grid[tc];
+    double cheb[2 * MMAX];
+    for (int i = 0; i < 2 * MMAX; ++i) cheb[i] = g_cheb[i];
+    double xi = gc.nodes[a][jp];
+    double L[MMAX];
+    lagrange_axis(gp, a, m, cheb, cheb + MMAX, xi, L);
+    double dc = P.dirs[3 * P.bp_dir[bp] + a] - P.dirs[3 * P.bp_sddir[bp] + a];
+    double s, co;
+    sincos(P.kappa * xi * dc, &s, &co);
+    P.E[P.bp_E_off[bp] + r] = cmk(co * L[j], s * L[j]);
+    (void)ci;
+}
+
+// Coupling matrices S_b[nu,mu] = g_c(xi_{t,nu}, xi_{s,mu})
+//   = exp(i kappa (r - <xi_t - xi_s, c>)) / (4 pi r).  CTA per block.
+__global__ void k_S(PlanD P) {
+    const int b = blockIdx.x;
+    const int m = P.m, k = P.k;
+    __shared__ GridD gt, gs;
+    __shared__ double c[3];
+    if (threadIdx.x == 0) {
+        gt = P.grid[P.blk_t[b]];
+        gs = P.grid[P.blk_s[b]];
+        for (int a = 0; a < 3; ++a) c[a] = P.dirs[3 * P.blk_dir[b] + a];
+    }
+    __syncthreads();
+    double2* S = P.S + (size_t)b * k * k;
+    const double inv4pi = 1.0 / (4.0 * M_PI);
+    for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) {
+        int nu = idx % k, mu = idx / k;
+        double d0 = gt.nodes[0][nu % m] - gs.nodes[0][mu % m];
+        double d1 = gt.nodes[1][(nu / m) % m] - gs.nodes[1][(mu / m) % m];
+        double d2 = gt.nodes[2][nu / (m * m)] - gs.nodes[2][mu / (m * m)];
+        double r = sqrt((d0 * d0 + d1 * d1) + d2 * d2);
+        double dcv = (d0 * c[0] + d1 * c[1]) + d2 * c[2];
+        double s, co;
+        sincos(P.kappa * (r - dcv), &s, &co);
+        double f = inv4pi / r;
+        S[idx] = cmk(co * f, s * f);
+    }
+}
+
+void launch_quad(const PlanD& P, cudaStream_t s) {
+    k_cheb<<<1, 32, 0, s>>>(P.m);
+    int tot = P.n * 7;
+    k_quad<<<(tot + 255) / 256, 256, 0, s>>>(P);
+}
+void launch_grid(const PlanD& P, cudaStream_t s) { k_grid<<<(P.nclusters + 127) / 128, 128, 0, s>>>(P); }
+void launch_leafV(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStream_t s) {
+    if (!nbps) return;
+    size_t sm = (size_t)maxrows * 7 * sizeof(double2) + (size_t)maxrows * 7 * 3 * P.m * sizeof(double);
+    k_leafV<<<nbps, 256, sm, s>>>(P, bps);
+}
+void launch_E(const PlanD& P, const int* bps, int nbps, cudaStream_t s) {
+    if (!nbps) return;
+    int tot = nbps * 6 * P.m * P.m;
+    k_E<<<(tot + 255) / 256, 256, 0, s>>>(P, bps, nbps);
+}
+void launch_S(const PlanD& P, cudaStream_t s) {
+    if (!P.nblk) return;
+    k_S<<<P.nblk, 256, 0, s>>>(P);
+}
+
+// ============================================================== recompression (§3.2)
+
+__device__ inline void zero_lower(double2* A, int lda, int rows, int cols) {
+    for (int idx = threadIdx.x; idx < rows * cols; idx += blockDim.x) {
+        int i = idx % rows, j = idx / rows;
+        if (i > j) A[i + (size_t)j * lda] = cmk(0.0, 0.0);
+    }
+}
+
+// Basis weights (Eq. 18; [BO10, Alg. 16] generalised to directions):
+// leaf with #t > k: R_tc = R of QR(V_tc); non-leaf: R_tc = R of QR([R_{t1c1} E_{t1c}; R_{t2c2} E_{t2c}]).
+// One CTA per basis pair of one level.
+__global__ void k_basis(PlanD P, const int* bps, int lda) {
+    extern __shared__ double2 sm[];
+    const int bp = bps[blockIdx.x];
+    const int k = P.k, m = P.m;
+    double2* A = sm;
+    double2* Ef = sm + (size_t)lda * k;
+    double2* sh = Ef + 6 * m * m;
+    int rows;
+    if (P.bp_child0[bp] < 0) {
+        const int t = P.bp_t[bp];
+        rows = P.c_size[t];
+        const double2* V = P.V + P.bp_V_off[bp];
+        for (int idx = threadIdx.x; idx < rows * k; idx += blockDim.x) A[idx % rows + (size_t)(idx / rows) * lda] = V[idx];
+        __syncthreads();
+    } else {
+        int c0 = P.bp_child0[bp], c1 = P.bp_child1[bp];
+        int r0 = P.bp_R_rows[c0], r1 = P.bp_R_rows[c1];
+        const double2* R0 = P.R + P.bp_R_off[c0];
+        const double2* R1 = P.R + P.bp_R_off[c1];
+        for (int idx = threadIdx.x; idx < r0 * k; idx += blockDim.x) A[idx % r0 + (size_t)(idx / r0) * lda] = R0[idx];
+        for (int idx = threadIdx.x; idx < r1 * k; idx += blockDim.x) A[r0 + idx % r1 + (size_t)(idx / r1) * lda] = R1[idx];
+        const double2* Eg = P.E + P.bp_E_off[bp];
+        for (int idx = threadIdx.x; idx < 6 * m * m; idx += blockDim.x) Ef[idx] = Eg[idx];
+        __syncthreads();
+        kron_apply(A, lda, r0, m, Ef, false);
+        kron_apply(A + r0, lda, r1, m, Ef + 3 * m * m, false);
+        rows = r0 + r1;
+    }
+    const int out = P.bp_R_rows[bp];
+    if (rows > k) {
+        cta_qr(A, lda, rows, k, sh);
+        zero_lower(A, lda, k, k);
+        __syncthreads();
+    }
+    double2* R = P.R + P.bp_R_off[bp];
+    for (int idx = threadIdx.x; idx < out * k; idx += blockDim.x) R[idx] = A[idx % out + (size_t)(idx / out) * lda];
+}
+
+void launch_basis(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStream_t s) {
+    if (!nbps) return;
+    int lda = odd_ld(maxrows);
+    size_t sm = ((size_t)lda * P.k + 6 * P.m * P.m + 2) * sizeof(double2);
+    k_basis<<<nbps, 256, sm, s>>>(P, bps, lda);
+}
+
+// Block weights (DESIGN reading Q12): ||G_b||_F^2 = ||R_tc S_b R_sc^*||_F^2 (W = P R, Eq. 18);
+// w_b = 1/||G_b||_F for the block-relative modes, 1 for FROB_CLUSTERREL.  CTA per block.
+__global__ void k_block_weights(PlanD P, int mode, int ldu) {
+    extern __shared__ double2 sm[];
+    __shared__ double red[32];
+    const int b = blockIdx.x, k = P.k;
+    const int bt = P.blk_bprow[b], bs = P.blk_bpcol[b];
+    const int rt = P.bp_R_rows[bt], rs = P.bp_R_rows[bs];
+    const double2* Rt = P.R + P.bp_R_off[bt];
+    const double2* Rs = P.R + P.bp_R_off[bs];
+    const double2* S = P.S + (size_t)b * k * k;
+    double2* U = sm;  // rt x k
+    for (int idx = threadIdx.x; idx < rt * k; idx += blockDim.x) {
+        int i = idx % rt, nu = idx / rt;
+        double2 acc = cmk(0.0, 0.0);
+        for (int mu = 0; mu < k; ++mu) cfma(acc, Rt[i + (size_t)mu * rt], S[mu + (size_t)nu * k]);
+        U[i + (size_t)nu * ldu] = acc;
+    }
+    __syncthreads();
+    double part = 0.0;
+    for (int idx = threadIdx.x; idx < rt * rs; idx += blockDim.x) {
+        int i = idx % rt, j = idx / rt;
+        double2 acc = cmk(0.0, 0.0);
+        for (int nu = 0; nu < k; ++nu) cfma_bj(acc, U[i + (size_t)nu * ldu], Rs[j + (size_t)nu * rs]);
+        part += cabs2(acc);
+    }
+    part = warp_sum(part);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+        P.normG2[b] = s;
+        P.omega[b] = (mode == 1) ? 1.0 : 1.0 / sqrt(s);
+    }
+}
+
+void launch_block_weights(const PlanD& P, int mode, cudaStream_t s) {
+    if (!P.nblk) return;
+    int ldu = odd_ld(P.k);
+    size_t sm = (size_t)ldu * P.k * sizeof(double2);
+    k_block_weights<<<P.nblk, 256, sm, s>>>(P, mode, ldu);
+}
+
+// Total weights, one CTA per pair of one level (top-down):
+//   Z_tc = [w_b S_b R_sc^* (s in row(t,c)) | E_{tc+} Zhat_{t+c+}^* (c+ in sd^{-1}(c))],
+//   Zhat_tc = R factor of the skinny QR of Z_tc^* (rows stacked incrementally,
+//   R <- qr([R; next rows]) whenever the buffer is full; gamma = 0 at the root).
+// Row pass: Z^* rows w_b R_sc S_b^*.  Column pass (adjoint): w_b R_tc S_b.
+__global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, int lda, int bufrows) {
+    extern __shared__ double2 sm[];
+    const int p = p0 + blockIdx.x;
+    const int k = P.k, m = P.m;
+    double2* A = sm;
+    double2* Ef = sm + (size_t)lda * k;
+    double2* sh = Ef + 3 * m * m;
+    int cur = 0;
+    bool compressed = false;
+    for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) {
+        const int b = X.blk[ib];
+        const int obp = row ? P.blk_bpcol[b] : P.blk_bprow[b];
+        const int r = P.bp_R_rows[obp];
+        if (cur + r > bufrows) {
+            cta_qr(A, lda, cur, k, sh);
+            cur = min(cur, k);
+            zero_lower(A, lda, cur, k);
+            compressed = true;
+            __syncthreads();
+        }
+        const double2* Ro = P.R + P.bp_R_off[obp];
+        const double2* S = P.S + (size_t)b * k * k;
+        const double w = P.omega[b];
+        for (int idx = threadIdx.x; idx < r * k; idx += blockDim.x) {
+            int i = idx % r, nu = idx / r;
+            double2 acc = cmk(0.0, 0.0);
+            if (row) {
+                for (int mu = 0; mu < k; ++mu) cfma_bj(acc, Ro[i + (size_t)mu * r], S[nu + (size_t)mu * k]);
+            } else {
+                for (int mu = 0; mu < k; ++mu) cfma(acc, Ro[i + (size_t)mu * r], S[mu + (size_t)nu * k]);
+            }
+            A[cur + i + (size_t)nu * lda] = cscale(acc, w);
+        }
+        cur += r;
+        __syncthreads();
+    }
+    for (int ip = X.par_ptr[p]; ip < X.par_ptr[p + 1]; ++ip) {
+        const int pp = X.par[ip];
+        const int ci = X.par_child[ip];
+        const int r = X.Z_rows[pp];
+        if (cur + r > bufrows) {
+            cta_qr(A, lda, cur, k, sh);
+            cur = min(cur, k);
+            zero_lower(A, lda, cur, k);
+            compressed = true;
+            __syncthreads();
+        }
+        const double2* Zp = X.Z + X.Z_off[pp];
+        const double2* Eg = P.E + P.bp_E_off[X.bp[pp]] + ci * 3 * m * m;
+        for (int idx = threadIdx.x; idx < 3 * m * m; idx += blockDim.x) Ef[idx] = Eg[idx];
+        for (int idx = threadIdx.x; idx < r * k; idx += blockDim.x)
+            A[cur + idx % r + (size_t)(idx / r) * lda] = Zp[idx];
+        __syncthreads();
+        kron_apply(A + cur, lda, r, m, Ef, true);  // Zhat_{t+c+} E_{tc+}^*
+        cur += r;
+    }
+    if (cur > k) {
+        cta_qr(A, lda, cur, k, sh);
+        cur = k;
+        zero_lower(A, lda, k, k);
+        __syncthreads();
+    }
+    (void)compressed;
+    const int zr = X.Z_rows[p];
+    double2* Z = X.Z + X.Z_off[p];
+    for (int idx = threadIdx.x; idx < zr * k; idx += blockDim.x) {
+        int i = idx % zr;
+        Z[idx] = (i < cur) ? A[i + (size_t)(idx / zr) * lda] : cmk(0.0, 0.0);
+    }
+}
+
+void launch_total_weights(const PlanD& P, bool row, int p0, int np, int bufrows, cudaStream_t s) {
+    if (!np) return;
+    int lda = odd_ld(bufrows);
+    size_t sm = ((size_t)lda * P.k + 3 * P.m * P.m + 2) * sizeof(double2);
+    k_total_weights<<<np, 256, sm, s>>>(P, row ? P.row : P.col, row, p0, lda, bufrows);
+}
+
+// Truncation, one CTA per pair of one level (bottom-up):
+//   leaf:     M = V_tc Zhat_tc^*;  non-leaf: Vhat = [C_{t1c1} E_{t1c}; C_{t2c2} E_{t2c}], M = Vhat Zhat^*
+//   left singular vectors/values of M (one-sided Jacobi; a wide M is first reduced by the
+//   QR of M^*: M = R^* Q^*), rank k_tc by the rule of `mode`, Q = first k_tc vectors
+//   (leaf: Q_tc, non-leaf: Qhat = [F_{t1c}; F_{t2c}]), C_tc = Q^* V_tc or Qhat^* Vhat (Eq. 19).
+__global__ void k_truncate(PlanD P, PassD X, int p0, int ldv, int ldb, int ldw, double eps, int mode) {
+    extern __shared__ double2 sm[];
+    __shared__ int flag;
+    __shared__ int s_rank;
+    __shared__ double2 sh[2];
+    const int p = p0 + blockIdx.x;
+    const int k = P.k, m = P.m;
+    const int bp = X.bp[p];
+    const bool leaf = X.child0[p] < 0;
+    const int zr = X.Z_rows[p];
+    const double2* Z = X.Z + X.Z_off[p];
+    double2* Vt = sm;                                 // rowsM x k, ld ldv
+    double2* B = Vt + (size_t)ldv * k;                // M (rowsM x zr) or M^* (zr x rowsM), ld ldb
+    double2* W = B + (size_t)ldb * max(ldv, 1);       // R^* (rowsM x rowsM), ld ldw
+    double2* Ef = W + (size_t)ldw * ldv;              // 6 m^2
+    double* sig = reinterpret_cast<double*>(Ef + 6 * m * m);  // ncol
+    int* ord = reinterpret_cast<int*>(sig + ldv + ldb);        // ncol
+    int rowsM;
+    int k1 = 0;
+    if (leaf) {
+        const int t = P.bp_t[bp];
+        rowsM = P.c_size[t];
+        const double2* V = P.V + P.bp_V_off[bp];
+        for (int idx = threadIdx.x; idx < rowsM * k; idx += blockDim.x) Vt[idx % rowsM + (size_t)(idx / rowsM) * ldv] = V[idx];
+        __syncthreads();
+    } else {
+        const int c0 = X.child0[p], c1 = X.child1[p];
+        k1 = X.rank[c0];
+        const int k2 = X.rank[c1];
+        const int l0 = X.kb[c0], l1 = X.kb[c1];
+        const double2* C0 = X.C + X.C_off[c0];
+        const double2* C1 = X.C + X.C_off[c1];
+        for (int idx = threadIdx.x; idx < k1 * k; idx += blockDim.x) Vt[idx % k1 + (size_t)(idx / k1) * ldv] = C0[idx % k1 + (size_t)(idx / k1) * l0];
+        for (int idx = threadIdx.x; idx < k2 * k; idx += blockDim.x) Vt[k1 + idx % k2 + (size_t)(idx / k2) * ldv] = C1[idx % k2 + (size_t)(idx / k2) * l1];
+        const double2* Eg = P.E + P.bp_E_off[bp];
+        for (int idx = threadIdx.x; idx < 6 * m * m; idx += blockDim.x) Ef[idx] = Eg[idx];
+        __syncthreads();
+        kron_apply(Vt, ldv, k1, m, Ef, false);
+        kron_apply(Vt + k1, ldv, k2, m, Ef + 3 * m * m, false);
+        rowsM = k1 + k2;
+    }
+    const int ldq = leaf ? rowsM : X.rowsb[p];
+    double2* Qg = X.Q + X.Q_off[p];
+    double2* Cg = X.C + X.C_off[p];
+    const int kb = X.kb[p];
+    if (rowsM == 0 || zr == 0) {
+        if (threadIdx.x == 0) {
+            X.rank[p] = 0;
+            X.nsig[p] = 0;
+            X.disc[p] = 0.0;
+        }
+        return;
+    }
+    int ncol;
+    double2* Wm;
+    int ldwm;
+    if (rowsM >= zr) {
+        // tall: W = M = Vt Zhat^*  (rowsM x zr)
+        for (int idx = threadIdx.x; idx < rowsM * zr; idx += blockDim.x) {
+            int i = idx % rowsM, j = idx / rowsM;
+            double2 acc = cmk(0.0, 0.0);
+            for (int nu = 0; nu < k; ++nu) cfma_bj(acc, Vt[i + (size_t)nu * ldv], Z[j + (size_t)nu * zr]);
+            B[i + (size_t)j * ldb] = acc;
+        }
+        ncol = zr;
+        Wm = B;
+        ldwm = ldb;
+        __syncthreads();
+    } else {
+        // wide: M^* = Zhat Vt^* (zr x rowsM) = Q R, then M = R^* Q^*: same left vectors as R^*
+        for (int idx = threadIdx.x; idx < zr * rowsM; idx += blockDim.x) {
+            int j = idx % zr, i = idx / zr;
+            double2 acc = cmk(0.0, 0.0);
+            for (int nu = 0; nu < k; ++nu) cfma_bj(acc, Z[j + (size_t)nu * zr], Vt[i + (size_t)nu * ldv]);
+            B[j + (size_t)i * ldb] = acc;
+        }
+        cta_qr(B, ldb, zr, rowsM, sh);
+        for (int idx = threadIdx.x; idx < rowsM * rowsM; idx += blockDim.x) {
+            int i = idx % rowsM, j = idx / rowsM;
+            W[i + (size_t)j * ldw] = (j <= i) ? cconj(B[j + (size_t)i * ldb]) : cmk(0.0, 0.0);
+        }
+        ncol = rowsM;
+        Wm = W;
+        ldwm = ldw;
+        __syncthreads();
+    }
+    cta_jacobi(Wm, ldwm, rowsM, ncol, &flag);
+    // singular values = column norms; order by decreasing value (ties: lower index first)
+    for (int j = threadIdx.x; j < ncol; j += blockDim.x) {
+        double s = 0.0;
+        for (int i = 0; i < rowsM; ++i) s += cabs2(Wm[i + (size_t)j * ldwm]);
+        sig[j] = sqrt(s);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < ncol; j += blockDim.x) {
+        int pos = 0;
+        double sj = sig[j];
+        for (int i = 0; i < ncol; ++i) {
+            double si = sig[i];
+            pos += (si > sj) || (si == sj && i < j);
+        }
+        ord[pos] = j;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // rank rule (DESIGN reading Q12), tail sums from the smallest value
+        double* so = X.sigma + X.sig_off[p];
+        for (int a = 0; a < ncol; ++a) so[a] = sig[ord[a]];
+        double tail[260];
+        double acc = 0.0;
+        tail[ncol] = 0.0;
+        for (int a = ncol - 1; a >= 0; --a) {
+            double s = so[a];
+            acc += s * s;
+            tail[a] = acc;
+        }
+        int kk = ncol;
+        if (mode == 2) {
+            for (int a = 0; a <= ncol; ++a) {
+                double nxt = a < ncol ? so[a] : 0.0;
+                if (nxt <= eps) { kk = a; break; }
+            }
+        } else {
+            double thr = (mode == 0) ? eps * eps : eps * eps * tail[0];
+            for (int a = 0; a <= ncol; ++a)
+                if (tail[a] <= thr) { kk = a; break; }
+        }
+        if (kk > kb) kk = kb;
+        s_rank = kk;
+        X.rank[p] = kk;
+        X.nsig[p] = ncol;
+        X.disc[p] = tail[kk];
+    }
+    __syncthreads();
+    const int kk = s_rank;
+    // Q columns = normalised sorted columns of W
+    for (int idx = threadIdx.x; idx < rowsM * kk; idx += blockDim.x) {
+        int i = idx % rowsM, a = idx / rowsM;
+        int j = ord[a];
+        double s = sig[j];
+        double2 v = Wm[i + (size_t)j * ldwm];
+        Qg[i + (size_t)a * ldq] = s > 0.0 ? cscale(v, 1.0 / s) : cmk(0.0, 0.0);
+    }
+    // C = Q^* Vt  (kk x k), ld kb
+    for (int idx = threadIdx.x; idx < kk * k; idx += blockDim.x) {
+        int a = idx % kk, nu = idx / kk;
+        int j = ord[a];
+        double s = sig[j];
+        double2 acc = cmk(0.0, 0.0);
+        for (int i = 0; i < rowsM; ++i) cfma_cj(acc, Wm[i + (size_t)j * ldwm], Vt[i + (size_t)nu * ldv]);
+        Cg[a + (size_t)nu * kb] = s > 0.0 ? cscale(acc, 1.0 / s) : cmk(0.0, 0.0);
+    }
+    (void)k1;
+}
+
+void launch_truncate(const PlanD& P, bool row, int p0, int np, int maxrowsM, int maxZrows, double eps, int mode,
+                     cudaStream_t s) {
+    if (!np) return;
+    int ldv = odd_ld(max(maxrowsM, 1));
+    int ldb = odd_ld(max(maxrowsM, maxZrows));
+    int ldw = ldv;
+    size_t sm = ((size_t)ldv * P.k + (size_t)ldb * ldv + (size_t)ldw * ldv + 6 * P.m * P.m) * sizeof(double2) +
+                (size_t)(ldv + ldb) * sizeof(double) + (size_t)(ldv + ldb) * sizeof(int) + 64;
+    k_truncate<<<np, 256, sm, s>>>(P, row ? P.row : P.col, p0, ldv, ldb, ldw, eps, mode);
+}
+
+// Projection (Lemma Projections): T_b = C_tc S_b, S~_b = T_b C'_sc^*.  CTA per block.
+__global__ void k_project(PlanD P, int ldt) {
+    extern __shared__ double2 sm[];
+    const int b = blockIdx.x, k = P.k;
+    const int pr = P.blk_prow[b], pc = P.blk_pcol[b];
+    const int kt = P.row.rank[pr], ks = P.col.rank[pc];
+    const int lt = P.row.kb[pr], ls = P.col.kb[pc];
+    const double2* Ct = P.row.C + P.row.C_off[pr];
+    const double2* Cs = P.col.C + P.col.C_off[pc];
+    const double2* S = P.S + (size_t)b * k * k;
+    double2* T = sm;
+    for (int idx = threadIdx.x; idx < kt * k; idx += blockDim.x) {
+        int a = idx % kt, mu = idx / kt;
+        double2 acc = cmk(0.0, 0.0);
+        for (int nu = 0; nu < k; ++nu) cfma(acc, Ct[a + (size_t)nu * lt], S[nu + (size_t)mu * k]);
+        T[a + (size_t)mu * ldt] = acc;
+    }
+    __syncthreads();
+    double2* St = P.St + P.blk_St_off[b];
+    for (int idx = threadIdx.x; idx < kt * ks; idx += blockDim.x) {
+        int a = idx % kt, c = idx / kt;
+        double2 acc = cmk(0.0, 0.0);
+        for (int mu = 0; mu < k; ++mu) cfma_bj(acc, T[a + (size_t)mu * ldt], Cs[c + (size_t)mu * ls]);
+        St[a + (size_t)c * lt] = acc;
+    }
+}
+
+void launch_project(const PlanD& P, int maxkrow, cudaStream_t s) {
+    if (!P.nblk) return;
+    int ldt = odd_ld(max(maxkrow, 1));
+    size_t sm = (size_t)ldt * P.k * sizeof(double2);
+    k_project<<<P.nblk, 128, sm, s>>>(P, ldt);
+}
+
+// ============================================================== matvec (far field)
+// Forward transformation on the column basis: xh_sc = B_sc^* x|_s, nested through the
+// transfers (V, E for ORIG; Q', F' for RECOMP).  Coefficients stored with stride k.
+__global__ void k_mv_forward(PlanD P, bool recomp, int p0, const double2* xp, double2* xh) {
+    const PassD& X = P.col;
+    const int p = p0 + blockIdx.x, k = P.k, m = P.m;
+    const int bp = X.bp[p];
+    const bool leaf = X.child0[p] < 0;
+    const int kout = recomp ? X.rank[p] : k;
+    for (int a = threadIdx.x; a < kout; a += blockDim.x) {
+        double2 acc = cmk(0.0, 0.0);
+        if (leaf) {
+            const int t = P.bp_t[bp];
+            const int nt = P.c_size[t];
+            const double2* x = xp + P.c_begin[t];
+            const double2* B = recomp ? (X.Q + X.Q_off[p]) : (P.V + P.bp_V_off[bp]);
+            for (int i = 0; i < nt; ++i) cfma_cj(acc, B[i + (size_t)a * nt], x[i]);
+        } else {
+            const int ch[2] = {X.child0[p], X.child1[p]};
+            if (recomp) {
+                const double2* F = X.Q + X.Q_off[p];
+                const int ldf = X.rowsb[p];
+                int off = 0;
+                for (int c = 0; c < 2; ++c) {
+                    const int kc = X.rank[ch[c]];
+                    for (int r = 0; r < kc; ++r) cfma_cj(acc, F[off + r + (size_t)a * ldf], xh[(size_t)ch[c] * k + r]);
+                    off += kc;
+                }
+            } else {
+                const double2* Eg = P.E + P.bp_E_off[bp];
+                int jx = a % m, jy = (a / m) % m, jz = a / (m * m);
+                for (int c = 0; c < 2; ++c) {
+                    const double2* F = Eg + c * 3 * m * m;
+                    for (int nup = 0; nup < k; ++nup) {
+                        int px = nup % m, py = (nup / m) % m, pz = nup / (m * m);
+                        double2 e = cmul(cmul(F[px * m + jx], F[m * m + py * m + jy]), F[2 * m * m + pz * m + jz]);
+                        cfma_cj(acc, e, xh[(size_t)ch[c] * k + nup]);
+                    }
+                }
+            }
+        }
+        xh[(size_t)p * k + a] = acc;
+    }
+}
+
+// Coupling: yh_tc = sum_{b=(t,s,c)} S_b xh_sc (ORIG) or S~_b xh'_sc (RECOMP).
+__global__ void k_mv_couple(PlanD P, bool recomp, const double2* xh, double2* yh) {
+    const PassD& X = P.row;
+    const int p = blockIdx.x, k = P.k;
+    const int kout = recomp ? X.rank[p] : k;
+    for (int a = threadIdx.x; a < kout; a += blockDim.x) {
+        double2 acc = cmk(0.0, 0.0);
+        for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) {
+            const int b = X.blk[ib];
+            const int pc = P.blk_pcol[b];
+            const double2* x = xh + (size_t)pc * k;
+            if (recomp) {
+                const double2* St = P.St + P.blk_St_off[b];
+                const int ks = P.col.rank[pc];
+                const int lt = X.kb[p];
+                for (int c = 0; c < ks; ++c) cfma(acc, St[a + (size_t)c * lt], x[c]);
+            } else {
+                const double2* S = P.S + (size_t)b * k * k;
+                for (int c = 0; c < k; ++c) cfma(acc, S[a + (size_t)c * k], x[c]);
+            }
+        }
+        yh[(size_t)p * k + a] = acc;
+    }
+}
+
+// Backward transformation (top-down): yh_{t'c'} += T yh_{tc} for every parent (t,c) with
+// sd(c) = c'; T = E_{t'c} (ORIG) or F_{t'c} (RECOMP).
+__global__ void k_mv_backward(PlanD P, bool recomp, int p0, double2* yh) {
+    const PassD& X = P.row;
+    const int p = p0 + blockIdx.x, k = P.k, m = P.m;
+    const int kout = recomp ? X.rank[p] : k;
+    for (int a = threadIdx.x; a < kout; a += blockDim.x) {
+        double2 acc = yh[(size_t)p * k + a];
+        for (int ip = X.par_ptr[p]; ip < X.par_ptr[p + 1]; ++ip) {
+            const int pp = X.par[ip];
+            const int ci = X.par_child[ip];
+            const double2* v = yh + (size_t)pp * k;
+            if (recomp) {
+                const double2* F = X.Q + X.Q_off[pp];
+                const int ldf = X.rowsb[pp];
+                const int off = ci == 0 ? 0 : X.rank[X.child0[pp]];
+                const int kp = X.rank[pp];
+                for (int c = 0; c < kp; ++c) cfma(acc, F[off + a + (size_t)c * ldf], v[c]);
+            } else {
+                const double2* F = P.E + P.bp_E_off[X.bp[pp]] + ci * 3 * m * m;
+                int px = a % m, py = (a / m) % m, pz = a / (m * m);
+                for (int nu = 0; nu < k; ++nu) {
+                    int jx = nu % m, jy = (nu / m) % m, jz = nu / (m * m);
+                    double2 e = cmul(cmul(F[px * m + jx], F[m * m + py * m + jy]), F[2 * m * m + pz * m + jz]);
+                    cfma(acc, e, v[nu]);
+                }
+            }
+        }
+        yh[(size_t)p * k + a] = acc;
+    }
+}
+
+// Leaf output: y|_t = sum_{c} B_tc yh_tc over the row pairs of each leaf cluster.
+__global__ void k_mv_leaf_out(PlanD P, bool recomp, const int* lc, const int* lc_ptr, const double2* yh, double2* yp) {
+    const PassD& X = P.row;
+    const int g = blockIdx.x, k = P.k;
+    const int p_first = lc[lc_ptr[g]];
+    const int t = P.bp_t[X.bp[p_first]];
+    const int nt = P.c_size[t];
+    for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+        double2 acc = cmk(0.0, 0.0);
+        for (int q = lc_ptr[g]; q < lc_ptr[g + 1]; ++q) {
+            const int p = lc[q];
+            const double2* v = yh + (size_t)p * k;
+            if (recomp) {
+                const double2* Q = X.Q + X.Q_off[p];
+                const int kp = X.rank[p];
+                for (int a = 0; a < kp; ++a) cfma(acc, Q[i + (size_t)a * nt], v[a]);
+            } else {
+                const double2* V = P.V + P.bp_V_off[X.bp[p]];
+                for (int a = 0; a < k; ++a) cfma(acc, V[i + (size_t)a * nt], v[a]);
+            }
+        }
+        yp[P.c_begin[t] + i] = acc;
+    }
+}
+
+__global__ void k_permute(const int64_t* perm, const double2* in, double2* out, int n, bool gather) {
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    if (gather)
+        out[p] = in[perm[p]];
+    else
+        out[perm[p]] = in[p];
+}
+
+void launch_mv_forward(const PlanD& P, bool recomp, int p0, int np, const double2* xp, double2* xh, cudaStream_t s) {
+    if (np) k_mv_forward<<<np, 64, 0, s>>>(P, recomp, p0, xp, xh);
+}
+void launch_mv_couple(const PlanD& P, bool recomp, const double2* xh, double2* yh, cudaStream_t s) {
+    if (P.row.npairs) k_mv_couple<<<P.row.npairs, 64, 0, s>>>(P, recomp, xh, yh);
+}
+void launch_mv_backward(const PlanD& P, bool recomp, int p0, int np, double2* yh, cudaStream_t s) {
+    if (np) k_mv_backward<<<np, 64, 0, s>>>(P, recomp, p0, yh);
+}
+void launch_mv_leaf_out(const PlanD& P, bool recomp, const int* lc, const int* lc_ptr, int nlc, const double2* yh,
+                        double2* yp, cudaStream_t s) {
+    if (nlc) k_mv_leaf_out<<<nlc, 64, 0, s>>>(P, recomp, lc, lc_ptr, yh, yp);
+}
+void launch_permute(const int64_t* perm, const double2* in, double2* out, int n, bool gather, cudaStream_t s) {
+    k_permute<<<(n + 255) / 256, 256, 0, s>>>(perm, in, out, n, gather);
+}
+
+}  // namespace dh2
+
+namespace dh2 {
+// Opt the shared-memory-heavy kernels into the full 227 KB dynamic shared memory of sm_100a.
+void configure_kernels() {
+    static bool done = false;
+    if (done) return;
+    done = true;
+    const int maxsm = 227 * 1024;
+    cudaFuncSetAttribute(k_leafV, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+    cudaFuncSetAttribute(k_basis, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+    cudaFuncSetAttribute(k_block_weights, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+    cudaFuncSetAttribute(k_total_weights, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+    cudaFuncSetAttribute(k_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+    cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+}
+}  // namespace dh2

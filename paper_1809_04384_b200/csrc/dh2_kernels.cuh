@@ -1,0 +1,104 @@
+// Kernel declarations and the device-side plan shared by dh2_kernels.cu and dh2_api.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dh2_device.cuh"
+
+namespace dh2 {
+
+// Per-pass (row basis or column basis) device tables; "pair" = active (t,c) of that pass.
+struct PassD {
+    int npairs;
+    const int* bp;        // pair -> basis pair id
+    const int* child0;    // pair -> pass-local child pair (t1, sd c), -1 at leaves
+    const int* child1;
+    const int64_t* Z_off; // Zhat slab offset (double2 units), Zhat is Zrows x k, ld = Zrows
+    const int* Z_rows;    // r_Z = min(#rows of Z^*, k)
+    const int* blk_ptr;   // CSR: contributing admissible blocks of the pair
+    const int* blk;
+    const int* par_ptr;   // CSR: parent pairs (t+, c+) with sd(c+) = c
+    const int* par;       // parent pass-local pair id
+    const int* par_child; // which child of t+ the pair's cluster is (selects E factor)
+    const int* rowsb;     // bound on #rows of the truncated matrix (leaf #t, else kb1 + kb2)
+    const int* kb;        // bound on the new rank, min(rowsb, r_Z)
+    const int64_t* C_off; // C slab, kb x k, ld kb
+    const int64_t* Q_off; // leaf: Q (#t x kb, ld #t); non-leaf: Qhat = [F1; F2] (rowsb x kb, ld rowsb)
+    const int64_t* sig_off;  // singular values, min(rowsb, r_Z) doubles
+    double2* Z;
+    double2* C;
+    double2* Q;
+    double* sigma;
+    int* rank;
+    int* nsig;            // number of singular values computed
+    double* disc;         // discarded sum of squares per pair
+};
+
+struct PlanD {
+    int n, m, k, nclusters;
+    double kappa;
+    // geometry
+    const double* xyz;
+    const int64_t* tri;
+    const int64_t* perm;
+    double4* qp;  // n*7 quadrature points (x, y, z, |tau| w) in cluster order
+    const double* c_lo;
+    const double* c_hi;
+    const int64_t* c_begin;
+    const int* c_size;
+    GridD* grid;
+    const double* dirs;  // all directions, 3 doubles each (global index)
+    // basis pairs
+    int nbp;
+    const int* bp_t;
+    const int* bp_dir;      // global direction index of c
+    const int* bp_sddir;    // global direction index of sd(c) (children's direction), -1 at leaves
+    const int* bp_child0;
+    const int* bp_child1;
+    const int64_t* bp_V_off;  // leaf V slab (#t x k, ld #t), -1 for non-leaf
+    const int64_t* bp_R_off;  // basis weight slab (Rrows x k, ld Rrows)
+    const int* bp_R_rows;
+    const int64_t* bp_E_off;  // 2 * 3 m^2 complex transfer factors, -1 at leaves
+    double2* V;
+    double2* R;
+    double2* E;
+    // blocks
+    int nblk;
+    const int* blk_t;
+    const int* blk_s;
+    const int* blk_dir;
+    const int* blk_bprow;
+    const int* blk_bpcol;
+    const int* blk_prow;  // row-pass pair id of (t,c)
+    const int* blk_pcol;  // col-pass pair id of (s,c)
+    const int64_t* blk_St_off;  // kb_row x kb_col slab, ld kb_row
+    double2* S;           // nblk * k * k
+    double2* St;
+    double* omega;
+    double* normG2;
+    PassD row, col;
+};
+
+// setup (Eq. 10)
+void launch_quad(const PlanD& P, cudaStream_t s);
+void launch_grid(const PlanD& P, cudaStream_t s);
+void launch_leafV(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStream_t s);
+void launch_E(const PlanD& P, const int* bps, int nbps, cudaStream_t s);
+void launch_S(const PlanD& P, cudaStream_t s);
+// recompression (§3.2)
+void launch_basis(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStream_t s);
+void launch_block_weights(const PlanD& P, int mode, cudaStream_t s);
+void launch_total_weights(const PlanD& P, bool row, int p0, int np, int bufrows, cudaStream_t s);
+void launch_truncate(const PlanD& P, bool row, int p0, int np, int maxrowsM, int maxZrows, double eps, int mode,
+                     cudaStream_t s);
+void launch_project(const PlanD& P, int maxkrow, cudaStream_t s);
+// matvec (forward / coupling / backward)
+void launch_mv_forward(const PlanD& P, bool recomp, int p0, int np, const double2* xp, double2* xh,
+                       cudaStream_t s);
+void launch_mv_couple(const PlanD& P, bool recomp, const double2* xh, double2* yh, cudaStream_t s);
+void launch_mv_backward(const PlanD& P, bool recomp, int p0, int np, double2* yh, cudaStream_t s);
+void launch_mv_leaf_out(const PlanD& P, bool recomp, const int* lc, const int* lc_ptr, int nlc, const double2* yh,
+                        double2* yp, cudaStream_t s);
+void launch_permute(const int64_t* perm, const double2* in, double2* out, int n, bool gather, cudaStream_t s);
+
+}  // namespace dh2
