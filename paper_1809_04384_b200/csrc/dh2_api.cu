@@ -20,7 +20,7 @@
 #include "dh2_kernels.cuh"
 
 namespace dh2 {
-void configure_kernels();
+cudaError_t configure_kernels();
 }
 
 using namespace dh2;
@@ -175,7 +175,8 @@ struct dh2_ctx {
         } else {
             f();
         }
-        CK(cudaGetLastError());
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) throw CudaError("launch of kernel class '" + cls + "': " + cudaGetErrorString(e));
         kstat[cls].launches += nl;
         launches_total += nl;
     }
@@ -880,7 +881,7 @@ int dh2_build_interp(const dh2_mesh* mesh, const dh2_params* params, const dh2_d
         if (structure_only) return;
         CK(cudaStreamCreateWithFlags(&C->own_stream, cudaStreamNonBlocking));
         C->stream = C->own_stream;
-        configure_kernels();
+        CK(configure_kernels());
         upload_all(C.get(), mesh->xyz, mesh->nv, mesh->tri);
         run_setup(C.get());
         C->finish();

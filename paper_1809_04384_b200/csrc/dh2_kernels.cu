@@ -748,17 +748,24 @@ void launch_permute(const int64_t* perm, const double2* in, double2* out, int n,
 }  // namespace dh2
 
 namespace dh2 {
-// Opt the shared-memory-heavy kernels into the full 227 KB dynamic shared memory of sm_100a.
-void configure_kernels() {
-    static bool done = false;
-    if (done) return;
-    done = true;
-    const int maxsm = 227 * 1024;
-    cudaFuncSetAttribute(k_leafV, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_basis, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_block_weights, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_total_weights, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+// Opt the shared-memory-heavy kernels into the full dynamic shared memory of sm_100a
+// (227 KB per CTA minus the kernel's static shared memory).  Returns the first error.
+cudaError_t configure_kernels() {
+    static cudaError_t done = cudaErrorNotReady;
+    if (done != cudaErrorNotReady) return done;
+    int dev = 0, optin = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const void* ks[] = {(const void*)k_leafV, (const void*)k_basis, (const void*)k_block_weights,
+                        (const void*)k_total_weights, (const void*)k_truncate, (const void*)k_project};
+    for (const void* f : ks) {
+        if (e != cudaSuccess) break;
+        cudaFuncAttributes a;
+        e = cudaFuncGetAttributes(&a, f);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)a.sharedSizeBytes);
+    }
+    done = e;
+    return e;
 }
 }  // namespace dh2
