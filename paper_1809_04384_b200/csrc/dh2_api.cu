@@ -80,7 +80,7 @@ struct PassH {
     std::vector<int> total_rows;
     // device
     DevBuf<int> d_bp, d_child0, d_child1, d_Z_rows, d_blk_ptr, d_blk, d_par_ptr, d_par, d_par_child, d_rowsb, d_kb,
-        d_rank, d_nsig, d_lc, d_lc_ptr;
+        d_rank, d_nsig, d_lc, d_lc_ptr, d_sweeps;
     DevBuf<int64_t> d_Z_off, d_C_off, d_Q_off, d_sig_off;
     DevBuf<double2> d_Z, d_C, d_Q;
     DevBuf<double> d_sigma, d_disc;
@@ -446,6 +446,7 @@ void upload_pass(dh2_ctx* C, PassH& X, PassD& D) {
     X.d_rank.alloc(np);
     X.d_nsig.alloc(np);
     X.d_disc.alloc(np);
+    X.d_sweeps.alloc(np);
     X.d_Z.alloc(X.Z_total);
     X.d_C.alloc(X.C_total);
     X.d_Q.alloc(X.Q_total);
@@ -473,6 +474,7 @@ void upload_pass(dh2_ctx* C, PassH& X, PassD& D) {
     D.rank = X.d_rank.p;
     D.nsig = X.d_nsig.p;
     D.disc = X.d_disc.p;
+    D.sweeps = X.d_sweeps.p;
 }
 
 size_t plan_bytes(const dh2_ctx* C) {
@@ -693,7 +695,9 @@ void run_recompress(dh2_ctx* C, double eps, int mode) {
             for (int p = p0; p < p0 + np; ++p)
                 if (X.child0[p] >= 0) maxrows = std::max(maxrows, X.rank[X.child0[p]] + X.rank[X.child1[p]]);
             int maxz = X.lev_max_zrows[l];
-            C->timed("truncate", 1, [&] { launch_truncate(P, row, p0, np, maxrows, maxz, eps, mode, s); });
+            bool all_leaf = true;
+            for (int p = p0; p < p0 + np; ++p) all_leaf = all_leaf && X.child0[p] < 0;
+            C->timed("truncate", 1, [&] { launch_truncate(P, row, p0, np, maxrows, maxz, all_leaf, eps, mode, s); });
             CK(cudaMemcpyAsync(X.rank.data() + p0, X.d_rank.p + p0, np * sizeof(int), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             double fl = 0;
@@ -1046,6 +1050,7 @@ int dh2_export(const dh2_ctx* C, const char* name, void* buf, int64_t* nbytes) {
             else if (base == "rank") it = dv(X->d_rank);
             else if (base == "nsig") it = dv(X->d_nsig);
             else if (base == "disc") it = dv(X->d_disc);
+            else if (base == "sweeps") it = dv(X->d_sweeps);
             else throw std::invalid_argument("unknown export name " + nm);
         } else if (nm == "perm") it = hv(T.perm);
         else if (nm == "c_begin") it = hv(T.begin);

@@ -221,4 +221,172 @@ __device__ inline int cta_jacobi(double2* W, int ld, int m, int n, int* flag) {
     return sweep;
 }
 
+// Householder QR with column pivoting (R factor + pivot order) of the M x N column-major
+// smem matrix B, in place.  Pivot = remaining column of largest norm (first on ties); norms
+// are recomputed exactly after every step (no downdating).  On return piv[j] = original
+// column placed at position j, R = upper trapezoid of B[0:min(M,N), :] in pivoted order.
+__device__ inline void cta_qrcp(double2* B, int ldb, int M, int N, int* piv, double* nrm, double2* sh, int* s_piv) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int K = min(M, N);
+    for (int c = tid; c < N; c += blockDim.x) piv[c] = c;
+    __syncthreads();
+    for (int c = warp; c < N; c += nw) {
+        double s = 0.0;
+        for (int i = lane; i < M; i += 32) s += cabs2(B[i + (size_t)c * ldb]);
+        s = warp_sum(s);
+        if (lane == 0) nrm[c] = s;
+    }
+    __syncthreads();
+    for (int j = 0; j < K; ++j) {
+        if (warp == 0) {
+            double best = -1.0;
+            int bi = j;
+            for (int c = j + lane; c < N; c += 32) {
+                double v = nrm[c];
+                if (v > best) { best = v; bi = c; }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+            }
+            if (lane == 0) *s_piv = bi;
+        }
+        __syncthreads();
+        const int pc = *s_piv;
+        if (pc != j) {
+            for (int i = tid; i < M; i += blockDim.x) {
+                double2 a = B[i + (size_t)j * ldb];
+                B[i + (size_t)j * ldb] = B[i + (size_t)pc * ldb];
+                B[i + (size_t)pc * ldb] = a;
+            }
+            if (tid == 0) {
+                int t = piv[j]; piv[j] = piv[pc]; piv[pc] = t;
+                double v = nrm[j]; nrm[j] = nrm[pc]; nrm[pc] = v;
+            }
+        }
+        __syncthreads();
+        double2* colj = B + (size_t)j * ldb;
+        if (warp == 0) {
+            double s = 0.0;
+            for (int i = j + 1 + lane; i < M; i += 32) s += cabs2(colj[i]);
+            s = warp_sum(s);
+            if (lane == 0) {
+                double2 alpha = colj[j];
+                double tau = 0.0;
+                double2 beta = alpha;
+                if (s > 0.0) {
+                    double aa = sqrt(cabs2(alpha));
+                    double xn = sqrt(s + aa * aa);
+                    double2 ph = aa > 0.0 ? cscale(alpha, 1.0 / aa) : cmk(1.0, 0.0);
+                    beta = cscale(ph, -xn);
+                    colj[j] = cscale(ph, aa + xn);
+                    tau = 1.0 / (xn * (xn + aa));
+                }
+                sh[0] = beta;
+                sh[1] = cmk(tau, 0.0);
+            }
+        }
+        __syncthreads();
+        const double tau = sh[1].x;
+        for (int c = j + 1 + warp; c < N; c += nw) {
+            double2* colc = B + (size_t)c * ldb;
+            if (tau != 0.0) {
+                double2 w = cmk(0.0, 0.0);
+                for (int i = j + lane; i < M; i += 32) cfma_cj(w, colj[i], colc[i]);
+                w = cscale(warp_sum2(w), tau);
+                for (int i = j + lane; i < M; i += 32) colc[i] = csub(colc[i], cmul(colj[i], w));
+            }
+            double s = 0.0;
+            for (int i = j + 1 + lane; i < M; i += 32) s += cabs2(colc[i]);
+            s = warp_sum(s);
+            if (lane == 0) nrm[c] = s;
+        }
+        __syncthreads();
+        if (tid == 0) colj[j] = sh[0];
+    }
+    __syncthreads();
+}
+
+// One-sided Jacobi on the vectors x_p = conj(R[p, 0:len]) (rows of the smem matrix R,
+// column-major, leading dimension ldr), p < nv: on return the x_p are mutually orthogonal,
+// i.e. the columns of R^* are U diag(s).  Round-robin ordering, one warp per pair, squared
+// norms carried in nrm[] and updated by the exact rotation identities
+// a' = a - t|g|, b' = b + t|g| (recomputed at every sweep).  Returns the sweeps done.
+__device__ inline int cta_jacobi_rows(double2* R, int ldr, int nv, int len, double* nrm, int* flag) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    if (nv <= 1) {
+        if (nv == 1 && warp == 0) {
+            double s = 0.0;
+            for (int i = lane; i < len; i += 32) s += cabs2(R[(size_t)i * ldr]);
+            s = warp_sum(s);
+            if (lane == 0) nrm[0] = s;
+        }
+        __syncthreads();
+        return 0;
+    }
+    const int np = nv + (nv & 1);
+    const int nr = np - 1;
+    const double tol = fmax((double)len, 1.0) * 2.220446049250313e-16;
+    const double tol2 = tol * tol;
+    int sweep = 0;
+    for (; sweep < 60; ++sweep) {
+        for (int p = warp; p < nv; p += nw) {
+            double s = 0.0;
+            for (int i = lane; i < len; i += 32) s += cabs2(R[p + (size_t)i * ldr]);
+            s = warp_sum(s);
+            if (lane == 0) nrm[p] = s;
+        }
+        if (tid == 0) *flag = 0;
+        __syncthreads();
+        for (int r = 0; r < nr; ++r) {
+            for (int pi = warp; pi < np / 2; pi += nw) {
+                const int i1 = np - 1 - pi;
+                int p = 0, q;
+                if (pi != 0) { p = pi - 1 + r; if (p >= nr) p -= nr; ++p; }
+                q = i1 - 1 + r; if (q >= nr) q -= nr; ++q;
+                if (p >= nv || q >= nv) continue;
+                const double al = nrm[p], be = nrm[q];
+                double2 ga = cmk(0.0, 0.0);  // <x_p, x_q> = sum_i R[p,i] conj(R[q,i])
+                for (int i = lane; i < len; i += 32) cfma_bj(ga, R[p + (size_t)i * ldr], R[q + (size_t)i * ldr]);
+                ga = warp_sum2(ga);
+                const double g2 = cabs2(ga);
+                // rotate iff |g| > tol sqrt(al be)  (squared test, no square roots)
+                if (g2 > tol2 * (al * be) && al > 0.0 && be > 0.0) {
+                    const double ig = rsqrt(g2);  // 1/|g|
+                    const double g = g2 * ig;
+                    const double zeta = 0.5 * (be - al) * ig;
+                    const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+                    const double c = rsqrt(fma(t, t, 1.0));
+                    const double sn = c * t;
+                    // x_q <- e x_q with e = e^{-i phi}; on the rows of R (conjugated) the factor is ga/|g|
+                    const double2 ec = cmk(ga.x * ig, ga.y * ig);
+                    for (int i = lane; i < len; i += 32) {
+                        const double2 a = R[p + (size_t)i * ldr];
+                        const double2 b = cmul(ec, R[q + (size_t)i * ldr]);
+                        R[p + (size_t)i * ldr] = csub(cscale(a, c), cscale(b, sn));
+                        R[q + (size_t)i * ldr] = cadd(cscale(a, sn), cscale(b, c));
+                    }
+                    if (lane == 0) {
+                        nrm[p] = al - t * g;
+                        nrm[q] = be + t * g;
+                        *flag = 1;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if (*flag == 0) break;
+        __syncthreads();
+    }
+    for (int p = warp; p < nv; p += nw) {
+        double s = 0.0;
+        for (int i = lane; i < len; i += 32) s += cabs2(R[p + (size_t)i * ldr]);
+        s = warp_sum(s);
+        if (lane == 0) nrm[p] = s;
+    }
+    __syncthreads();
+    return sweep;
+}
+
 }  // namespace dh2

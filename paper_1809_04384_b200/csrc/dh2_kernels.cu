@@ -389,13 +389,14 @@ void launch_total_weights(const PlanD& P, bool row, int p0, int np, int bufrows,
 
 // Truncation, one CTA per pair of one level (bottom-up):
 //   leaf:     M = V_tc Zhat_tc^*;  non-leaf: Vhat = [C_{t1c1} E_{t1c}; C_{t2c2} E_{t2c}], M = Vhat Zhat^*
-//   left singular vectors/values of M (one-sided Jacobi; a wide M is first reduced by the
-//   QR of M^*: M = R^* Q^*), rank k_tc by the rule of `mode`, Q = first k_tc vectors
-//   (leaf: Q_tc, non-leaf: Qhat = [F_{t1c}; F_{t2c}]), C_tc = Q^* V_tc or Qhat^* Vhat (Eq. 19).
-__global__ void k_truncate(PlanD P, PassD X, int p0, int ldv, int ldb, int ldw, double eps, int mode) {
+//   left singular vectors/values of M: QR with column pivoting of M^* = Zhat Vt^* (M^* Pi = Q R,
+//   so M = Pi R^* Q^*), then one-sided Jacobi on the graded columns of R^* (QR-preconditioned
+//   Jacobi: high relative accuracy, few sweeps; no Gram matrix is formed, DESIGN reading Q13);
+//   rank k_tc by the rule of `mode`, Q = first k_tc vectors (leaf: Q_tc, non-leaf:
+//   Qhat = [F_{t1c}; F_{t2c}]), C_tc = Q^* V_tc or Qhat^* Vhat (Eq. 19).
+__global__ void __launch_bounds__(128) k_truncate(PlanD P, PassD X, int p0, int ldv, int ldb, double eps, int mode) {
     extern __shared__ double2 sm[];
-    __shared__ int flag;
-    __shared__ int s_rank;
+    __shared__ int flag, s_piv, s_rank;
     __shared__ double2 sh[2];
     const int p = p0 + blockIdx.x;
     const int k = P.k, m = P.m;
@@ -403,35 +404,35 @@ __global__ void k_truncate(PlanD P, PassD X, int p0, int ldv, int ldb, int ldw, 
     const bool leaf = X.child0[p] < 0;
     const int zr = X.Z_rows[p];
     const double2* Z = X.Z + X.Z_off[p];
-    double2* Vt = sm;                                 // rowsM x k, ld ldv
-    double2* B = Vt + (size_t)ldv * k;                // M (rowsM x zr) or M^* (zr x rowsM), ld ldb
-    double2* W = B + (size_t)ldb * max(ldv, 1);       // R^* (rowsM x rowsM), ld ldw
-    double2* Ef = W + (size_t)ldw * ldv;              // 6 m^2
-    double* sig = reinterpret_cast<double*>(Ef + 6 * m * m);  // ncol
-    int* ord = reinterpret_cast<int*>(sig + ldv + ldb);        // ncol
+    double2* Vs = sm;                                  // non-leaf Vhat (rowsM x k, ld ldv)
+    double2* B = Vs + (leaf ? 0 : (size_t)ldv * k);    // M^* (zr x rowsM, ld ldb)
+    double2* Ef = B + (size_t)ldb * ldv;               // 6 m^2 (non-leaf)
+    double* nrm = reinterpret_cast<double*>(Ef + (leaf ? 0 : 6 * m * m));  // ldv
+    int* piv = reinterpret_cast<int*>(nrm + ldv);      // ldv
+    int* ord = piv + ldv;                              // ldv
     int rowsM;
-    int k1 = 0;
+    const double2* Vt;
+    int ldvt;
     if (leaf) {
-        const int t = P.bp_t[bp];
-        rowsM = P.c_size[t];
-        const double2* V = P.V + P.bp_V_off[bp];
-        for (int idx = threadIdx.x; idx < rowsM * k; idx += blockDim.x) Vt[idx % rowsM + (size_t)(idx / rowsM) * ldv] = V[idx];
-        __syncthreads();
+        rowsM = P.c_size[P.bp_t[bp]];
+        Vt = P.V + P.bp_V_off[bp];
+        ldvt = rowsM;
     } else {
         const int c0 = X.child0[p], c1 = X.child1[p];
-        k1 = X.rank[c0];
-        const int k2 = X.rank[c1];
+        const int k1 = X.rank[c0], k2 = X.rank[c1];
         const int l0 = X.kb[c0], l1 = X.kb[c1];
         const double2* C0 = X.C + X.C_off[c0];
         const double2* C1 = X.C + X.C_off[c1];
-        for (int idx = threadIdx.x; idx < k1 * k; idx += blockDim.x) Vt[idx % k1 + (size_t)(idx / k1) * ldv] = C0[idx % k1 + (size_t)(idx / k1) * l0];
-        for (int idx = threadIdx.x; idx < k2 * k; idx += blockDim.x) Vt[k1 + idx % k2 + (size_t)(idx / k2) * ldv] = C1[idx % k2 + (size_t)(idx / k2) * l1];
+        for (int idx = threadIdx.x; idx < k1 * k; idx += blockDim.x) Vs[idx % k1 + (size_t)(idx / k1) * ldv] = C0[idx % k1 + (size_t)(idx / k1) * l0];
+        for (int idx = threadIdx.x; idx < k2 * k; idx += blockDim.x) Vs[k1 + idx % k2 + (size_t)(idx / k2) * ldv] = C1[idx % k2 + (size_t)(idx / k2) * l1];
         const double2* Eg = P.E + P.bp_E_off[bp];
         for (int idx = threadIdx.x; idx < 6 * m * m; idx += blockDim.x) Ef[idx] = Eg[idx];
         __syncthreads();
-        kron_apply(Vt, ldv, k1, m, Ef, false);
-        kron_apply(Vt + k1, ldv, k2, m, Ef + 3 * m * m, false);
+        kron_apply(Vs, ldv, k1, m, Ef, false);
+        kron_apply(Vs + k1, ldv, k2, m, Ef + 3 * m * m, false);
         rowsM = k1 + k2;
+        Vt = Vs;
+        ldvt = ldv;
     }
     const int ldq = leaf ? rowsM : X.rowsb[p];
     double2* Qg = X.Q + X.Q_off[p];
@@ -445,52 +446,25 @@ __global__ void k_truncate(PlanD P, PassD X, int p0, int ldv, int ldb, int ldw, 
         }
         return;
     }
-    int ncol;
-    double2* Wm;
-    int ldwm;
-    if (rowsM >= zr) {
-        // tall: W = M = Vt Zhat^*  (rowsM x zr)
-        for (int idx = threadIdx.x; idx < rowsM * zr; idx += blockDim.x) {
-            int i = idx % rowsM, j = idx / rowsM;
-            double2 acc = cmk(0.0, 0.0);
-            for (int nu = 0; nu < k; ++nu) cfma_bj(acc, Vt[i + (size_t)nu * ldv], Z[j + (size_t)nu * zr]);
-            B[i + (size_t)j * ldb] = acc;
-        }
-        ncol = zr;
-        Wm = B;
-        ldwm = ldb;
-        __syncthreads();
-    } else {
-        // wide: M^* = Zhat Vt^* (zr x rowsM) = Q R, then M = R^* Q^*: same left vectors as R^*
-        for (int idx = threadIdx.x; idx < zr * rowsM; idx += blockDim.x) {
-            int j = idx % zr, i = idx / zr;
-            double2 acc = cmk(0.0, 0.0);
-            for (int nu = 0; nu < k; ++nu) cfma_bj(acc, Z[j + (size_t)nu * zr], Vt[i + (size_t)nu * ldv]);
-            B[j + (size_t)i * ldb] = acc;
-        }
-        cta_qr(B, ldb, zr, rowsM, sh);
-        for (int idx = threadIdx.x; idx < rowsM * rowsM; idx += blockDim.x) {
-            int i = idx % rowsM, j = idx / rowsM;
-            W[i + (size_t)j * ldw] = (j <= i) ? cconj(B[j + (size_t)i * ldb]) : cmk(0.0, 0.0);
-        }
-        ncol = rowsM;
-        Wm = W;
-        ldwm = ldw;
-        __syncthreads();
+    // B = M^* = Zhat Vt^*  (zr x rowsM)
+    for (int idx = threadIdx.x; idx < zr * rowsM; idx += blockDim.x) {
+        int j = idx % zr, i = idx / zr;
+        double2 acc = cmk(0.0, 0.0);
+        for (int nu = 0; nu < k; ++nu) cfma_bj(acc, Z[j + (size_t)nu * zr], Vt[i + (size_t)nu * ldvt]);
+        B[j + (size_t)i * ldb] = acc;
     }
-    cta_jacobi(Wm, ldwm, rowsM, ncol, &flag);
-    // singular values = column norms; order by decreasing value (ties: lower index first)
-    for (int j = threadIdx.x; j < ncol; j += blockDim.x) {
-        double s = 0.0;
-        for (int i = 0; i < rowsM; ++i) s += cabs2(Wm[i + (size_t)j * ldwm]);
-        sig[j] = sqrt(s);
-    }
+    cta_qrcp(B, ldb, zr, rowsM, piv, nrm, sh, &s_piv);
+    const int ncol = min(zr, rowsM);
+    zero_lower(B, ldb, ncol, rowsM);  // drop the Householder vectors below the diagonal of R
     __syncthreads();
+    const int nsw = cta_jacobi_rows(B, ldb, ncol, rowsM, nrm, &flag);
+    if (threadIdx.x == 0) X.sweeps[p] = nsw;
+    // singular values = norms of the rows of R; order by decreasing value (ties: lower index)
     for (int j = threadIdx.x; j < ncol; j += blockDim.x) {
         int pos = 0;
-        double sj = sig[j];
+        const double sj = nrm[j];
         for (int i = 0; i < ncol; ++i) {
-            double si = sig[i];
+            const double si = nrm[i];
             pos += (si > sj) || (si == sj && i < j);
         }
         ord[pos] = j;
@@ -499,63 +473,58 @@ __global__ void k_truncate(PlanD P, PassD X, int p0, int ldv, int ldb, int ldw, 
     if (threadIdx.x == 0) {
         // rank rule (DESIGN reading Q12), tail sums from the smallest value
         double* so = X.sigma + X.sig_off[p];
-        for (int a = 0; a < ncol; ++a) so[a] = sig[ord[a]];
-        double tail[260];
-        double acc = 0.0;
-        tail[ncol] = 0.0;
-        for (int a = ncol - 1; a >= 0; --a) {
-            double s = so[a];
-            acc += s * s;
-            tail[a] = acc;
-        }
+        for (int a = 0; a < ncol; ++a) so[a] = sqrt(nrm[ord[a]]);
+        double acc = 0.0, thr = 0.0, tot = 0.0;
+        for (int a = ncol - 1; a >= 0; --a) tot += so[a] * so[a];
+        thr = (mode == 0 || mode == 2) ? eps * eps : eps * eps * tot;
         int kk = ncol;
+        double disc = 0.0;
         if (mode == 2) {
-            for (int a = 0; a <= ncol; ++a) {
-                double nxt = a < ncol ? so[a] : 0.0;
-                if (nxt <= eps) { kk = a; break; }
-            }
+            kk = 0;
+            while (kk < ncol && so[kk] > eps) ++kk;
+            for (int a = ncol - 1; a >= kk; --a) disc += so[a] * so[a];
         } else {
-            double thr = (mode == 0) ? eps * eps : eps * eps * tail[0];
-            for (int a = 0; a <= ncol; ++a)
-                if (tail[a] <= thr) { kk = a; break; }
+            // smallest k with tail(k) <= thr: walk up from the smallest value
+            kk = ncol;
+            for (int a = ncol - 1; a >= 0; --a) {
+                acc += so[a] * so[a];
+                if (acc <= thr) { kk = a; disc = acc; } else break;
+            }
         }
         if (kk > kb) kk = kb;
         s_rank = kk;
         X.rank[p] = kk;
         X.nsig[p] = ncol;
-        X.disc[p] = tail[kk];
+        X.disc[p] = disc;
     }
     __syncthreads();
     const int kk = s_rank;
-    // Q columns = normalised sorted columns of W
+    // Q[piv[j], a] = conj(R[ord[a], j]) / s ; C[a, nu] = sum_j R[ord[a], j] / s * Vt[piv[j], nu]
     for (int idx = threadIdx.x; idx < rowsM * kk; idx += blockDim.x) {
-        int i = idx % rowsM, a = idx / rowsM;
-        int j = ord[a];
-        double s = sig[j];
-        double2 v = Wm[i + (size_t)j * ldwm];
-        Qg[i + (size_t)a * ldq] = s > 0.0 ? cscale(v, 1.0 / s) : cmk(0.0, 0.0);
+        const int j = idx % rowsM, a = idx / rowsM;
+        const int r = ord[a];
+        const double s = sqrt(nrm[r]);
+        const double2 v = B[r + (size_t)j * ldb];
+        Qg[piv[j] + (size_t)a * ldq] = s > 0.0 ? cmk(v.x / s, -v.y / s) : cmk(0.0, 0.0);
     }
-    // C = Q^* Vt  (kk x k), ld kb
     for (int idx = threadIdx.x; idx < kk * k; idx += blockDim.x) {
-        int a = idx % kk, nu = idx / kk;
-        int j = ord[a];
-        double s = sig[j];
+        const int a = idx % kk, nu = idx / kk;
+        const int r = ord[a];
+        const double s = sqrt(nrm[r]);
         double2 acc = cmk(0.0, 0.0);
-        for (int i = 0; i < rowsM; ++i) cfma_cj(acc, Wm[i + (size_t)j * ldwm], Vt[i + (size_t)nu * ldv]);
+        for (int j = 0; j < rowsM; ++j) cfma(acc, B[r + (size_t)j * ldb], Vt[piv[j] + (size_t)nu * ldvt]);
         Cg[a + (size_t)nu * kb] = s > 0.0 ? cscale(acc, 1.0 / s) : cmk(0.0, 0.0);
     }
-    (void)k1;
 }
 
-void launch_truncate(const PlanD& P, bool row, int p0, int np, int maxrowsM, int maxZrows, double eps, int mode,
-                     cudaStream_t s) {
+void launch_truncate(const PlanD& P, bool row, int p0, int np, int maxrowsM, int maxZrows, bool leaf_level, double eps,
+                     int mode, cudaStream_t s) {
     if (!np) return;
     int ldv = odd_ld(max(maxrowsM, 1));
-    int ldb = odd_ld(max(maxrowsM, maxZrows));
-    int ldw = ldv;
-    size_t sm = ((size_t)ldv * P.k + (size_t)ldb * ldv + (size_t)ldw * ldv + 6 * P.m * P.m) * sizeof(double2) +
-                (size_t)(ldv + ldb) * sizeof(double) + (size_t)(ldv + ldb) * sizeof(int) + 64;
-    k_truncate<<<np, 256, sm, s>>>(P, row ? P.row : P.col, p0, ldv, ldb, ldw, eps, mode);
+    int ldb = odd_ld(max(maxZrows, 1));
+    size_t sm = ((leaf_level ? 0 : (size_t)ldv * P.k + 6 * P.m * P.m) + (size_t)ldb * ldv) * sizeof(double2) +
+                (size_t)ldv * (sizeof(double) + 2 * sizeof(int)) + 16;
+    k_truncate<<<np, 128, sm, s>>>(P, row ? P.row : P.col, p0, ldv, ldb, eps, mode);
 }
 
 // Projection (Lemma Projections): T_b = C_tc S_b, S~_b = T_b C'_sc^*.  CTA per block.

@@ -32,6 +32,7 @@ struct PassD {
     int* rank;
     int* nsig;            // number of singular values computed
     double* disc;         // discarded sum of squares per pair
+    int* sweeps;          // Jacobi sweeps used per pair (diagnostics / executed-flop model)
 };
 
 struct PlanD {
@@ -89,8 +90,8 @@ void launch_S(const PlanD& P, cudaStream_t s);
 void launch_basis(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStream_t s);
 void launch_block_weights(const PlanD& P, int mode, cudaStream_t s);
 void launch_total_weights(const PlanD& P, bool row, int p0, int np, int bufrows, cudaStream_t s);
-void launch_truncate(const PlanD& P, bool row, int p0, int np, int maxrowsM, int maxZrows, double eps, int mode,
-                     cudaStream_t s);
+void launch_truncate(const PlanD& P, bool row, int p0, int np, int maxrowsM, int maxZrows, bool leaf_level, double eps,
+                     int mode, cudaStream_t s);
 void launch_project(const PlanD& P, int maxkrow, cudaStream_t s);
 // matvec (forward / coupling / backward)
 void launch_mv_forward(const PlanD& P, bool recomp, int p0, int np, const double2* xp, double2* xh,
