@@ -121,13 +121,15 @@ struct dh2_ctx {
     std::vector<int> basis_maxrows;
     int max_leaf = 0;
     // blocks
-    std::vector<int> blk_t, blk_s, blk_dir, blk_bprow, blk_bpcol, blk_prow, blk_pcol;
+    std::vector<int> blk_t, blk_s, blk_dir, blk_bprow, blk_bpcol, blk_prow, blk_pcol, blk_mirror;
+    int64_t mirror_missing = 0;
     std::vector<int64_t> blk_St_off;
     int64_t St_total = 0;
     PassH row, col;
     // device
     DevBuf<double> d_xyz, d_c_lo, d_c_hi, d_dirs, d_omega, d_normG2;
     DevBuf<int64_t> d_tri, d_perm, d_c_begin, d_bp_V_off, d_bp_R_off, d_bp_E_off, d_blk_St_off;
+    DevBuf<int> d_blk_mirror;
     DevBuf<int> d_c_size, d_bp_t, d_bp_dir, d_bp_sddir, d_bp_child0, d_bp_child1, d_bp_R_rows, d_blk_t, d_blk_s,
         d_blk_dir, d_blk_bprow, d_blk_bpcol, d_blk_prow, d_blk_pcol;
     std::vector<std::unique_ptr<DevBuf<int>>> d_lists;
@@ -416,6 +418,22 @@ void build_tables(dh2_ctx* C) {
         }
         if (!X.lc.empty()) X.lc_ptr.push_back((int)X.lc.size());
     }
+    // antipodal mirror b' = (s, t, -c) of every block: S_{b'} = S_b^T exactly (DESIGN §total weights)
+    {
+        std::unordered_map<uint64_t, int> ts;
+        for (int b = 0; b < nb; ++b) ts[key(S.blocks[b].t, S.blocks[b].s)] = b;
+        C->blk_mirror.assign(nb, -1);
+        for (int b = 0; b < nb; ++b) {
+            const Block& B = S.blocks[b];
+            auto it = ts.find(key(B.s, B.t));
+            if (it == ts.end()) { ++C->mirror_missing; continue; }
+            int l = (int)T.level[B.t];
+            const auto& D = S.D(l);
+            int64_t c2 = S.blocks[it->second].c;
+            bool neg = D[3 * c2] == -D[3 * B.c] && D[3 * c2 + 1] == -D[3 * B.c + 1] && D[3 * c2 + 2] == -D[3 * B.c + 2];
+            if (neg) C->blk_mirror[b] = it->second; else ++C->mirror_missing;
+        }
+    }
     C->blk_St_off.assign(nb, 0);
     for (int b = 0; b < nb; ++b) {
         C->blk_St_off[b] = C->St_total;
@@ -522,6 +540,7 @@ void upload_all(dh2_ctx* C, const double* xyz, int64_t nv, const int64_t* tri) {
     C->d_blk_prow.upload(C->blk_prow, s);
     C->d_blk_pcol.upload(C->blk_pcol, s);
     C->d_blk_St_off.upload(C->blk_St_off, s);
+    C->d_blk_mirror.upload(C->blk_mirror, s);
     auto up_list = [&](const std::vector<int>& v) -> const int* {
         C->d_lists.emplace_back(new DevBuf<int>());
         C->d_lists.back()->upload(v, s);
@@ -672,9 +691,7 @@ void run_recompress(dh2_ctx* C, double eps, int mode) {
         for (int l = 0; l <= L; ++l) {
             int p0 = X.lev_ptr[l], np = X.lev_ptr[l + 1] - p0;
             if (!np) continue;
-            int mt = X.lev_max_total[l];
-            int bufrows = mt <= 2 * k ? std::max(mt, 1) : 2 * k;
-            C->timed("total_weights", 1, [&] { launch_total_weights(P, row, p0, np, bufrows, s); });
+            C->timed("total_weights", 1, [&] { launch_total_weights(P, row, p0, np, C->d_blk_mirror.p, s); });
             double fl = 0;
             for (int p = p0; p < p0 + np; ++p) {
                 for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) {
@@ -682,7 +699,7 @@ void run_recompress(dh2_ctx* C, double eps, int mode) {
                     fl += 8.0 * C->bp_R_rows[row ? C->blk_bpcol[b] : C->blk_bprow[b]] * (double)k * k;
                 }
                 for (int ip = X.par_ptr[p]; ip < X.par_ptr[p + 1]; ++ip) fl += 8.0 * 3 * X.Z_rows[X.par[ip]] * (double)k * m;
-                if (X.total_rows[p] > k) fl += qr_flops(std::min(X.total_rows[p], bufrows), k);
+                if (X.total_rows[p] > k) fl += 8.0 * X.total_rows[p] * (double)k * k;  // structured QR appends
             }
             C->kstat["total_weights"].flops += fl;
         }
@@ -983,7 +1000,7 @@ int dh2_get_stats(const dh2_ctx* C, char* buf, int64_t* len) {
       << ", \"row_pairs\": " << nrow << ", \"col_pairs\": " << ncol << ", \"basis_pairs\": " << C->bp_t.size()
       << ", \"host_build_ms\": " << C->host_build_ms << ", \"launches_total\": " << C->launches_total
       << ", \"E_row\": " << C->E_row << ", \"E_col\": " << C->E_col << ", \"far2\": " << C->far2
-      << ", \"device_bytes\": " << plan_bytes(C) << ", \"kernels\": {";
+      << ", \"device_bytes\": " << plan_bytes(C) << ", \"mirror_missing\": " << C->mirror_missing << ", \"kernels\": {";
     bool first = true;
     for (auto& kv : C->kstat) {
         if (!first) o << ", ";
@@ -1086,6 +1103,7 @@ int dh2_export(const dh2_ctx* C, const char* name, void* buf, int64_t* nbytes) {
         else if (nm == "blk_St_off") it = hv(C->blk_St_off);
         else if (nm == "blk_prow") it = hv(C->blk_prow);
         else if (nm == "blk_pcol") it = hv(C->blk_pcol);
+        else if (nm == "blk_mirror") it = hv(C->blk_mirror);
         else if (nm == "VR") it = dv(C->d_VR);
         else if (nm == "E") it = dv(C->d_E);
         else if (nm == "S") it = dv(C->d_S);

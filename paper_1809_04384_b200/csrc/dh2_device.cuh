@@ -56,6 +56,41 @@ __device__ __forceinline__ double2 warp_sum2(double2 v) {
     return v;
 }
 
+// Lane groups: G consecutive lanes (G a power of two, 2..32) cooperate on one vector so a
+// warp works on 32/G independent vectors at once; shuffles use the group's own mask.
+struct LaneGroup {
+    int G, gl, gid, ng;
+    unsigned mask;
+};
+__device__ __forceinline__ LaneGroup lane_group(int G) {
+    LaneGroup g;
+    g.G = G;
+    g.gl = threadIdx.x & (G - 1);
+    g.gid = threadIdx.x / G;
+    g.ng = blockDim.x / G;
+    const int lane = threadIdx.x & 31;
+    g.mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+    return g;
+}
+// smallest power of two >= ceil(len / per_lane), clamped to [lo, 32]
+__device__ __forceinline__ int group_size_for(int len, int per_lane, int lo) {
+    int need = (len + per_lane - 1) / per_lane;
+    int G = lo;
+    while (G < need && G < 32) G <<= 1;
+    return G;
+}
+__device__ __forceinline__ double group_sum(double v, const LaneGroup& g) {
+    for (int o = g.G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(g.mask, v, o);
+    return v;
+}
+__device__ __forceinline__ double2 group_sum2(double2 v, const LaneGroup& g) {
+    for (int o = g.G >> 1; o > 0; o >>= 1) {
+        v.x += __shfl_xor_sync(g.mask, v.x, o);
+        v.y += __shfl_xor_sync(g.mask, v.y, o);
+    }
+    return v;
+}
+
 // Lagrange basis of the Chebyshev points of the first kind on one axis, evaluated at x
 // (P:245-248): L_j(xhat) = prod_{i != j} (xhat - z_i)/(z_j - z_i), xhat = (x - mid)/half.
 // A collapsed (flat) axis has L_j = delta_{j0} (DESIGN reading Q7).
@@ -146,13 +181,14 @@ __device__ inline void cta_qr(double2* A, int lda, int M, int N, double2* sh /* 
         __syncthreads();
         const double tau = sh[1].x;
         if (tau != 0.0) {
-            for (int c = j + 1 + warp; c < N; c += nw) {
+            const LaneGroup g = lane_group(group_size_for(M - j, 4, 4));
+            for (int c = j + 1 + g.gid; c < N; c += g.ng) {
                 double2* colc = A + (size_t)c * lda;
                 double2 w = cmk(0.0, 0.0);
-                for (int i = j + lane; i < M; i += 32) cfma_cj(w, colj[i], colc[i]);
-                w = warp_sum2(w);
+                for (int i = j + g.gl; i < M; i += g.G) cfma_cj(w, colj[i], colc[i]);
+                w = group_sum2(w, g);
                 w = cscale(w, tau);
-                for (int i = j + lane; i < M; i += 32) {
+                for (int i = j + g.gl; i < M; i += g.G) {
                     double2 u = colj[i];
                     colc[i] = csub(colc[i], cmul(u, w));
                 }
@@ -289,18 +325,19 @@ __device__ inline void cta_qrcp(double2* B, int ldb, int M, int N, int* piv, dou
         }
         __syncthreads();
         const double tau = sh[1].x;
-        for (int c = j + 1 + warp; c < N; c += nw) {
+        const LaneGroup g = lane_group(group_size_for(M - j, 4, 4));
+        for (int c = j + 1 + g.gid; c < N; c += g.ng) {
             double2* colc = B + (size_t)c * ldb;
             if (tau != 0.0) {
                 double2 w = cmk(0.0, 0.0);
-                for (int i = j + lane; i < M; i += 32) cfma_cj(w, colj[i], colc[i]);
-                w = cscale(warp_sum2(w), tau);
-                for (int i = j + lane; i < M; i += 32) colc[i] = csub(colc[i], cmul(colj[i], w));
+                for (int i = j + g.gl; i < M; i += g.G) cfma_cj(w, colj[i], colc[i]);
+                w = cscale(group_sum2(w, g), tau);
+                for (int i = j + g.gl; i < M; i += g.G) colc[i] = csub(colc[i], cmul(colj[i], w));
             }
             double s = 0.0;
-            for (int i = j + 1 + lane; i < M; i += 32) s += cabs2(colc[i]);
-            s = warp_sum(s);
-            if (lane == 0) nrm[c] = s;
+            for (int i = j + 1 + g.gl; i < M; i += g.G) s += cabs2(colc[i]);
+            s = group_sum(s, g);
+            if (g.gl == 0) nrm[c] = s;
         }
         __syncthreads();
         if (tid == 0) colj[j] = sh[0];
@@ -314,13 +351,14 @@ __device__ inline void cta_qrcp(double2* B, int ldb, int M, int N, int* piv, dou
 // norms carried in nrm[] and updated by the exact rotation identities
 // a' = a - t|g|, b' = b + t|g| (recomputed at every sweep).  Returns the sweeps done.
 __device__ inline int cta_jacobi_rows(double2* R, int ldr, int nv, int len, double* nrm, int* flag) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int tid = threadIdx.x;
+    const LaneGroup g = lane_group(group_size_for(len, 4, 4));
     if (nv <= 1) {
-        if (nv == 1 && warp == 0) {
+        if (nv == 1 && g.gid == 0) {
             double s = 0.0;
-            for (int i = lane; i < len; i += 32) s += cabs2(R[(size_t)i * ldr]);
-            s = warp_sum(s);
-            if (lane == 0) nrm[0] = s;
+            for (int i = g.gl; i < len; i += g.G) s += cabs2(R[(size_t)i * ldr]);
+            s = group_sum(s, g);
+            if (g.gl == 0) nrm[0] = s;
         }
         __syncthreads();
         return 0;
@@ -331,16 +369,16 @@ __device__ inline int cta_jacobi_rows(double2* R, int ldr, int nv, int len, doub
     const double tol2 = tol * tol;
     int sweep = 0;
     for (; sweep < 60; ++sweep) {
-        for (int p = warp; p < nv; p += nw) {
+        for (int p = g.gid; p < nv; p += g.ng) {
             double s = 0.0;
-            for (int i = lane; i < len; i += 32) s += cabs2(R[p + (size_t)i * ldr]);
-            s = warp_sum(s);
-            if (lane == 0) nrm[p] = s;
+            for (int i = g.gl; i < len; i += g.G) s += cabs2(R[p + (size_t)i * ldr]);
+            s = group_sum(s, g);
+            if (g.gl == 0) nrm[p] = s;
         }
         if (tid == 0) *flag = 0;
         __syncthreads();
         for (int r = 0; r < nr; ++r) {
-            for (int pi = warp; pi < np / 2; pi += nw) {
+            for (int pi = g.gid; pi < np / 2; pi += g.ng) {
                 const int i1 = np - 1 - pi;
                 int p = 0, q;
                 if (pi != 0) { p = pi - 1 + r; if (p >= nr) p -= nr; ++p; }
@@ -348,28 +386,28 @@ __device__ inline int cta_jacobi_rows(double2* R, int ldr, int nv, int len, doub
                 if (p >= nv || q >= nv) continue;
                 const double al = nrm[p], be = nrm[q];
                 double2 ga = cmk(0.0, 0.0);  // <x_p, x_q> = sum_i R[p,i] conj(R[q,i])
-                for (int i = lane; i < len; i += 32) cfma_bj(ga, R[p + (size_t)i * ldr], R[q + (size_t)i * ldr]);
-                ga = warp_sum2(ga);
+                for (int i = g.gl; i < len; i += g.G) cfma_bj(ga, R[p + (size_t)i * ldr], R[q + (size_t)i * ldr]);
+                ga = group_sum2(ga, g);
                 const double g2 = cabs2(ga);
-                // rotate iff |g| > tol sqrt(al be)  (squared test, no square roots)
+                // rotate iff |gamma| > tol sqrt(al be)  (squared test, no square roots)
                 if (g2 > tol2 * (al * be) && al > 0.0 && be > 0.0) {
-                    const double ig = rsqrt(g2);  // 1/|g|
-                    const double g = g2 * ig;
+                    const double ig = rsqrt(g2);  // 1/|gamma|
+                    const double gm = g2 * ig;
                     const double zeta = 0.5 * (be - al) * ig;
                     const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
                     const double c = rsqrt(fma(t, t, 1.0));
                     const double sn = c * t;
-                    // x_q <- e x_q with e = e^{-i phi}; on the rows of R (conjugated) the factor is ga/|g|
+                    // x_q <- e x_q with e = e^{-i phi}; on the rows of R (conjugated) the factor is gamma/|gamma|
                     const double2 ec = cmk(ga.x * ig, ga.y * ig);
-                    for (int i = lane; i < len; i += 32) {
+                    for (int i = g.gl; i < len; i += g.G) {
                         const double2 a = R[p + (size_t)i * ldr];
                         const double2 b = cmul(ec, R[q + (size_t)i * ldr]);
                         R[p + (size_t)i * ldr] = csub(cscale(a, c), cscale(b, sn));
                         R[q + (size_t)i * ldr] = cadd(cscale(a, sn), cscale(b, c));
                     }
-                    if (lane == 0) {
-                        nrm[p] = al - t * g;
-                        nrm[q] = be + t * g;
+                    if (g.gl == 0) {
+                        nrm[p] = al - t * gm;
+                        nrm[q] = be + t * gm;
                         *flag = 1;
                     }
                 }
@@ -379,11 +417,11 @@ __device__ inline int cta_jacobi_rows(double2* R, int ldr, int nv, int len, doub
         if (*flag == 0) break;
         __syncthreads();
     }
-    for (int p = warp; p < nv; p += nw) {
+    for (int p = g.gid; p < nv; p += g.ng) {
         double s = 0.0;
-        for (int i = lane; i < len; i += 32) s += cabs2(R[p + (size_t)i * ldr]);
-        s = warp_sum(s);
-        if (lane == 0) nrm[p] = s;
+        for (int i = g.gl; i < len; i += g.G) s += cabs2(R[p + (size_t)i * ldr]);
+        s = group_sum(s, g);
+        if (g.gl == 0) nrm[p] = s;
     }
     __syncthreads();
     return sweep;

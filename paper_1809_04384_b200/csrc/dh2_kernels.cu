@@ -304,87 +304,182 @@ void launch_block_weights(const PlanD& P, int mode, cudaStream_t s) {
     k_block_weights<<<P.nblk, 256, sm, s>>>(P, mode, ldu);
 }
 
+// Annihilate the nb x k chunk B into the k x k upper-triangular smem matrix R:
+// [R; B] = Q [R'; 0] by k structured Householder reflections, each touching row j of R and
+// the nb rows of B only (the rows of R below j are zero in column j).
+__device__ inline void cta_qr_append(double2* R, int ldr, double2* B, int ldb, int nb, int k, double2* sh) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const LaneGroup g = lane_group(group_size_for(nb + 1, 4, 4));
+    __syncthreads();
+    for (int j = 0; j < k; ++j) {
+        double2* bj = B + (size_t)j * ldb;
+        if (warp == 0) {
+            double s = 0.0;
+            for (int i = lane; i < nb; i += 32) s += cabs2(bj[i]);
+            s = warp_sum(s);
+            if (lane == 0) {
+                double2 alpha = R[j + (size_t)j * ldr];
+                double tau = 0.0;
+                double2 beta = alpha, u0 = cmk(0.0, 0.0);
+                if (s > 0.0) {
+                    double aa = sqrt(cabs2(alpha));
+                    double xn = sqrt(s + aa * aa);
+                    double2 ph = aa > 0.0 ? cscale(alpha, 1.0 / aa) : cmk(1.0, 0.0);
+                    beta = cscale(ph, -xn);
+                    u0 = cscale(ph, aa + xn);
+                    tau = 1.0 / (xn * (xn + aa));
+                }
+                sh[0] = beta;
+                sh[1] = cmk(tau, 0.0);
+                sh[2] = u0;
+            }
+        }
+        __syncthreads();
+        const double tau = sh[1].x;
+        if (tau != 0.0) {
+            const double2 u0 = sh[2];
+            for (int c = j + 1 + g.gid; c < k; c += g.ng) {
+                double2* bc = B + (size_t)c * ldb;
+                double2 w = cmk(0.0, 0.0);
+                if (g.gl == 0) cfma_cj(w, u0, R[j + (size_t)c * ldr]);
+                for (int i = g.gl; i < nb; i += g.G) cfma_cj(w, bj[i], bc[i]);
+                w = cscale(group_sum2(w, g), tau);
+                if (g.gl == 0) R[j + (size_t)c * ldr] = csub(R[j + (size_t)c * ldr], cmul(u0, w));
+                for (int i = g.gl; i < nb; i += g.G) bc[i] = csub(bc[i], cmul(bj[i], w));
+            }
+        }
+        __syncthreads();
+        if (tid == 0) R[j + (size_t)j * ldr] = sh[0];
+    }
+    __syncthreads();
+}
+
+// out[i, nu] = w * sum_mu X[i0+i, mu] * op(S)[mu, nu] for i < nb (nb <= 32), X = rx x k
+// column-major (global), written to the smem chunk B (ld ldb).  op(S)[mu, nu] is read as
+// Sg[nu + mu k] (conjugated if conj_s): the row pass uses S_b^* (Sg = S_b, conj), the column
+// pass uses S_b = S_{b'}^T with b' the antipodal mirror block (Sg = S_{b'}, no conj), so
+// both read S contiguously along nu.  Each thread keeps 8 rows of one column nu.
+__device__ inline void chunk_gemm_S(const double2* X, int rx, int i0, int nb, const double2* Sg, bool conj_s, bool strided,
+                                    double w, int k, double2* B, int ldb) {
+    const int nthr = blockDim.x;
+    const int ncg = nthr / k;  // row groups (k divides blockDim for k in {8, 27->no} handled below)
+    if (ncg >= 1 && nthr % k == 0) {
+        const int nu = threadIdx.x % k, rg = threadIdx.x / k;
+        for (int ib = rg * 8; ib < nb; ib += ncg * 8) {
+            double2 acc[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) acc[r] = cmk(0.0, 0.0);
+            const int nr = min(8, nb - ib);
+            for (int mu = 0; mu < k; ++mu) {
+                double2 sv = strided ? Sg[mu + (size_t)nu * k] : Sg[nu + (size_t)mu * k];
+                if (conj_s) sv.y = -sv.y;
+                const double2* xr = X + i0 + ib + (size_t)mu * rx;
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+                    if (r < nr) cfma(acc[r], xr[r], sv);
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+                if (r < nr) B[ib + r + (size_t)nu * ldb] = cscale(acc[r], w);
+        }
+    } else {
+        for (int idx = threadIdx.x; idx < nb * k; idx += nthr) {
+            const int i = idx % nb, nu = idx / nb;
+            double2 acc = cmk(0.0, 0.0);
+            for (int mu = 0; mu < k; ++mu) {
+                double2 sv = strided ? Sg[mu + (size_t)nu * k] : Sg[nu + (size_t)mu * k];
+                if (conj_s) sv.y = -sv.y;
+                cfma(acc, X[i0 + i + (size_t)mu * rx], sv);
+            }
+            B[i + (size_t)nu * ldb] = cscale(acc, w);
+        }
+    }
+}
+
 // Total weights, one CTA per pair of one level (top-down):
 //   Z_tc = [w_b S_b R_sc^* (s in row(t,c)) | E_{tc+} Zhat_{t+c+}^* (c+ in sd^{-1}(c))],
-//   Zhat_tc = R factor of the skinny QR of Z_tc^* (rows stacked incrementally,
-//   R <- qr([R; next rows]) whenever the buffer is full; gamma = 0 at the root).
-// Row pass: Z^* rows w_b R_sc S_b^*.  Column pass (adjoint): w_b R_tc S_b.
-__global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, int lda, int bufrows) {
+//   Zhat_tc = R factor of the skinny QR of Z_tc^* (gamma = 0 at the root).
+// The rows of Z_tc^* are produced in chunks of <= 32 rows and annihilated into the k x k
+// triangle R (structured Householder); if Z_tc^* has <= k rows it is stored as is (P = I).
+// Row pass: rows w_b R_sc S_b^*.  Column pass (adjoint): rows w_b R_tc S_b.
+__global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, const int* mirror, int ldr, int ldb) {
     extern __shared__ double2 sm[];
+    __shared__ double2 sh[3];
     const int p = p0 + blockIdx.x;
     const int k = P.k, m = P.m;
-    double2* A = sm;
-    double2* Ef = sm + (size_t)lda * k;
-    double2* sh = Ef + 3 * m * m;
-    int cur = 0;
-    bool compressed = false;
+    const int CH = 32;
+    double2* R = sm;                                // k x k (ld ldr)
+    double2* B = R + (size_t)ldr * k;               // CH x k (ld ldb)
+    double2* Ef = B + (size_t)ldb * k;              // 3 m^2
+    const int zr = X.Z_rows[p];
+    // total rows of Z^*
+    int total = 0;
+    for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) {
+        const int b = X.blk[ib];
+        total += P.bp_R_rows[row ? P.blk_bpcol[b] : P.blk_bprow[b]];
+    }
+    for (int ip = X.par_ptr[p]; ip < X.par_ptr[p + 1]; ++ip) total += X.Z_rows[X.par[ip]];
+    const bool qr = total > k;
+    if (qr)
+        for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) R[idx % k + (size_t)(idx / k) * ldr] = cmk(0.0, 0.0);
+    int cur = 0;  // rows stored directly (no-QR case)
     for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) {
         const int b = X.blk[ib];
         const int obp = row ? P.blk_bpcol[b] : P.blk_bprow[b];
         const int r = P.bp_R_rows[obp];
-        if (cur + r > bufrows) {
-            cta_qr(A, lda, cur, k, sh);
-            cur = min(cur, k);
-            zero_lower(A, lda, cur, k);
-            compressed = true;
-            __syncthreads();
-        }
         const double2* Ro = P.R + P.bp_R_off[obp];
-        const double2* S = P.S + (size_t)b * k * k;
         const double w = P.omega[b];
-        for (int idx = threadIdx.x; idx < r * k; idx += blockDim.x) {
-            int i = idx % r, nu = idx / r;
-            double2 acc = cmk(0.0, 0.0);
-            if (row) {
-                for (int mu = 0; mu < k; ++mu) cfma_bj(acc, Ro[i + (size_t)mu * r], S[nu + (size_t)mu * k]);
-            } else {
-                for (int mu = 0; mu < k; ++mu) cfma(acc, Ro[i + (size_t)mu * r], S[mu + (size_t)nu * k]);
-            }
-            A[cur + i + (size_t)nu * lda] = cscale(acc, w);
+        const int mb = row ? b : mirror[b];
+        const double2* Sg = P.S + (size_t)(mb >= 0 ? mb : b) * k * k;
+        const bool strided = !row && mb < 0;
+        for (int i0 = 0; i0 < r; i0 += CH) {
+            const int nb = min(CH, r - i0);
+            double2* dst = qr ? B : R + cur;
+            const int ldd = qr ? ldb : ldr;
+            __syncthreads();
+            chunk_gemm_S(Ro, r, i0, nb, Sg, row, strided, w, k, dst, ldd);
+            if (qr)
+                cta_qr_append(R, ldr, B, ldb, nb, k, sh);
+            else
+                cur += nb;
         }
-        cur += r;
-        __syncthreads();
     }
     for (int ip = X.par_ptr[p]; ip < X.par_ptr[p + 1]; ++ip) {
         const int pp = X.par[ip];
         const int ci = X.par_child[ip];
         const int r = X.Z_rows[pp];
-        if (cur + r > bufrows) {
-            cta_qr(A, lda, cur, k, sh);
-            cur = min(cur, k);
-            zero_lower(A, lda, cur, k);
-            compressed = true;
-            __syncthreads();
-        }
         const double2* Zp = X.Z + X.Z_off[pp];
         const double2* Eg = P.E + P.bp_E_off[X.bp[pp]] + ci * 3 * m * m;
+        __syncthreads();
         for (int idx = threadIdx.x; idx < 3 * m * m; idx += blockDim.x) Ef[idx] = Eg[idx];
-        for (int idx = threadIdx.x; idx < r * k; idx += blockDim.x)
-            A[cur + idx % r + (size_t)(idx / r) * lda] = Zp[idx];
-        __syncthreads();
-        kron_apply(A + cur, lda, r, m, Ef, true);  // Zhat_{t+c+} E_{tc+}^*
-        cur += r;
+        for (int i0 = 0; i0 < r; i0 += CH) {
+            const int nb = min(CH, r - i0);
+            double2* dst = qr ? B : R + cur;
+            const int ldd = qr ? ldb : ldr;
+            __syncthreads();
+            for (int idx = threadIdx.x; idx < nb * k; idx += blockDim.x)
+                dst[idx % nb + (size_t)(idx / nb) * ldd] = Zp[i0 + idx % nb + (size_t)(idx / nb) * r];
+            __syncthreads();
+            kron_apply(dst, ldd, nb, m, Ef, true);  // Zhat_{t+c+} E_{tc+}^*
+            if (qr)
+                cta_qr_append(R, ldr, B, ldb, nb, k, sh);
+            else
+                cur += nb;
+        }
     }
-    if (cur > k) {
-        cta_qr(A, lda, cur, k, sh);
-        cur = k;
-        zero_lower(A, lda, k, k);
-        __syncthreads();
-    }
-    (void)compressed;
-    const int zr = X.Z_rows[p];
+    __syncthreads();
     double2* Z = X.Z + X.Z_off[p];
     for (int idx = threadIdx.x; idx < zr * k; idx += blockDim.x) {
-        int i = idx % zr;
-        Z[idx] = (i < cur) ? A[i + (size_t)(idx / zr) * lda] : cmk(0.0, 0.0);
+        const int i = idx % zr, nu = idx / zr;
+        Z[idx] = (qr && i > nu) ? cmk(0.0, 0.0) : R[i + (size_t)nu * ldr];
     }
 }
 
-void launch_total_weights(const PlanD& P, bool row, int p0, int np, int bufrows, cudaStream_t s) {
+void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* mirror, cudaStream_t s) {
     if (!np) return;
-    int lda = odd_ld(bufrows);
-    size_t sm = ((size_t)lda * P.k + 3 * P.m * P.m + 2) * sizeof(double2);
-    k_total_weights<<<np, 256, sm, s>>>(P, row ? P.row : P.col, row, p0, lda, bufrows);
+    const int ldr = odd_ld(P.k), ldb = odd_ld(32);
+    size_t sm = ((size_t)ldr * P.k + (size_t)ldb * P.k + 3 * P.m * P.m) * sizeof(double2);
+    k_total_weights<<<np, 256, sm, s>>>(P, row ? P.row : P.col, row, p0, mirror, ldr, ldb);
 }
 
 // Truncation, one CTA per pair of one level (bottom-up):
