@@ -211,11 +211,17 @@ def main():
         ms = float(t.item())
     value = world * n / (ms * 1e-3) / 1e6
 
-    # per kernel class over the timed region
-    kern = {}
+    # per kernel class over the timed region (classes "name@level" are grouped by name;
+    # "truncate_row@8" -> class "truncate", detail kept per level)
+    kern, detail = {}, {}
     for cls, v1 in s1["kernels"].items():
         v0 = s0["kernels"].get(cls, {"launches": 0, "ms": 0.0, "flops": 0.0, "bytes": 0.0})
-        kern[cls] = {key: v1[key] - v0[key] for key in ("launches", "ms", "flops", "bytes")}
+        d = {key: v1[key] - v0[key] for key in ("launches", "ms", "flops", "bytes")}
+        detail[cls] = d
+        base = cls.split("@")[0].replace("_row", "").replace("_col", "")
+        agg = kern.setdefault(base, {"launches": 0, "ms": 0.0, "flops": 0.0, "bytes": 0.0})
+        for key in agg:
+            agg[key] += d[key]
     launches = s1["launches_total"] - s0["launches_total"]
     dom = max(kern.items(), key=lambda kv: kv[1]["ms"])
     dname, d = dom
@@ -278,7 +284,8 @@ def main():
                            "blocks": s1["blocks"], "row_pairs": s1["row_pairs"], "basis_pairs": s1["basis_pairs"]},
                 "seconds_per_step": ms * 1e-3,
                 "roofline": roof, "cpu_baseline": cpu, "clocks": clocks, "e2e": e2e, "gpu_launches": launches,
-                "phases": phases}
+                "phases": phases,
+                "launch_detail_ms_per_step": {c: round(v["ms"] / args.steps, 4) for c, v in sorted(detail.items())}}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -659,7 +659,7 @@ void run_recompress(dh2_ctx* C, double eps, int mode) {
     for (int l = L; l >= 0; --l) {
         int nb = (int)C->basis_lists[l].size();
         if (!nb) continue;
-        C->timed("basis", 1, [&] { launch_basis(P, C->d_basis_list[l], nb, C->basis_maxrows[l], s); });
+        C->timed("basis@" + std::to_string(l), 1, [&] { launch_basis(P, C->d_basis_list[l], nb, C->basis_maxrows[l], s); });
         double fl = 0;
         for (int id : C->basis_lists[l]) {
             int rows;
@@ -672,10 +672,10 @@ void run_recompress(dh2_ctx* C, double eps, int mode) {
             }
             if (rows > k) fl += qr_flops(rows, k);
         }
-        C->kstat["basis"].flops += fl;
+        C->kstat["basis@" + std::to_string(l)].flops += fl;
     }
     // block weights
-    C->timed("block_weights", 1, [&] { launch_block_weights(P, mode, s); });
+    C->timed("block_weights", 1, [&] { launch_block_weights(P, mode, C->d_blk_mirror.p, s); });
     {
         double fl = 0;
         for (size_t b = 0; b < C->st.blocks.size(); ++b) {
@@ -691,7 +691,7 @@ void run_recompress(dh2_ctx* C, double eps, int mode) {
         for (int l = 0; l <= L; ++l) {
             int p0 = X.lev_ptr[l], np = X.lev_ptr[l + 1] - p0;
             if (!np) continue;
-            C->timed("total_weights", 1, [&] { launch_total_weights(P, row, p0, np, C->d_blk_mirror.p, s); });
+            C->timed(std::string(row ? "total_weights_row@" : "total_weights_col@") + std::to_string(l), 1, [&] { launch_total_weights(P, row, p0, np, C->d_blk_mirror.p, s); });
             double fl = 0;
             for (int p = p0; p < p0 + np; ++p) {
                 for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) {
@@ -701,7 +701,7 @@ void run_recompress(dh2_ctx* C, double eps, int mode) {
                 for (int ip = X.par_ptr[p]; ip < X.par_ptr[p + 1]; ++ip) fl += 8.0 * 3 * X.Z_rows[X.par[ip]] * (double)k * m;
                 if (X.total_rows[p] > k) fl += 8.0 * X.total_rows[p] * (double)k * k;  // structured QR appends
             }
-            C->kstat["total_weights"].flops += fl;
+            C->kstat[std::string(row ? "total_weights_row@" : "total_weights_col@") + std::to_string(l)].flops += fl;
         }
         // truncation, bottom-up
         X.rank.assign(X.bp.size(), 0);
@@ -714,7 +714,7 @@ void run_recompress(dh2_ctx* C, double eps, int mode) {
             int maxz = X.lev_max_zrows[l];
             bool all_leaf = true;
             for (int p = p0; p < p0 + np; ++p) all_leaf = all_leaf && X.child0[p] < 0;
-            C->timed("truncate", 1, [&] { launch_truncate(P, row, p0, np, maxrows, maxz, all_leaf, eps, mode, s); });
+            C->timed(std::string(row ? "truncate_row@" : "truncate_col@") + std::to_string(l), 1, [&] { launch_truncate(P, row, p0, np, maxrows, maxz, all_leaf, eps, mode, s); });
             CK(cudaMemcpyAsync(X.rank.data() + p0, X.d_rank.p + p0, np * sizeof(int), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             double fl = 0;
@@ -728,7 +728,7 @@ void run_recompress(dh2_ctx* C, double eps, int mode) {
                 fl += 8.0 * 10.0 * rows * n * n;  // SVD, C_svd = 10 model (DESIGN §flop model)
                 fl += 8.0 * X.rank[p] * rows * k;  // C
             }
-            C->kstat["truncate"].flops += fl;
+            C->kstat[std::string(row ? "truncate_row@" : "truncate_col@") + std::to_string(l)].flops += fl;
         }
     }
     // projection

@@ -261,7 +261,10 @@ __device__ inline int cta_jacobi(double2* W, int ld, int m, int n, int* flag) {
 // smem matrix B, in place.  Pivot = remaining column of largest norm (first on ties); norms
 // are recomputed exactly after every step (no downdating).  On return piv[j] = original
 // column placed at position j, R = upper trapezoid of B[0:min(M,N), :] in pivoted order.
-__device__ inline void cta_qrcp(double2* B, int ldb, int M, int N, int* piv, double* nrm, double2* sh, int* s_piv) {
+// If rank_rel2 > 0 the factorisation stops at the first step j whose trailing block has
+// ||B[j:, j:]||_F^2 <= rank_rel2 * ||B||_F^2 (numerical rank); returns the steps done.
+__device__ inline int cta_qrcp(double2* B, int ldb, int M, int N, int* piv, double* nrm, double2* sh, int* s_piv,
+                               double rank_rel2) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
     const int K = min(M, N);
     for (int c = tid; c < N; c += blockDim.x) piv[c] = c;
@@ -273,23 +276,31 @@ __device__ inline void cta_qrcp(double2* B, int ldb, int M, int N, int* piv, dou
         if (lane == 0) nrm[c] = s;
     }
     __syncthreads();
-    for (int j = 0; j < K; ++j) {
+    __shared__ double s_total;
+    int j = 0;
+    for (; j < K; ++j) {
         if (warp == 0) {
-            double best = -1.0;
+            double best = -1.0, rem = 0.0;
             int bi = j;
             for (int c = j + lane; c < N; c += 32) {
                 double v = nrm[c];
+                rem += v;
                 if (v > best) { best = v; bi = c; }
             }
             for (int o = 16; o > 0; o >>= 1) {
                 double ob = __shfl_xor_sync(0xffffffffu, best, o);
                 int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                rem += __shfl_xor_sync(0xffffffffu, rem, o);
                 if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
             }
-            if (lane == 0) *s_piv = bi;
+            if (lane == 0) {
+                if (j == 0) s_total = rem;
+                *s_piv = (rank_rel2 > 0.0 && rem <= rank_rel2 * s_total) ? -1 : bi;
+            }
         }
         __syncthreads();
         const int pc = *s_piv;
+        if (pc < 0) break;  // numerical rank reached (uniform across the CTA)
         if (pc != j) {
             for (int i = tid; i < M; i += blockDim.x) {
                 double2 a = B[i + (size_t)j * ldb];
@@ -343,6 +354,7 @@ __device__ inline void cta_qrcp(double2* B, int ldb, int M, int N, int* piv, dou
         if (tid == 0) colj[j] = sh[0];
     }
     __syncthreads();
+    return j;
 }
 
 // One-sided Jacobi on the vectors x_p = conj(R[p, 0:len]) (rows of the smem matrix R,
@@ -425,6 +437,257 @@ __device__ inline int cta_jacobi_rows(double2* R, int ldr, int nv, int len, doub
     }
     __syncthreads();
     return sweep;
+}
+
+
+// ------------------------------------------------------------------ compile-time specialised
+// One-sided Jacobi on the rows of R (see cta_jacobi_rows) for len <= G*E: every vector is
+// held by a group of G lanes, E elements per lane, fully unrolled; the two vectors of a pair
+// stay in registers between the inner product and the rotation.
+template <int G, int E>
+__device__ inline int jacobi_rows_t(double2* R, int ldr, int nv, int len, double* nrm, int* flag) {
+    const int tid = threadIdx.x;
+    const int gl = tid & (G - 1), gid = tid / G, ng = blockDim.x / G;
+    const unsigned mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((tid & 31) & ~(G - 1)));
+    const int st = G * ldr;  // stride between a lane's elements
+    __syncthreads();  // R was just written by the caller
+    if (nv <= 1) {
+        if (nv == 1 && gid == 0) {
+            double s = 0.0;
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+                if (gl + G * e < len) s += cabs2(R[(gl + G * e) * ldr]);
+            for (int o = G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(mask, s, o);
+            if (gl == 0) nrm[0] = s;
+        }
+        __syncthreads();
+        return 0;
+    }
+    const int np = nv + (nv & 1);
+    const int nr = np - 1;
+    const double tol = fmax((double)len, 1.0) * 2.220446049250313e-16;
+    const double tol2 = tol * tol;
+    int sweep = 0;
+    for (; sweep < 60; ++sweep) {
+        for (int p = gid; p < nv; p += ng) {
+            const double2* rp = R + p + gl * ldr;
+            double s = 0.0;
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+                if (gl + G * e < len) s += cabs2(rp[e * st]);
+            for (int o = G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(mask, s, o);
+            if (gl == 0) nrm[p] = s;
+        }
+        if (tid == 0) *flag = 0;
+        __syncthreads();
+        for (int r = 0; r < nr; ++r) {
+            for (int pi = gid; pi < np / 2; pi += ng) {
+                const int i1 = np - 1 - pi;
+                int p = 0, q;
+                if (pi != 0) { p = pi - 1 + r; if (p >= nr) p -= nr; ++p; }
+                q = i1 - 1 + r; if (q >= nr) q -= nr; ++q;
+                if (p >= nv || q >= nv) continue;
+                double2* rp = R + p + gl * ldr;
+                double2* rq = R + q + gl * ldr;
+                double2 a[E], b[E];
+                double2 ga = cmk(0.0, 0.0);
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    if (gl + G * e < len) {
+                        a[e] = rp[e * st];
+                        b[e] = rq[e * st];
+                    } else {
+                        a[e] = cmk(0.0, 0.0);
+                        b[e] = cmk(0.0, 0.0);
+                    }
+                    cfma_bj(ga, a[e], b[e]);
+                }
+                for (int o = G >> 1; o > 0; o >>= 1) {
+                    ga.x += __shfl_xor_sync(mask, ga.x, o);
+                    ga.y += __shfl_xor_sync(mask, ga.y, o);
+                }
+                const double al = nrm[p], be = nrm[q];
+                const double g2 = cabs2(ga);
+                if (g2 > tol2 * (al * be) && al > 0.0 && be > 0.0) {
+                    const double ig = rsqrt(g2);
+                    const double gm = g2 * ig;
+                    const double zeta = 0.5 * (be - al) * ig;
+                    const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+                    const double c = rsqrt(fma(t, t, 1.0));
+                    const double sn = c * t;
+                    const double2 ec = cmk(ga.x * ig, ga.y * ig);
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        if (gl + G * e < len) {
+                            const double2 bb = cmul(ec, b[e]);
+                            rp[e * st] = cmk(c * a[e].x - sn * bb.x, c * a[e].y - sn * bb.y);
+                            rq[e * st] = cmk(sn * a[e].x + c * bb.x, sn * a[e].y + c * bb.y);
+                        }
+                    }
+                    if (gl == 0) {
+                        nrm[p] = al - t * gm;
+                        nrm[q] = be + t * gm;
+                        *flag = 1;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if (*flag == 0) break;
+        __syncthreads();
+    }
+    for (int p = gid; p < nv; p += ng) {
+        const double2* rp = R + p + gl * ldr;
+        double s = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+            if (gl + G * e < len) s += cabs2(rp[e * st]);
+        for (int o = G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(mask, s, o);
+        if (gl == 0) nrm[p] = s;
+    }
+    __syncthreads();
+    return sweep;
+}
+
+// dispatch on the vector length (falls back to the generic version beyond 128)
+__device__ inline int jacobi_rows_auto(double2* R, int ldr, int nv, int len, double* nrm, int* flag) {
+    if (len <= 16) return jacobi_rows_t<4, 4>(R, ldr, nv, len, nrm, flag);
+    if (len <= 32) return jacobi_rows_t<8, 4>(R, ldr, nv, len, nrm, flag);
+    if (len <= 64) return jacobi_rows_t<16, 4>(R, ldr, nv, len, nrm, flag);
+    if (len <= 128) return jacobi_rows_t<32, 4>(R, ldr, nv, len, nrm, flag);
+    return cta_jacobi_rows(R, ldr, nv, len, nrm, flag);
+}
+
+// Pivoted QR (see cta_qrcp) for M <= G*E rows: column updates by groups of G lanes holding
+// E elements each (unrolled, column values kept in registers for dot, update and norm).
+template <int G, int E>
+__device__ inline int qrcp_t(double2* B, int ldb, int M, int N, int* piv, double* nrm, double2* sh, int* s_piv,
+                             double rank_rel2) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gl = tid & (G - 1), gid = tid / G, ng = blockDim.x / G;
+    const unsigned mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+    const int K = min(M, N);
+    __shared__ double s_total;
+    __syncthreads();  // B was just written by the caller
+    for (int c = tid; c < N; c += blockDim.x) piv[c] = c;
+    for (int c = gid; c < N; c += ng) {
+        const double2* bc = B + c * ldb + gl;
+        double s = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+            if (gl + G * e < M) s += cabs2(bc[G * e]);
+        for (int o = G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(mask, s, o);
+        if (gl == 0) nrm[c] = s;
+    }
+    __syncthreads();
+    int j = 0;
+    for (; j < K; ++j) {
+        if (warp == 0) {
+            double best = -1.0, rem = 0.0;
+            int bi = j;
+            for (int c = j + lane; c < N; c += 32) {
+                const double v = nrm[c];
+                rem += v;
+                if (v > best) { best = v; bi = c; }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                rem += __shfl_xor_sync(0xffffffffu, rem, o);
+                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+            }
+            const int pc = (rank_rel2 > 0.0 && j > 0 && rem <= rank_rel2 * s_total) ? -1 : bi;
+            // swap columns j <-> pc (warp 0) and form the Householder vector of column j
+            if (lane == 0) {
+                if (j == 0) s_total = rem;
+                *s_piv = pc;
+            }
+            if (pc >= 0) {
+                if (pc != j) {
+                    for (int i = lane; i < M; i += 32) {
+                        const double2 t = B[i + j * ldb];
+                        B[i + j * ldb] = B[i + pc * ldb];
+                        B[i + pc * ldb] = t;
+                    }
+                    if (lane == 0) {
+                        const int t = piv[j]; piv[j] = piv[pc]; piv[pc] = t;
+                        const double v = nrm[j]; nrm[j] = nrm[pc]; nrm[pc] = v;
+                    }
+                }
+                __syncwarp();
+                double2* colj = B + j * ldb;
+                double s = 0.0;
+                for (int i = j + 1 + lane; i < M; i += 32) s += cabs2(colj[i]);
+                s = warp_sum(s);
+                if (lane == 0) {
+                    const double2 alpha = colj[j];
+                    double tau = 0.0;
+                    double2 beta = alpha;
+                    if (s > 0.0) {
+                        const double aa = sqrt(cabs2(alpha));
+                        const double xn = sqrt(s + aa * aa);
+                        const double2 ph = aa > 0.0 ? cscale(alpha, 1.0 / aa) : cmk(1.0, 0.0);
+                        beta = cscale(ph, -xn);
+                        colj[j] = cscale(ph, aa + xn);
+                        tau = 1.0 / (xn * (xn + aa));
+                    }
+                    sh[0] = beta;
+                    sh[1] = cmk(tau, 0.0);
+                }
+            }
+        }
+        __syncthreads();
+        if (*s_piv < 0) break;
+        const double tau = sh[1].x;
+        const double2* colj = B + j * ldb;
+        double2 u[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int i = gl + G * e;
+            u[e] = (i >= j && i < M) ? colj[i] : cmk(0.0, 0.0);
+        }
+        for (int c = j + 1 + gid; c < N; c += ng) {
+            double2* bc = B + c * ldb;
+            double2 x[E];
+            double2 w = cmk(0.0, 0.0);
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int i = gl + G * e;
+                x[e] = (i < M) ? bc[i] : cmk(0.0, 0.0);
+                cfma_cj(w, u[e], x[e]);
+            }
+            for (int o = G >> 1; o > 0; o >>= 1) {
+                w.x += __shfl_xor_sync(mask, w.x, o);
+                w.y += __shfl_xor_sync(mask, w.y, o);
+            }
+            w = cscale(w, tau);
+            double s = 0.0;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int i = gl + G * e;
+                if (i >= j && i < M) {
+                    x[e] = csub(x[e], cmul(u[e], w));
+                    bc[i] = x[e];
+                }
+                if (i > j && i < M) s += cabs2(x[e]);
+            }
+            for (int o = G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(mask, s, o);
+            if (gl == 0) nrm[c] = s;
+        }
+        __syncthreads();
+        if (tid == 0) B[j + j * ldb] = sh[0];
+    }
+    __syncthreads();
+    return j;
+}
+
+__device__ inline int qrcp_auto(double2* B, int ldb, int M, int N, int* piv, double* nrm, double2* sh, int* s_piv,
+                                double rank_rel2) {
+    if (M <= 16) return qrcp_t<4, 4>(B, ldb, M, N, piv, nrm, sh, s_piv, rank_rel2);
+    if (M <= 32) return qrcp_t<8, 4>(B, ldb, M, N, piv, nrm, sh, s_piv, rank_rel2);
+    if (M <= 64) return qrcp_t<16, 4>(B, ldb, M, N, piv, nrm, sh, s_piv, rank_rel2);
+    if (M <= 128) return qrcp_t<32, 4>(B, ldb, M, N, piv, nrm, sh, s_piv, rank_rel2);
+    return cta_qrcp(B, ldb, M, N, piv, nrm, sh, s_piv, rank_rel2);
 }
 
 }  // namespace dh2

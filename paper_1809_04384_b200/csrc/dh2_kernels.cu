@@ -212,97 +212,6 @@ __device__ inline void zero_lower(double2* A, int lda, int rows, int cols) {
     }
 }
 
-// Basis weights (Eq. 18; [BO10, Alg. 16] generalised to directions):
-// leaf with #t > k: R_tc = R of QR(V_tc); non-leaf: R_tc = R of QR([R_{t1c1} E_{t1c}; R_{t2c2} E_{t2c}]).
-// One CTA per basis pair of one level.
-__global__ void k_basis(PlanD P, const int* bps, int lda) {
-    extern __shared__ double2 sm[];
-    const int bp = bps[blockIdx.x];
-    const int k = P.k, m = P.m;
-    double2* A = sm;
-    double2* Ef = sm + (size_t)lda * k;
-    double2* sh = Ef + 6 * m * m;
-    int rows;
-    if (P.bp_child0[bp] < 0) {
-        const int t = P.bp_t[bp];
-        rows = P.c_size[t];
-        const double2* V = P.V + P.bp_V_off[bp];
-        for (int idx = threadIdx.x; idx < rows * k; idx += blockDim.x) A[idx % rows + (size_t)(idx / rows) * lda] = V[idx];
-        __syncthreads();
-    } else {
-        int c0 = P.bp_child0[bp], c1 = P.bp_child1[bp];
-        int r0 = P.bp_R_rows[c0], r1 = P.bp_R_rows[c1];
-        const double2* R0 = P.R + P.bp_R_off[c0];
-        const double2* R1 = P.R + P.bp_R_off[c1];
-        for (int idx = threadIdx.x; idx < r0 * k; idx += blockDim.x) A[idx % r0 + (size_t)(idx / r0) * lda] = R0[idx];
-        for (int idx = threadIdx.x; idx < r1 * k; idx += blockDim.x) A[r0 + idx % r1 + (size_t)(idx / r1) * lda] = R1[idx];
-        const double2* Eg = P.E + P.bp_E_off[bp];
-        for (int idx = threadIdx.x; idx < 6 * m * m; idx += blockDim.x) Ef[idx] = Eg[idx];
-        __syncthreads();
-        kron_apply(A, lda, r0, m, Ef, false);
-        kron_apply(A + r0, lda, r1, m, Ef + 3 * m * m, false);
-        rows = r0 + r1;
-    }
-    const int out = P.bp_R_rows[bp];
-    if (rows > k) {
-        cta_qr(A, lda, rows, k, sh);
-        zero_lower(A, lda, k, k);
-        __syncthreads();
-    }
-    double2* R = P.R + P.bp_R_off[bp];
-    for (int idx = threadIdx.x; idx < out * k; idx += blockDim.x) R[idx] = A[idx % out + (size_t)(idx / out) * lda];
-}
-
-void launch_basis(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStream_t s) {
-    if (!nbps) return;
-    int lda = odd_ld(maxrows);
-    size_t sm = ((size_t)lda * P.k + 6 * P.m * P.m + 2) * sizeof(double2);
-    k_basis<<<nbps, 256, sm, s>>>(P, bps, lda);
-}
-
-// Block weights (DESIGN reading Q12): ||G_b||_F^2 = ||R_tc S_b R_sc^*||_F^2 (W = P R, Eq. 18);
-// w_b = 1/||G_b||_F for the block-relative modes, 1 for FROB_CLUSTERREL.  CTA per block.
-__global__ void k_block_weights(PlanD P, int mode, int ldu) {
-    extern __shared__ double2 sm[];
-    __shared__ double red[32];
-    const int b = blockIdx.x, k = P.k;
-    const int bt = P.blk_bprow[b], bs = P.blk_bpcol[b];
-    const int rt = P.bp_R_rows[bt], rs = P.bp_R_rows[bs];
-    const double2* Rt = P.R + P.bp_R_off[bt];
-    const double2* Rs = P.R + P.bp_R_off[bs];
-    const double2* S = P.S + (size_t)b * k * k;
-    double2* U = sm;  // rt x k
-    for (int idx = threadIdx.x; idx < rt * k; idx += blockDim.x) {
-        int i = idx % rt, nu = idx / rt;
-        double2 acc = cmk(0.0, 0.0);
-        for (int mu = 0; mu < k; ++mu) cfma(acc, Rt[i + (size_t)mu * rt], S[mu + (size_t)nu * k]);
-        U[i + (size_t)nu * ldu] = acc;
-    }
-    __syncthreads();
-    double part = 0.0;
-    for (int idx = threadIdx.x; idx < rt * rs; idx += blockDim.x) {
-        int i = idx % rt, j = idx / rt;
-        double2 acc = cmk(0.0, 0.0);
-        for (int nu = 0; nu < k; ++nu) cfma_bj(acc, U[i + (size_t)nu * ldu], Rs[j + (size_t)nu * rs]);
-        part += cabs2(acc);
-    }
-    part = warp_sum(part);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-        P.normG2[b] = s;
-        P.omega[b] = (mode == 1) ? 1.0 : 1.0 / sqrt(s);
-    }
-}
-
-void launch_block_weights(const PlanD& P, int mode, cudaStream_t s) {
-    if (!P.nblk) return;
-    int ldu = odd_ld(P.k);
-    size_t sm = (size_t)ldu * P.k * sizeof(double2);
-    k_block_weights<<<P.nblk, 256, sm, s>>>(P, mode, ldu);
-}
 
 // Annihilate the nb x k chunk B into the k x k upper-triangular smem matrix R:
 // [R; B] = Q [R'; 0] by k structured Householder reflections, each touching row j of R and
@@ -394,6 +303,123 @@ __device__ inline void chunk_gemm_S(const double2* X, int rx, int i0, int nb, co
             B[i + (size_t)nu * ldb] = cscale(acc, w);
         }
     }
+}
+
+// Basis weights (Eq. 18; [BO10, Alg. 16] generalised to directions), one CTA per
+// basis pair of one level: leaf with #t > k: R_tc = R of QR(V_tc); non-leaf:
+// R_tc = R of QR([R_{t1c1} E_{t1c}; R_{t2c2} E_{t2c}]).  Rows are streamed in chunks of <= 32,
+// transformed by the Kronecker-factored E and annihilated into a k x k triangle (structured
+// Householder); if the stack has <= k rows it is the weight itself (P = I) and is written out.
+__global__ void k_basis(PlanD P, const int* bps, int ldr, int ldb) {
+    extern __shared__ double2 sm[];
+    __shared__ double2 sh[3];
+    const int bp = bps[blockIdx.x];
+    const int k = P.k, m = P.m;
+    const int CH = 32;
+    double2* R = sm;                      // k x k (QR case only)
+    double2* B = R + (size_t)ldr * k;     // CH x k chunk
+    double2* Ef = B + (size_t)ldb * k;    // 6 m^2
+    const bool leaf = P.bp_child0[bp] < 0;
+    int src_bp[2] = {bp, -1};
+    int nsrc = 1, total;
+    if (leaf) {
+        total = P.c_size[P.bp_t[bp]];
+    } else {
+        src_bp[0] = P.bp_child0[bp];
+        src_bp[1] = P.bp_child1[bp];
+        nsrc = 2;
+        total = P.bp_R_rows[src_bp[0]] + P.bp_R_rows[src_bp[1]];
+        const double2* Eg = P.E + P.bp_E_off[bp];
+        for (int idx = threadIdx.x; idx < 6 * m * m; idx += blockDim.x) Ef[idx] = Eg[idx];
+    }
+    const bool qr = total > k;
+    double2* Rout = P.R + P.bp_R_off[bp];
+    const int out = P.bp_R_rows[bp];
+    if (qr)
+        for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) R[idx % k + (size_t)(idx / k) * ldr] = cmk(0.0, 0.0);
+    int cur = 0;
+    for (int sidx = 0; sidx < nsrc; ++sidx) {
+        const int r = leaf ? total : P.bp_R_rows[src_bp[sidx]];
+        const double2* X = leaf ? (P.V + P.bp_V_off[bp]) : (P.R + P.bp_R_off[src_bp[sidx]]);
+        for (int i0 = 0; i0 < r; i0 += CH) {
+            const int nb = min(CH, r - i0);
+            __syncthreads();
+            for (int idx = threadIdx.x; idx < nb * k; idx += blockDim.x)
+                B[idx % nb + (size_t)(idx / nb) * ldb] = X[i0 + idx % nb + (size_t)(idx / nb) * r];
+            __syncthreads();
+            if (!leaf) kron_apply(B, ldb, nb, m, Ef + sidx * 3 * m * m, false);
+            if (qr) {
+                cta_qr_append(R, ldr, B, ldb, nb, k, sh);
+            } else {
+                for (int idx = threadIdx.x; idx < nb * k; idx += blockDim.x)
+                    Rout[cur + idx % nb + (size_t)(idx / nb) * out] = B[idx % nb + (size_t)(idx / nb) * ldb];
+                cur += nb;
+            }
+        }
+    }
+    if (qr) {
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) {
+            const int i = idx % k, nu = idx / k;
+            Rout[idx] = (i > nu) ? cmk(0.0, 0.0) : R[i + (size_t)nu * ldr];
+        }
+    }
+}
+
+void launch_basis(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStream_t s) {
+    if (!nbps) return;
+    const int ldr = odd_ld(P.k), ldb = odd_ld(32);
+    const bool any_qr = maxrows > P.k;
+    size_t sm = ((any_qr ? (size_t)ldr * P.k : 0) + (size_t)ldb * P.k + 6 * P.m * P.m) * sizeof(double2);
+    k_basis<<<nbps, 256, sm, s>>>(P, bps, any_qr ? ldr : 0, ldb);
+}
+
+// Block weights (DESIGN reading R12): ||G_b||_F^2 = ||R_tc S_b R_sc^*||_F^2 (W = P R, Eq. 18);
+// w_b = 1/||G_b||_F for the block-relative modes, 1 for FROB_CLUSTERREL.  CTA per block:
+// U = R_tc S_b (register-blocked, S read coalesced through the mirror block), then
+// ||U R_sc^*||_F^2 with a fixed-order reduction.
+__global__ void k_block_weights(PlanD P, int mode, int ldu, const int* mirror) {
+    extern __shared__ double2 sm[];
+    __shared__ double red[32];
+    const int b = blockIdx.x, k = P.k;
+    const int bt = P.blk_bprow[b], bs = P.blk_bpcol[b];
+    const int rt = P.bp_R_rows[bt], rs = P.bp_R_rows[bs];
+    const double2* Rt = P.R + P.bp_R_off[bt];
+    const double2* Rs = P.R + P.bp_R_off[bs];
+    const int mb = mirror[b];
+    const double2* Sg = P.S + (size_t)(mb >= 0 ? mb : b) * k * k;
+    double2* U = sm;  // rt x k
+    chunk_gemm_S(Rt, rt, 0, rt, Sg, false, mb < 0, 1.0, k, U, ldu);
+    __syncthreads();
+    double part = 0.0;
+    const int tj = (rs + 1) / 2;
+    for (int tile = threadIdx.x; tile < rt * tj; tile += blockDim.x) {
+        const int i = tile % rt, j0 = (tile / rt) * 2;
+        double2 a0 = cmk(0.0, 0.0), a1 = cmk(0.0, 0.0);
+        const bool two = j0 + 1 < rs;
+        for (int nu = 0; nu < k; ++nu) {
+            const double2 u = U[i + (size_t)nu * ldu];
+            cfma_bj(a0, u, Rs[j0 + (size_t)nu * rs]);
+            if (two) cfma_bj(a1, u, Rs[j0 + 1 + (size_t)nu * rs]);
+        }
+        part += cabs2(a0) + cabs2(a1);
+    }
+    part = warp_sum(part);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sum = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) sum += red[w];
+        P.normG2[b] = sum;
+        P.omega[b] = (mode == 1) ? 1.0 : 1.0 / sqrt(sum);
+    }
+}
+
+void launch_block_weights(const PlanD& P, int mode, const int* mirror, cudaStream_t s) {
+    if (!P.nblk) return;
+    int ldu = odd_ld(P.k);
+    size_t sm = (size_t)ldu * P.k * sizeof(double2);
+    k_block_weights<<<P.nblk, 256, sm, s>>>(P, mode, ldu, mirror);
 }
 
 // Total weights, one CTA per pair of one level (top-down):
@@ -541,18 +567,39 @@ __global__ void __launch_bounds__(128) k_truncate(PlanD P, PassD X, int p0, int 
         }
         return;
     }
-    // B = M^* = Zhat Vt^*  (zr x rowsM)
-    for (int idx = threadIdx.x; idx < zr * rowsM; idx += blockDim.x) {
-        int j = idx % zr, i = idx / zr;
-        double2 acc = cmk(0.0, 0.0);
-        for (int nu = 0; nu < k; ++nu) cfma_bj(acc, Z[j + (size_t)nu * zr], Vt[i + (size_t)nu * ldvt]);
-        B[j + (size_t)i * ldb] = acc;
+    // B = M^* = Zhat Vt^*  (zr x rowsM), 4 x 4 register tiles
+    {
+        const int tj = (zr + 3) / 4, ti = (rowsM + 3) / 4;
+        for (int tile = threadIdx.x; tile < tj * ti; tile += blockDim.x) {
+            const int j0 = (tile % tj) * 4, i0 = (tile / tj) * 4;
+            double2 acc[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] = cmk(0.0, 0.0);
+            for (int nu = 0; nu < k; ++nu) {
+                double2 zv[4], vv[4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) zv[a] = (j0 + a < zr) ? Z[j0 + a + (size_t)nu * zr] : cmk(0.0, 0.0);
+#pragma unroll
+                for (int b = 0; b < 4; ++b) vv[b] = (i0 + b < rowsM) ? Vt[i0 + b + (size_t)nu * ldvt] : cmk(0.0, 0.0);
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) cfma_bj(acc[a][b], zv[a], vv[b]);
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    if (j0 + a < zr && i0 + b < rowsM) B[j0 + a + (size_t)(i0 + b) * ldb] = acc[a][b];
+        }
     }
-    cta_qrcp(B, ldb, zr, rowsM, piv, nrm, sh, &s_piv);
-    const int ncol = min(zr, rowsM);
+    // pivoted QR, stopped at the numerical rank (trailing ||.||_F <= 1e-15 ||M||_F)
+    const int ncol = qrcp_auto(B, ldb, zr, rowsM, piv, nrm, sh, &s_piv, 1e-30);
     zero_lower(B, ldb, ncol, rowsM);  // drop the Householder vectors below the diagonal of R
     __syncthreads();
-    const int nsw = cta_jacobi_rows(B, ldb, ncol, rowsM, nrm, &flag);
+    const int nsw = jacobi_rows_auto(B, ldb, ncol, rowsM, nrm, &flag);
     if (threadIdx.x == 0) X.sweeps[p] = nsw;
     // singular values = norms of the rows of R; order by decreasing value (ties: lower index)
     for (int j = threadIdx.x; j < ncol; j += blockDim.x) {

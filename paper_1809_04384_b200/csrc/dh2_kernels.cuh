@@ -88,7 +88,7 @@ void launch_E(const PlanD& P, const int* bps, int nbps, cudaStream_t s);
 void launch_S(const PlanD& P, cudaStream_t s);
 // recompression (§3.2)
 void launch_basis(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStream_t s);
-void launch_block_weights(const PlanD& P, int mode, cudaStream_t s);
+void launch_block_weights(const PlanD& P, int mode, const int* mirror, cudaStream_t s);
 void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* mirror, cudaStream_t s);
 void launch_truncate(const PlanD& P, bool row, int p0, int np, int maxrowsM, int maxZrows, bool leaf_level, double eps,
                      int mode, cudaStream_t s);

@@ -1,0 +1,61 @@
+// Test-only harness: runs the device building blocks of dh2_device.cuh on batches of small
+// matrices (one CTA per matrix) so tests can compare them with numpy.  Not part of libdh2.so.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../paper_1809_04384_b200/csrc/dh2_device.cuh"
+
+using namespace dh2;
+
+// op: 0 = cta_qr (R), 1 = cta_qrcp (R, piv), 2 = qrcp_auto (R, piv), 3 = cta_jacobi_rows on the
+// rows of the input, 4 = jacobi_rows_auto on the rows of the input.
+__global__ void k_devtest(int op, const double2* in, double2* out, int* iout, double* dout, int M, int N, int ld) {
+    extern __shared__ double2 smem[];
+    __shared__ double2 sh[4];
+    __shared__ int s_piv, flag;
+    double2* A = smem;
+    double* nrm = reinterpret_cast<double*>(A + (size_t)ld * N);
+    int* piv = reinterpret_cast<int*>(nrm + N + M);
+    const double2* X = in + (size_t)blockIdx.x * M * N;
+    for (int idx = threadIdx.x; idx < M * N; idx += blockDim.x) A[idx % M + (idx / M) * ld] = X[idx];
+    __syncthreads();
+    int res = 0;
+    if (op == 0) cta_qr(A, ld, M, N, sh);
+    if (op == 1) res = cta_qrcp(A, ld, M, N, piv, nrm, sh, &s_piv, 0.0);
+    if (op == 2) res = qrcp_auto(A, ld, M, N, piv, nrm, sh, &s_piv, 0.0);
+    if (op == 3) res = cta_jacobi_rows(A, ld, M, N, nrm, &flag);
+    if (op == 4) res = jacobi_rows_auto(A, ld, M, N, nrm, &flag);
+    if (op == 5) res = cta_qrcp(A, ld, M, N, piv, nrm, sh, &s_piv, 1e-30);
+    if (op == 6) res = qrcp_auto(A, ld, M, N, piv, nrm, sh, &s_piv, 1e-30);
+    __syncthreads();
+    double2* Y = out + (size_t)blockIdx.x * M * N;
+    for (int idx = threadIdx.x; idx < M * N; idx += blockDim.x) Y[idx] = A[idx % M + (idx / M) * ld];
+    if (threadIdx.x == 0) iout[(size_t)blockIdx.x * (N + 1)] = res;
+    for (int c = threadIdx.x; c < N; c += blockDim.x) iout[(size_t)blockIdx.x * (N + 1) + 1 + c] = (op == 1 || op == 2 || op >= 5) ? piv[c] : 0;
+    for (int c = threadIdx.x; c < M; c += blockDim.x) dout[(size_t)blockIdx.x * M + c] = (op == 3 || op == 4) ? nrm[c] : 0.0;
+}
+
+extern "C" int devtest_run(int op, const double* in, double* out, int* iout, double* dout, int batch, int M, int N,
+                           int threads) {
+    int ld = (M | 1);
+    size_t sm = (size_t)ld * N * sizeof(double2) + (size_t)(N + M) * sizeof(double) + (size_t)(N + M) * sizeof(int) + 64;
+    double2 *din, *dout2;
+    int* di;
+    double* dd;
+    size_t nb = (size_t)batch * M * N * sizeof(double2);
+    if (cudaMalloc(&din, nb) || cudaMalloc(&dout2, nb) || cudaMalloc(&di, (size_t)batch * (N + 1) * sizeof(int)) ||
+        cudaMalloc(&dd, (size_t)batch * M * sizeof(double)))
+        return -1;
+    cudaMemcpy(din, in, nb, cudaMemcpyHostToDevice);
+    cudaFuncSetAttribute(k_devtest, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    k_devtest<<<batch, threads, sm>>>(op, din, dout2, di, dd, M, N, ld);
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(out, dout2, nb, cudaMemcpyDeviceToHost);
+    cudaMemcpy(iout, di, (size_t)batch * (N + 1) * sizeof(int), cudaMemcpyDeviceToHost);
+    cudaMemcpy(dout, dd, (size_t)batch * M * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(din);
+    cudaFree(dout2);
+    cudaFree(di);
+    cudaFree(dd);
+    return e == cudaSuccess ? 0 : -2;
+}

@@ -1,0 +1,137 @@
+"""Unit tests of the device building blocks (QR, pivoted QR, one-sided Jacobi) against numpy,
+through a test-only CUDA harness (tests/cuda/devtest.cu) built with the same flags."""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "cuda", "devtest.cu")
+LIB = os.path.join(HERE, "cuda", "libdevtest.so")
+
+
+@pytest.fixture(scope="module")
+def dev():
+    hdr = os.path.join(HERE, "..", "paper_1809_04384_b200", "csrc", "dh2_device.cuh")
+    if not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(SRC), os.path.getmtime(hdr)):
+        subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-shared",
+                        "-Xcompiler", "-fPIC", "-o", LIB, SRC], check=True)
+    lib = ctypes.CDLL(LIB)
+    lib.devtest_run.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+    return lib
+
+
+def run(lib, op, A, threads=128):
+    batch, M, N = A.shape
+    a = np.ascontiguousarray(A.transpose(0, 2, 1)).astype(np.complex128)  # column-major per matrix
+    out = np.empty_like(a)
+    iout = np.empty(batch * (N + 1), dtype=np.int32)
+    dout = np.empty(batch * M, dtype=np.float64)
+    rc = lib.devtest_run(op, a.ctypes.data, out.ctypes.data, iout.ctypes.data, dout.ctypes.data, batch, M, N, threads)
+    assert rc == 0
+    return out.transpose(0, 2, 1), iout.reshape(batch, N + 1), dout.reshape(batch, M)
+
+
+def graded(rng, batch, M, N, decay):
+    U = np.linalg.qr(rng.normal(size=(batch, M, M)) + 1j * rng.normal(size=(batch, M, M)))[0]
+    V = np.linalg.qr(rng.normal(size=(batch, N, N)) + 1j * rng.normal(size=(batch, N, N)))[0]
+    k = min(M, N)
+    s = decay ** np.arange(k)
+    S = np.zeros((batch, M, N))
+    S[:, np.arange(k), np.arange(k)] = s
+    return U @ S @ V.conj().transpose(0, 2, 1), s
+
+
+@pytest.mark.parametrize("M,N", [(5, 3), (27, 5), (52, 32), (64, 64), (100, 64), (128, 64)])
+@pytest.mark.parametrize("op", [0, 1, 2])
+def test_qr_variants(dev, op, M, N):
+    rng = np.random.default_rng(M * 100 + N)
+    A = rng.normal(size=(6, M, N)) + 1j * rng.normal(size=(6, M, N))
+    out, iout, _ = run(dev, op, A)
+    K = min(M, N)
+    for b in range(6):
+        R = np.triu(out[b][:K])
+        piv = iout[b, 1:] if op else np.arange(N)
+        Ap = A[b][:, piv]
+        assert sorted(piv.tolist()) == list(range(N))
+        G = Ap.conj().T @ Ap
+        assert np.abs(R.conj().T @ R - G).max() <= 1e-13 * np.abs(G).max()
+        if op:  # pivoting makes |r_jj| non-increasing
+            d = np.abs(np.diag(R))
+            assert np.all(d[1:] <= d[:-1] * (1 + 1e-12))
+
+
+@pytest.mark.parametrize("nv,L", [(2, 3), (5, 5), (5, 12), (14, 20), (32, 32), (20, 64), (32, 100)])
+@pytest.mark.parametrize("op", [3, 4])
+def test_jacobi_rows(dev, op, nv, L):
+    rng = np.random.default_rng(nv * 1000 + L)
+    X, s = graded(rng, 5, nv, L, 0.3)
+    out, iout, dout = run(dev, op, X)
+    for b in range(5):
+        Y = out[b]
+        # rows mutually orthogonal, row space preserved, norms = singular values
+        G = Y @ Y.conj().T
+        off = G - np.diag(np.diag(G))
+        assert np.abs(off).max() <= 1e-14 * np.abs(G).max() * nv
+        sv = np.sort(np.sqrt(np.real(np.diag(G))))[::-1]
+        ref = np.linalg.svd(X[b], compute_uv=False)
+        assert np.abs(sv - ref).max() <= 1e-13 * ref[0]
+        assert np.allclose(np.sort(np.sqrt(dout[b][:nv]))[::-1], ref, rtol=0, atol=1e-13 * ref[0])
+
+
+@pytest.mark.parametrize("M,N", [(27, 13), (16, 14), (52, 32), (64, 64)])
+@pytest.mark.parametrize("op", [5, 6])
+def test_qrcp_rank_stop(dev, op, M, N):
+    """With the numerical-rank stop enabled, full-rank graded matrices are factorised completely,
+    and an exactly rank-r matrix stops at r with the leading rows exact."""
+    rng = np.random.default_rng(7)
+    A, s = graded(rng, 4, M, N, 0.6)
+    out, iout, _ = run(dev, op, A)
+    K = min(M, N)
+    assert np.all(iout[:, 0] == K), iout[:, 0]
+    r = 5
+    B = A[:, :, :r] @ (rng.normal(size=(4, r, N)) + 1j * rng.normal(size=(4, r, N)))
+    out, iout, _ = run(dev, op, B)
+    assert np.all(iout[:, 0] <= r + 1), iout[:, 0]
+    for b in range(4):
+        k = iout[b, 0]
+        R = np.triu(out[b][:k])
+        Bp = B[b][:, iout[b, 1:]]
+        G = Bp.conj().T @ Bp
+        assert np.abs(R.conj().T @ R - G).max() <= 1e-12 * np.abs(G).max()
+
+
+@pytest.mark.parametrize("op", [5, 6])
+def test_qrcp_on_oracle_truncation_matrices(dev, op):
+    """M^* = Zhat Vhat^* of every non-leaf row pair of P1 (from the oracle): the rank-stopped
+    pivoted QR keeps R^*R = (M^* Pi)^*(M^* Pi) up to the dropped trailing block."""
+    from conftest import oracle_run
+    rc = oracle_run("P1")
+    st, ct = rc.st, rc.st.ct
+    mats = []
+    for l in st.active_levels:
+        for (t, c) in st.row_pairs[l]:
+            if ct.is_leaf(t):
+                continue
+            c2 = st.sd(l, c)
+            Vh = np.vstack([rc.row.C[(int(ch), c2)] @ rc.E(int(ch), c) for ch in ct.children[t]])
+            mats.append((Vh @ rc.row.Zhat[(t, c)].conj().T).conj().T)
+    shapes = {}
+    for A in mats:
+        shapes.setdefault(A.shape, []).append(A)
+    for (M, N), As in shapes.items():
+        A = np.stack(As)
+        out, iout, _ = run(dev, op, A)
+        for b in range(len(As)):
+            k = iout[b, 0]
+            R = np.triu(out[b][:k])
+            Ap = A[b][:, iout[b, 1:]]
+            sv = np.linalg.svd(A[b], compute_uv=False)
+            svR = np.linalg.svd(R, compute_uv=False)
+            n = min(len(sv), len(svR))
+            assert np.abs(sv[:n] - svR[:n]).max() <= 1e-13 * sv[0], (M, N, k, sv, svR)
+            assert np.all(sv[n:] <= 1e-14 * sv[0]), (M, N, k, sv)
