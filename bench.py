@@ -226,8 +226,15 @@ def main():
     dom = max(kern.items(), key=lambda kv: kv[1]["ms"])
     dname, d = dom
     achieved = d["flops"] / (d["ms"] * 1e-3) / 1e12 if d["ms"] > 0 else 0.0
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(dname)
+        traffic = tr["bytes_per_launch"] if tr else None
+    except Exception:
+        traffic = None
     roof = {"kernel": dname, "bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-            "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+            "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+            "traffic_note": "DRAM bytes of one full-capture launch (largest level) from profiles/ncu_traffic.json",
             "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (no FP64 entry in MEASURED_PEAKS.json)",
             "share_of_step": d["ms"] / (ms * args.steps) if ms > 0 else None,
             "avg_launch_ms": d["ms"] / max(d["launches"], 1)}
