@@ -115,7 +115,52 @@ __device__ __forceinline__ void lagrange_axis(const GridD& g, int a, int m, cons
 // E = Ez (x) Ey (x) Ex, nu = jx + m jy + m^2 jz (Eq. 10 with separable phase); X occupies
 // rows [0, rows) of the column-major smem matrix X (leading dimension ld).  Ef holds the
 // three m x m factors, Ef[a*m*m + jp*m + j] = E_a[j', j].  Each thread owns whole fibres.
+template <int MM>
+__device__ inline void kron_apply_t(double2* X, int ld, int rows, const double2* Ef, bool adjoint) {
+    constexpr int m2 = MM * MM;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const int stride = a == 0 ? 1 : (a == 1 ? MM : m2);
+        const double2* F = Ef + a * m2;  // factor stays in shared memory (register budget)
+        const int nfib = rows * m2;
+        for (int fb = threadIdx.x; fb < nfib; fb += blockDim.x) {
+            const int i = fb % rows;
+            const int r = fb / rows;
+            const int lo = r % stride, hi = r / stride;
+            double2* xp = X + i + (lo + hi * stride * MM) * ld;
+            double2 in[MM];
+#pragma unroll
+            for (int j = 0; j < MM; ++j) in[j] = xp[j * stride * ld];
+#pragma unroll
+            for (int j = 0; j < MM; ++j) {
+                double2 acc = cmk(0.0, 0.0);
+                if (!adjoint) {
+#pragma unroll
+                    for (int jp = 0; jp < MM; ++jp) cfma(acc, in[jp], F[jp * MM + j]);
+                } else {
+#pragma unroll
+                    for (int jp = 0; jp < MM; ++jp) cfma_bj(acc, in[jp], F[j * MM + jp]);
+                }
+                xp[j * stride * ld] = acc;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__device__ inline void kron_apply_generic(double2* X, int ld, int rows, int m, const double2* Ef, bool adjoint);
+
 __device__ inline void kron_apply(double2* X, int ld, int rows, int m, const double2* Ef, bool adjoint) {
+    switch (m) {
+        case 2: kron_apply_t<2>(X, ld, rows, Ef, adjoint); return;
+        case 3: kron_apply_t<3>(X, ld, rows, Ef, adjoint); return;
+        case 4: kron_apply_t<4>(X, ld, rows, Ef, adjoint); return;
+        case 5: kron_apply_t<5>(X, ld, rows, Ef, adjoint); return;
+        default: kron_apply_generic(X, ld, rows, m, Ef, adjoint); return;
+    }
+}
+
+__device__ inline void kron_apply_generic(double2* X, int ld, int rows, int m, const double2* Ef, bool adjoint) {
     const int k = m * m * m;
     const int m2 = m * m;
     for (int a = 0; a < 3; ++a) {

@@ -213,40 +213,35 @@ __device__ inline void zero_lower(double2* A, int lda, int rows, int cols) {
 }
 
 
-// Annihilate the nb x k chunk B into the k x k upper-triangular smem matrix R:
+// Annihilate the nb x k chunk B (nb <= 32) into the k x k upper-triangular smem matrix R:
 // [R; B] = Q [R'; 0] by k structured Householder reflections, each touching row j of R and
-// the nb rows of B only (the rows of R below j are zero in column j).
+// the nb rows of B only (the rows of R below j are zero in column j).  One barrier per
+// reflection: every warp computes the norm of B[:, j] and the reflector scalars itself; the
+// new diagonal beta_j is stored one step later (nobody reads R[j, j] during step j+1).
 __device__ inline void cta_qr_append(double2* R, int ldr, double2* B, int ldb, int nb, int k, double2* sh) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
     const LaneGroup g = lane_group(group_size_for(nb + 1, 4, 4));
+    (void)sh;
     __syncthreads();
+    int prev = -1;
+    double2 prev_beta = cmk(0.0, 0.0);
     for (int j = 0; j < k; ++j) {
-        double2* bj = B + (size_t)j * ldb;
-        if (warp == 0) {
-            double s = 0.0;
-            for (int i = lane; i < nb; i += 32) s += cabs2(bj[i]);
-            s = warp_sum(s);
-            if (lane == 0) {
-                double2 alpha = R[j + (size_t)j * ldr];
-                double tau = 0.0;
-                double2 beta = alpha, u0 = cmk(0.0, 0.0);
-                if (s > 0.0) {
-                    double aa = sqrt(cabs2(alpha));
-                    double xn = sqrt(s + aa * aa);
-                    double2 ph = aa > 0.0 ? cscale(alpha, 1.0 / aa) : cmk(1.0, 0.0);
-                    beta = cscale(ph, -xn);
-                    u0 = cscale(ph, aa + xn);
-                    tau = 1.0 / (xn * (xn + aa));
-                }
-                sh[0] = beta;
-                sh[1] = cmk(tau, 0.0);
-                sh[2] = u0;
-            }
+        if (tid == 0 && prev >= 0) R[prev + (size_t)prev * ldr] = prev_beta;
+        const double2* bj = B + (size_t)j * ldb;
+        double s = (lane < nb) ? cabs2(bj[lane]) : 0.0;
+        s = warp_sum(s);
+        const double2 alpha = R[j + (size_t)j * ldr];
+        double tau = 0.0;
+        double2 beta = alpha, u0 = cmk(0.0, 0.0);
+        if (s > 0.0) {
+            const double aa = sqrt(cabs2(alpha));
+            const double xn = sqrt(s + aa * aa);
+            const double2 ph = aa > 0.0 ? cscale(alpha, 1.0 / aa) : cmk(1.0, 0.0);
+            beta = cscale(ph, -xn);
+            u0 = cscale(ph, aa + xn);
+            tau = 1.0 / (xn * (xn + aa));
         }
-        __syncthreads();
-        const double tau = sh[1].x;
         if (tau != 0.0) {
-            const double2 u0 = sh[2];
             for (int c = j + 1 + g.gid; c < k; c += g.ng) {
                 double2* bc = B + (size_t)c * ldb;
                 double2 w = cmk(0.0, 0.0);
@@ -257,9 +252,72 @@ __device__ inline void cta_qr_append(double2* R, int ldr, double2* B, int ldb, i
                 for (int i = g.gl; i < nb; i += g.G) bc[i] = csub(bc[i], cmul(bj[i], w));
             }
         }
+        prev = j;
+        prev_beta = beta;
         __syncthreads();
-        if (tid == 0) R[j + (size_t)j * ldr] = sh[0];
     }
+    if (tid == 0 && prev >= 0) R[prev + (size_t)prev * ldr] = prev_beta;
+    __syncthreads();
+}
+
+// Same as cta_qr_append for nb <= 32 with compile-time lane groups: 16 lanes per column,
+// 2 rows of B per lane (rows gl and gl+16) plus row j of R on lane 0.
+__device__ inline void cta_qr_append32(double2* R, int ldr, double2* B, int ldb, int nb, int k) {
+    constexpr int G = 16;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int gl = tid & (G - 1), gid = tid / G, ng = blockDim.x / G;
+    const unsigned mask = 0xffffu << (lane & 16);
+    const bool r0 = gl < nb, r1 = gl + G < nb;
+    __syncthreads();
+    int prev = -1;
+    double2 prev_beta = cmk(0.0, 0.0);
+    for (int j = 0; j < k; ++j) {
+        if (tid == 0 && prev >= 0) R[prev + prev * ldr] = prev_beta;
+        const double2* bj = B + j * ldb;
+        double s = (lane < nb) ? cabs2(bj[lane]) : 0.0;
+        s = warp_sum(s);
+        const double2 alpha = R[j + j * ldr];
+        double tau = 0.0;
+        double2 beta = alpha, u0 = cmk(0.0, 0.0);
+        if (s > 0.0) {
+            const double aa = sqrt(cabs2(alpha));
+            const double xn = sqrt(s + aa * aa);
+            const double2 ph = aa > 0.0 ? cscale(alpha, 1.0 / aa) : cmk(1.0, 0.0);
+            beta = cscale(ph, -xn);
+            u0 = cscale(ph, aa + xn);
+            tau = 1.0 / (xn * (xn + aa));
+        }
+        if (tau != 0.0) {
+            const double2 ua = r0 ? bj[gl] : cmk(0.0, 0.0);
+            const double2 ub = r1 ? bj[gl + G] : cmk(0.0, 0.0);
+            for (int c = j + 1 + gid; c < k; c += ng) {
+                double2* bc = B + c * ldb;
+                const double2 xa = r0 ? bc[gl] : cmk(0.0, 0.0);
+                const double2 xb = r1 ? bc[gl + G] : cmk(0.0, 0.0);
+                double2 rj = cmk(0.0, 0.0);
+                double2 w = cmk(0.0, 0.0);
+                if (gl == 0) {
+                    rj = R[j + c * ldr];
+                    cfma_cj(w, u0, rj);
+                }
+                cfma_cj(w, ua, xa);
+                cfma_cj(w, ub, xb);
+#pragma unroll
+                for (int o = G >> 1; o > 0; o >>= 1) {
+                    w.x += __shfl_xor_sync(mask, w.x, o);
+                    w.y += __shfl_xor_sync(mask, w.y, o);
+                }
+                w = cscale(w, tau);
+                if (gl == 0) R[j + c * ldr] = csub(rj, cmul(u0, w));
+                if (r0) bc[gl] = csub(xa, cmul(ua, w));
+                if (r1) bc[gl + G] = csub(xb, cmul(ub, w));
+            }
+        }
+        prev = j;
+        prev_beta = beta;
+        __syncthreads();
+    }
+    if (tid == 0 && prev >= 0) R[prev + prev * ldr] = prev_beta;
     __syncthreads();
 }
 
@@ -274,15 +332,35 @@ __device__ inline void chunk_gemm_S(const double2* X, int rx, int i0, int nb, co
     const int ncg = nthr / k;  // row groups (k divides blockDim for k in {8, 27->no} handled below)
     if (ncg >= 1 && nthr % k == 0) {
         const int nu = threadIdx.x % k, rg = threadIdx.x / k;
+        const int sstep = strided ? 1 : k;                 // distance between consecutive mu
+        const double2* sp = Sg + (strided ? (size_t)nu * k : (size_t)nu);
+        const double sgn = conj_s ? -1.0 : 1.0;
         for (int ib = rg * 8; ib < nb; ib += ncg * 8) {
             double2 acc[8];
 #pragma unroll
             for (int r = 0; r < 8; ++r) acc[r] = cmk(0.0, 0.0);
             const int nr = min(8, nb - ib);
-            for (int mu = 0; mu < k; ++mu) {
-                double2 sv = strided ? Sg[mu + (size_t)nu * k] : Sg[nu + (size_t)mu * k];
-                if (conj_s) sv.y = -sv.y;
-                const double2* xr = X + i0 + ib + (size_t)mu * rx;
+            const double2* xb = X + i0 + ib;
+            int mu = 0;
+            for (; mu + 4 <= k; mu += 4) {
+                double2 sv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    sv[u] = sp[(mu + u) * sstep];
+                    sv[u].y *= sgn;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double2* xr = xb + (size_t)(mu + u) * rx;
+#pragma unroll
+                    for (int r = 0; r < 8; ++r)
+                        if (r < nr) cfma(acc[r], xr[r], sv[u]);
+                }
+            }
+            for (; mu < k; ++mu) {
+                double2 sv = sp[mu * sstep];
+                sv.y *= sgn;
+                const double2* xr = xb + (size_t)mu * rx;
 #pragma unroll
                 for (int r = 0; r < 8; ++r)
                     if (r < nr) cfma(acc[r], xr[r], sv);
@@ -349,7 +427,7 @@ __global__ void k_basis(PlanD P, const int* bps, int ldr, int ldb) {
             __syncthreads();
             if (!leaf) kron_apply(B, ldb, nb, m, Ef + sidx * 3 * m * m, false);
             if (qr) {
-                cta_qr_append(R, ldr, B, ldb, nb, k, sh);
+                cta_qr_append32(R, ldr, B, ldb, nb, k);
             } else {
                 for (int idx = threadIdx.x; idx < nb * k; idx += blockDim.x)
                     Rout[cur + idx % nb + (size_t)(idx / nb) * out] = B[idx % nb + (size_t)(idx / nb) * ldb];
@@ -378,7 +456,7 @@ void launch_basis(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStr
 // w_b = 1/||G_b||_F for the block-relative modes, 1 for FROB_CLUSTERREL.  CTA per block:
 // U = R_tc S_b (register-blocked, S read coalesced through the mirror block), then
 // ||U R_sc^*||_F^2 with a fixed-order reduction.
-__global__ void k_block_weights(PlanD P, int mode, int ldu, const int* mirror) {
+__global__ void __launch_bounds__(256, 3) k_block_weights(PlanD P, int mode, int ldu, const int* mirror) {
     extern __shared__ double2 sm[];
     __shared__ double red[32];
     const int b = blockIdx.x, k = P.k;
@@ -465,7 +543,7 @@ __global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, const int* m
             __syncthreads();
             chunk_gemm_S(Ro, r, i0, nb, Sg, row, strided, w, k, dst, ldd);
             if (qr)
-                cta_qr_append(R, ldr, B, ldb, nb, k, sh);
+                cta_qr_append32(R, ldr, B, ldb, nb, k);
             else
                 cur += nb;
         }
@@ -488,7 +566,7 @@ __global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, const int* m
             __syncthreads();
             kron_apply(dst, ldd, nb, m, Ef, true);  // Zhat_{t+c+} E_{tc+}^*
             if (qr)
-                cta_qr_append(R, ldr, B, ldb, nb, k, sh);
+                cta_qr_append32(R, ldr, B, ldb, nb, k);
             else
                 cur += nb;
         }
