@@ -712,8 +712,13 @@ void run_recompress(dh2_ctx* C, double eps, int mode) {
             for (int p = p0; p < p0 + np; ++p)
                 if (X.child0[p] >= 0) maxrows = std::max(maxrows, X.rank[X.child0[p]] + X.rank[X.child1[p]]);
             int maxz = X.lev_max_zrows[l];
-            bool all_leaf = true;
-            for (int p = p0; p < p0 + np; ++p) all_leaf = all_leaf && X.child0[p] < 0;
+            bool all_leaf = true, any_leaf = false;
+            for (int p = p0; p < p0 + np; ++p) {
+                all_leaf = all_leaf && X.child0[p] < 0;
+                any_leaf = any_leaf || X.child0[p] < 0;
+            }
+            if (any_leaf && !all_leaf)  // median-split trees never mix leaves and inner clusters on a level
+                throw NotImpl("a tree level mixing leaf and non-leaf clusters is not supported by k_truncate");
             C->timed(std::string(row ? "truncate_row@" : "truncate_col@") + std::to_string(l), 1, [&] { launch_truncate(P, row, p0, np, maxrows, maxz, all_leaf, eps, mode, s); });
             CK(cudaMemcpyAsync(X.rank.data() + p0, X.d_rank.p + p0, np * sizeof(int), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));

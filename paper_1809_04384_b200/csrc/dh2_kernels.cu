@@ -593,14 +593,15 @@ void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* m
 //   Jacobi: high relative accuracy, few sweeps; no Gram matrix is formed, DESIGN reading Q13);
 //   rank k_tc by the rule of `mode`, Q = first k_tc vectors (leaf: Q_tc, non-leaf:
 //   Qhat = [F_{t1c}; F_{t2c}]), C_tc = Q^* V_tc or Qhat^* Vhat (Eq. 19).
-__global__ void __launch_bounds__(128) k_truncate(PlanD P, PassD X, int p0, int ldv, int ldb, double eps, int mode) {
+template <bool LEAF>
+__global__ void __launch_bounds__(128, LEAF ? 6 : 4) k_truncate(PlanD P, PassD X, int p0, int ldv, int ldb, double eps, int mode) {
     extern __shared__ double2 sm[];
     __shared__ int flag, s_piv, s_rank;
     __shared__ double2 sh[2];
     const int p = p0 + blockIdx.x;
     const int k = P.k, m = P.m;
     const int bp = X.bp[p];
-    const bool leaf = X.child0[p] < 0;
+    constexpr bool leaf = LEAF;  // one instance per kind of level (all pairs of a level are alike)
     const int zr = X.Z_rows[p];
     const double2* Z = X.Z + X.Z_off[p];
     double2* Vs = sm;                                  // non-leaf Vhat (rowsM x k, ld ldv)
@@ -612,7 +613,7 @@ __global__ void __launch_bounds__(128) k_truncate(PlanD P, PassD X, int p0, int 
     int rowsM;
     const double2* Vt;
     int ldvt;
-    if (leaf) {
+    if constexpr (leaf) {
         rowsM = P.c_size[P.bp_t[bp]];
         Vt = P.V + P.bp_V_off[bp];
         ldvt = rowsM;
@@ -645,32 +646,33 @@ __global__ void __launch_bounds__(128) k_truncate(PlanD P, PassD X, int p0, int 
         }
         return;
     }
-    // B = M^* = Zhat Vt^*  (zr x rowsM), 4 x 4 register tiles
+    // B = M^* = Zhat Vt^*  (zr x rowsM), 2 x 4 register tiles
     {
-        const int tj = (zr + 3) / 4, ti = (rowsM + 3) / 4;
+        constexpr int TJ = 2, TI = 4;
+        const int tj = (zr + TJ - 1) / TJ, ti = (rowsM + TI - 1) / TI;
         for (int tile = threadIdx.x; tile < tj * ti; tile += blockDim.x) {
-            const int j0 = (tile % tj) * 4, i0 = (tile / tj) * 4;
-            double2 acc[4][4];
+            const int j0 = (tile % tj) * TJ, i0 = (tile / tj) * TI;
+            double2 acc[TJ][TI];
 #pragma unroll
-            for (int a = 0; a < 4; ++a)
+            for (int a = 0; a < TJ; ++a)
 #pragma unroll
-                for (int b = 0; b < 4; ++b) acc[a][b] = cmk(0.0, 0.0);
+                for (int b = 0; b < TI; ++b) acc[a][b] = cmk(0.0, 0.0);
             for (int nu = 0; nu < k; ++nu) {
-                double2 zv[4], vv[4];
+                double2 zv[TJ], vv[TI];
 #pragma unroll
-                for (int a = 0; a < 4; ++a) zv[a] = (j0 + a < zr) ? Z[j0 + a + (size_t)nu * zr] : cmk(0.0, 0.0);
+                for (int a = 0; a < TJ; ++a) zv[a] = (j0 + a < zr) ? Z[j0 + a + nu * zr] : cmk(0.0, 0.0);
 #pragma unroll
-                for (int b = 0; b < 4; ++b) vv[b] = (i0 + b < rowsM) ? Vt[i0 + b + (size_t)nu * ldvt] : cmk(0.0, 0.0);
+                for (int b = 0; b < TI; ++b) vv[b] = (i0 + b < rowsM) ? Vt[i0 + b + nu * ldvt] : cmk(0.0, 0.0);
 #pragma unroll
-                for (int a = 0; a < 4; ++a)
+                for (int a = 0; a < TJ; ++a)
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) cfma_bj(acc[a][b], zv[a], vv[b]);
+                    for (int b = 0; b < TI; ++b) cfma_bj(acc[a][b], zv[a], vv[b]);
             }
 #pragma unroll
-            for (int a = 0; a < 4; ++a)
+            for (int a = 0; a < TJ; ++a)
 #pragma unroll
-                for (int b = 0; b < 4; ++b)
-                    if (j0 + a < zr && i0 + b < rowsM) B[j0 + a + (size_t)(i0 + b) * ldb] = acc[a][b];
+                for (int b = 0; b < TI; ++b)
+                    if (j0 + a < zr && i0 + b < rowsM) B[j0 + a + (i0 + b) * ldb] = acc[a][b];
         }
     }
     // pivoted QR, stopped at the numerical rank (trailing ||.||_F <= 1e-15 ||M||_F)
@@ -744,7 +746,10 @@ void launch_truncate(const PlanD& P, bool row, int p0, int np, int maxrowsM, int
     int ldb = odd_ld(max(maxZrows, 1));
     size_t sm = ((leaf_level ? 0 : (size_t)ldv * P.k + 6 * P.m * P.m) + (size_t)ldb * ldv) * sizeof(double2) +
                 (size_t)ldv * (sizeof(double) + 2 * sizeof(int)) + 16;
-    k_truncate<<<np, 128, sm, s>>>(P, row ? P.row : P.col, p0, ldv, ldb, eps, mode);
+    if (leaf_level)
+        k_truncate<true><<<np, 128, sm, s>>>(P, row ? P.row : P.col, p0, ldv, ldb, eps, mode);
+    else
+        k_truncate<false><<<np, 128, sm, s>>>(P, row ? P.row : P.col, p0, ldv, ldb, eps, mode);
 }
 
 // Projection (Lemma Projections): T_b = C_tc S_b, S~_b = T_b C'_sc^*.  CTA per block.
@@ -946,7 +951,8 @@ cudaError_t configure_kernels() {
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     const void* ks[] = {(const void*)k_leafV, (const void*)k_basis, (const void*)k_block_weights,
-                        (const void*)k_total_weights, (const void*)k_truncate, (const void*)k_project};
+                        (const void*)k_total_weights, (const void*)k_truncate<true>, (const void*)k_truncate<false>,
+                        (const void*)k_project};
     for (const void* f : ks) {
         if (e != cudaSuccess) break;
         cudaFuncAttributes a;
