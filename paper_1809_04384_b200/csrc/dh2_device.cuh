@@ -735,4 +735,66 @@ __device__ inline int qrcp_auto(double2* B, int ldb, int M, int N, int* piv, dou
     return cta_qrcp(B, ldb, M, N, piv, nrm, sh, s_piv, rank_rel2);
 }
 
+
+// ------------------------------------------------------------------ FP64 tensor cores (DMMA)
+// D = A B + C for one 8x8x4 f64 tile (mma.sync m8n8k4; SASS DMMA).  Fragments: lane holds
+// A[lane/4][lane%4], B[lane%4][lane/4], C/D[lane/4][2(lane%4)+{0,1}].
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// Complex 8x8 tile accumulator: (re, im) = (re, im) + a * b with 4 real DMMAs.
+struct ZTile {
+    double r0, r1, i0, i1;
+};
+__device__ __forceinline__ void ztile_mma(ZTile& t, double2 a, double2 b) {
+    dmma884(t.r0, t.r1, a.x, b.x);
+    dmma884(t.r0, t.r1, -a.y, b.y);
+    dmma884(t.i0, t.i1, a.x, b.y);
+    dmma884(t.i0, t.i1, a.y, b.x);
+}
+
+// out[i, nu] = w * sum_mu X[i0+i, mu] * op(S)[mu, nu] for i < nb, nu < k, on the FP64 tensor
+// cores.  X: rx x k column-major (global); op(S)[mu, nu] = Sg[nu + mu k] (conjugated if
+// conj_s) or Sg[mu + nu k] if strided.  Requires k % 32 == 0.  Each warp owns one 8-row tile
+// and four 8-column tiles, reusing its A fragment across them.
+__device__ inline void chunk_gemm_S_dmma(const double2* X, int rx, int i0, int nb, const double2* Sg, bool conj_s,
+                                         bool strided, double w, int k, double2* out, int ldo) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int nrt = (nb + 7) >> 3, nct4 = k >> 5;
+    const int ar = lane >> 2, ac = lane & 3;
+    const double sgn = conj_s ? -1.0 : 1.0;
+    for (int task = warp; task < nrt * nct4; task += nw) {
+        const int rt = task % nrt, cq = task / nrt;
+        const int row = rt * 8 + ar;
+        const bool rok = row < nb;
+        ZTile t[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) t[q] = ZTile{0.0, 0.0, 0.0, 0.0};
+        const double2* xa = X + i0 + row;
+        for (int mu = 0; mu < k; mu += 4) {
+            const int mm = mu + ac;
+            const double2 a = rok ? xa[mm * rx] : cmk(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int nu = (cq * 4 + q) * 8 + ar;
+                double2 b = strided ? Sg[mm + nu * k] : Sg[nu + mm * k];
+                b.y *= sgn;
+                ztile_mma(t[q], a, b);
+            }
+        }
+        const int orow = rt * 8 + ar;
+        if (orow < nb) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int oc = (cq * 4 + q) * 8 + 2 * ac;
+                out[orow + oc * ldo] = cmk(w * t[q].r0, w * t[q].i0);
+                out[orow + (oc + 1) * ldo] = cmk(w * t[q].r1, w * t[q].i1);
+            }
+        }
+    }
+}
+
 }  // namespace dh2

@@ -467,7 +467,10 @@ __global__ void __launch_bounds__(256, 3) k_block_weights(PlanD P, int mode, int
     const int mb = mirror[b];
     const double2* Sg = P.S + (size_t)(mb >= 0 ? mb : b) * k * k;
     double2* U = sm;  // rt x k
-    chunk_gemm_S(Rt, rt, 0, rt, Sg, false, mb < 0, 1.0, k, U, ldu);
+    if ((k & 31) == 0)  // FP64 tensor cores (DMMA)
+        chunk_gemm_S_dmma(Rt, rt, 0, rt, Sg, false, mb < 0, 1.0, k, U, ldu);
+    else
+        chunk_gemm_S(Rt, rt, 0, rt, Sg, false, mb < 0, 1.0, k, U, ldu);
     __syncthreads();
     double part = 0.0;
     const int tj = (rs + 1) / 2;
@@ -541,7 +544,10 @@ __global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, const int* m
             double2* dst = qr ? B : R + cur;
             const int ldd = qr ? ldb : ldr;
             __syncthreads();
-            chunk_gemm_S(Ro, r, i0, nb, Sg, row, strided, w, k, dst, ldd);
+            if ((k & 31) == 0)  // FP64 tensor cores (DMMA) for the dense contraction
+                chunk_gemm_S_dmma(Ro, r, i0, nb, Sg, row, strided, w, k, dst, ldd);
+            else
+                chunk_gemm_S(Ro, r, i0, nb, Sg, row, strided, w, k, dst, ldd);
             if (qr)
                 cta_qr_append32(R, ldr, B, ldb, nb, k);
             else

@@ -59,3 +59,23 @@ extern "C" int devtest_run(int op, const double* in, double* out, int* iout, dou
     cudaFree(dd);
     return e == cudaSuccess ? 0 : -2;
 }
+
+// out (nb x k) = w * X (nb x k) * op(S): X and S column-major, conj_s/strided as in the library.
+__global__ void k_devgemm(const double2* X, const double2* S, double2* out, int nb, int k, int conj_s, int strided) {
+    chunk_gemm_S_dmma(X, nb, 0, nb, S, conj_s != 0, strided != 0, 0.5, k, out, nb);
+}
+extern "C" int devtest_gemm(const double* X, const double* S, double* out, int nb, int k, int conj_s, int strided) {
+    double2 *dx, *ds, *dout;
+    cudaMalloc(&dx, (size_t)nb * k * 16);
+    cudaMalloc(&ds, (size_t)k * k * 16);
+    cudaMalloc(&dout, (size_t)nb * k * 16);
+    cudaMemcpy(dx, X, (size_t)nb * k * 16, cudaMemcpyHostToDevice);
+    cudaMemcpy(ds, S, (size_t)k * k * 16, cudaMemcpyHostToDevice);
+    k_devgemm<<<1, 256>>>(dx, ds, dout, nb, k, conj_s, strided);
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(out, dout, (size_t)nb * k * 16, cudaMemcpyDeviceToHost);
+    cudaFree(dx);
+    cudaFree(ds);
+    cudaFree(dout);
+    return e == cudaSuccess ? 0 : -2;
+}

@@ -135,3 +135,25 @@ def test_qrcp_on_oracle_truncation_matrices(dev, op):
             n = min(len(sv), len(svR))
             assert np.abs(sv[:n] - svR[:n]).max() <= 1e-13 * sv[0], (M, N, k, sv, svR)
             assert np.all(sv[n:] <= 1e-14 * sv[0]), (M, N, k, sv)
+
+
+@pytest.mark.parametrize("nb", [1, 8, 13, 32, 64])
+@pytest.mark.parametrize("conj_s,strided", [(1, 0), (0, 0), (0, 1)])
+def test_dmma_gemm(dev, nb, conj_s, strided):
+    """FP64 tensor-core (DMMA) complex GEMM: out = 0.5 X op(S) to 1e-14 relative."""
+    rng = np.random.default_rng(nb * 10 + conj_s + 2 * strided)
+    k = 64
+    X = rng.normal(size=(nb, k)) + 1j * rng.normal(size=(nb, k))
+    S = rng.normal(size=(k, k)) + 1j * rng.normal(size=(k, k))
+    Xc = np.ascontiguousarray(X.T).astype(np.complex128)   # column-major
+    Sc = np.ascontiguousarray(S.T).astype(np.complex128)   # column-major: Sg[i + j k] = S[i, j]
+    out = np.empty(nb * k, dtype=np.complex128)
+    dev.devtest_gemm.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 4
+    assert dev.devtest_gemm(Xc.ctypes.data, Sc.ctypes.data, out.ctypes.data, nb, k, conj_s, strided) == 0
+    got = out.reshape(k, nb).T
+    # op(S)[mu, nu] = Sg[nu + mu k] = S[nu, mu] (transposed), or Sg[mu + nu k] = S[mu, nu] if strided
+    opS = S if strided else S.T
+    if conj_s:
+        opS = opS.conj()
+    ref = 0.5 * X @ opS
+    assert np.abs(got - ref).max() <= 1e-14 * np.abs(ref).max() * 4
