@@ -154,7 +154,8 @@ int dh2_get_stats(const dh2_ctx* ctx, char* buf, int64_t* len);
  * buf (nbytes = size of buf; buf = NULL returns the size in *nbytes).  Names and
  * layouts are listed in DESIGN.md §"Export names" (structure arrays, offsets,
  * and the device pools V, E, S, R, omega, Zhat_row/col, rank_row/col,
- * sigma_row/col, Q_row/col, F_row/col, C_row/col, St). */
+ * sigma_row/col, Q_row/col, F_row/col, C_row/col, St).  "<name>@<offset>:<count>"
+ * exports the element slice [offset, offset + count) of the array. */
 int dh2_export(const dh2_ctx* ctx, const char* name, void* buf, int64_t* nbytes);
 
 /* Release all memory of ctx (NULL is a no-op). */

@@ -858,15 +858,16 @@ struct ExportItem {
     const void* p;
     size_t bytes;
     bool device;
+    size_t elem;
 };
 
 template <typename T>
 ExportItem hv(const std::vector<T>& v) {
-    return {v.data(), v.size() * sizeof(T), false};
+    return {v.data(), v.size() * sizeof(T), false, sizeof(T)};
 }
 template <typename T>
 ExportItem dv(const DevBuf<T>& b) {
-    return {b.p, b.n * sizeof(T), true};
+    return {b.p, b.n * sizeof(T), true, sizeof(T)};
 }
 
 }  // namespace
@@ -1033,7 +1034,19 @@ int dh2_export(const dh2_ctx* C, const char* name, void* buf, int64_t* nbytes) {
         const Structure& S = C->st;
         const ClusterTree& T = S.ct;
         std::string nm(name);
-        ExportItem it{nullptr, 0, false};
+        // optional element slice: "<name>@<offset>:<count>"
+        size_t sl_off = 0, sl_cnt = 0;
+        bool sliced = false;
+        const size_t at = nm.find('@');
+        if (at != std::string::npos) {
+            const size_t colon = nm.find(':', at);
+            if (colon == std::string::npos) throw std::invalid_argument("slice syntax is name@offset:count");
+            sl_off = std::stoull(nm.substr(at + 1, colon - at - 1));
+            sl_cnt = std::stoull(nm.substr(colon + 1));
+            nm = nm.substr(0, at);
+            sliced = true;
+        }
+        ExportItem it{nullptr, 0, false, 1};
         auto pairs_arr = [&](const std::vector<std::vector<Pair>>& P) {
             tmp64.clear();
             for (size_t l = 0; l < P.size(); ++l)
@@ -1116,6 +1129,11 @@ int dh2_export(const dh2_ctx* C, const char* name, void* buf, int64_t* nbytes) {
         else if (nm == "omega") it = dv(C->d_omega);
         else if (nm == "normG2") it = dv(C->d_normG2);
         else throw std::invalid_argument("unknown export name " + nm);
+        if (sliced) {
+            if ((sl_off + sl_cnt) * it.elem > it.bytes) throw std::invalid_argument("export slice out of range for " + nm);
+            it.p = static_cast<const char*>(it.p) + sl_off * it.elem;
+            it.bytes = sl_cnt * it.elem;
+        }
         if (!buf) {
             *nbytes = (int64_t)it.bytes;
             return;

@@ -1,0 +1,120 @@
+"""C3 (BASELINE configs[2]: sphere n = 32768, kappa = 32, m = 4, eps = 1e-5) at full size on the
+GPU, checked on seeded samples of outputs that the oracle computes one by one (oracle/lazy.py:
+the same §3.2 formulas evaluated on the dependency cone of each sampled pair), plus
+properties that hold at any size."""
+import numpy as np
+import pytest
+
+from synth import get_config, mesh_for
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c3():
+    from paper_1809_04384_b200 import DH2
+    from oracle.structure import DH2Structure
+    from oracle.lazy import LazyRecompression
+    cfg = get_config("C3")
+    xyz, tri = mesh_for(cfg)
+    h = DH2(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"])
+    h.recompress(cfg["eps"])
+    st = DH2Structure(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"])
+    yield h, st, LazyRecompression(st, cfg["eps"]), cfg
+    h.close()
+
+
+def _slice(h, name, off, cnt, dtype):
+    return h.export("%s@%d:%d" % (name, off, cnt), dtype)
+
+
+def test_c3_structure_matches(c3):
+    h, st, lz, cfg = c3
+    assert np.array_equal(h.export("blocks", np.int64).reshape(-1, 3), st.blocks)
+    rp = h.export("row_pairs", np.int64).reshape(-1, 3)
+    assert len(rp) == sum(len(p) for p in st.row_pairs)
+
+
+@pytest.mark.parametrize("side", ["row", "col"])
+def test_c3_sampled_pairs(c3, side):
+    """Per level, 12 seeded pairs: singular values (1e-12 sigma_1), ranks, Zhat^*Zhat (1e-11)."""
+    h, st, lz, cfg = c3
+    k = st.k
+    pairs = h.export(side + "_pairs", np.int64).reshape(-1, 3)
+    lev_ptr = h.export("lev_ptr_" + side, np.int32)
+    sig_off = h.export("sig_off_" + side, np.int64)
+    nsig = h.export("nsig_" + side, np.int32)
+    rank = h.export("rank_" + side, np.int32)
+    z_off = h.export("Z_off_" + side, np.int64)
+    z_rows = h.export("Z_rows_" + side, np.int32)
+    rng = np.random.default_rng(11 if side == "row" else 12)
+    checked = 0
+    for l in range(len(lev_ptr) - 1):
+        a, b = lev_ptr[l], lev_ptr[l + 1]
+        if b <= a:
+            continue
+        for p in rng.choice(np.arange(a, b), size=min(12, b - a), replace=False):
+            _, t, c = (int(v) for v in pairs[p])
+            tr = lz.truncate(side, t, c)
+            so = tr["sigma"]
+            sg = _slice(h, "sigma_" + side, sig_off[p], nsig[p], np.float64)
+            n = min(len(so), len(sg))
+            s1 = so[0]
+            assert np.abs(sg[:n] - so[:n]).max(initial=0.0) <= 1e-12 * s1, (side, l, t, c)
+            assert np.all(so[n:] <= 1e-12 * s1)
+            assert rank[p] == tr["rank"], (side, l, t, c)
+            zr = int(z_rows[p])
+            Zg = _slice(h, "Z_" + side, z_off[p], zr * k, np.complex128).reshape(k, zr).T
+            Zo = lz.Zhat(side, t, c)
+            G0 = Zo.conj().T @ Zo
+            assert np.abs(Zg.conj().T @ Zg - G0).max() <= 1e-11 * np.abs(G0).max()
+            checked += 1
+    assert checked >= 50
+
+
+def test_c3_sampled_basis_weights_and_block_norms(c3):
+    h, st, lz, cfg = c3
+    k = st.k
+    bp = h.export("basis_pairs", np.int64).reshape(-1, 3)
+    R_off = h.export("bp_R_off", np.int64)
+    R_rows = h.export("bp_R_rows", np.int32)
+    rng = np.random.default_rng(5)
+    for i in rng.choice(len(bp), size=60, replace=False):
+        _, t, c = (int(v) for v in bp[i])
+        r = int(R_rows[i])
+        Rg = _slice(h, "VR", R_off[i], r * k, np.complex128).reshape(k, r).T
+        Ro = lz.R(t, c)
+        G0 = Ro.conj().T @ Ro
+        assert np.abs(Rg.conj().T @ Rg - G0).max() <= 1e-12 * np.abs(G0).max()
+    g2 = h.export("normG2", np.float64)
+    for b in rng.choice(len(st.blocks), size=60, replace=False):
+        assert abs(np.sqrt(g2[b]) * lz.omega(int(b)) - 1.0) <= 1e-12
+
+
+def test_c3_certified_bound(c3):
+    """Weighted global error sum_b w_b^2 (||G_b||^2 - ||S~_b||^2) <= E_row + E_col, from the GPU's
+    own factors (identity (iii) of DESIGN §5 makes this exact in exact arithmetic)."""
+    h, st, lz, cfg = c3
+    s = h.stats()
+    g2 = h.export("normG2", np.float64)
+    w = h.export("omega", np.float64)
+    st_off = h.export("blk_St_off", np.int64)
+    prow, pcol = h.export("blk_prow", np.int32), h.export("blk_pcol", np.int32)
+    kr, kc = h.export("rank_row", np.int32), h.export("rank_col", np.int32)
+    kbr = h.export("kb_row", np.int32)
+    kbc = h.export("kb_col", np.int32)
+    nb = len(st.blocks)
+    err = 0.0
+    chunk = 4096
+    for b0 in range(0, nb, chunk):
+        b1 = min(nb, b0 + chunk)
+        last = b1 - 1
+        end = st_off[last] + kbr[prow[last]] * kbc[pcol[last]]
+        St = _slice(h, "St", st_off[b0], end - st_off[b0], np.complex128)
+        for b in range(b0, b1):
+            off = st_off[b] - st_off[b0]
+            ld = kbr[prow[b]]
+            m = St[off:off + ld * kc[pcol[b]]].reshape(kc[pcol[b]], ld)[:, :kr[prow[b]]] if ld else np.zeros(0)
+            err += w[b] ** 2 * (g2[b] - np.sum(np.abs(m) ** 2))
+    assert err <= (s["E_row"] + s["E_col"]) * (1 + 1e-6) + 1e-12
+    assert abs(s["E_row"] - s["E_col"]) <= 1e-8 * s["E_row"]  # antipodal symmetry of the problem
