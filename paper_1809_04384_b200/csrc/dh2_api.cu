@@ -143,7 +143,7 @@ struct dh2_ctx {
     std::vector<std::tuple<std::string, cudaEvent_t, cudaEvent_t>> pending;
     std::vector<cudaEvent_t> ev_pool;
     int64_t launches_total = 0;
-    double host_build_ms = 0.0;
+    double host_build_ms = 0.0, host_tables_ms = 0.0;
     double E_row = 0, E_col = 0, far2 = 0;
 
     ~dh2_ctx() {
@@ -903,7 +903,9 @@ int dh2_build_interp(const dh2_mesh* mesh, const dh2_params* params, const dh2_d
         prm.eta1 = p.eta1;
         prm.eta2 = p.eta2;
         C->st.build(mesh->xyz, mesh->nv, mesh->tri, mesh->nt, prm);
+        auto tt = std::chrono::steady_clock::now();
         build_tables(C.get());
+        C->host_tables_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tt).count();
         C->host_build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         if (structure_only) return;
         CK(cudaStreamCreateWithFlags(&C->own_stream, cudaStreamNonBlocking));
@@ -1004,7 +1006,9 @@ int dh2_get_stats(const dh2_ctx* C, char* buf, int64_t* len) {
     o << "{\"n\": " << C->n << ", \"k\": " << C->k << ", \"depth\": " << S.ct.depth
       << ", \"clusters\": " << C->nclusters << ", \"blocks\": " << S.blocks.size() << ", \"near\": " << S.near.size()
       << ", \"row_pairs\": " << nrow << ", \"col_pairs\": " << ncol << ", \"basis_pairs\": " << C->bp_t.size()
-      << ", \"host_build_ms\": " << C->host_build_ms << ", \"launches_total\": " << C->launches_total
+      << ", \"host_build_ms\": " << C->host_build_ms << ", \"host_phases_ms\": {\"tree\": " << S.ms_tree
+      << ", \"dirs\": " << S.ms_dirs << ", \"blocks\": " << S.ms_blocks << ", \"closure\": " << S.ms_closure
+      << ", \"tables\": " << C->host_tables_ms << "}, \"launches_total\": " << C->launches_total
       << ", \"E_row\": " << C->E_row << ", \"E_col\": " << C->E_col << ", \"far2\": " << C->far2
       << ", \"device_bytes\": " << plan_bytes(C) << ", \"mirror_missing\": " << C->mirror_missing << ", \"kernels\": {";
     bool first = true;

@@ -2,6 +2,7 @@
 #include "dh2_host.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <numeric>
 #include <stdexcept>
@@ -249,7 +250,12 @@ void Structure::build(const double* xyz, int64_t nv, const int64_t* tri, int64_t
     (void)nv;
     p = prm;
     k = p.m * p.m * p.m;
+    using clk = std::chrono::steady_clock;
+    auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    auto t0 = clk::now();
     build_tree(xyz, tri, nt);
+    auto t1 = clk::now();
+    ms_tree = ms(t0, t1);
     int L = ct.depth;
     d_level.assign(L + 1, 0.0);
     mdir.assign(L + 1, 0);
@@ -265,7 +271,11 @@ void Structure::build(const double* xyz, int64_t nv, const int64_t* tri, int64_t
     dirs.assign(L + 1, {});
     dirs_ready.assign(L + 1, 0);
     sd_cache.assign(L + 1, {});
+    auto t2 = clk::now();
+    ms_dirs = ms(t1, t2);
     build_blocks();
+    auto t3 = clk::now();
+    ms_blocks = ms(t2, t3);
     row_pairs = closure(true);
     col_pairs = closure(false);
     basis_pairs.assign(L + 1, {});
@@ -280,6 +290,7 @@ void Structure::build(const double* xyz, int64_t nv, const int64_t* tri, int64_t
     // make sure every level that hosts pairs has its direction set materialised
     for (int l = 0; l <= L; ++l)
         if (!basis_pairs[l].empty()) D(l);
+    ms_closure = ms(t3, clk::now());
 }
 
 }  // namespace dh2

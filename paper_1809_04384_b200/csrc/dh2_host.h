@@ -53,6 +53,7 @@ struct Structure {
     std::vector<std::pair<int64_t, int64_t>> near;  // inadmissible leaves L-
     std::vector<std::vector<Pair>> row_pairs, col_pairs, basis_pairs;  // per level, sorted
     int first_level = -1;  // first level with any pair
+    double ms_tree = 0, ms_dirs = 0, ms_blocks = 0, ms_closure = 0;  // host phase timings
 
     void build(const double* xyz, int64_t nv, const int64_t* tri, int64_t nt, const Params& prm);
     const std::vector<double>& D(int level);
