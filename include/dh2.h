@@ -141,6 +141,17 @@ int dh2_storage(const dh2_ctx* ctx, int32_t which, dh2_storage_report* out);
  * context's own stream.  The caller keeps ownership of the stream. */
 int dh2_set_stream(dh2_ctx* ctx, void* cuda_stream);
 
+/* Options (take effect at the next dh2_recompress):
+ *   "adjoint_symmetry" (0 | 1, default 1): derive the column pass from the row pass.  For the
+ *     single-layer operator W = V and, with antipodal direction sets (DESIGN
+ *     readings R2/R4), V_{s,-c} = conj(V_{s,c}) and S_{(s,t,-c)} = S_{(t,s,c)}^T, so the
+ *     column-pass matrices of (s,c) are the complex conjugates of the row-pass
+ *     matrices of (s,-c): Zhat', sigma', k', Q', F', C' follow by conjugation.  Used only if
+ *     dh2_build_interp verified that correspondence on the whole structure (stats key
+ *     "adjoint_symmetry"); otherwise, or with value 0, both passes run.
+ * Errors: DH2_EINVAL for an unknown name or value. */
+int dh2_set_option(dh2_ctx* ctx, const char* name, int64_t value);
+
 /* Profiling: when enabled, every kernel class is bracketed by CUDA events on the
  * context's stream; dh2_get_stats then reports per-class device time. */
 int dh2_set_profiling(dh2_ctx* ctx, int32_t enable);

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <tuple>
 #include <sstream>
 #include <stdexcept>
 #include <string>
@@ -123,6 +124,13 @@ struct dh2_ctx {
     // blocks
     std::vector<int> blk_t, blk_s, blk_dir, blk_bprow, blk_bpcol, blk_prow, blk_pcol, blk_mirror;
     int64_t mirror_missing = 0;
+    // adjoint symmetry: column pair p = (s,c) <-> row pair col2row[p] = (s,-c)
+    std::vector<int> col2row;
+    bool sym_ok = false;     // structure admits it (checked in build_tables)
+    int sym_opt = 1;         // dh2_set_option("adjoint_symmetry")
+    bool sym_used = false;   // the last dh2_recompress derived the column pass from the row pass
+    std::string sym_why;     // why sym_ok is false
+    DevBuf<int> d_col2row;
     std::vector<int64_t> blk_St_off;
     int64_t St_total = 0;
     PassH row, col;
@@ -198,6 +206,70 @@ struct dh2_ctx {
 namespace {
 
 inline uint64_t key(int64_t t, int64_t c) { return ((uint64_t)t << 32) | (uint64_t)c; }
+
+// Adjoint symmetry of the single-layer DH^2 (W = V; column pass =
+// row pass on G^*).  With antipodal direction sets (DESIGN R2/R4), V_{s,-c} =
+// conj(V_{s,c}), E likewise, and the mirror block (s,t,-c) has S = S_b^T.  The column-pass
+// matrix of (s,c), rows w_b R_tc S_b over t in col(s,c) plus inherited E Zhat'^*, is then the
+// complex conjugate of the row-pass matrix of (s,-c), so Zhat', sigma', k', Q', F', C' are
+// the conjugates of the row results at (s,-c).  This checks that the structure has exactly
+// that correspondence (pairs, blocks, parents, children, bounds); otherwise two passes run.
+void check_symmetry(dh2_ctx* C) {
+    Structure& S = C->st;
+    const int L = S.ct.depth;
+    const PassH &R = C->row, &X = C->col;
+    C->sym_ok = false;
+    C->col2row.clear();
+    if (C->mirror_missing) { C->sym_why = "blocks without an antipodal mirror"; return; }
+    if (R.bp.size() != X.bp.size()) { C->sym_why = "row and column pair counts differ"; return; }
+    std::unordered_map<uint64_t, int> rowpid;
+    for (size_t q = 0; q < R.bp.size(); ++q) rowpid[key(C->bp_t[R.bp[q]], C->bp_c[R.bp[q]])] = (int)q;
+    std::vector<std::vector<int64_t>> neg(L + 1);
+    for (int l = 0; l <= L; ++l) {
+        if (S.basis_pairs[l].empty()) continue;
+        const auto& D = S.D(l);
+        const int nd = (int)D.size() / 3;
+        std::map<std::tuple<double, double, double>, int64_t> idx;
+        for (int c = 0; c < nd; ++c) idx[{D[3 * c] + 0.0, D[3 * c + 1] + 0.0, D[3 * c + 2] + 0.0}] = c;
+        neg[l].assign(nd, -1);
+        for (int c = 0; c < nd; ++c) {
+            auto it = idx.find({-D[3 * c] + 0.0, -D[3 * c + 1] + 0.0, -D[3 * c + 2] + 0.0});
+            if (it != idx.end()) neg[l][c] = it->second;
+        }
+    }
+    std::vector<int> c2r(X.bp.size(), -1);
+    for (size_t p = 0; p < X.bp.size(); ++p) {
+        const int id = X.bp[p];
+        const int64_t nc = neg[C->bp_level[id]][C->bp_c[id]];
+        auto it = nc < 0 ? rowpid.end() : rowpid.find(key(C->bp_t[id], nc));
+        if (it == rowpid.end()) { C->sym_why = "column pair without a row pair at -c"; return; }
+        c2r[p] = it->second;
+    }
+    for (size_t p = 0; p < X.bp.size(); ++p) {
+        const int q = c2r[p];
+        if (X.Z_rows[p] != R.Z_rows[q] || X.total_rows[p] != R.total_rows[q] || X.kb[p] != R.kb[q] ||
+            X.rowsb[p] != R.rowsb[q]) { C->sym_why = "bounds differ"; return; }
+        if ((X.child0[p] < 0) != (R.child0[q] < 0)) { C->sym_why = "leaf mismatch"; return; }
+        if (X.child0[p] >= 0 && (c2r[X.child0[p]] != R.child0[q] || c2r[X.child1[p]] != R.child1[q])) {
+            C->sym_why = "children differ"; return;
+        }
+        std::vector<int> a, b;
+        for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) a.push_back(C->blk_mirror[X.blk[ib]]);
+        for (int ib = R.blk_ptr[q]; ib < R.blk_ptr[q + 1]; ++ib) b.push_back(R.blk[ib]);
+        std::sort(a.begin(), a.end());
+        std::sort(b.begin(), b.end());
+        if (a != b) { C->sym_why = "block sets differ"; return; }
+        std::vector<int> pa, pb;
+        for (int ip = X.par_ptr[p]; ip < X.par_ptr[p + 1]; ++ip) pa.push_back(c2r[X.par[ip]] * 2 + X.par_child[ip]);
+        for (int ip = R.par_ptr[q]; ip < R.par_ptr[q + 1]; ++ip) pb.push_back(R.par[ip] * 2 + R.par_child[ip]);
+        std::sort(pa.begin(), pa.end());
+        std::sort(pb.begin(), pb.end());
+        if (pa != pb) { C->sym_why = "parents differ"; return; }
+    }
+    C->col2row.swap(c2r);
+    C->sym_ok = true;
+    C->sym_why.clear();
+}
 
 void build_tables(dh2_ctx* C) {
     Structure& S = C->st;
@@ -434,6 +506,7 @@ void build_tables(dh2_ctx* C) {
             if (neg) C->blk_mirror[b] = it->second; else ++C->mirror_missing;
         }
     }
+    check_symmetry(C);
     C->blk_St_off.assign(nb, 0);
     for (int b = 0; b < nb; ++b) {
         C->blk_St_off[b] = C->St_total;
@@ -441,7 +514,7 @@ void build_tables(dh2_ctx* C) {
     }
 }
 
-void upload_pass(dh2_ctx* C, PassH& X, PassD& D) {
+void upload_pass(dh2_ctx* C, PassH& X, PassD& D, bool alloc_Z) {
     cudaStream_t s = C->stream;
     X.d_bp.upload(X.bp, s);
     X.d_child0.upload(X.child0, s);
@@ -465,7 +538,7 @@ void upload_pass(dh2_ctx* C, PassH& X, PassD& D) {
     X.d_nsig.alloc(np);
     X.d_disc.alloc(np);
     X.d_sweeps.alloc(np);
-    X.d_Z.alloc(X.Z_total);
+    if (alloc_Z) X.d_Z.alloc(X.Z_total);
     X.d_C.alloc(X.C_total);
     X.d_Q.alloc(X.Q_total);
     X.d_sigma.alloc(X.sig_total);
@@ -500,7 +573,7 @@ size_t plan_bytes(const dh2_ctx* C) {
     b += (size_t)C->VR_total * 16 + (size_t)C->E_total * 16 + C->st.blocks.size() * (size_t)C->k * C->k * 16;
     b += (size_t)C->St_total * 16;
     for (const PassH* X : {&C->row, &C->col})
-        b += (size_t)(X->Z_total + X->C_total + X->Q_total) * 16 + (size_t)X->sig_total * 8;
+        b += (size_t)((X == &C->col && C->sym_ok ? 0 : X->Z_total) + X->C_total + X->Q_total) * 16 + (size_t)X->sig_total * 8;
     b += (size_t)C->n * 7 * 32 + (size_t)C->nclusters * sizeof(GridD);
     return b;
 }
@@ -610,8 +683,9 @@ void upload_all(dh2_ctx* C, const double* xyz, int64_t nv, const int64_t* tri) {
     P.St = C->d_St.p;
     P.omega = C->d_omega.p;
     P.normG2 = C->d_normG2.p;
-    upload_pass(C, C->row, P.row);
-    upload_pass(C, C->col, P.col);
+    upload_pass(C, C->row, P.row, true);
+    upload_pass(C, C->col, P.col, !C->sym_ok);  // column Zhat only when two passes can run
+    if (C->sym_ok) C->d_col2row.upload(C->col2row, s);
 }
 
 // Device set-up (§2): quadrature points, grids, leaf V, E factors, S.
@@ -684,9 +758,29 @@ void run_recompress(dh2_ctx* C, double eps, int mode) {
         }
         C->kstat["block_weights"].flops += fl;
     }
+    const bool sym = C->sym_ok && C->sym_opt;
+    if (!sym && !C->col.d_Z.p && C->col.Z_total) {  // two passes requested on a symmetric structure
+        C->col.d_Z.alloc(C->col.Z_total);
+        C->P.col.Z = C->col.d_Z.p;
+    }
+    C->sym_used = sym;
     for (int side = 0; side < 2; ++side) {
         PassH& X = side == 0 ? C->row : C->col;
         const bool row = side == 0;
+        if (!row && sym) {
+            // column pass = conjugate of the row pass at -c (check_symmetry)
+            const int np = (int)X.bp.size();
+            C->timed("mirror_col", 1, [&] { launch_mirror_pass(P, C->d_col2row.p, np, s); });
+            X.rank.resize(np);
+            for (int p = 0; p < np; ++p) X.rank[p] = C->row.rank[C->col2row[p]];
+            double by = 0;
+            for (int p = 0; p < np; ++p) {
+                const int kk = X.rank[p];
+                by += 2.0 * 16.0 * ((double)kk * k + (double)X.rowsb[p] * kk);
+            }
+            C->kstat["mirror_col"].bytes += by;
+            continue;
+        }
         // total weights, top-down
         for (int l = 0; l <= L; ++l) {
             int p0 = X.lev_ptr[l], np = X.lev_ptr[l + 1] - p0;
@@ -991,6 +1085,17 @@ int dh2_set_stream(dh2_ctx* C, void* stream) {
     return DH2_OK;
 }
 
+int dh2_set_option(dh2_ctx* C, const char* name, int64_t value) {
+    if (!C || !name) return fail(nullptr, DH2_EINVAL, "null argument");
+    const std::string nm(name);
+    if (nm == "adjoint_symmetry") {
+        if (value != 0 && value != 1) return fail(C, DH2_EINVAL, "adjoint_symmetry must be 0 or 1");
+        C->sym_opt = (int)value;
+        return DH2_OK;
+    }
+    return fail(C, DH2_EINVAL, "unknown option " + nm);
+}
+
 int dh2_set_profiling(dh2_ctx* C, int32_t enable) {
     if (!C) return fail(nullptr, DH2_EINVAL, "null context");
     C->profiling = enable != 0;
@@ -1010,7 +1115,10 @@ int dh2_get_stats(const dh2_ctx* C, char* buf, int64_t* len) {
       << ", \"dirs\": " << S.ms_dirs << ", \"blocks\": " << S.ms_blocks << ", \"closure\": " << S.ms_closure
       << ", \"tables\": " << C->host_tables_ms << "}, \"launches_total\": " << C->launches_total
       << ", \"E_row\": " << C->E_row << ", \"E_col\": " << C->E_col << ", \"far2\": " << C->far2
-      << ", \"device_bytes\": " << plan_bytes(C) << ", \"mirror_missing\": " << C->mirror_missing << ", \"kernels\": {";
+      << ", \"device_bytes\": " << plan_bytes(C) << ", \"mirror_missing\": " << C->mirror_missing
+      << ", \"adjoint_symmetry\": {\"available\": " << (C->sym_ok ? "true" : "false") << ", \"enabled\": " << C->sym_opt
+      << ", \"used\": " << (C->sym_used ? "true" : "false") << ", \"why_not\": \"" << C->sym_why << "\"}"
+      << ", \"kernels\": {";
     bool first = true;
     for (auto& kv : C->kstat) {
         if (!first) o << ", ";
@@ -1050,6 +1158,7 @@ int dh2_export(const dh2_ctx* C, const char* name, void* buf, int64_t* nbytes) {
             nm = nm.substr(0, at);
             sliced = true;
         }
+        static thread_local std::vector<double2> tmpz;
         ExportItem it{nullptr, 0, false, 1};
         auto pairs_arr = [&](const std::vector<std::vector<Pair>>& P) {
             tmp64.clear();
@@ -1082,7 +1191,33 @@ int dh2_export(const dh2_ctx* C, const char* name, void* buf, int64_t* nbytes) {
             else if (base == "Q_off") it = hv(X->Q_off);
             else if (base == "sig_off") it = hv(X->sig_off);
             else if (base == "lev_ptr") it = hv(X->lev_ptr);
-            else if (base == "Z") it = dv(X->d_Z);
+            else if (base == "Z" && X == &C->col && C->sym_used) {
+                // column Zhat = conj(row Zhat at -c) (k_mirror_pass); materialised here on demand,
+                // only for the requested element range
+                require_device(C);
+                CK(cudaSetDevice(C->device));
+                const size_t lo = sliced ? sl_off : 0, hi = sliced ? sl_off + sl_cnt : (size_t)C->col.Z_total;
+                if (hi > (size_t)C->col.Z_total) throw std::invalid_argument("export slice out of range for " + nm);
+                if (!buf) {
+                    *nbytes = (int64_t)((hi - lo) * sizeof(double2));
+                    return;
+                }
+                tmpz.assign(hi - lo, double2{0.0, 0.0});
+                const auto& off = C->col.Z_off;
+                size_t p = std::upper_bound(off.begin(), off.end(), (int64_t)lo) - off.begin();
+                p = p ? p - 1 : 0;
+                for (; p < C->col.bp.size() && (size_t)off[p] < hi; ++p) {
+                    const size_t a0 = std::max((size_t)off[p], lo);
+                    const size_t a1 = std::min((size_t)off[p] + (size_t)C->col.Z_rows[p] * C->k, hi);
+                    if (a1 <= a0) continue;
+                    const int q = C->col2row[p];
+                    CK(cudaMemcpy(tmpz.data() + (a0 - lo), C->row.d_Z.p + C->row.Z_off[q] + (a0 - off[p]),
+                                  (a1 - a0) * sizeof(double2), cudaMemcpyDeviceToHost));
+                    for (size_t i = a0; i < a1; ++i) tmpz[i - lo].y = -tmpz[i - lo].y;
+                }
+                it = hv(tmpz);
+                sliced = false;  // tmpz holds exactly the requested range
+            } else if (base == "Z") it = dv(X->d_Z);
             else if (base == "C") it = dv(X->d_C);
             else if (base == "Q") it = dv(X->d_Q);
             else if (base == "sigma") it = dv(X->d_sigma);

@@ -758,6 +758,39 @@ void launch_truncate(const PlanD& P, bool row, int p0, int np, int maxrowsM, int
         k_truncate<false><<<np, 128, sm, s>>>(P, row ? P.row : P.col, p0, ldv, ldb, eps, mode);
 }
 
+// Column pass from the row pass by adjoint symmetry (check_symmetry in
+// dh2_api.cu): for the column pair p = (s,c) and the row pair q = (s,-c), the column-pass
+// matrices are the complex conjugates of the row-pass ones, so k' = k, sigma' = sigma,
+// Q' = conj(Q) (F' = conj(F)) and C' = conj(C).  CTA per column pair.
+__global__ void k_mirror_pass(PlanD P, const int* col2row) {
+    const int p = blockIdx.x;
+    const int q = col2row[p];
+    const PassD& R = P.row;
+    const PassD& X = P.col;
+    const int kk = R.rank[q], ns = R.nsig[q], kb = X.kb[p];
+    if (threadIdx.x == 0) {
+        X.rank[p] = kk;
+        X.nsig[p] = ns;
+        X.disc[p] = R.disc[q];
+        X.sweeps[p] = R.sweeps[q];
+    }
+    for (int i = threadIdx.x; i < ns; i += blockDim.x) X.sigma[X.sig_off[p] + i] = R.sigma[R.sig_off[q] + i];
+    const double2* Cr = R.C + R.C_off[q];
+    double2* Cc = X.C + X.C_off[p];
+    for (int idx = threadIdx.x; idx < kk * P.k; idx += blockDim.x) {
+        const int a = idx % kk, nu = idx / kk;
+        Cc[a + (size_t)nu * kb] = cconj(Cr[a + (size_t)nu * kb]);
+    }
+    const int ldq = X.child0[p] < 0 ? P.c_size[P.bp_t[X.bp[p]]] : X.rowsb[p];
+    const double2* Qr = R.Q + R.Q_off[q];
+    double2* Qc = X.Q + X.Q_off[p];
+    for (int idx = threadIdx.x; idx < ldq * kk; idx += blockDim.x) Qc[idx] = cconj(Qr[idx]);
+}
+
+void launch_mirror_pass(const PlanD& P, const int* col2row, int np, cudaStream_t s) {
+    if (np) k_mirror_pass<<<np, 128, 0, s>>>(P, col2row);
+}
+
 // Projection (Lemma Projections): T_b = C_tc S_b, S~_b = T_b C'_sc^*.  CTA per block.
 __global__ void k_project(PlanD P, int ldt) {
     extern __shared__ double2 sm[];

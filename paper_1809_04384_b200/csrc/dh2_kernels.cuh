@@ -92,6 +92,7 @@ void launch_block_weights(const PlanD& P, int mode, const int* mirror, cudaStrea
 void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* mirror, cudaStream_t s);
 void launch_truncate(const PlanD& P, bool row, int p0, int np, int maxrowsM, int maxZrows, bool leaf_level, double eps,
                      int mode, cudaStream_t s);
+void launch_mirror_pass(const PlanD& P, const int* col2row, int np, cudaStream_t s);
 void launch_project(const PlanD& P, int maxkrow, cudaStream_t s);
 // matvec (forward / coupling / backward)
 void launch_mv_forward(const PlanD& P, bool recomp, int p0, int np, const double2* xp, double2* xh,

@@ -21,7 +21,7 @@ DH2_HOST_PTRS, DH2_DEVICE_PTRS = 0, 1
 
 # every symbol include/dh2.h declares
 EXPORTED = ["dh2_build_interp", "dh2_setup_device", "dh2_recompress", "dh2_matvec", "dh2_storage",
-            "dh2_set_stream", "dh2_set_profiling", "dh2_get_stats", "dh2_export", "dh2_destroy", "dh2_last_error"]
+            "dh2_set_stream", "dh2_set_option", "dh2_set_profiling", "dh2_get_stats", "dh2_export", "dh2_destroy", "dh2_last_error"]
 
 
 class dh2_mesh(ctypes.Structure):
@@ -72,6 +72,7 @@ def load_library(path=LIB_PATH):
     lib.dh2_storage.argtypes = [vp, ctypes.c_int32, P(dh2_storage_report)]
     lib.dh2_set_stream.argtypes = [vp, vp]
     lib.dh2_set_profiling.argtypes = [vp, ctypes.c_int32]
+    lib.dh2_set_option.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64]
     lib.dh2_get_stats.argtypes = [vp, ctypes.c_char_p, P(ctypes.c_int64)]
     lib.dh2_export.argtypes = [vp, ctypes.c_char_p, vp, P(ctypes.c_int64)]
     lib.dh2_destroy.argtypes = [vp]
@@ -144,6 +145,9 @@ class DH2:
 
     def set_stream(self, stream_ptr):
         self._check(self.lib.dh2_set_stream(self.h, ctypes.c_void_p(stream_ptr)))
+
+    def set_option(self, name, value):
+        self._check(self.lib.dh2_set_option(self.h, name.encode(), int(value)))
 
     def set_profiling(self, on=True):
         self._check(self.lib.dh2_set_profiling(self.h, 1 if on else 0))

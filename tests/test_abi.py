@@ -111,3 +111,20 @@ def test_storage_orig_matches_oracle(lib):
     got = h.storage(0)
     for key in ("row_basis_bytes", "col_basis_bytes", "coupling_bytes", "nearfield_bytes", "kb_per_dof_matrix"):
         assert got[key] == ref[key], key
+
+
+@pytest.mark.parametrize("name", ["P0", "P1", "P2", "P3", "C1", "C2"])
+def test_adjoint_symmetry_structure(name):
+    """SURVEY NEXT-1 precondition, checked by the library on the host structure: every block
+    has its antipodal mirror (s,t,-c) and every column pair (s,c) corresponds to the row pair
+    (s,-c) with the same blocks (mirrored), parents, children and bounds."""
+    h, _, _ = _structure_ctx(get_config(name))
+    s = h.stats()
+    assert s["mirror_missing"] == 0
+    assert s["adjoint_symmetry"]["available"], s["adjoint_symmetry"]
+    assert s["row_pairs"] == s["col_pairs"]
+    with pytest.raises(Exception):
+        h.set_option("adjoint_symmetry", 2)
+    with pytest.raises(Exception):
+        h.set_option("no_such_option", 1)
+    h.close()

@@ -19,15 +19,22 @@ SMALL = ["P0", "P1", "P2", "P3", "C1"]
 _GPU = {}
 
 
-def gpu_run(name, eps=None, mode="FROB_BLOCKREL"):
+# (config, adjoint symmetry): the default path derives the column pass from the row pass
+# (dh2_set_option "adjoint_symmetry"); the two-pass path is checked on the small configs too.
+CASES = [(n, 1) for n in SMALL + ["C2"]] + [(n, 0) for n in SMALL]
+
+
+def gpu_run(name, eps=None, mode="FROB_BLOCKREL", sym=1):
     from paper_1809_04384_b200 import DH2
     from gpu_view import GpuView
-    key = (name, eps, mode)
+    key = (name, eps, mode, sym)
     if key not in _GPU:
         cfg = get_config(name)
         xyz, tri = mesh_for(cfg)
         h = DH2(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"])
+        h.set_option("adjoint_symmetry", sym)
         h.recompress(cfg["eps"] if eps is None else eps, mode)
+        assert h.stats()["adjoint_symmetry"]["used"] == bool(sym)
         rc = oracle_run(name, eps, mode)
         _GPU[key] = (h, GpuView(h, rc.st), rc)
     return _GPU[key]
@@ -57,10 +64,10 @@ def test_G1_setup_entrywise(name):
         assert _rel(g.S(int(b)), rc.S(int(b))) <= 1e-13
 
 
-@pytest.mark.parametrize("name", SMALL + ["C2"])
-def test_G2_weight_grams(name):
+@pytest.mark.parametrize("name,sym", CASES)
+def test_G2_weight_grams(name, sym):
     """R^*R per basis pair <= 1e-12 ||R||^2; Zhat^*Zhat per pair <= 1e-11 ||Zhat||^2."""
-    h, g, rc = gpu_run(name)
+    h, g, rc = gpu_run(name, sym=sym)
     st = rc.st
     for l in st.active_levels:
         for (t, c) in st.basis_pairs[l]:
@@ -87,9 +94,9 @@ def _rank_zone_ok(sig, k_gpu, k_orc, eps):
     return abs(np.sqrt(q) - eps) <= 1e-12 * max(sig[0], 1e-300)
 
 
-@pytest.mark.parametrize("name", SMALL + ["C2"])
-def test_G3_ranks_and_singular_values(name):
-    h, g, rc = gpu_run(name)
+@pytest.mark.parametrize("name,sym", CASES)
+def test_G3_ranks_and_singular_values(name, sym):
+    h, g, rc = gpu_run(name, sym=sym)
     for side in ("row", "col"):
         go, oo = getattr(g, side), getattr(rc, side)
         mism = 0
@@ -105,10 +112,10 @@ def test_G3_ranks_and_singular_values(name):
         assert mism == 0, "rank mismatches inside the tie zone: re-run with forced ranks"
 
 
-@pytest.mark.parametrize("name", SMALL + ["C2"])
-def test_G4_matvec(name):
+@pytest.mark.parametrize("name,sym", CASES)
+def test_G4_matvec(name, sym):
     """3 seeded x: ||y_gpu - y_orc|| <= 1e-10 ||G_far x|| (RECOMP); ORIG to 1e-12."""
-    h, g, rc = gpu_run(name)
+    h, g, rc = gpu_run(name, sym=sym)
     for seed in (1, 2, 3):
         x = seeded_vector(rc.st.n, seed)
         yo = ops.matvec(rc, x, "orig")
@@ -120,11 +127,11 @@ def test_G4_matvec(name):
         assert np.linalg.norm(yrg - yr) <= 1e-10 * ref
 
 
-@pytest.mark.parametrize("name", SMALL)
-def test_G5_dense_blocks(name):
+@pytest.mark.parametrize("name,sym", [c for c in CASES if c[0] in SMALL])
+def test_G5_dense_blocks(name, sym):
     """Every block densely expanded from both factor sets:
     sqrt(sum_b ||G~_b^gpu - G~_b^orc||^2) <= 1e-10 ||G_far||_F; GPU bases orthonormal."""
-    h, g, rc = gpu_run(name)
+    h, g, rc = gpu_run(name, sym=sym)
     st = rc.st
     qr_g, qc_g, qr_o, qc_o = {}, {}, {}, {}
     num = 0.0
@@ -137,9 +144,9 @@ def test_G5_dense_blocks(name):
         assert np.abs(Q.conj().T @ Q - np.eye(Q.shape[1])).max(initial=0.0) <= 1e-12
 
 
-@pytest.mark.parametrize("name", SMALL + ["C2"])
-def test_G6_certified_sums(name):
-    h, g, rc = gpu_run(name)
+@pytest.mark.parametrize("name,sym", CASES)
+def test_G6_certified_sums(name, sym):
+    h, g, rc = gpu_run(name, sym=sym)
     s = h.stats()
     Er, Ec = rc.discarded(rc.row), rc.discarded(rc.col)
     assert abs(s["E_row"] - Er) <= 1e-10 * max(Er, 1e-300) + 1e-16 * rc.far_norm2()
