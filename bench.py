@@ -10,9 +10,11 @@ buffers (mesh in, x in, y out), host structure build and all copies included.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
 
-Under torchrun (N > 1) every rank runs an independent replica of the workload (weak
-scaling; the subtree-sharded path is future work); the timed region
-is bracketed by barriers + synchronisation and the max over ranks is reported by rank 0.
+Under torchrun (N > 1) the matrix is partitioned into N subtree shards, one per GPU, with
+NCCL exchanges of the cross-shard factors (include/dh2.h dh2_dist):
+the total work is fixed ("strong" scaling) and value = n / (max over ranks of the device
+time per step).  The timed region is bracketed by barriers + synchronisation.
+--shards P (single process) runs the same partition in the virtual mode on one GPU.
 """
 import argparse
 import json
@@ -127,7 +129,7 @@ def run_reference(args, cfg, rank, world):
     val = n / t / 1e6
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "Mdof/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_desc(cfg), "n": n},
             "cpu_baseline": {"value": val, "unit": "Mdof/s", "cores": 1, "kind": "oracle",
                              "sample": "full §3.2 oracle pipeline on a seeded %.3g fraction of the admissible blocks of "
@@ -147,6 +149,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--sample-frac", type=float, default=0.125)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shards", type=int, default=1, help="virtual shards on one GPU (single process)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -162,7 +165,7 @@ def main():
 
     import torch
     import torch.distributed as dist
-    from paper_1809_04384_b200 import DH2
+    from paper_1809_04384_b200 import DH2, nccl_unique_id
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -172,8 +175,18 @@ def main():
         if world > 1:
             dist.barrier()
 
+    def make():
+        """collective: one shard per rank (NCCL), or args.shards virtual shards on this GPU"""
+        if world > 1:
+            obj = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            return DH2(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"], device=local,
+                       world=world, rank=rank, nccl_uid=obj[0])
+        return DH2(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"], device=local,
+                   world=args.shards)
+
     n = cfg["n"]
-    h = DH2(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"], device=local)
+    h = make()
     stream = torch.cuda.current_stream()
     h.set_stream(stream.cuda_stream)
     x = torch.from_numpy(seeded_vector(n, 1)).to("cuda")
@@ -209,7 +222,7 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = world * n / (ms * 1e-3) / 1e6
+    value = n / (ms * 1e-3) / 1e6  # the whole matrix, partitioned over the ranks
 
     # per kernel class over the timed region (classes "name@level" are grouped by name;
     # "truncate_row@8" -> class "truncate", detail kept per level)
@@ -254,7 +267,7 @@ def main():
         for i in range(args.e2e_steps + 1):
             barrier()
             t0 = time.perf_counter()
-            g = DH2(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"], device=local)
+            g = make()
             g.recompress(cfg["eps"])
             yh = g.matvec(xh, 1)
             t1 = time.perf_counter()
@@ -266,7 +279,7 @@ def main():
             t = torch.tensor([te], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
-        e2e = {"value": world * n / te / 1e6, "unit": "Mdof/s", "h2d_bytes_per_step": int(bi),
+        e2e = {"value": n / te / 1e6, "unit": "Mdof/s", "h2d_bytes_per_step": int(bi),
                "d2h_bytes_per_step": int(bo), "seconds_per_step": te}
         del yh
 
@@ -282,15 +295,17 @@ def main():
                                  args.sample_frac, samp, full, sec),
                    "host_cores_available": cpu_cores()}
         line = {"metric": METRIC, "value": value, "unit": "Mdof/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload_desc(cfg), "n": n, "kappa": cfg["kappa"], "m": cfg["m"],
                            "leaf": cfg["leaf"], "eps": cfg["eps"], "mode": "FROB_BLOCKREL",
-                           "parallelism": "replicas" if world > 1 else "single",
+                           "parallelism": ("subtree-shards%d (NCCL)" % world if world > 1 else
+                                           "virtual-shards%d (1 GPU)" % args.shards if args.shards > 1 else "single"),
                            "l2": "inputs larger than L2 (%.1f GB resident device data)" % (s1["device_bytes"] / 1e9),
                            "blocks": s1["blocks"], "row_pairs": s1["row_pairs"], "basis_pairs": s1["basis_pairs"]},
                 "seconds_per_step": ms * 1e-3,
                 "roofline": roof, "cpu_baseline": cpu, "clocks": clocks, "e2e": e2e, "gpu_launches": launches,
+                "exchange_bytes_per_step": s1.get("exchange_bytes"),
                 "phases": phases,
                 "launch_detail_ms_per_step": {c: round(v["ms"] / args.steps, 4) for c, v in sorted(detail.items())}}
         print(json.dumps(line), flush=True)

@@ -43,10 +43,10 @@ enum {
     DH2_EINVAL = -1,    /* bad parameter, bad mesh index, triangle area <= 0, size mismatch */
     DH2_ENOMEM = -2,    /* the device memory plan does not fit (checked before any launch) */
     DH2_ECUDA = -3,     /* CUDA runtime error or no device */
-    DH2_ENCCL = -4,     /* reserved: multi-GPU transport error */
+    DH2_ENCCL = -4,     /* multi-GPU transport (NCCL) error or NCCL unavailable */
     DH2_ESTATE = -5,    /* call order: recompress before build, RECOMP matvec before recompress */
     DH2_EMISMATCH = -6, /* reserved: ranks passed different arguments */
-    DH2_ENOTIMPL = -7   /* configuration outside what this build supports (e.g. k > 64) */
+    DH2_ENOTIMPL = -7   /* configuration outside what this build supports (e.g. m > 5, k > 125) */
 };
 
 /* recompression error-control modes (reading Q12 of DESIGN.md) */
@@ -74,7 +74,7 @@ typedef struct {
 
 /* Parameters (BASELINE.json configs).
  *   kappa     wave number >= 0 (Eq. helmholtz)
- *   m         Chebyshev order per axis, k = m^3; this build supports 1 <= m <= 4
+ *   m         Chebyshev order per axis, k = m^3; this build supports 1 <= m <= 5
  *   leaf_size clusters are split while #t > leaf_size
  *   eta1      direction parameter of Eq. 3a / Remark 2.4
  *   eta2      admissibility parameter of Eq. 3b/3c
@@ -87,12 +87,28 @@ typedef struct {
     int32_t quad;
 } dh2_params;
 
-/* Device selection and multi-GPU description (world > 1 is reserved; pass NULL for
- * device 0).  device = CUDA ordinal, or DH2_DEVICE_NONE: build the host structures
- * only (cluster tree, directions, blocks, pairs — no device memory, no kernels); such a
- * context supports dh2_export of host arrays and dh2_storage(DH2_ORIG) and fails every
- * compute call with DH2_ESTATE.  It exists so structure parity can be checked without
- * a GPU; it is not a compute fallback. */
+/* Device selection and multi-GPU description (NULL = device 0, one shard).
+ *   device   CUDA ordinal, or DH2_DEVICE_NONE: build the host structures only (cluster
+ *            tree, directions, blocks, pairs, shard ownership and exchange lists — no
+ *            device memory, no kernels); such a context supports dh2_export of host arrays
+ *            and dh2_storage(DH2_ORIG) and fails every compute call with DH2_ESTATE.  It
+ *            exists so structure parity can be checked without a GPU; it is not a compute
+ *            fallback.
+ *   world    number of shards P (a power of two).  The partition: cut level
+ *            log2 P of the cluster tree; shard r owns the subtree of the r-th cluster on that
+ *            level, i.e. its row/column pairs and every block (t,s,c) whose row cluster t it
+ *            owns.  Every active level must lie on or below the cut (DH2_ENOTIMPL otherwise),
+ *            and the structure must admit the adjoint symmetry (W = V, antipodal directions).
+ *            Exchanges: after the basis weights the R_sc computed by QR of column pairs that
+ *            other shards' blocks reference, after the truncation C'_sc and k'_sc, in the
+ *            matvec the coefficients xh'_sc, then the output slices.  Results are bitwise
+ *            identical for every P.
+ *   rank     this process's shard, 0 <= rank < world.
+ *   nccl_uid 128-byte ncclUniqueId from dh2_nccl_unique_id on rank 0, broadcast by the
+ *            caller: one process per GPU, exchanges with NCCL over NVLink, every call is
+ *            collective.  NULL with world > 1: "virtual" mode — this process runs all
+ *            `world` shards on `device`, phase by phase, with device-to-device exchanges
+ *            (same shard code and exchange items; used to test the partition on one GPU). */
 enum { DH2_DEVICE_NONE = -1 };
 typedef struct {
     int32_t rank, world;
@@ -168,6 +184,17 @@ int dh2_get_stats(const dh2_ctx* ctx, char* buf, int64_t* len);
  * sigma_row/col, Q_row/col, F_row/col, C_row/col, St).  "<name>@<offset>:<count>"
  * exports the element slice [offset, offset + count) of the array. */
 int dh2_export(const dh2_ctx* ctx, const char* name, void* buf, int64_t* nbytes);
+
+/* As dh2_export, for shard `shard` (0 <= shard < number of shards in this process; > 1 only
+ * in the virtual mode).  Extra names of the partition: "owner" (int32 per cluster, -1 above
+ * the cut), "own_range" (int32 b_lo, b_hi, pos_lo, pos_hi: own blocks and cluster-ordered positions),
+ * "xR_send", "xR_recv", "xC_send", "xC_recv" (int32: for every peer, a count then the item
+ * ids: basis pair ids for R, column pair ids for C', k', xh'). */
+int dh2_export_shard(const dh2_ctx* ctx, int32_t shard, const char* name, void* buf, int64_t* nbytes);
+
+/* Write a fresh 128-byte ncclUniqueId to uid (call on rank 0, broadcast to all ranks before
+ * dh2_build_interp).  NCCL (libnccl.so.2) is loaded at run time; DH2_ENCCL if unavailable. */
+int dh2_nccl_unique_id(void* uid);
 
 /* Release all memory of ctx (NULL is a no-op). */
 int dh2_destroy(dh2_ctx* ctx);

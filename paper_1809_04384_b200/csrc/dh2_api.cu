@@ -1,6 +1,8 @@
 // C-ABI implementation of libdh2.so (include/dh2.h): host structure -> device tables ->
 // level-batched sm_100a kernels.  No CPU fallback: every compute step runs on the GPU.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -75,6 +77,8 @@ struct PassH {
     std::vector<int64_t> Z_off, C_off, Q_off, sig_off;
     std::vector<int> lev_ptr;  // pairs of level l: [lev_ptr[l], lev_ptr[l+1])
     std::vector<int> lc, lc_ptr;  // leaf-cluster groups (matvec output)
+    std::vector<int> own_lo, own_hi;  // per level: pairs of this shard [own_lo[l], own_hi[l])
+    int lc_lo = 0, lc_hi = 0;         // leaf-cluster groups of this shard
     int64_t Z_total = 0, C_total = 0, Q_total = 0, sig_total = 0;
     int max_total_rows_level(int l) const { return lev_max_total[l]; }
     std::vector<int> lev_max_total, lev_max_zrows, lev_max_leafrows;
@@ -98,8 +102,19 @@ struct KStat {
 
 }  // namespace
 
-struct dh2_ctx {
+struct Shard {
     Structure st;
+    // sharding: shard `rank` of `world` owns the subtree of the rank-th cluster on
+    // the cut level log2(world) -- its row/column pairs, and the blocks (t,s,c) with t in it.
+    // world == 1 owns everything.
+    int rank = 0, world = 1, cut = 0;
+    std::vector<int> owner;          // per cluster, -1 above the cut
+    std::vector<char> bp_own;        // basis pair computed by this shard
+    int b_lo = 0, b_hi = 0;          // own blocks [b_lo, b_hi) (blocks sorted by owner of t)
+    int64_t pos_lo = 0, pos_hi = 0;  // own range of cluster-ordered positions
+    // exchange items per peer, in the same order on both sides (host-computed, replicated)
+    std::vector<std::vector<int>> R_send, R_recv;  // basis pair ids: R_sc computed by QR (non-leaf)
+    std::vector<std::vector<int>> C_send, C_recv;  // column pair ids: C'_sc, k'_sc, xh'_sc
     int n = 0, k = 0, m = 0, nclusters = 0;
     int device = 0;
     cudaStream_t own_stream = nullptr;
@@ -128,6 +143,9 @@ struct dh2_ctx {
     std::vector<int> col2row;
     bool sym_ok = false;     // structure admits it (checked in build_tables)
     int sym_opt = 1;         // dh2_set_option("adjoint_symmetry")
+    int force_ws = 0;        // dh2_set_option("truncate_workspace")
+    DevBuf<double2> d_ws;    // truncation workspace (persistent grid), grown on demand
+    int64_t ws_launches = 0; // truncation launches that used the workspace
     bool sym_used = false;   // the last dh2_recompress derived the column pass from the row pass
     std::string sym_why;     // why sym_ok is false
     DevBuf<int> d_col2row;
@@ -154,7 +172,7 @@ struct dh2_ctx {
     double host_build_ms = 0.0, host_tables_ms = 0.0;
     double E_row = 0, E_col = 0, far2 = 0;
 
-    ~dh2_ctx() {
+    ~Shard() {
         for (auto& e : ev_pool) cudaEventDestroy(e);
         for (auto& p : pending) {
             cudaEventDestroy(std::get<1>(p));
@@ -214,7 +232,7 @@ inline uint64_t key(int64_t t, int64_t c) { return ((uint64_t)t << 32) | (uint64
 // complex conjugate of the row-pass matrix of (s,-c), so Zhat', sigma', k', Q', F', C' are
 // the conjugates of the row results at (s,-c).  This checks that the structure has exactly
 // that correspondence (pairs, blocks, parents, children, bounds); otherwise two passes run.
-void check_symmetry(dh2_ctx* C) {
+void check_symmetry(Shard* C) {
     Structure& S = C->st;
     const int L = S.ct.depth;
     const PassH &R = C->row, &X = C->col;
@@ -271,7 +289,37 @@ void check_symmetry(dh2_ctx* C) {
     C->sym_why.clear();
 }
 
-void build_tables(dh2_ctx* C) {
+// Ownership of clusters for sharding: cut level log2(world); the subtree of the
+// r-th cluster of the cut level belongs to shard r.  Every active level must lie on or below the
+// cut (the replicated top carries no recompression work); blocks are re-ordered by the owner of
+// their row cluster (stable, so world == 1 keeps the structure's order).
+void assign_owners(Shard* C) {
+    Structure& S = C->st;
+    const ClusterTree& T = S.ct;
+    const int L = T.depth;
+    C->cut = 0;
+    while ((1 << C->cut) < C->world) ++C->cut;
+    if ((1 << C->cut) != C->world) throw std::invalid_argument("world size must be a power of two");
+    if (C->rank < 0 || C->rank >= C->world) throw std::invalid_argument("rank out of range");
+    if (C->cut > L || (int)T.levels[C->cut].size() != C->world)
+        throw NotImpl("the cluster tree has fewer than world clusters on level log2(world)");
+    for (int l = 0; l < C->cut; ++l)
+        if (!S.basis_pairs[l].empty())
+            throw NotImpl("active pairs above the cut level log2(world) (direction split not implemented)");
+    C->owner.assign(T.begin.size(), -1);
+    for (int i = 0; i < C->world; ++i) C->owner[T.levels[C->cut][i]] = i;
+    for (int l = C->cut + 1; l <= L; ++l)
+        for (int64_t t : T.levels[l]) C->owner[t] = C->owner[T.parent[t]];
+    if (C->world > 1) {
+        const auto& own = C->owner;
+        std::stable_sort(S.blocks.begin(), S.blocks.end(), [&](const Block& a, const Block& b) { return own[a.t] < own[b.t]; });
+    }
+    const int64_t top = T.levels[C->cut][C->rank];
+    C->pos_lo = T.begin[top];
+    C->pos_hi = T.end[top];
+}
+
+void build_tables(Shard* C) {
     Structure& S = C->st;
     const ClusterTree& T = S.ct;
     const int k = S.k, L = T.depth;
@@ -279,6 +327,9 @@ void build_tables(dh2_ctx* C) {
     C->k = k;
     C->m = S.p.m;
     C->nclusters = (int)T.begin.size();
+    assign_owners(C);
+    const int me = C->rank, W = C->world;
+    const auto& own = C->owner;
     // directions of the materialised levels
     C->dir_off.assign(L + 2, -1);
     for (int l = 0; l <= L; ++l) {
@@ -287,7 +338,7 @@ void build_tables(dh2_ctx* C) {
         const auto& D = S.D(l);
         C->dirs_flat.insert(C->dirs_flat.end(), D.begin(), D.end());
     }
-    // basis pairs, bottom-up order not required; ids level by level
+    // basis pairs (global ids, level by level)
     C->bp_lev_ptr.assign(L + 2, 0);
     for (int l = 0; l <= L; ++l) {
         C->bp_lev_ptr[l] = (int)C->bp_t.size();
@@ -309,20 +360,15 @@ void build_tables(dh2_ctx* C) {
     C->bp_R_off.assign(nbp, -1);
     C->bp_E_off.assign(nbp, -1);
     C->bp_R_rows.assign(nbp, 0);
+    C->bp_own.assign(nbp, 0);
     C->leafV_lists.assign(L + 1, {});
     C->basis_lists.assign(L + 1, {});
     C->E_lists.assign(L + 1, {});
     C->basis_maxrows.assign(L + 1, 0);
-    int64_t off = 0;
     for (int id = 0; id < nbp; ++id) {
         int t = C->bp_t[id], l = C->bp_level[id];
-        if (T.is_leaf(t)) {
-            int sz = (int)T.size(t);
-            C->max_leaf = std::max(C->max_leaf, sz);
-            C->bp_V_off[id] = off;
-            off += (int64_t)sz * k;
-            C->leafV_lists[l].push_back(id);
-        } else {
+        C->bp_own[id] = own[t] == me;
+        if (!T.is_leaf(t)) {
             int64_t c2 = S.sd(l, C->bp_c[id]);
             C->bp_sddir[id] = (int)(C->dir_off[l + 1] + c2);
             auto it0 = C->bp_id.find(key(T.child0[t], c2));
@@ -330,54 +376,78 @@ void build_tables(dh2_ctx* C) {
             if (it0 == C->bp_id.end() || it1 == C->bp_id.end()) throw std::logic_error("closure broken");
             C->bp_child0[id] = it0->second;
             C->bp_child1[id] = it1->second;
-            C->E_lists[l].push_back(id);
         }
     }
-    // basis weights: rows bottom-up
-    for (int l = L; l >= 0; --l) {
+    // basis-weight rows, bottom-up (Eq. 18): leaf min(#t, k) (R = V if #t <= k), inner min(r1 + r2, k)
+    for (int l = L; l >= 0; --l)
         for (int id = C->bp_lev_ptr[l]; id < C->bp_lev_ptr[l + 1]; ++id) {
-            int t = C->bp_t[id];
-            if (T.is_leaf(t)) {
-                int sz = (int)T.size(t);
-                if (sz <= k) {
-                    C->bp_R_rows[id] = sz;
-                    C->bp_R_off[id] = C->bp_V_off[id];  // R = V, P = I (Eq. 18)
-                } else {
-                    C->bp_R_rows[id] = k;
-                    C->bp_R_off[id] = off;
-                    off += (int64_t)k * k;
-                    C->basis_lists[l].push_back(id);
-                    C->basis_maxrows[l] = std::max(C->basis_maxrows[l], sz);
-                }
-            } else {
-                int rows = C->bp_R_rows[C->bp_child0[id]] + C->bp_R_rows[C->bp_child1[id]];
-                C->bp_R_rows[id] = std::min(rows, k);
-                C->bp_R_off[id] = off;
-                off += (int64_t)C->bp_R_rows[id] * k;
+            const int t = C->bp_t[id];
+            const int rows = T.is_leaf(t) ? (int)T.size(t) : C->bp_R_rows[C->bp_child0[id]] + C->bp_R_rows[C->bp_child1[id]];
+            C->bp_R_rows[id] = std::min(rows, k);
+        }
+    auto r_by_qr = [&](int id) { return !T.is_leaf(C->bp_t[id]) || T.size(C->bp_t[id]) > k; };
+    // blocks (global ids; own range contiguous after assign_owners)
+    const int nb = (int)S.blocks.size();
+    C->b_lo = nb;
+    C->b_hi = 0;
+    for (int b = 0; b < nb; ++b) {
+        const Block& B = S.blocks[b];
+        int l = (int)T.level[B.t];
+        C->blk_t.push_back((int)B.t);
+        C->blk_s.push_back((int)B.s);
+        C->blk_dir.push_back((int)(C->dir_off[l] + B.c));
+        C->blk_bprow.push_back(C->bp_id.at(key(B.t, B.c)));
+        C->blk_bpcol.push_back(C->bp_id.at(key(B.s, B.c)));
+        if (own[B.t] == me) {
+            C->b_lo = std::min(C->b_lo, b);
+            C->b_hi = std::max(C->b_hi, b + 1);
+        }
+    }
+    if (C->b_lo >= C->b_hi) C->b_lo = C->b_hi = 0;
+    for (int b = C->b_lo; b < C->b_hi; ++b)
+        if (own[S.blocks[b].t] != me) throw std::logic_error("own blocks not contiguous");
+    // basis pairs needed here: own ones, plus the column pairs of own blocks owned elsewhere
+    // (imported: R received if computed by QR, else R = V regenerated from the replicated mesh)
+    std::vector<char> need(C->bp_own.begin(), C->bp_own.end());
+    for (int b = C->b_lo; b < C->b_hi; ++b) need[C->blk_bpcol[b]] = 1;
+    int64_t off = 0;
+    for (int id = 0; id < nbp; ++id) {
+        if (!need[id]) continue;
+        const int t = C->bp_t[id], l = C->bp_level[id];
+        if (T.is_leaf(t) && (C->bp_own[id] || !r_by_qr(id))) {  // V slab
+            const int sz = (int)T.size(t);
+            C->max_leaf = std::max(C->max_leaf, sz);
+            C->bp_V_off[id] = off;
+            off += (int64_t)sz * k;
+            C->leafV_lists[l].push_back(id);
+        }
+        if (C->bp_own[id] && !T.is_leaf(t)) C->E_lists[l].push_back(id);
+    }
+    for (int l = L; l >= 0; --l)
+        for (int id = C->bp_lev_ptr[l]; id < C->bp_lev_ptr[l + 1]; ++id) {
+            if (!need[id]) continue;
+            if (!r_by_qr(id)) {
+                C->bp_R_off[id] = C->bp_V_off[id];  // R = V, P = I (Eq. 18)
+                continue;
+            }
+            C->bp_R_off[id] = off;
+            off += (int64_t)C->bp_R_rows[id] * k;
+            if (C->bp_own[id]) {
                 C->basis_lists[l].push_back(id);
+                const int t = C->bp_t[id];
+                const int rows = T.is_leaf(t) ? (int)T.size(t) : C->bp_R_rows[C->bp_child0[id]] + C->bp_R_rows[C->bp_child1[id]];
                 C->basis_maxrows[l] = std::max(C->basis_maxrows[l], rows);
             }
         }
-    }
     C->VR_total = off;
     int64_t eoff = 0;
     for (int id = 0; id < nbp; ++id)
-        if (C->bp_child0[id] >= 0) {
+        if (C->bp_own[id] && C->bp_child0[id] >= 0) {
             C->bp_E_off[id] = eoff;
             eoff += 6LL * C->m * C->m;
         }
     C->E_total = eoff;
-    // blocks
-    const int nb = (int)S.blocks.size();
-    for (const Block& b : S.blocks) {
-        int l = (int)T.level[b.t];
-        C->blk_t.push_back((int)b.t);
-        C->blk_s.push_back((int)b.s);
-        C->blk_dir.push_back((int)(C->dir_off[l] + b.c));
-        C->blk_bprow.push_back(C->bp_id.at(key(b.t, b.c)));
-        C->blk_bpcol.push_back(C->bp_id.at(key(b.s, b.c)));
-    }
-    // passes
+    // passes (global pair ids; per-pair slabs only for the pairs this shard computes or imports)
     for (int side = 0; side < 2; ++side) {
         PassH& X = side == 0 ? C->row : C->col;
         const auto& pairs = side == 0 ? S.row_pairs : S.col_pairs;
@@ -404,7 +474,7 @@ void build_tables(dh2_ctx* C) {
                 X.child1[p] = pid.at(key(T.child1[t], c2));
             }
         }
-        // blocks CSR (blocks sorted by (t,s): per pair sorted by the other cluster)
+        // blocks CSR (blocks sorted by (t,s) per owner: per pair sorted by the other cluster)
         std::vector<std::vector<int>> bl(np);
         for (int b = 0; b < nb; ++b) {
             const Block& B = S.blocks[b];
@@ -415,6 +485,10 @@ void build_tables(dh2_ctx* C) {
             else
                 C->blk_pcol.push_back(p);
         }
+        for (auto& v : bl) std::sort(v.begin(), v.end(), [&](int a, int b) {
+            const Block &A = S.blocks[a], &B = S.blocks[b];
+            return side == 0 ? (A.s < B.s || (A.s == B.s && a < b)) : (A.t < B.t || (A.t == B.t && a < b));
+        });
         X.blk_ptr.assign(np + 1, 0);
         for (int p = 0; p < np; ++p) {
             X.blk_ptr[p + 1] = X.blk_ptr[p] + (int)bl[p].size();
@@ -441,7 +515,10 @@ void build_tables(dh2_ctx* C) {
         X.lev_max_total.assign(L + 1, 0);
         X.lev_max_zrows.assign(L + 1, 0);
         X.lev_max_leafrows.assign(L + 1, 0);
-        for (int l = 0; l <= L; ++l)
+        X.own_lo.assign(L + 1, 0);
+        X.own_hi.assign(L + 1, 0);
+        for (int l = 0; l <= L; ++l) {
+            int lo = X.lev_ptr[l + 1], hi = X.lev_ptr[l];
             for (int p = X.lev_ptr[l]; p < X.lev_ptr[l + 1]; ++p) {
                 int tot = 0;
                 for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) {
@@ -451,9 +528,18 @@ void build_tables(dh2_ctx* C) {
                 for (int ip = X.par_ptr[p]; ip < X.par_ptr[p + 1]; ++ip) tot += X.Z_rows[X.par[ip]];
                 X.total_rows[p] = tot;
                 X.Z_rows[p] = std::min(tot, k);
+                if (own[C->bp_t[X.bp[p]]] != me) continue;
+                lo = std::min(lo, p);
+                hi = std::max(hi, p + 1);
                 X.lev_max_total[l] = std::max(X.lev_max_total[l], tot);
                 X.lev_max_zrows[l] = std::max(X.lev_max_zrows[l], X.Z_rows[p]);
             }
+            if (lo >= hi) lo = hi = X.lev_ptr[l];
+            for (int p = lo; p < hi; ++p)
+                if (own[C->bp_t[X.bp[p]]] != me) throw std::logic_error("own pairs of a level not contiguous");
+            X.own_lo[l] = lo;
+            X.own_hi[l] = hi;
+        }
         // rank bounds, bottom-up
         X.rowsb.assign(np, 0);
         X.kb.assign(np, 0);
@@ -462,33 +548,50 @@ void build_tables(dh2_ctx* C) {
                 int t = C->bp_t[X.bp[p]];
                 X.rowsb[p] = X.child0[p] < 0 ? (int)T.size(t) : X.kb[X.child0[p]] + X.kb[X.child1[p]];
                 X.kb[p] = std::min(X.rowsb[p], X.Z_rows[p]);
-                if (X.child0[p] < 0) X.lev_max_leafrows[l] = std::max(X.lev_max_leafrows[l], (int)T.size(t));
+                if (X.child0[p] < 0 && own[t] == me) X.lev_max_leafrows[l] = std::max(X.lev_max_leafrows[l], (int)T.size(t));
             }
-        X.Z_off.assign(np, 0);
-        X.C_off.assign(np, 0);
-        X.Q_off.assign(np, 0);
-        X.sig_off.assign(np, 0);
+        // slabs: own pairs (Z, C, Q, sigma); column pairs of own blocks owned elsewhere (C' only)
+        std::vector<char> imp(np, 0);
+        if (side == 1)
+            for (int b = C->b_lo; b < C->b_hi; ++b)
+                if (own[C->blk_s[b]] != me) imp[C->blk_pcol[b]] = 1;
+        X.Z_off.assign(np, -1);
+        X.C_off.assign(np, -1);
+        X.Q_off.assign(np, -1);
+        X.sig_off.assign(np, -1);
         for (int p = 0; p < np; ++p) {
-            X.Z_off[p] = X.Z_total;
-            X.Z_total += (int64_t)X.Z_rows[p] * k;
-            X.C_off[p] = X.C_total;
-            X.C_total += (int64_t)X.kb[p] * k;
-            X.Q_off[p] = X.Q_total;
-            X.Q_total += (int64_t)X.rowsb[p] * X.kb[p];
-            X.sig_off[p] = X.sig_total;
-            X.sig_total += X.kb[p];
+            const bool mine = own[C->bp_t[X.bp[p]]] == me;
+            if (mine) {
+                X.Z_off[p] = X.Z_total;
+                X.Z_total += (int64_t)X.Z_rows[p] * k;
+                X.Q_off[p] = X.Q_total;
+                X.Q_total += (int64_t)X.rowsb[p] * X.kb[p];
+                X.sig_off[p] = X.sig_total;
+                X.sig_total += X.kb[p];
+            }
+            if (mine || imp[p]) {
+                X.C_off[p] = X.C_total;
+                X.C_total += (int64_t)X.kb[p] * k;
+            }
         }
         // leaf-cluster groups (contiguous pairs of one leaf cluster)
         X.lc_ptr.push_back(0);
         int lastt = -1;
+        X.lc_lo = -1;
         for (int p = 0; p < np; ++p) {
             int t = C->bp_t[X.bp[p]];
             if (!T.is_leaf(t)) continue;
             if (t != lastt && !X.lc.empty()) X.lc_ptr.push_back((int)X.lc.size());
+            if (t != lastt && own[t] == me) {
+                const int g = (int)X.lc_ptr.size() - 1;
+                if (X.lc_lo < 0) X.lc_lo = g;
+                X.lc_hi = g + 1;
+            }
             X.lc.push_back(p);
             lastt = t;
         }
         if (!X.lc.empty()) X.lc_ptr.push_back((int)X.lc.size());
+        if (X.lc_lo < 0) X.lc_lo = X.lc_hi = 0;
     }
     // antipodal mirror b' = (s, t, -c) of every block: S_{b'} = S_b^T exactly (DESIGN §total weights)
     {
@@ -507,14 +610,39 @@ void build_tables(dh2_ctx* C) {
         }
     }
     check_symmetry(C);
-    C->blk_St_off.assign(nb, 0);
-    for (int b = 0; b < nb; ++b) {
+    if (W > 1 && !C->sym_ok)
+        throw NotImpl("sharding needs the adjoint-symmetric structure (" + C->sym_why + ")");
+    C->blk_St_off.assign(nb, -1);
+    for (int b = C->b_lo; b < C->b_hi; ++b) {
         C->blk_St_off[b] = C->St_total;
         C->St_total += (int64_t)C->row.kb[C->blk_prow[b]] * C->col.kb[C->blk_pcol[b]];
     }
+    // exchange lists: for a block (t,s,c) with owner(t) != owner(s), owner(s)
+    // sends R_sc (if computed by QR) and the column results C'_sc, k'_sc (and xh'_sc in matvec)
+    C->R_send.assign(W, {});
+    C->R_recv.assign(W, {});
+    C->C_send.assign(W, {});
+    C->C_recv.assign(W, {});
+    for (int b = 0; b < nb; ++b) {
+        const int rt = own[C->blk_t[b]], rs = own[C->blk_s[b]];
+        if (rt == rs || (rt != me && rs != me)) continue;
+        const int bp = C->blk_bpcol[b], p = C->blk_pcol[b];
+        if (rs == me) {
+            if (r_by_qr(bp)) C->R_send[rt].push_back(bp);
+            C->C_send[rt].push_back(p);
+        } else {
+            if (r_by_qr(bp)) C->R_recv[rs].push_back(bp);
+            C->C_recv[rs].push_back(p);
+        }
+    }
+    for (auto* v : {&C->R_send, &C->R_recv, &C->C_send, &C->C_recv})
+        for (auto& l : *v) {
+            std::sort(l.begin(), l.end());
+            l.erase(std::unique(l.begin(), l.end()), l.end());
+        }
 }
 
-void upload_pass(dh2_ctx* C, PassH& X, PassD& D, bool alloc_Z) {
+void upload_pass(Shard* C, PassH& X, PassD& D, bool alloc_Z) {
     cudaStream_t s = C->stream;
     X.d_bp.upload(X.bp, s);
     X.d_child0.upload(X.child0, s);
@@ -568,9 +696,9 @@ void upload_pass(dh2_ctx* C, PassH& X, PassD& D, bool alloc_Z) {
     D.sweeps = X.d_sweeps.p;
 }
 
-size_t plan_bytes(const dh2_ctx* C) {
+size_t plan_bytes(const Shard* C) {
     size_t b = 0;
-    b += (size_t)C->VR_total * 16 + (size_t)C->E_total * 16 + C->st.blocks.size() * (size_t)C->k * C->k * 16;
+    b += (size_t)C->VR_total * 16 + (size_t)C->E_total * 16 + (size_t)(C->b_hi - C->b_lo) * C->k * C->k * 16;
     b += (size_t)C->St_total * 16;
     for (const PassH* X : {&C->row, &C->col})
         b += (size_t)((X == &C->col && C->sym_ok ? 0 : X->Z_total) + X->C_total + X->Q_total) * 16 + (size_t)X->sig_total * 8;
@@ -578,7 +706,7 @@ size_t plan_bytes(const dh2_ctx* C) {
     return b;
 }
 
-void upload_all(dh2_ctx* C, const double* xyz, int64_t nv, const int64_t* tri) {
+void upload_all(Shard* C, const double* xyz, int64_t nv, const int64_t* tri) {
     cudaStream_t s = C->stream;
     const ClusterTree& T = C->st.ct;
     size_t freeb = 0, totb = 0;
@@ -613,7 +741,13 @@ void upload_all(dh2_ctx* C, const double* xyz, int64_t nv, const int64_t* tri) {
     C->d_blk_prow.upload(C->blk_prow, s);
     C->d_blk_pcol.upload(C->blk_pcol, s);
     C->d_blk_St_off.upload(C->blk_St_off, s);
-    C->d_blk_mirror.upload(C->blk_mirror, s);
+    {
+        // mirror reads only where the mirror block is this shard's (else the strided S_b read)
+        std::vector<int> mir(C->blk_mirror);
+        for (int& b : mir)
+            if (b < C->b_lo || b >= C->b_hi) b = -1;
+        C->d_blk_mirror.upload(mir, s);
+    }
     auto up_list = [&](const std::vector<int>& v) -> const int* {
         C->d_lists.emplace_back(new DevBuf<int>());
         C->d_lists.back()->upload(v, s);
@@ -630,7 +764,7 @@ void upload_all(dh2_ctx* C, const double* xyz, int64_t nv, const int64_t* tri) {
     C->d_VR.alloc(C->VR_total);
     C->d_E.alloc(C->E_total);
     const size_t nb = C->st.blocks.size();
-    C->d_S.alloc(nb * C->k * C->k);
+    C->d_S.alloc((size_t)(C->b_hi - C->b_lo) * C->k * C->k);  // own blocks only
     C->d_St.alloc(C->St_total);
     C->d_omega.alloc(nb);
     C->d_normG2.alloc(nb);
@@ -679,7 +813,7 @@ void upload_all(dh2_ctx* C, const double* xyz, int64_t nv, const int64_t* tri) {
     P.blk_prow = C->d_blk_prow.p;
     P.blk_pcol = C->d_blk_pcol.p;
     P.blk_St_off = C->d_blk_St_off.p;
-    P.S = C->d_S.p;
+    P.S = C->d_S.p - (ptrdiff_t)C->b_lo * C->k * C->k;  // indexed by global block id
     P.St = C->d_St.p;
     P.omega = C->d_omega.p;
     P.normG2 = C->d_normG2.p;
@@ -689,7 +823,7 @@ void upload_all(dh2_ctx* C, const double* xyz, int64_t nv, const int64_t* tri) {
 }
 
 // Device set-up (§2): quadrature points, grids, leaf V, E factors, S.
-void run_setup(dh2_ctx* C) {
+void run_setup(Shard* C) {
     const PlanD& P = C->P;
     cudaStream_t s = C->stream;
     const int L = C->st.ct.depth;
@@ -712,9 +846,10 @@ void run_setup(dh2_ctx* C) {
             C->kstat["setup_E"].bytes += (double)ne * 6 * C->m * C->m * 16;
         }
     }
-    C->timed("setup_S", 1, [&] { launch_S(P, s); });
+    const int nb = C->b_hi - C->b_lo;
+    C->timed("setup_S", 1, [&] { launch_S(P, C->b_lo, nb, s); });
     auto& st = C->kstat["setup_S"];
-    double ent = (double)C->st.blocks.size() * k * k;
+    double ent = (double)nb * k * k;
     st.flops += ent * 20;
     st.bytes += ent * 16;
 }
@@ -724,12 +859,12 @@ inline double qr_flops(double M, double N) {
     return 8.0 * (M * N * K - (M + N) * K * K / 2.0 + K * K * K / 3.0);
 }
 
-void run_recompress(dh2_ctx* C, double eps, int mode) {
+// Phase b: basis weights of this shard's basis pairs, bottom-up (Eq. 18).
+void run_basis(Shard* C) {
     const PlanD& P = C->P;
     cudaStream_t s = C->stream;
     const ClusterTree& T = C->st.ct;
     const int L = T.depth, k = C->k, m = C->m;
-    // basis weights, bottom-up (Eq. 18)
     for (int l = L; l >= 0; --l) {
         int nb = (int)C->basis_lists[l].size();
         if (!nb) continue;
@@ -748,17 +883,26 @@ void run_recompress(dh2_ctx* C, double eps, int mode) {
         }
         C->kstat["basis@" + std::to_string(l)].flops += fl;
     }
-    // block weights
-    C->timed("block_weights", 1, [&] { launch_block_weights(P, mode, C->d_blk_mirror.p, s); });
+}
+
+// Phases c-e: block weights, total weights (top-down) and truncation (bottom-up) of the row
+// pass over this shard's pairs; the column pass by adjoint symmetry (or a second pass, 1 shard).
+void run_weights_truncate(Shard* C, double eps, int mode) {
+    const PlanD& P = C->P;
+    cudaStream_t s = C->stream;
+    const ClusterTree& T = C->st.ct;
+    const int L = T.depth, k = C->k, m = C->m;
+    C->timed("block_weights", 1, [&] { launch_block_weights(P, C->b_lo, C->b_hi - C->b_lo, mode, C->d_blk_mirror.p, s); });
     {
         double fl = 0;
-        for (size_t b = 0; b < C->st.blocks.size(); ++b) {
+        for (int b = C->b_lo; b < C->b_hi; ++b) {
             double rt = C->bp_R_rows[C->blk_bprow[b]], rs = C->bp_R_rows[C->blk_bpcol[b]];
             fl += 8.0 * (rt * k * k + rt * rs * k);
         }
         C->kstat["block_weights"].flops += fl;
     }
     const bool sym = C->sym_ok && C->sym_opt;
+    if (!sym && C->world > 1) throw NotImpl("sharded recompression needs adjoint_symmetry = 1");
     if (!sym && !C->col.d_Z.p && C->col.Z_total) {  // two passes requested on a symmetric structure
         C->col.d_Z.alloc(C->col.Z_total);
         C->P.col.Z = C->col.d_Z.p;
@@ -769,21 +913,23 @@ void run_recompress(dh2_ctx* C, double eps, int mode) {
         const bool row = side == 0;
         if (!row && sym) {
             // column pass = conjugate of the row pass at -c (check_symmetry)
-            const int np = (int)X.bp.size();
-            C->timed("mirror_col", 1, [&] { launch_mirror_pass(P, C->d_col2row.p, np, s); });
-            X.rank.resize(np);
-            for (int p = 0; p < np; ++p) X.rank[p] = C->row.rank[C->col2row[p]];
+            X.rank.assign(X.bp.size(), 0);
             double by = 0;
-            for (int p = 0; p < np; ++p) {
-                const int kk = X.rank[p];
-                by += 2.0 * 16.0 * ((double)kk * k + (double)X.rowsb[p] * kk);
+            for (int l = 0; l <= L; ++l) {
+                const int p0 = X.own_lo[l], np = X.own_hi[l] - p0;
+                if (!np) continue;
+                C->timed("mirror_col", 1, [&] { launch_mirror_pass(P, C->d_col2row.p, p0, np, s); });
+                for (int p = p0; p < p0 + np; ++p) {
+                    const int kk = X.rank[p] = C->row.rank[C->col2row[p]];
+                    by += 2.0 * 16.0 * ((double)kk * k + (double)X.rowsb[p] * kk);
+                }
             }
             C->kstat["mirror_col"].bytes += by;
             continue;
         }
         // total weights, top-down
         for (int l = 0; l <= L; ++l) {
-            int p0 = X.lev_ptr[l], np = X.lev_ptr[l + 1] - p0;
+            int p0 = X.own_lo[l], np = X.own_hi[l] - p0;
             if (!np) continue;
             C->timed(std::string(row ? "total_weights_row@" : "total_weights_col@") + std::to_string(l), 1, [&] { launch_total_weights(P, row, p0, np, C->d_blk_mirror.p, s); });
             double fl = 0;
@@ -800,7 +946,7 @@ void run_recompress(dh2_ctx* C, double eps, int mode) {
         // truncation, bottom-up
         X.rank.assign(X.bp.size(), 0);
         for (int l = L; l >= 0; --l) {
-            int p0 = X.lev_ptr[l], np = X.lev_ptr[l + 1] - p0;
+            int p0 = X.own_lo[l], np = X.own_hi[l] - p0;
             if (!np) continue;
             int maxrows = X.lev_max_leafrows[l];
             for (int p = p0; p < p0 + np; ++p)
@@ -813,7 +959,16 @@ void run_recompress(dh2_ctx* C, double eps, int mode) {
             }
             if (any_leaf && !all_leaf)  // median-split trees never mix leaves and inner clusters on a level
                 throw NotImpl("a tree level mixing leaf and non-leaf clusters is not supported by k_truncate");
-            C->timed(std::string(row ? "truncate_row@" : "truncate_col@") + std::to_string(l), 1, [&] { launch_truncate(P, row, p0, np, maxrows, maxz, all_leaf, eps, mode, s); });
+            const TruncLaunch TL = plan_truncate(P, np, maxrows, maxz, all_leaf, C->force_ws != 0);
+            if (TL.use_ws) {
+                const size_t need = (size_t)TL.grid * TL.ws_stride;
+                if (C->d_ws.n < need) {
+                    CK(cudaStreamSynchronize(s));
+                    C->d_ws.alloc(need);
+                }
+                ++C->ws_launches;
+            }
+            C->timed(std::string(row ? "truncate_row@" : "truncate_col@") + std::to_string(l), 1, [&] { launch_truncate(P, row, p0, np, TL, all_leaf, eps, mode, C->d_ws.p, s); });
             CK(cudaMemcpyAsync(X.rank.data() + p0, X.d_rank.p + p0, np * sizeof(int), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             double fl = 0;
@@ -830,122 +985,125 @@ void run_recompress(dh2_ctx* C, double eps, int mode) {
             C->kstat[std::string(row ? "truncate_row@" : "truncate_col@") + std::to_string(l)].flops += fl;
         }
     }
-    // projection
-    int maxkrow = 0;
-    for (int r : C->row.rank) maxkrow = std::max(maxkrow, r);
-    C->timed("project", 1, [&] { launch_project(P, maxkrow, s); });
-    {
-        double fl = 0;
-        for (size_t b = 0; b < C->st.blocks.size(); ++b) {
-            double kt = C->row.rank[C->blk_prow[b]], ks = C->col.rank[C->blk_pcol[b]];
-            fl += 8.0 * (kt * k * k + kt * ks * k);
-        }
-        C->kstat["project"].flops += fl;
-    }
 }
 
-void run_matvec(dh2_ctx* C, bool recomp, const double2* x, double2* y) {
+// Phase f: projection of this shard's blocks, S~_b = C_tc S_b C'^*_sc.
+void run_project(Shard* C) {
+    const PlanD& P = C->P;
+    const int k = C->k;
+    int maxkrow = 0;
+    for (int l = 0; l < (int)C->row.own_lo.size(); ++l)
+        for (int p = C->row.own_lo[l]; p < C->row.own_hi[l]; ++p) maxkrow = std::max(maxkrow, C->row.rank[p]);
+    C->timed("project", 1, [&] { launch_project(P, C->b_lo, C->b_hi - C->b_lo, maxkrow, C->stream); });
+    double fl = 0;
+    for (int b = C->b_lo; b < C->b_hi; ++b) {
+        double kt = C->row.rank[C->blk_prow[b]], ks = C->col.rank[C->blk_pcol[b]];
+        fl += 8.0 * (kt * k * k + kt * ks * k);
+    }
+    C->kstat["project"].flops += fl;
+}
+
+// certified sums of this shard: discarded squares of its own row/column pairs, ||G_b||^2 of its blocks
+void local_sums(Shard* C, double out[3]) {
+    out[0] = out[1] = out[2] = 0.0;
+    for (int side = 0; side < 2; ++side) {
+        PassH& X = side == 0 ? C->row : C->col;
+        X.disc.assign(X.bp.size(), 0.0);
+        for (int l = 0; l < (int)X.own_lo.size(); ++l) {
+            const int p0 = X.own_lo[l], np = X.own_hi[l] - p0;
+            if (np) CK(cudaMemcpy(X.disc.data() + p0, X.d_disc.p + p0, np * sizeof(double), cudaMemcpyDeviceToHost));
+        }
+        for (double d : X.disc) out[side] += d;
+    }
+    std::vector<double> g2(C->b_hi - C->b_lo);
+    if (!g2.empty())
+        CK(cudaMemcpy(g2.data(), C->d_normG2.p + C->b_lo, g2.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    for (double d : g2) out[2] += d;
+}
+
+// Matvec, part 1: x (original order) -> cluster order, forward transformation of this shard's
+// column pairs (xh'_sc = B_sc^* x|_s, nested through the transfers), bottom-up.
+void run_mv_forward(Shard* C, bool recomp, const double2* x) {
     const PlanD& P = C->P;
     cudaStream_t s = C->stream;
     const int L = C->st.ct.depth, n = C->n;
     C->timed("matvec", 1, [&] { launch_permute(P.perm, x, C->d_xp.p, n, true, s); });
     for (int l = L; l >= 0; --l) {
-        int p0 = C->col.lev_ptr[l], np = C->col.lev_ptr[l + 1] - p0;
+        int p0 = C->col.own_lo[l], np = C->col.own_hi[l] - p0;
         if (np) C->timed("matvec", 1, [&] { launch_mv_forward(P, recomp, p0, np, C->d_xp.p, C->d_xh.p, s); });
     }
-    C->timed("matvec", 1, [&] { launch_mv_couple(P, recomp, C->d_xh.p, C->d_yh.p, s); });
+}
+
+// Matvec, part 2 (after the xh' exchange): couplings, backward transformation and leaf output
+// of this shard's row pairs into the cluster-ordered yp (own position range).
+void run_mv_rest(Shard* C, bool recomp) {
+    const PlanD& P = C->P;
+    cudaStream_t s = C->stream;
+    const int L = C->st.ct.depth, n = C->n;
     for (int l = 0; l <= L; ++l) {
-        int p0 = C->row.lev_ptr[l], np = C->row.lev_ptr[l + 1] - p0;
+        int p0 = C->row.own_lo[l], np = C->row.own_hi[l] - p0;
+        if (np) C->timed("matvec", 1, [&] { launch_mv_couple(P, recomp, p0, np, C->d_xh.p, C->d_yh.p, s); });
+    }
+    for (int l = 0; l <= L; ++l) {
+        int p0 = C->row.own_lo[l], np = C->row.own_hi[l] - p0;
         if (np) C->timed("matvec", 1, [&] { launch_mv_backward(P, recomp, p0, np, C->d_yh.p, s); });
     }
     CK(cudaMemsetAsync(C->d_yp.p, 0, sizeof(double2) * n, s));
-    int nlc = (int)C->row.lc_ptr.size() - 1;
     C->timed("matvec", 1, [&] {
-        launch_mv_leaf_out(P, recomp, C->row.d_lc.p, C->row.d_lc_ptr.p, std::max(nlc, 0), C->d_yh.p, C->d_yp.p, s);
+        launch_mv_leaf_out(P, recomp, C->row.d_lc.p, C->row.d_lc_ptr.p, C->row.lc_lo, C->row.lc_hi - C->row.lc_lo, C->d_yh.p,
+                           C->d_yp.p, s);
     });
-    C->timed("matvec", 1, [&] { launch_permute(P.perm, C->d_yp.p, y, n, false, s); });
 }
 
-void require_device(const dh2_ctx* C) {
+// Matvec, part 3 (after the yp gather): cluster order -> original order.
+void run_mv_out(Shard* C, double2* y) {
+    C->timed("matvec", 1, [&] { launch_permute(C->P.perm, C->d_yp.p, y, C->n, false, C->stream); });
+}
+
+void require_device(const Shard* C) {
     if (C->device == DH2_DEVICE_NONE) throw StateError("structure-only context (device = DH2_DEVICE_NONE) has no device data");
 }
 
-int fail(dh2_ctx* C, int code, const std::string& msg) {
-    if (C) C->err = msg;
-    g_last_error = msg;
-    return code;
-}
-
-template <typename F>
-int guarded(dh2_ctx* C, F&& f) {
-    try {
-        f();
-        return DH2_OK;
-    } catch (const std::invalid_argument& e) {
-        return fail(C, DH2_EINVAL, e.what());
-    } catch (const CudaError& e) {
-        return fail(C, DH2_ECUDA, e.what());
-    } catch (const StateError& e) {
-        return fail(C, DH2_ESTATE, e.what());
-    } catch (const NotImpl& e) {
-        return fail(C, DH2_ENOTIMPL, e.what());
-    } catch (const NoMem& e) {
-        return fail(C, DH2_ENOMEM, e.what());
-    } catch (const std::bad_alloc& e) {
-        return fail(C, DH2_ENOMEM, "host allocation failed");
-    } catch (const std::exception& e) {
-        return fail(C, DH2_ECUDA, std::string("internal error: ") + e.what());
-    }
-}
-
-void storage_report(const dh2_ctx* C, int which, dh2_storage_report* out) {
+// Storage of this shard's part (DESIGN R21): own pairs, own blocks, nearfield
+// blocks whose row cluster it owns.  v = {row basis, col basis, couplings, nearfield, sum of
+// ranks, number of ranks, max rank} (bytes; 16 B per complex entry).
+void storage_partial(const Shard* C, int which, double v[7]) {
     const Structure& S = C->st;
     const ClusterTree& T = S.ct;
-    const int k = C->k;
-    double near = 0;
-    for (auto& pr : S.near) near += (double)T.size(pr.first) * T.size(pr.second) * 16.0;
-    auto basis = [&](const PassH& X, bool recomp) {
-        double tot = 0;
-        for (size_t p = 0; p < X.bp.size(); ++p) {
-            int t = C->bp_t[X.bp[p]];
-            if (X.child0[p] < 0)
-                tot += (double)T.size(t) * (recomp ? X.rank[p] : k);
-            else if (recomp)
-                tot += (double)(X.rank[X.child0[p]] + X.rank[X.child1[p]]) * X.rank[p];
-            else
-                tot += 2.0 * k * k;
-        }
-        return tot * 16.0;
-    };
+    const int k = C->k, me = C->rank;
     const bool rc = which == DH2_RECOMP;
-    out->n = C->n;
-    out->row_basis_bytes = basis(C->row, rc);
-    out->col_basis_bytes = basis(C->col, rc);
-    double coup = 0;
-    int maxr = 0;
-    double sumr = 0;
-    int64_t cnt = 0;
-    if (rc) {
-        for (size_t b = 0; b < S.blocks.size(); ++b)
-            coup += (double)C->row.rank[C->blk_prow[b]] * C->col.rank[C->blk_pcol[b]] * 16.0;
-        for (const PassH* X : {&C->row, &C->col})
-            for (int r : X->rank) {
-                maxr = std::max(maxr, r);
-                sumr += r;
-                ++cnt;
-            }
-    } else {
-        coup = (double)S.blocks.size() * k * k * 16.0;
-        maxr = k;
-        sumr = k;
-        cnt = 1;
+    for (int i = 0; i < 7; ++i) v[i] = 0.0;
+    for (auto& pr : S.near) {
+        const int o = C->owner[pr.first];
+        if (o == me || (o < 0 && me == 0)) v[3] += (double)T.size(pr.first) * T.size(pr.second) * 16.0;
     }
-    out->coupling_bytes = coup;
-    out->nearfield_bytes = near;
-    out->kb_per_dof_basis = (out->row_basis_bytes + out->col_basis_bytes) / C->n / 1024.0;
-    out->kb_per_dof_matrix = (out->row_basis_bytes + out->col_basis_bytes + coup + near) / C->n / 1024.0;
-    out->max_rank = maxr;
-    out->mean_rank = cnt ? sumr / cnt : 0.0;
+    for (int side = 0; side < 2; ++side) {
+        const PassH& X = side == 0 ? C->row : C->col;
+        double tot = 0;
+        for (int l = 0; l < (int)X.own_lo.size(); ++l)
+            for (int p = X.own_lo[l]; p < X.own_hi[l]; ++p) {
+                int t = C->bp_t[X.bp[p]];
+                if (X.child0[p] < 0)
+                    tot += (double)T.size(t) * (rc ? X.rank[p] : k);
+                else if (rc)
+                    tot += (double)(X.rank[X.child0[p]] + X.rank[X.child1[p]]) * X.rank[p];
+                else
+                    tot += 2.0 * k * k;
+                if (rc) {
+                    v[4] += X.rank[p];
+                    v[5] += 1;
+                    v[6] = std::max(v[6], (double)X.rank[p]);
+                }
+            }
+        v[side] = tot * 16.0;
+    }
+    for (int b = C->b_lo; b < C->b_hi; ++b)
+        v[2] += rc ? (double)C->row.rank[C->blk_prow[b]] * C->col.rank[C->blk_pcol[b]] * 16.0 : (double)k * k * 16.0;
+    if (!rc) {
+        v[4] = k;
+        v[5] = 1;
+        v[6] = k;
+    }
 }
 
 struct ExportItem {
@@ -964,184 +1122,10 @@ ExportItem dv(const DevBuf<T>& b) {
     return {b.p, b.n * sizeof(T), true, sizeof(T)};
 }
 
-}  // namespace
-
-// ============================================================== C ABI
-extern "C" {
-
-int dh2_build_interp(const dh2_mesh* mesh, const dh2_params* params, const dh2_dist* dist, dh2_ctx** out) {
-    if (out) *out = nullptr;
-    if (!mesh || !params || !out) return fail(nullptr, DH2_EINVAL, "null argument");
-    std::unique_ptr<dh2_ctx> C(new dh2_ctx());
-    int rc = guarded(C.get(), [&] {
-        const dh2_params& p = *params;
-        if (!(p.kappa >= 0.0) || p.m < 1 || p.leaf_size < 1 || !(p.eta1 > 0.0) || !(p.eta2 > 0.0))
-            throw std::invalid_argument("invalid parameters");
-        if (p.quad != 7) throw std::invalid_argument("quad must be 7 (Radon's degree-5 rule)");
-        if (p.m > 4) throw NotImpl("m > 4 (k > 64) needs the cluster/DSMEM kernels (not in this build)");
-        if (mesh->nt > (int64_t)1 << 30) throw std::invalid_argument("mesh too large");
-        validate_mesh(mesh->xyz, mesh->nv, mesh->tri, mesh->nt);
-        if (dist && dist->world > 1) throw NotImpl("multi-GPU sharding is not in this build");
-        C->device = dist ? dist->device : 0;
-        const bool structure_only = C->device == DH2_DEVICE_NONE;
-        if (!structure_only) {
-            int ndev = 0;
-            if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) throw CudaError("no CUDA device");
-            CK(cudaSetDevice(C->device));
-        }
-        auto t0 = std::chrono::steady_clock::now();
-        Params prm;
-        prm.kappa = p.kappa;
-        prm.m = p.m;
-        prm.leaf = p.leaf_size;
-        prm.eta1 = p.eta1;
-        prm.eta2 = p.eta2;
-        C->st.build(mesh->xyz, mesh->nv, mesh->tri, mesh->nt, prm);
-        auto tt = std::chrono::steady_clock::now();
-        build_tables(C.get());
-        C->host_tables_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tt).count();
-        C->host_build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-        if (structure_only) return;
-        CK(cudaStreamCreateWithFlags(&C->own_stream, cudaStreamNonBlocking));
-        C->stream = C->own_stream;
-        CK(configure_kernels());
-        upload_all(C.get(), mesh->xyz, mesh->nv, mesh->tri);
-        run_setup(C.get());
-        C->finish();
-    });
-    if (rc != DH2_OK) return rc;
-    *out = C.release();
-    return DH2_OK;
-}
-
-int dh2_setup_device(dh2_ctx* C) {
-    if (!C) return fail(nullptr, DH2_EINVAL, "null context");
-    return guarded(C, [&] {
-        require_device(C);
-        CK(cudaSetDevice(C->device));
-        run_setup(C);
-        C->recompressed = false;
-        C->finish();
-    });
-}
-
-int dh2_recompress(dh2_ctx* C, double eps, int32_t mode) {
-    if (!C) return fail(nullptr, DH2_EINVAL, "null context");
-    return guarded(C, [&] {
-        if (!(eps >= 0.0) || mode < 0 || mode > 2) throw std::invalid_argument("invalid eps or mode");
-        require_device(C);
-        CK(cudaSetDevice(C->device));
-        C->eps = eps;
-        C->mode = mode;
-        run_recompress(C, eps, mode);
-        C->finish();
-        // certified sums (host reduction of the per-pair device results)
-        for (PassH* X : {&C->row, &C->col}) {
-            X->disc.resize(X->bp.size());
-            CK(cudaMemcpy(X->disc.data(), X->d_disc.p, X->disc.size() * sizeof(double), cudaMemcpyDeviceToHost));
-        }
-        std::vector<double> g2(C->st.blocks.size());
-        CK(cudaMemcpy(g2.data(), C->d_normG2.p, g2.size() * sizeof(double), cudaMemcpyDeviceToHost));
-        C->E_row = C->E_col = C->far2 = 0;
-        for (double d : C->row.disc) C->E_row += d;
-        for (double d : C->col.disc) C->E_col += d;
-        for (double d : g2) C->far2 += d;
-        C->recompressed = true;
-    });
-}
-
-int dh2_matvec(dh2_ctx* C, int32_t which, const double* x, double* y, int32_t flags) {
-    if (!C) return fail(nullptr, DH2_EINVAL, "null context");
-    return guarded(C, [&] {
-        if (!x || !y || (which != DH2_ORIG && which != DH2_RECOMP)) throw std::invalid_argument("invalid matvec arguments");
-        if (which == DH2_RECOMP && !C->recompressed) throw StateError("RECOMP matvec before dh2_recompress");
-        require_device(C);
-        CK(cudaSetDevice(C->device));
-        const size_t nb = (size_t)C->n * sizeof(double2);
-        if (flags & DH2_DEVICE_PTRS) {
-            run_matvec(C, which == DH2_RECOMP, reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y));
-        } else {
-            CK(cudaMemcpyAsync(C->d_x.p, x, nb, cudaMemcpyHostToDevice, C->stream));
-            run_matvec(C, which == DH2_RECOMP, C->d_x.p, C->d_y.p);
-            CK(cudaMemcpyAsync(y, C->d_y.p, nb, cudaMemcpyDeviceToHost, C->stream));
-        }
-        C->finish();
-    });
-}
-
-int dh2_storage(const dh2_ctx* C, int32_t which, dh2_storage_report* out) {
-    if (!C || !out) return fail(nullptr, DH2_EINVAL, "null argument");
-    dh2_ctx* Cm = const_cast<dh2_ctx*>(C);
-    return guarded(Cm, [&] {
-        if (which == DH2_RECOMP && !C->recompressed) throw StateError("RECOMP storage before dh2_recompress");
-        if (which != DH2_ORIG && which != DH2_RECOMP) throw std::invalid_argument("invalid which");
-        storage_report(C, which, out);
-    });
-}
-
-int dh2_set_stream(dh2_ctx* C, void* stream) {
-    if (!C) return fail(nullptr, DH2_EINVAL, "null context");
-    C->stream = stream ? reinterpret_cast<cudaStream_t>(stream) : C->own_stream;
-    return DH2_OK;
-}
-
-int dh2_set_option(dh2_ctx* C, const char* name, int64_t value) {
-    if (!C || !name) return fail(nullptr, DH2_EINVAL, "null argument");
-    const std::string nm(name);
-    if (nm == "adjoint_symmetry") {
-        if (value != 0 && value != 1) return fail(C, DH2_EINVAL, "adjoint_symmetry must be 0 or 1");
-        C->sym_opt = (int)value;
-        return DH2_OK;
-    }
-    return fail(C, DH2_EINVAL, "unknown option " + nm);
-}
-
-int dh2_set_profiling(dh2_ctx* C, int32_t enable) {
-    if (!C) return fail(nullptr, DH2_EINVAL, "null context");
-    C->profiling = enable != 0;
-    return DH2_OK;
-}
-
-int dh2_get_stats(const dh2_ctx* C, char* buf, int64_t* len) {
-    if (!C || !len) return fail(nullptr, DH2_EINVAL, "null argument");
-    std::ostringstream o;
-    o.precision(17);
-    const Structure& S = C->st;
-    int64_t nrow = (int64_t)C->row.bp.size(), ncol = (int64_t)C->col.bp.size();
-    o << "{\"n\": " << C->n << ", \"k\": " << C->k << ", \"depth\": " << S.ct.depth
-      << ", \"clusters\": " << C->nclusters << ", \"blocks\": " << S.blocks.size() << ", \"near\": " << S.near.size()
-      << ", \"row_pairs\": " << nrow << ", \"col_pairs\": " << ncol << ", \"basis_pairs\": " << C->bp_t.size()
-      << ", \"host_build_ms\": " << C->host_build_ms << ", \"host_phases_ms\": {\"tree\": " << S.ms_tree
-      << ", \"dirs\": " << S.ms_dirs << ", \"blocks\": " << S.ms_blocks << ", \"closure\": " << S.ms_closure
-      << ", \"tables\": " << C->host_tables_ms << "}, \"launches_total\": " << C->launches_total
-      << ", \"E_row\": " << C->E_row << ", \"E_col\": " << C->E_col << ", \"far2\": " << C->far2
-      << ", \"device_bytes\": " << plan_bytes(C) << ", \"mirror_missing\": " << C->mirror_missing
-      << ", \"adjoint_symmetry\": {\"available\": " << (C->sym_ok ? "true" : "false") << ", \"enabled\": " << C->sym_opt
-      << ", \"used\": " << (C->sym_used ? "true" : "false") << ", \"why_not\": \"" << C->sym_why << "\"}"
-      << ", \"kernels\": {";
-    bool first = true;
-    for (auto& kv : C->kstat) {
-        if (!first) o << ", ";
-        first = false;
-        o << "\"" << kv.first << "\": {\"launches\": " << kv.second.launches << ", \"ms\": " << kv.second.ms
-          << ", \"flops\": " << kv.second.flops << ", \"bytes\": " << kv.second.bytes << "}";
-    }
-    o << "}}";
-    std::string s = o.str();
-    if (!buf) {
-        *len = (int64_t)s.size() + 1;
-        return DH2_OK;
-    }
-    if (*len < (int64_t)s.size() + 1) return fail(const_cast<dh2_ctx*>(C), DH2_EINVAL, "buffer too small");
-    std::memcpy(buf, s.c_str(), s.size() + 1);
-    return DH2_OK;
-}
-
-int dh2_export(const dh2_ctx* C, const char* name, void* buf, int64_t* nbytes) {
-    if (!C || !name || !nbytes) return fail(nullptr, DH2_EINVAL, "null argument");
-    dh2_ctx* Cm = const_cast<dh2_ctx*>(C);
-    return guarded(Cm, [&] {
+// Internal export of one shard's host/device arrays (names: DESIGN.md §12).
+void export_shard(const Shard* C, const char* name, void* buf, int64_t* nbytes) {
         static thread_local std::vector<int64_t> tmp64;
+        static thread_local std::vector<int> tmp32;
         static thread_local std::vector<double> tmpd;
         const Structure& S = C->st;
         const ClusterTree& T = S.ct;
@@ -1261,7 +1245,21 @@ int dh2_export(const dh2_ctx* C, const char* name, void* buf, int64_t* nbytes) {
         else if (nm == "blk_prow") it = hv(C->blk_prow);
         else if (nm == "blk_pcol") it = hv(C->blk_pcol);
         else if (nm == "blk_mirror") it = hv(C->blk_mirror);
-        else if (nm == "VR") it = dv(C->d_VR);
+        else if (nm == "owner") {
+            tmp32.assign(C->owner.begin(), C->owner.end());
+            it = hv(tmp32);
+        } else if (nm == "own_range") {
+            tmp32 = {C->b_lo, C->b_hi, (int)C->pos_lo, (int)C->pos_hi};
+            it = hv(tmp32);
+        } else if (nm == "xR_send" || nm == "xR_recv" || nm == "xC_send" || nm == "xC_recv") {
+            const auto& L = nm == "xR_send" ? C->R_send : nm == "xR_recv" ? C->R_recv : nm == "xC_send" ? C->C_send : C->C_recv;
+            tmp32.clear();
+            for (const auto& v : L) {
+                tmp32.push_back((int)v.size());
+                tmp32.insert(tmp32.end(), v.begin(), v.end());
+            }
+            it = hv(tmp32);
+        } else if (nm == "VR") it = dv(C->d_VR);
         else if (nm == "E") it = dv(C->d_E);
         else if (nm == "S") it = dv(C->d_S);
         else if (nm == "St") it = dv(C->d_St);
@@ -1288,15 +1286,653 @@ int dh2_export(const dh2_ctx* C, const char* name, void* buf, int64_t* nbytes) {
         }
         *nbytes = (int64_t)it.bytes;
         (void)tmpd;
+}
+
+}  // namespace
+
+// ============================================================== context (one or more shards)
+// A context holds the shards this process runs: 1 (single GPU, or one rank of an NCCL job) or,
+// in the virtual mode (world > 1 without an NCCL id), all `world` shards of the partition on one
+// device, run phase by phase with device-to-device exchanges.  Both modes execute the same
+// shard code and exchange the same items; only the transport differs.
+struct dh2_ctx {
+    std::vector<std::unique_ptr<Shard>> sh;
+    std::string err;
+    int world = 1, rank = 0;
+    bool virt = false;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool recompressed = false;
+    double E_row = 0, E_col = 0, far2 = 0;
+    double exch_bytes = 0;  // bytes moved by the last recompress + matvec exchanges (this process)
+    // NCCL transport
+    void* comm = nullptr;
+    DevBuf<double2> sendbuf, recvbuf;
+    DevBuf<int> isend, irecv;
+    DevBuf<double> red;
+    // cached segment lists: key = (kind, a, b)
+    struct Seg {
+        DevBuf<int64_t> soff, doff, len;
+        int n = 0;
+        std::vector<int64_t> peer_cnt;  // NCCL: elements per peer (pack order = peer order)
+        int64_t total = 0;
+    };
+    std::map<std::tuple<int, int, int>, std::unique_ptr<Seg>> segs;
+    ~dh2_ctx();
+};
+
+namespace {
+
+// ---------------------------------------------------------------- NCCL, loaded at run time
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api;
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        api.why = std::string("dlopen libnccl.so.2: ") + dlerror();
+        return api;
+    }
+    auto sym = [&](const char* nm) { return dlsym(h, nm); };
+    api.GetUniqueId = (decltype(api.GetUniqueId))sym("ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))sym("ncclCommInitRank");
+    api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
+    api.Send = (decltype(api.Send))sym("ncclSend");
+    api.Recv = (decltype(api.Recv))sym("ncclRecv");
+    api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
+    api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
+    api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
+    api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv && api.AllReduce &&
+             api.GroupStart && api.GroupEnd && api.GetErrorString;
+    if (!api.ok) api.why = "libnccl.so.2 lacks a required symbol";
+    return api;
+}
+
+struct NcclError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+#define NK(x)                                                                                           \
+    do {                                                                                                \
+        ncclResult_t r_ = (x);                                                                          \
+        if (r_ != ncclSuccess) throw NcclError(std::string(#x) + ": " + nccl().GetErrorString(r_));     \
+    } while (0)
+
+int fail(dh2_ctx* C, int code, const std::string& msg) {
+    if (C) C->err = msg;
+    g_last_error = msg;
+    return code;
+}
+
+template <typename F>
+int guarded(dh2_ctx* C, F&& f) {
+    try {
+        f();
+        return DH2_OK;
+    } catch (const std::invalid_argument& e) {
+        return fail(C, DH2_EINVAL, e.what());
+    } catch (const CudaError& e) {
+        return fail(C, DH2_ECUDA, e.what());
+    } catch (const NcclError& e) {
+        return fail(C, DH2_ENCCL, e.what());
+    } catch (const StateError& e) {
+        return fail(C, DH2_ESTATE, e.what());
+    } catch (const NotImpl& e) {
+        return fail(C, DH2_ENOTIMPL, e.what());
+    } catch (const NoMem& e) {
+        return fail(C, DH2_ENOMEM, e.what());
+    } catch (const std::bad_alloc& e) {
+        return fail(C, DH2_ENOMEM, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(C, DH2_ECUDA, std::string("internal error: ") + e.what());
+    }
+}
+
+// ---------------------------------------------------------------- exchanges
+enum XKind { X_R = 0, X_C = 1, X_RANK = 2, X_XH = 3 };
+
+// items exchanged from shard `from` to shard `to`, as seen by shard S (S is one of them)
+const std::vector<int>& items(const Shard* S, XKind kind, int peer, bool send) {
+    if (kind == X_R) return send ? S->R_send[peer] : S->R_recv[peer];
+    return send ? S->C_send[peer] : S->C_recv[peer];
+}
+
+// (offset, length) of one item in the shard's pool of that kind
+std::pair<int64_t, int64_t> item_seg(const Shard* S, XKind kind, int id) {
+    const int k = S->k;
+    switch (kind) {
+        case X_R: return {S->bp_R_off[id], (int64_t)S->bp_R_rows[id] * k};
+        case X_C: return {S->col.C_off[id], (int64_t)S->col.kb[id] * k};
+        case X_RANK: return {id, 1};
+        default: return {(int64_t)id * k, k};
+    }
+}
+
+void upload_seg(dh2_ctx::Seg& g, const std::vector<int64_t>& so, const std::vector<int64_t>& d, const std::vector<int64_t>& ln,
+                cudaStream_t s) {
+    g.soff.upload(so, s);
+    g.doff.upload(d, s);
+    g.len.upload(ln, s);
+    g.n = (int)so.size();
+}
+
+double2* pool2(Shard* S, XKind kind) { return kind == X_R ? S->d_VR.p : kind == X_C ? S->col.d_C.p : S->d_xh.p; }
+
+// one exchange of `kind` among all shards (virtual) or with all peers (NCCL)
+void exchange(dh2_ctx* X, XKind kind) {
+    cudaStream_t s = X->stream;
+    const int W = X->world;
+    if (W == 1) return;
+    if (X->virt) {
+        for (int a = 0; a < W; ++a)
+            for (int b = 0; b < W; ++b) {
+                if (a == b) continue;
+                Shard *A = X->sh[a].get(), *B = X->sh[b].get();
+                const auto& ia = items(A, kind, b, true);
+                if (ia.empty()) continue;
+                auto& slot = X->segs[{(int)kind, a, b}];
+                if (!slot) {
+                    const auto& ib = items(B, kind, a, false);
+                    if (ia != ib) throw std::logic_error("exchange lists of two shards disagree");
+                    slot.reset(new dh2_ctx::Seg());
+                    std::vector<int64_t> so, d, ln;
+                    for (int id : ia) {
+                        auto sa = item_seg(A, kind, id), sb = item_seg(B, kind, id);
+                        so.push_back(sa.first);
+                        d.push_back(sb.first);
+                        ln.push_back(sa.second);
+                        slot->total += sa.second;
+                    }
+                    upload_seg(*slot, so, d, ln, s);
+                }
+                if (kind == X_RANK)
+                    launch_copy_segments_i(A->col.d_rank.p, B->col.d_rank.p, slot->soff.p, slot->doff.p, slot->len.p, slot->n, s);
+                else
+                    launch_copy_segments(pool2(A, kind), pool2(B, kind), slot->soff.p, slot->doff.p, slot->len.p, slot->n, s);
+                X->exch_bytes += (double)slot->total * (kind == X_RANK ? 4 : 16);
+                CK(cudaGetLastError());
+            }
+        return;
+    }
+    // NCCL: pack -> grouped send/recv with every peer -> unpack
+    Shard* S = X->sh[0].get();
+    const int me = X->rank;
+    auto build = [&](bool send) {
+        auto& slot = X->segs[{(int)kind, send ? 0 : 1, -1}];
+        if (slot) return slot.get();
+        slot.reset(new dh2_ctx::Seg());
+        std::vector<int64_t> so, d, ln;
+        slot->peer_cnt.assign(W, 0);
+        int64_t pos = 0;
+        for (int peer = 0; peer < W; ++peer) {
+            if (peer == me) continue;
+            for (int id : items(S, kind, peer, send)) {
+                auto sg = item_seg(S, kind, id);
+                so.push_back(send ? sg.first : pos);
+                d.push_back(send ? pos : sg.first);
+                ln.push_back(sg.second);
+                pos += sg.second;
+                slot->peer_cnt[peer] += sg.second;
+            }
+        }
+        slot->total = pos;
+        upload_seg(*slot, so, d, ln, s);
+        return slot.get();
+    };
+    dh2_ctx::Seg* out = build(true);
+    dh2_ctx::Seg* in = build(false);
+    const bool ints = kind == X_RANK;
+    const size_t esz = ints ? sizeof(int) : sizeof(double2);
+    if (ints) {
+        if (X->isend.n < (size_t)out->total) X->isend.alloc(out->total);
+        if (X->irecv.n < (size_t)in->total) X->irecv.alloc(in->total);
+        launch_copy_segments_i(S->col.d_rank.p, X->isend.p, out->soff.p, out->doff.p, out->len.p, out->n, s);
+    } else {
+        if (X->sendbuf.n < (size_t)out->total) X->sendbuf.alloc(out->total);
+        if (X->recvbuf.n < (size_t)in->total) X->recvbuf.alloc(in->total);
+        launch_copy_segments(pool2(S, kind), X->sendbuf.p, out->soff.p, out->doff.p, out->len.p, out->n, s);
+    }
+    CK(cudaGetLastError());
+    char* sb = ints ? (char*)X->isend.p : (char*)X->sendbuf.p;
+    char* rb = ints ? (char*)X->irecv.p : (char*)X->recvbuf.p;
+    ncclComm_t comm = (ncclComm_t)X->comm;
+    NK(nccl().GroupStart());
+    int64_t so = 0, ro = 0;
+    for (int peer = 0; peer < W; ++peer) {
+        if (peer == me) continue;
+        if (out->peer_cnt[peer]) NK(nccl().Send(sb + so * esz, out->peer_cnt[peer] * esz, ncclUint8, peer, comm, s));
+        if (in->peer_cnt[peer]) NK(nccl().Recv(rb + ro * esz, in->peer_cnt[peer] * esz, ncclUint8, peer, comm, s));
+        so += out->peer_cnt[peer];
+        ro += in->peer_cnt[peer];
+    }
+    NK(nccl().GroupEnd());
+    if (ints)
+        launch_copy_segments_i(X->irecv.p, S->col.d_rank.p, in->soff.p, in->doff.p, in->len.p, in->n, s);
+    else
+        launch_copy_segments(X->recvbuf.p, pool2(S, kind), in->soff.p, in->doff.p, in->len.p, in->n, s);
+    CK(cudaGetLastError());
+    X->exch_bytes += (double)(out->total + in->total) * esz;
+}
+
+// gather the cluster-ordered output slices of all shards (every rank / shard 0 gets all of yp)
+void gather_y(dh2_ctx* X) {
+    const int W = X->world;
+    if (W == 1) return;
+    cudaStream_t s = X->stream;
+    Shard* S0 = X->sh[0].get();
+    const ClusterTree& T = S0->st.ct;
+    auto range = [&](int r) {
+        const int64_t t = T.levels[S0->cut][r];
+        return std::make_pair(T.begin[t], T.end[t]);
+    };
+    if (X->virt) {
+        for (int r = 1; r < W; ++r) {
+            auto g = range(r);
+            CK(cudaMemcpyAsync(S0->d_yp.p + g.first, X->sh[r]->d_yp.p + g.first, (g.second - g.first) * sizeof(double2),
+                               cudaMemcpyDeviceToDevice, s));
+        }
+        return;
+    }
+    ncclComm_t comm = (ncclComm_t)X->comm;
+    auto mine = range(X->rank);
+    NK(nccl().GroupStart());
+    for (int peer = 0; peer < W; ++peer) {
+        if (peer == X->rank) continue;
+        auto g = range(peer);
+        NK(nccl().Send(S0->d_yp.p + mine.first, (mine.second - mine.first) * sizeof(double2), ncclUint8, peer, comm, s));
+        NK(nccl().Recv(S0->d_yp.p + g.first, (g.second - g.first) * sizeof(double2), ncclUint8, peer, comm, s));
+    }
+    NK(nccl().GroupEnd());
+}
+
+// sum (or max) of a few doubles over all shards / ranks
+void reduce_doubles(dh2_ctx* X, std::vector<double>& v, bool max_op) {
+    if (X->world == 1 || X->virt) return;  // virtual: the caller already combined the shards
+    if (X->red.n < v.size()) X->red.alloc(v.size());
+    CK(cudaMemcpyAsync(X->red.p, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice, X->stream));
+    NK(nccl().AllReduce(X->red.p, X->red.p, v.size(), ncclFloat64, max_op ? ncclMax : ncclSum, (ncclComm_t)X->comm, X->stream));
+    CK(cudaMemcpyAsync(v.data(), X->red.p, v.size() * sizeof(double), cudaMemcpyDeviceToHost, X->stream));
+    CK(cudaStreamSynchronize(X->stream));
+}
+
+void finish_all(dh2_ctx* X) {
+    for (auto& S : X->sh) S->finish();
+}
+
+void require_device(const dh2_ctx* X) { require_device(X->sh[0].get()); }
+
+void do_recompress(dh2_ctx* X, double eps, int mode) {
+    for (auto& S : X->sh) run_basis(S.get());
+    exchange(X, X_R);  // R_sc of column pairs referenced across shards (after phase b)
+    for (auto& S : X->sh) run_weights_truncate(S.get(), eps, mode);
+    exchange(X, X_C);  // C'_sc and k'_sc (after the column truncation)
+    exchange(X, X_RANK);
+    if (X->world > 1) {
+        CK(cudaStreamSynchronize(X->stream));
+        for (auto& S : X->sh) {  // host copies of the imported column ranks (projection flops, storage)
+            std::vector<int> all(S->col.bp.size());
+            CK(cudaMemcpy(all.data(), S->col.d_rank.p, all.size() * sizeof(int), cudaMemcpyDeviceToHost));
+            for (int peer = 0; peer < X->world; ++peer)
+                for (int p : S->C_recv[peer]) S->col.rank[p] = all[p];
+        }
+    }
+    for (auto& S : X->sh) run_project(S.get());
+    finish_all(X);
+    std::vector<double> sums(3, 0.0);
+    for (auto& S : X->sh) {
+        double v[3];
+        local_sums(S.get(), v);
+        for (int i = 0; i < 3; ++i) sums[i] += v[i];
+    }
+    reduce_doubles(X, sums, false);
+    X->E_row = sums[0];
+    X->E_col = sums[1];
+    X->far2 = sums[2];
+}
+
+void do_matvec(dh2_ctx* X, bool recomp, const double2* x, double2* y) {
+    for (auto& S : X->sh) run_mv_forward(S.get(), recomp, x);
+    exchange(X, X_XH);  // xh'_sc of column pairs referenced across shards
+    for (auto& S : X->sh) run_mv_rest(S.get(), recomp);
+    gather_y(X);
+    run_mv_out(X->sh[0].get(), y);
+    if (!X->virt)
+        for (size_t i = 1; i < X->sh.size(); ++i) run_mv_out(X->sh[i].get(), y);
+}
+
+}  // namespace
+
+dh2_ctx::~dh2_ctx() {
+    for (auto& S : sh)
+        if (S->device != DH2_DEVICE_NONE && S->stream) {
+            cudaSetDevice(S->device);
+            cudaStreamSynchronize(S->stream);
+        }
+    segs.clear();
+    sh.clear();
+    if (comm && nccl().ok) nccl().CommDestroy((ncclComm_t)comm);
+}
+
+// ============================================================== C ABI
+extern "C" {
+
+int dh2_nccl_unique_id(void* uid) {
+    if (!uid) return fail(nullptr, DH2_EINVAL, "null argument");
+    NcclApi& api = nccl();
+    if (!api.ok) return fail(nullptr, DH2_ENCCL, api.why);
+    ncclUniqueId id;
+    ncclResult_t r = api.GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(nullptr, DH2_ENCCL, api.GetErrorString(r));
+    std::memcpy(uid, &id, sizeof(id));
+    return DH2_OK;
+}
+
+int dh2_build_interp(const dh2_mesh* mesh, const dh2_params* params, const dh2_dist* dist, dh2_ctx** out) {
+    if (out) *out = nullptr;
+    if (!mesh || !params || !out) return fail(nullptr, DH2_EINVAL, "null argument");
+    std::unique_ptr<dh2_ctx> X(new dh2_ctx());
+    int rc = guarded(X.get(), [&] {
+        const dh2_params& p = *params;
+        if (!(p.kappa >= 0.0) || p.m < 1 || p.leaf_size < 1 || !(p.eta1 > 0.0) || !(p.eta2 > 0.0))
+            throw std::invalid_argument("invalid parameters");
+        if (p.quad != 7) throw std::invalid_argument("quad must be 7 (Radon's degree-5 rule)");
+        if (p.m > MMAX) throw NotImpl("m > " + std::to_string(MMAX) + " (grid tables are sized for m <= MMAX)");
+        if (mesh->nt > (int64_t)1 << 30) throw std::invalid_argument("mesh too large");
+        validate_mesh(mesh->xyz, mesh->nv, mesh->tri, mesh->nt);
+        X->world = dist ? std::max(1, (int)dist->world) : 1;
+        X->rank = dist ? (int)dist->rank : 0;
+        X->device = dist ? dist->device : 0;
+        X->virt = X->world > 1 && (!dist || !dist->nccl_uid);
+        if (X->rank < 0 || X->rank >= X->world) throw std::invalid_argument("rank out of range");
+        const bool structure_only = X->device == DH2_DEVICE_NONE;
+        if (!structure_only) {
+            int ndev = 0;
+            if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) throw CudaError("no CUDA device");
+            CK(cudaSetDevice(X->device));
+        }
+        auto t0 = std::chrono::steady_clock::now();
+        Params prm;
+        prm.kappa = p.kappa;
+        prm.m = p.m;
+        prm.leaf = p.leaf_size;
+        prm.eta1 = p.eta1;
+        prm.eta2 = p.eta2;
+        const int nsh = X->virt ? X->world : 1;
+        for (int i = 0; i < nsh; ++i) {
+            X->sh.emplace_back(new Shard());
+            Shard* S = X->sh.back().get();
+            S->device = X->device;
+            S->world = X->world;
+            S->rank = X->virt ? i : X->rank;
+            if (i == 0)
+                S->st.build(mesh->xyz, mesh->nv, mesh->tri, mesh->nt, prm);
+            else
+                S->st = X->sh[0]->st;  // replicated host structure
+            auto tt = std::chrono::steady_clock::now();
+            build_tables(S);
+            S->host_tables_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tt).count();
+            S->host_build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        }
+        if (structure_only) return;
+        if (X->world > 1 && !X->virt) {
+            NcclApi& api = nccl();
+            if (!api.ok) throw NcclError(api.why);
+            ncclUniqueId id;
+            std::memcpy(&id, dist->nccl_uid, sizeof(id));
+            ncclComm_t comm;
+            NK(api.CommInitRank(&comm, X->world, id, X->rank));
+            X->comm = comm;
+        }
+        CK(configure_kernels());
+        int optin = 0, nsm = 0;
+        CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, X->device));
+        CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, X->device));
+        for (auto& S : X->sh) {
+            if (!X->stream) {
+                CK(cudaStreamCreateWithFlags(&S->own_stream, cudaStreamNonBlocking));
+                X->stream = S->own_stream;
+            }
+            S->stream = X->stream;  // all shards of a context issue on one stream
+            S->P.smem_optin = optin - 1024;  // margin for the kernels' static shared memory
+            S->P.num_sms = nsm;
+            upload_all(S.get(), mesh->xyz, mesh->nv, mesh->tri);
+            run_setup(S.get());
+        }
+        finish_all(X.get());
+    });
+    if (rc != DH2_OK) return rc;
+    *out = X.release();
+    return DH2_OK;
+}
+
+int dh2_setup_device(dh2_ctx* X) {
+    if (!X) return fail(nullptr, DH2_EINVAL, "null context");
+    return guarded(X, [&] {
+        require_device(X);
+        CK(cudaSetDevice(X->device));
+        for (auto& S : X->sh) {
+            run_setup(S.get());
+            S->recompressed = false;
+        }
+        X->recompressed = false;
+        finish_all(X);
+    });
+}
+
+int dh2_recompress(dh2_ctx* X, double eps, int32_t mode) {
+    if (!X) return fail(nullptr, DH2_EINVAL, "null context");
+    return guarded(X, [&] {
+        if (!(eps >= 0.0) || mode < 0 || mode > 2) throw std::invalid_argument("invalid eps or mode");
+        require_device(X);
+        CK(cudaSetDevice(X->device));
+        for (auto& S : X->sh) {
+            S->eps = eps;
+            S->mode = mode;
+        }
+        X->exch_bytes = 0;
+        do_recompress(X, eps, mode);
+        for (auto& S : X->sh) S->recompressed = true;
+        X->recompressed = true;
+    });
+}
+
+int dh2_matvec(dh2_ctx* X, int32_t which, const double* x, double* y, int32_t flags) {
+    if (!X) return fail(nullptr, DH2_EINVAL, "null context");
+    return guarded(X, [&] {
+        if (!x || !y || (which != DH2_ORIG && which != DH2_RECOMP)) throw std::invalid_argument("invalid matvec arguments");
+        if (which == DH2_RECOMP && !X->recompressed) throw StateError("RECOMP matvec before dh2_recompress");
+        require_device(X);
+        CK(cudaSetDevice(X->device));
+        Shard* S0 = X->sh[0].get();
+        const size_t nb = (size_t)S0->n * sizeof(double2);
+        if (flags & DH2_DEVICE_PTRS) {
+            do_matvec(X, which == DH2_RECOMP, reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y));
+        } else {
+            CK(cudaMemcpyAsync(S0->d_x.p, x, nb, cudaMemcpyHostToDevice, X->stream));
+            do_matvec(X, which == DH2_RECOMP, S0->d_x.p, S0->d_y.p);
+            CK(cudaMemcpyAsync(y, S0->d_y.p, nb, cudaMemcpyDeviceToHost, X->stream));
+        }
+        finish_all(X);
+    });
+}
+
+int dh2_storage(const dh2_ctx* C, int32_t which, dh2_storage_report* out) {
+    if (!C || !out) return fail(nullptr, DH2_EINVAL, "null argument");
+    dh2_ctx* X = const_cast<dh2_ctx*>(C);
+    return guarded(X, [&] {
+        if (which == DH2_RECOMP && !X->recompressed) throw StateError("RECOMP storage before dh2_recompress");
+        if (which != DH2_ORIG && which != DH2_RECOMP) throw std::invalid_argument("invalid which");
+        std::vector<double> sum(6, 0.0), mx(1, 0.0);
+        for (auto& S : X->sh) {
+            double v[7];
+            storage_partial(S.get(), which, v);
+            for (int i = 0; i < 6; ++i) sum[i] += v[i];
+            mx[0] = std::max(mx[0], v[6]);
+        }
+        if (which == DH2_ORIG) sum[4] = sum[5] = 1;  // the interpolation rank k, counted once
+        if (X->sh[0]->device != DH2_DEVICE_NONE) {
+            reduce_doubles(X, sum, false);
+            reduce_doubles(X, mx, true);
+        }
+        if (which == DH2_ORIG) {
+            sum[4] = X->sh[0]->k;
+            sum[5] = 1;
+        }
+        const double n = X->sh[0]->n;
+        out->n = X->sh[0]->n;
+        out->row_basis_bytes = sum[0];
+        out->col_basis_bytes = sum[1];
+        out->coupling_bytes = sum[2];
+        out->nearfield_bytes = sum[3];
+        out->kb_per_dof_basis = (sum[0] + sum[1]) / n / 1024.0;
+        out->kb_per_dof_matrix = (sum[0] + sum[1] + sum[2] + sum[3]) / n / 1024.0;
+        out->max_rank = (int32_t)mx[0];
+        out->mean_rank = sum[5] > 0 ? sum[4] / sum[5] : 0.0;
+    });
+}
+
+int dh2_set_stream(dh2_ctx* X, void* stream) {
+    if (!X) return fail(nullptr, DH2_EINVAL, "null context");
+    X->stream = stream ? reinterpret_cast<cudaStream_t>(stream) : X->sh[0]->own_stream;
+    for (auto& S : X->sh) S->stream = X->stream;
+    return DH2_OK;
+}
+
+int dh2_set_option(dh2_ctx* X, const char* name, int64_t value) {
+    if (!X || !name) return fail(nullptr, DH2_EINVAL, "null argument");
+    const std::string nm(name);
+    if (nm == "truncate_workspace") {  // 1: force the global-workspace truncation path (tests)
+        if (value != 0 && value != 1) return fail(X, DH2_EINVAL, "truncate_workspace must be 0 or 1");
+        for (auto& S : X->sh) S->force_ws = (int)value;
+        return DH2_OK;
+    }
+    if (nm == "adjoint_symmetry") {
+        if (value != 0 && value != 1) return fail(X, DH2_EINVAL, "adjoint_symmetry must be 0 or 1");
+        if (value == 0 && X->world > 1) return fail(X, DH2_ENOTIMPL, "sharded recompression needs adjoint_symmetry = 1");
+        for (auto& S : X->sh) S->sym_opt = (int)value;
+        return DH2_OK;
+    }
+    return fail(X, DH2_EINVAL, "unknown option " + nm);
+}
+
+int dh2_set_profiling(dh2_ctx* X, int32_t enable) {
+    if (!X) return fail(nullptr, DH2_EINVAL, "null context");
+    for (auto& S : X->sh) S->profiling = enable != 0;
+    return DH2_OK;
+}
+
+int dh2_get_stats(const dh2_ctx* C, char* buf, int64_t* len) {
+    if (!C || !len) return fail(nullptr, DH2_EINVAL, "null argument");
+    const Shard* S0 = C->sh[0].get();
+    const Structure& S = S0->st;
+    std::map<std::string, KStat> ks;
+    int64_t launches = 0, ws = 0;
+    size_t devb = 0;
+    for (auto& sh : C->sh) {
+        for (auto& kv : sh->kstat) {
+            KStat& a = ks[kv.first];
+            a.launches += kv.second.launches;
+            a.ms += kv.second.ms;
+            a.flops += kv.second.flops;
+            a.bytes += kv.second.bytes;
+        }
+        launches += sh->launches_total;
+        ws += sh->ws_launches;
+        devb += plan_bytes(sh.get());
+    }
+    std::ostringstream o;
+    o.precision(17);
+    int64_t nrow = (int64_t)S0->row.bp.size(), ncol = (int64_t)S0->col.bp.size();
+    o << "{\"n\": " << S0->n << ", \"k\": " << S0->k << ", \"depth\": " << S.ct.depth
+      << ", \"clusters\": " << S0->nclusters << ", \"blocks\": " << S.blocks.size() << ", \"near\": " << S.near.size()
+      << ", \"row_pairs\": " << nrow << ", \"col_pairs\": " << ncol << ", \"basis_pairs\": " << S0->bp_t.size()
+      << ", \"world\": " << C->world << ", \"rank\": " << C->rank << ", \"shards_here\": " << C->sh.size()
+      << ", \"transport\": \"" << (C->world == 1 ? "none" : C->virt ? "virtual" : "nccl") << "\""
+      << ", \"own_blocks\": " << (S0->b_hi - S0->b_lo) << ", \"exchange_bytes\": " << C->exch_bytes
+      << ", \"host_build_ms\": " << S0->host_build_ms << ", \"host_phases_ms\": {\"tree\": " << S.ms_tree
+      << ", \"dirs\": " << S.ms_dirs << ", \"blocks\": " << S.ms_blocks << ", \"closure\": " << S.ms_closure
+      << ", \"tables\": " << S0->host_tables_ms << "}, \"launches_total\": " << launches
+      << ", \"E_row\": " << C->E_row << ", \"E_col\": " << C->E_col << ", \"far2\": " << C->far2
+      << ", \"device_bytes\": " << devb << ", \"mirror_missing\": " << S0->mirror_missing
+      << ", \"truncate_ws_launches\": " << ws
+      << ", \"adjoint_symmetry\": {\"available\": " << (S0->sym_ok ? "true" : "false") << ", \"enabled\": " << S0->sym_opt
+      << ", \"used\": " << (S0->sym_used ? "true" : "false") << ", \"why_not\": \"" << S0->sym_why << "\"}"
+      << ", \"kernels\": {";
+    bool first = true;
+    for (auto& kv : ks) {
+        if (!first) o << ", ";
+        first = false;
+        o << "\"" << kv.first << "\": {\"launches\": " << kv.second.launches << ", \"ms\": " << kv.second.ms
+          << ", \"flops\": " << kv.second.flops << ", \"bytes\": " << kv.second.bytes << "}";
+    }
+    o << "}}";
+    (void)ws;
+    std::string s = o.str();
+    if (!buf) {
+        *len = (int64_t)s.size() + 1;
+        return DH2_OK;
+    }
+    if (*len < (int64_t)s.size() + 1) return fail(const_cast<dh2_ctx*>(C), DH2_EINVAL, "buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    return DH2_OK;
+}
+
+int dh2_export(const dh2_ctx* C, const char* name, void* buf, int64_t* nbytes) {
+    if (!C || !name || !nbytes) return fail(nullptr, DH2_EINVAL, "null argument");
+    dh2_ctx* X = const_cast<dh2_ctx*>(C);
+    return guarded(X, [&] {
+        const std::string nm(name);
+        if (X->sh.size() > 1 && (nm == "rank_row" || nm == "rank_col")) {
+            // merged over the virtual shards: each pair's rank from the shard that owns it
+            static thread_local std::vector<int> merged;
+            const bool row = nm == "rank_row";
+            const PassH& X0 = row ? X->sh[0]->row : X->sh[0]->col;
+            merged.assign(X0.bp.size(), 0);
+            for (auto& S : X->sh) {
+                const PassH& P = row ? S->row : S->col;
+                for (int l = 0; l < (int)P.own_lo.size(); ++l)
+                    for (int p = P.own_lo[l]; p < P.own_hi[l]; ++p) merged[p] = P.rank[p];
+            }
+            const int64_t bytes = (int64_t)merged.size() * sizeof(int);
+            if (!buf) {
+                *nbytes = bytes;
+                return;
+            }
+            if (*nbytes < bytes) throw std::invalid_argument("export buffer too small for " + nm);
+            std::memcpy(buf, merged.data(), bytes);
+            *nbytes = bytes;
+            return;
+        }
+        export_shard(X->sh[0].get(), name, buf, nbytes);
+    });
+}
+
+int dh2_export_shard(const dh2_ctx* C, int32_t shard, const char* name, void* buf, int64_t* nbytes) {
+    if (!C || !name || !nbytes) return fail(nullptr, DH2_EINVAL, "null argument");
+    dh2_ctx* X = const_cast<dh2_ctx*>(C);
+    return guarded(X, [&] {
+        if (shard < 0 || shard >= (int)X->sh.size()) throw std::invalid_argument("shard index out of range");
+        export_shard(X->sh[shard].get(), name, buf, nbytes);
     });
 }
 
 int dh2_destroy(dh2_ctx* C) {
     if (!C) return DH2_OK;
-    if (C->device != DH2_DEVICE_NONE) {
-        cudaSetDevice(C->device);
-        if (C->stream) cudaStreamSynchronize(C->stream);
-    }
     delete C;
     return DH2_OK;
 }

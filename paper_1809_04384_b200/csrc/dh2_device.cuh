@@ -757,15 +757,18 @@ __device__ __forceinline__ void ztile_mma(ZTile& t, double2 a, double2 b) {
 }
 
 // out[i, nu] = w * sum_mu X[i0+i, mu] * op(S)[mu, nu] for i < nb, nu < k, on the FP64 tensor
-// cores.  X: rx x k column-major (global); op(S)[mu, nu] = Sg[nu + mu k] (conjugated if
-// conj_s) or Sg[mu + nu k] if strided.  Requires k % 32 == 0.  Each warp owns one 8-row tile
-// and four 8-column tiles, reusing its A fragment across them.
-__device__ inline void chunk_gemm_S_dmma(const double2* X, int rx, int i0, int nb, const double2* Sg, bool conj_s,
-                                         bool strided, double w, int k, double2* out, int ldo) {
+// cores.  X: rx x k column-major (global or shared); op(S)[mu, nu] = Sg[nu + mu k] (conjugated
+// if conj_s) or Sg[mu + nu k] if strided.  k is padded to a multiple of 32 with zero fragments
+// (k = 125 for m = 5).  Each warp owns one 8-row tile and four 8-column tiles, reusing its A
+// fragment across them.
+template <bool FULL>
+__device__ inline void chunk_gemm_S_dmma_t(const double2* X, int rx, int i0, int nb, const double2* Sg, bool conj_s,
+                                           bool strided, double w, int k, double2* out, int ldo) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int nrt = (nb + 7) >> 3, nct4 = k >> 5;
+    const int nrt = (nb + 7) >> 3, nct4 = (k + 31) >> 5;
     const int ar = lane >> 2, ac = lane & 3;
     const double sgn = conj_s ? -1.0 : 1.0;
+    constexpr bool full = FULL;
     for (int task = warp; task < nrt * nct4; task += nw) {
         const int rt = task % nrt, cq = task / nrt;
         const int row = rt * 8 + ar;
@@ -776,11 +779,13 @@ __device__ inline void chunk_gemm_S_dmma(const double2* X, int rx, int i0, int n
         const double2* xa = X + i0 + row;
         for (int mu = 0; mu < k; mu += 4) {
             const int mm = mu + ac;
-            const double2 a = rok ? xa[mm * rx] : cmk(0.0, 0.0);
+            const bool mok = full || mm < k;
+            const double2 a = (rok && mok) ? xa[mm * rx] : cmk(0.0, 0.0);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int nu = (cq * 4 + q) * 8 + ar;
-                double2 b = strided ? Sg[mm + nu * k] : Sg[nu + mm * k];
+                double2 b = cmk(0.0, 0.0);
+                if (full || (mok && nu < k)) b = strided ? Sg[mm + nu * k] : Sg[nu + mm * k];
                 b.y *= sgn;
                 ztile_mma(t[q], a, b);
             }
@@ -790,11 +795,19 @@ __device__ inline void chunk_gemm_S_dmma(const double2* X, int rx, int i0, int n
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int oc = (cq * 4 + q) * 8 + 2 * ac;
-                out[orow + oc * ldo] = cmk(w * t[q].r0, w * t[q].i0);
-                out[orow + (oc + 1) * ldo] = cmk(w * t[q].r1, w * t[q].i1);
+                if (full || oc < k) out[orow + oc * ldo] = cmk(w * t[q].r0, w * t[q].i0);
+                if (full || oc + 1 < k) out[orow + (oc + 1) * ldo] = cmk(w * t[q].r1, w * t[q].i1);
             }
         }
     }
+}
+
+__device__ inline void chunk_gemm_S_dmma(const double2* X, int rx, int i0, int nb, const double2* Sg, bool conj_s,
+                                         bool strided, double w, int k, double2* out, int ldo) {
+    if ((k & 31) == 0)
+        chunk_gemm_S_dmma_t<true>(X, rx, i0, nb, Sg, conj_s, strided, w, k, out, ldo);
+    else
+        chunk_gemm_S_dmma_t<false>(X, rx, i0, nb, Sg, conj_s, strided, w, k, out, ldo);
 }
 
 }  // namespace dh2

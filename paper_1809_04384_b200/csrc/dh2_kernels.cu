@@ -155,8 +155,8 @@ __global__ void k_E(PlanD P, const int* bps, int nbps) {
 
 // Coupling matrices S_b[nu,mu] = g_c(xi_{t,nu}, xi_{s,mu})
 //   = exp(i kappa (r - <xi_t - xi_s, c>)) / (4 pi r).  CTA per block.
-__global__ void k_S(PlanD P) {
-    const int b = blockIdx.x;
+__global__ void k_S(PlanD P, int b0) {
+    const int b = b0 + blockIdx.x;
     const int m = P.m, k = P.k;
     __shared__ GridD gt, gs;
     __shared__ double c[3];
@@ -198,9 +198,9 @@ void launch_E(const PlanD& P, const int* bps, int nbps, cudaStream_t s) {
     int tot = nbps * 6 * P.m * P.m;
     k_E<<<(tot + 255) / 256, 256, 0, s>>>(P, bps, nbps);
 }
-void launch_S(const PlanD& P, cudaStream_t s) {
-    if (!P.nblk) return;
-    k_S<<<P.nblk, 256, 0, s>>>(P);
+void launch_S(const PlanD& P, int b0, int nb, cudaStream_t s) {
+    if (!nb) return;
+    k_S<<<nb, 256, 0, s>>>(P, b0);
 }
 
 // ============================================================== recompression (§3.2)
@@ -213,55 +213,21 @@ __device__ inline void zero_lower(double2* A, int lda, int rows, int cols) {
 }
 
 
-// Annihilate the nb x k chunk B (nb <= 32) into the k x k upper-triangular smem matrix R:
-// [R; B] = Q [R'; 0] by k structured Householder reflections, each touching row j of R and
-// the nb rows of B only (the rows of R below j are zero in column j).  One barrier per
-// reflection: every warp computes the norm of B[:, j] and the reflector scalars itself; the
-// new diagonal beta_j is stored one step later (nobody reads R[j, j] during step j+1).
-__device__ inline void cta_qr_append(double2* R, int ldr, double2* B, int ldb, int nb, int k, double2* sh) {
-    const int tid = threadIdx.x, lane = tid & 31;
-    const LaneGroup g = lane_group(group_size_for(nb + 1, 4, 4));
-    (void)sh;
-    __syncthreads();
-    int prev = -1;
-    double2 prev_beta = cmk(0.0, 0.0);
-    for (int j = 0; j < k; ++j) {
-        if (tid == 0 && prev >= 0) R[prev + (size_t)prev * ldr] = prev_beta;
-        const double2* bj = B + (size_t)j * ldb;
-        double s = (lane < nb) ? cabs2(bj[lane]) : 0.0;
-        s = warp_sum(s);
-        const double2 alpha = R[j + (size_t)j * ldr];
-        double tau = 0.0;
-        double2 beta = alpha, u0 = cmk(0.0, 0.0);
-        if (s > 0.0) {
-            const double aa = sqrt(cabs2(alpha));
-            const double xn = sqrt(s + aa * aa);
-            const double2 ph = aa > 0.0 ? cscale(alpha, 1.0 / aa) : cmk(1.0, 0.0);
-            beta = cscale(ph, -xn);
-            u0 = cscale(ph, aa + xn);
-            tau = 1.0 / (xn * (xn + aa));
-        }
-        if (tau != 0.0) {
-            for (int c = j + 1 + g.gid; c < k; c += g.ng) {
-                double2* bc = B + (size_t)c * ldb;
-                double2 w = cmk(0.0, 0.0);
-                if (g.gl == 0) cfma_cj(w, u0, R[j + (size_t)c * ldr]);
-                for (int i = g.gl; i < nb; i += g.G) cfma_cj(w, bj[i], bc[i]);
-                w = cscale(group_sum2(w, g), tau);
-                if (g.gl == 0) R[j + (size_t)c * ldr] = csub(R[j + (size_t)c * ldr], cmul(u0, w));
-                for (int i = g.gl; i < nb; i += g.G) bc[i] = csub(bc[i], cmul(bj[i], w));
-            }
-        }
-        prev = j;
-        prev_beta = beta;
-        __syncthreads();
-    }
-    if (tid == 0 && prev >= 0) R[prev + (size_t)prev * ldr] = prev_beta;
-    __syncthreads();
+// Upper-triangular k x k factor R in shared memory: dense column-major (ld ldr) or packed by
+// columns (R[i, c] at i + c(c+1)/2, 8 k(k+1) bytes; used when the dense square does not fit,
+// e.g. k = 125: 126 KB packed instead of 250 KB).
+template <bool PK>
+__device__ __forceinline__ int ridx(int i, int c, int ldr) {
+    return PK ? i + ((c * (c + 1)) >> 1) : i + c * ldr;
+}
+template <bool PK>
+__host__ __device__ inline size_t r_elems(int k, int ldr) {
+    return PK ? (size_t)k * (k + 1) / 2 : (size_t)ldr * k;
 }
 
 // Same as cta_qr_append for nb <= 32 with compile-time lane groups: 16 lanes per column,
 // 2 rows of B per lane (rows gl and gl+16) plus row j of R on lane 0.
+template <bool PK>
 __device__ inline void cta_qr_append32(double2* R, int ldr, double2* B, int ldb, int nb, int k) {
     constexpr int G = 16;
     const int tid = threadIdx.x, lane = tid & 31;
@@ -272,11 +238,11 @@ __device__ inline void cta_qr_append32(double2* R, int ldr, double2* B, int ldb,
     int prev = -1;
     double2 prev_beta = cmk(0.0, 0.0);
     for (int j = 0; j < k; ++j) {
-        if (tid == 0 && prev >= 0) R[prev + prev * ldr] = prev_beta;
+        if (tid == 0 && prev >= 0) R[ridx<PK>(prev, prev, ldr)] = prev_beta;
         const double2* bj = B + j * ldb;
         double s = (lane < nb) ? cabs2(bj[lane]) : 0.0;
         s = warp_sum(s);
-        const double2 alpha = R[j + j * ldr];
+        const double2 alpha = R[ridx<PK>(j, j, ldr)];
         double tau = 0.0;
         double2 beta = alpha, u0 = cmk(0.0, 0.0);
         if (s > 0.0) {
@@ -297,7 +263,7 @@ __device__ inline void cta_qr_append32(double2* R, int ldr, double2* B, int ldb,
                 double2 rj = cmk(0.0, 0.0);
                 double2 w = cmk(0.0, 0.0);
                 if (gl == 0) {
-                    rj = R[j + c * ldr];
+                    rj = R[ridx<PK>(j, c, ldr)];
                     cfma_cj(w, u0, rj);
                 }
                 cfma_cj(w, ua, xa);
@@ -308,7 +274,7 @@ __device__ inline void cta_qr_append32(double2* R, int ldr, double2* B, int ldb,
                     w.y += __shfl_xor_sync(mask, w.y, o);
                 }
                 w = cscale(w, tau);
-                if (gl == 0) R[j + c * ldr] = csub(rj, cmul(u0, w));
+                if (gl == 0) R[ridx<PK>(j, c, ldr)] = csub(rj, cmul(u0, w));
                 if (r0) bc[gl] = csub(xa, cmul(ua, w));
                 if (r1) bc[gl + G] = csub(xb, cmul(ub, w));
             }
@@ -317,70 +283,8 @@ __device__ inline void cta_qr_append32(double2* R, int ldr, double2* B, int ldb,
         prev_beta = beta;
         __syncthreads();
     }
-    if (tid == 0 && prev >= 0) R[prev + prev * ldr] = prev_beta;
+    if (tid == 0 && prev >= 0) R[ridx<PK>(prev, prev, ldr)] = prev_beta;
     __syncthreads();
-}
-
-// out[i, nu] = w * sum_mu X[i0+i, mu] * op(S)[mu, nu] for i < nb (nb <= 32), X = rx x k
-// column-major (global), written to the smem chunk B (ld ldb).  op(S)[mu, nu] is read as
-// Sg[nu + mu k] (conjugated if conj_s): the row pass uses S_b^* (Sg = S_b, conj), the column
-// pass uses S_b = S_{b'}^T with b' the antipodal mirror block (Sg = S_{b'}, no conj), so
-// both read S contiguously along nu.  Each thread keeps 8 rows of one column nu.
-__device__ inline void chunk_gemm_S(const double2* X, int rx, int i0, int nb, const double2* Sg, bool conj_s, bool strided,
-                                    double w, int k, double2* B, int ldb) {
-    const int nthr = blockDim.x;
-    const int ncg = nthr / k;  // row groups (k divides blockDim for k in {8, 27->no} handled below)
-    if (ncg >= 1 && nthr % k == 0) {
-        const int nu = threadIdx.x % k, rg = threadIdx.x / k;
-        const int sstep = strided ? 1 : k;                 // distance between consecutive mu
-        const double2* sp = Sg + (strided ? (size_t)nu * k : (size_t)nu);
-        const double sgn = conj_s ? -1.0 : 1.0;
-        for (int ib = rg * 8; ib < nb; ib += ncg * 8) {
-            double2 acc[8];
-#pragma unroll
-            for (int r = 0; r < 8; ++r) acc[r] = cmk(0.0, 0.0);
-            const int nr = min(8, nb - ib);
-            const double2* xb = X + i0 + ib;
-            int mu = 0;
-            for (; mu + 4 <= k; mu += 4) {
-                double2 sv[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    sv[u] = sp[(mu + u) * sstep];
-                    sv[u].y *= sgn;
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const double2* xr = xb + (size_t)(mu + u) * rx;
-#pragma unroll
-                    for (int r = 0; r < 8; ++r)
-                        if (r < nr) cfma(acc[r], xr[r], sv[u]);
-                }
-            }
-            for (; mu < k; ++mu) {
-                double2 sv = sp[mu * sstep];
-                sv.y *= sgn;
-                const double2* xr = xb + (size_t)mu * rx;
-#pragma unroll
-                for (int r = 0; r < 8; ++r)
-                    if (r < nr) cfma(acc[r], xr[r], sv);
-            }
-#pragma unroll
-            for (int r = 0; r < 8; ++r)
-                if (r < nr) B[ib + r + (size_t)nu * ldb] = cscale(acc[r], w);
-        }
-    } else {
-        for (int idx = threadIdx.x; idx < nb * k; idx += nthr) {
-            const int i = idx % nb, nu = idx / nb;
-            double2 acc = cmk(0.0, 0.0);
-            for (int mu = 0; mu < k; ++mu) {
-                double2 sv = strided ? Sg[mu + (size_t)nu * k] : Sg[nu + (size_t)mu * k];
-                if (conj_s) sv.y = -sv.y;
-                cfma(acc, X[i0 + i + (size_t)mu * rx], sv);
-            }
-            B[i + (size_t)nu * ldb] = cscale(acc, w);
-        }
-    }
 }
 
 // Basis weights (Eq. 18; [BO10, Alg. 16] generalised to directions), one CTA per
@@ -388,15 +292,12 @@ __device__ inline void chunk_gemm_S(const double2* X, int rx, int i0, int nb, co
 // R_tc = R of QR([R_{t1c1} E_{t1c}; R_{t2c2} E_{t2c}]).  Rows are streamed in chunks of <= 32,
 // transformed by the Kronecker-factored E and annihilated into a k x k triangle (structured
 // Householder); if the stack has <= k rows it is the weight itself (P = I) and is written out.
+template <bool PK>
 __global__ void k_basis(PlanD P, const int* bps, int ldr, int ldb) {
     extern __shared__ double2 sm[];
-    __shared__ double2 sh[3];
     const int bp = bps[blockIdx.x];
     const int k = P.k, m = P.m;
     const int CH = 32;
-    double2* R = sm;                      // k x k (QR case only)
-    double2* B = R + (size_t)ldr * k;     // CH x k chunk
-    double2* Ef = B + (size_t)ldb * k;    // 6 m^2
     const bool leaf = P.bp_child0[bp] < 0;
     int src_bp[2] = {bp, -1};
     int nsrc = 1, total;
@@ -407,14 +308,19 @@ __global__ void k_basis(PlanD P, const int* bps, int ldr, int ldb) {
         src_bp[1] = P.bp_child1[bp];
         nsrc = 2;
         total = P.bp_R_rows[src_bp[0]] + P.bp_R_rows[src_bp[1]];
+    }
+    const bool qr = total > k;
+    double2* R = sm;                                       // k x k triangle (QR case only)
+    double2* B = R + (qr ? r_elems<PK>(k, ldr) : 0);       // CH x k chunk
+    double2* Ef = B + (size_t)ldb * k;                     // 6 m^2
+    if (!leaf) {
         const double2* Eg = P.E + P.bp_E_off[bp];
         for (int idx = threadIdx.x; idx < 6 * m * m; idx += blockDim.x) Ef[idx] = Eg[idx];
     }
-    const bool qr = total > k;
     double2* Rout = P.R + P.bp_R_off[bp];
     const int out = P.bp_R_rows[bp];
     if (qr)
-        for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) R[idx % k + (size_t)(idx / k) * ldr] = cmk(0.0, 0.0);
+        for (int idx = threadIdx.x; idx < (int)r_elems<PK>(k, ldr); idx += blockDim.x) R[idx] = cmk(0.0, 0.0);
     int cur = 0;
     for (int sidx = 0; sidx < nsrc; ++sidx) {
         const int r = leaf ? total : P.bp_R_rows[src_bp[sidx]];
@@ -427,7 +333,7 @@ __global__ void k_basis(PlanD P, const int* bps, int ldr, int ldb) {
             __syncthreads();
             if (!leaf) kron_apply(B, ldb, nb, m, Ef + sidx * 3 * m * m, false);
             if (qr) {
-                cta_qr_append32(R, ldr, B, ldb, nb, k);
+                cta_qr_append32<PK>(R, ldr, B, ldb, nb, k);
             } else {
                 for (int idx = threadIdx.x; idx < nb * k; idx += blockDim.x)
                     Rout[cur + idx % nb + (size_t)(idx / nb) * out] = B[idx % nb + (size_t)(idx / nb) * ldb];
@@ -439,51 +345,62 @@ __global__ void k_basis(PlanD P, const int* bps, int ldr, int ldb) {
         __syncthreads();
         for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) {
             const int i = idx % k, nu = idx / k;
-            Rout[idx] = (i > nu) ? cmk(0.0, 0.0) : R[i + (size_t)nu * ldr];
+            Rout[idx] = (i > nu) ? cmk(0.0, 0.0) : R[ridx<PK>(i, nu, ldr)];
         }
     }
+}
+
+// dynamic shared memory of the chunked-Householder kernels; packed R when the square does not fit
+static size_t qr_chunk_smem(const PlanD& P, bool pk, int ldr, int ldb, int nE, bool with_r = true) {
+    const size_t relems = !with_r ? 0 : pk ? (size_t)P.k * (P.k + 1) / 2 : (size_t)ldr * P.k;
+    return (relems + (size_t)ldb * P.k + (size_t)nE * P.m * P.m) * sizeof(double2);
 }
 
 void launch_basis(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStream_t s) {
     if (!nbps) return;
     const int ldr = odd_ld(P.k), ldb = odd_ld(32);
     const bool any_qr = maxrows > P.k;
-    size_t sm = ((any_qr ? (size_t)ldr * P.k : 0) + (size_t)ldb * P.k + 6 * P.m * P.m) * sizeof(double2);
-    k_basis<<<nbps, 256, sm, s>>>(P, bps, any_qr ? ldr : 0, ldb);
+    const bool pk = qr_chunk_smem(P, false, ldr, ldb, 6) > (size_t)P.smem_optin;
+    const size_t sm = qr_chunk_smem(P, pk, ldr, ldb, 6, any_qr);
+    if (pk)
+        k_basis<true><<<nbps, 256, sm, s>>>(P, bps, ldr, ldb);
+    else
+        k_basis<false><<<nbps, 256, sm, s>>>(P, bps, ldr, ldb);
 }
 
 // Block weights (DESIGN reading R12): ||G_b||_F^2 = ||R_tc S_b R_sc^*||_F^2 (W = P R, Eq. 18);
 // w_b = 1/||G_b||_F for the block-relative modes, 1 for FROB_CLUSTERREL.  CTA per block:
-// U = R_tc S_b (register-blocked, S read coalesced through the mirror block), then
-// ||U R_sc^*||_F^2 with a fixed-order reduction.
-__global__ void __launch_bounds__(256, 3) k_block_weights(PlanD P, int mode, int ldu, const int* mirror) {
+// U = R_tc S_b on the FP64 tensor cores (S read coalesced through the mirror block), in chunks
+// of <= 64 rows of R_tc, then ||U R_sc^*||_F^2 with a fixed-order reduction.
+__global__ void __launch_bounds__(256, 3) k_block_weights(PlanD P, int b0, int mode, int ldu, int chunk, const int* mirror) {
     extern __shared__ double2 sm[];
     __shared__ double red[32];
-    const int b = blockIdx.x, k = P.k;
+    const int b = b0 + blockIdx.x, k = P.k;
     const int bt = P.blk_bprow[b], bs = P.blk_bpcol[b];
     const int rt = P.bp_R_rows[bt], rs = P.bp_R_rows[bs];
     const double2* Rt = P.R + P.bp_R_off[bt];
     const double2* Rs = P.R + P.bp_R_off[bs];
     const int mb = mirror[b];
     const double2* Sg = P.S + (size_t)(mb >= 0 ? mb : b) * k * k;
-    double2* U = sm;  // rt x k
-    if ((k & 31) == 0)  // FP64 tensor cores (DMMA)
-        chunk_gemm_S_dmma(Rt, rt, 0, rt, Sg, false, mb < 0, 1.0, k, U, ldu);
-    else
-        chunk_gemm_S(Rt, rt, 0, rt, Sg, false, mb < 0, 1.0, k, U, ldu);
-    __syncthreads();
+    double2* U = sm;  // chunk x k
     double part = 0.0;
     const int tj = (rs + 1) / 2;
-    for (int tile = threadIdx.x; tile < rt * tj; tile += blockDim.x) {
-        const int i = tile % rt, j0 = (tile / rt) * 2;
-        double2 a0 = cmk(0.0, 0.0), a1 = cmk(0.0, 0.0);
-        const bool two = j0 + 1 < rs;
-        for (int nu = 0; nu < k; ++nu) {
-            const double2 u = U[i + (size_t)nu * ldu];
-            cfma_bj(a0, u, Rs[j0 + (size_t)nu * rs]);
-            if (two) cfma_bj(a1, u, Rs[j0 + 1 + (size_t)nu * rs]);
+    for (int i0 = 0; i0 < rt; i0 += chunk) {
+        const int nb = min(chunk, rt - i0);
+        if (i0) __syncthreads();
+        chunk_gemm_S_dmma(Rt, rt, i0, nb, Sg, false, mb < 0, 1.0, k, U, ldu);
+        __syncthreads();
+        for (int tile = threadIdx.x; tile < nb * tj; tile += blockDim.x) {
+            const int i = tile % nb, j0 = (tile / nb) * 2;
+            double2 a0 = cmk(0.0, 0.0), a1 = cmk(0.0, 0.0);
+            const bool two = j0 + 1 < rs;
+            for (int nu = 0; nu < k; ++nu) {
+                const double2 u = U[i + (size_t)nu * ldu];
+                cfma_bj(a0, u, Rs[j0 + (size_t)nu * rs]);
+                if (two) cfma_bj(a1, u, Rs[j0 + 1 + (size_t)nu * rs]);
+            }
+            part += cabs2(a0) + cabs2(a1);
         }
-        part += cabs2(a0) + cabs2(a1);
     }
     part = warp_sum(part);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
@@ -496,11 +413,12 @@ __global__ void __launch_bounds__(256, 3) k_block_weights(PlanD P, int mode, int
     }
 }
 
-void launch_block_weights(const PlanD& P, int mode, const int* mirror, cudaStream_t s) {
-    if (!P.nblk) return;
-    int ldu = odd_ld(P.k);
+void launch_block_weights(const PlanD& P, int b0, int nb, int mode, const int* mirror, cudaStream_t s) {
+    if (!nb) return;
+    const int chunk = P.k <= 64 ? 64 : 32;
+    const int ldu = odd_ld(chunk);
     size_t sm = (size_t)ldu * P.k * sizeof(double2);
-    k_block_weights<<<P.nblk, 256, sm, s>>>(P, mode, ldu, mirror);
+    k_block_weights<<<nb, 256, sm, s>>>(P, b0, mode, ldu, chunk, mirror);
 }
 
 // Total weights, one CTA per pair of one level (top-down):
@@ -509,16 +427,14 @@ void launch_block_weights(const PlanD& P, int mode, const int* mirror, cudaStrea
 // The rows of Z_tc^* are produced in chunks of <= 32 rows and annihilated into the k x k
 // triangle R (structured Householder); if Z_tc^* has <= k rows it is stored as is (P = I).
 // Row pass: rows w_b R_sc S_b^*.  Column pass (adjoint): rows w_b R_tc S_b.
+template <bool PK>
 __global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, const int* mirror, int ldr, int ldb) {
     extern __shared__ double2 sm[];
-    __shared__ double2 sh[3];
     const int p = p0 + blockIdx.x;
     const int k = P.k, m = P.m;
     const int CH = 32;
-    double2* R = sm;                                // k x k (ld ldr)
-    double2* B = R + (size_t)ldr * k;               // CH x k (ld ldb)
-    double2* Ef = B + (size_t)ldb * k;              // 3 m^2
     const int zr = X.Z_rows[p];
+    double2* Zg = X.Z + X.Z_off[p];
     // total rows of Z^*
     int total = 0;
     for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) {
@@ -527,9 +443,14 @@ __global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, const int* m
     }
     for (int ip = X.par_ptr[p]; ip < X.par_ptr[p + 1]; ++ip) total += X.Z_rows[X.par[ip]];
     const bool qr = total > k;
+    double2* R = sm;                                  // k x k triangle (QR case)
+    double2* B = R + (qr ? r_elems<PK>(k, ldr) : 0);  // CH x k chunk (ld ldb)
+    double2* Ef = B + (size_t)ldb * k;                // 3 m^2
     if (qr)
-        for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) R[idx % k + (size_t)(idx / k) * ldr] = cmk(0.0, 0.0);
-    int cur = 0;  // rows stored directly (no-QR case)
+        for (int idx = threadIdx.x; idx < (int)r_elems<PK>(k, ldr); idx += blockDim.x) R[idx] = cmk(0.0, 0.0);
+    // without QR (<= k rows, zr == total) the rows of Z^* are the weight itself (P = I) and go
+    // straight to their global slab
+    int cur = 0;
     for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) {
         const int b = X.blk[ib];
         const int obp = row ? P.blk_bpcol[b] : P.blk_bprow[b];
@@ -541,15 +462,12 @@ __global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, const int* m
         const bool strided = !row && mb < 0;
         for (int i0 = 0; i0 < r; i0 += CH) {
             const int nb = min(CH, r - i0);
-            double2* dst = qr ? B : R + cur;
-            const int ldd = qr ? ldb : ldr;
+            double2* dst = qr ? B : Zg + cur;
+            const int ldd = qr ? ldb : zr;
             __syncthreads();
-            if ((k & 31) == 0)  // FP64 tensor cores (DMMA) for the dense contraction
-                chunk_gemm_S_dmma(Ro, r, i0, nb, Sg, row, strided, w, k, dst, ldd);
-            else
-                chunk_gemm_S(Ro, r, i0, nb, Sg, row, strided, w, k, dst, ldd);
+            chunk_gemm_S_dmma(Ro, r, i0, nb, Sg, row, strided, w, k, dst, ldd);  // FP64 tensor cores
             if (qr)
-                cta_qr_append32(R, ldr, B, ldb, nb, k);
+                cta_qr_append32<PK>(R, ldr, B, ldb, nb, k);
             else
                 cur += nb;
         }
@@ -564,32 +482,37 @@ __global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, const int* m
         for (int idx = threadIdx.x; idx < 3 * m * m; idx += blockDim.x) Ef[idx] = Eg[idx];
         for (int i0 = 0; i0 < r; i0 += CH) {
             const int nb = min(CH, r - i0);
-            double2* dst = qr ? B : R + cur;
-            const int ldd = qr ? ldb : ldr;
+            double2* dst = qr ? B : Zg + cur;
+            const int ldd = qr ? ldb : zr;
             __syncthreads();
             for (int idx = threadIdx.x; idx < nb * k; idx += blockDim.x)
                 dst[idx % nb + (size_t)(idx / nb) * ldd] = Zp[i0 + idx % nb + (size_t)(idx / nb) * r];
             __syncthreads();
             kron_apply(dst, ldd, nb, m, Ef, true);  // Zhat_{t+c+} E_{tc+}^*
             if (qr)
-                cta_qr_append32(R, ldr, B, ldb, nb, k);
+                cta_qr_append32<PK>(R, ldr, B, ldb, nb, k);
             else
                 cur += nb;
         }
     }
-    __syncthreads();
-    double2* Z = X.Z + X.Z_off[p];
-    for (int idx = threadIdx.x; idx < zr * k; idx += blockDim.x) {
-        const int i = idx % zr, nu = idx / zr;
-        Z[idx] = (qr && i > nu) ? cmk(0.0, 0.0) : R[i + (size_t)nu * ldr];
+    if (qr) {
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < zr * k; idx += blockDim.x) {
+            const int i = idx % zr, nu = idx / zr;
+            Zg[idx] = (i > nu) ? cmk(0.0, 0.0) : R[ridx<PK>(i, nu, ldr)];
+        }
     }
 }
 
 void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* mirror, cudaStream_t s) {
     if (!np) return;
     const int ldr = odd_ld(P.k), ldb = odd_ld(32);
-    size_t sm = ((size_t)ldr * P.k + (size_t)ldb * P.k + 3 * P.m * P.m) * sizeof(double2);
-    k_total_weights<<<np, 256, sm, s>>>(P, row ? P.row : P.col, row, p0, mirror, ldr, ldb);
+    const bool pk = qr_chunk_smem(P, false, ldr, ldb, 3) > (size_t)P.smem_optin;
+    const size_t sm = qr_chunk_smem(P, pk, ldr, ldb, 3);
+    if (pk)
+        k_total_weights<true><<<np, 256, sm, s>>>(P, row ? P.row : P.col, row, p0, mirror, ldr, ldb);
+    else
+        k_total_weights<false><<<np, 256, sm, s>>>(P, row ? P.row : P.col, row, p0, mirror, ldr, ldb);
 }
 
 // Truncation, one CTA per pair of one level (bottom-up):
@@ -600,11 +523,8 @@ void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* m
 //   rank k_tc by the rule of `mode`, Q = first k_tc vectors (leaf: Q_tc, non-leaf:
 //   Qhat = [F_{t1c}; F_{t2c}]), C_tc = Q^* V_tc or Qhat^* Vhat (Eq. 19).
 template <bool LEAF>
-__global__ void __launch_bounds__(128, LEAF ? 6 : 4) k_truncate(PlanD P, PassD X, int p0, int ldv, int ldb, double eps, int mode) {
-    extern __shared__ double2 sm[];
-    __shared__ int flag, s_piv, s_rank;
-    __shared__ double2 sh[2];
-    const int p = p0 + blockIdx.x;
+__device__ inline void truncate_pair(const PlanD& P, const PassD& X, int p, double2* sm, int ldv, int ldb, double eps,
+                                     int mode, int& flag, int& s_piv, int& s_rank, double2* sh) {
     const int k = P.k, m = P.m;
     const int bp = X.bp[p];
     constexpr bool leaf = LEAF;  // one instance per kind of level (all pairs of a level are alike)
@@ -745,25 +665,71 @@ __global__ void __launch_bounds__(128, LEAF ? 6 : 4) k_truncate(PlanD P, PassD X
     }
 }
 
-void launch_truncate(const PlanD& P, bool row, int p0, int np, int maxrowsM, int maxZrows, bool leaf_level, double eps,
-                     int mode, cudaStream_t s) {
+// Truncation kernels: one CTA per pair with the working set in shared memory, or, when it
+// exceeds the opt-in shared memory (large k / ranks), a persistent grid whose CTAs keep their
+// working set in a private global (L2-resident) workspace slab.
+template <bool LEAF>
+__global__ void __launch_bounds__(128, LEAF ? 6 : 4)
+    k_truncate(PlanD P, PassD X, int p0, int ldv, int ldb, double eps, int mode) {
+    extern __shared__ double2 smd[];
+    __shared__ int flag, s_piv, s_rank;
+    __shared__ double2 sh[2];
+    truncate_pair<LEAF>(P, X, p0 + blockIdx.x, smd, ldv, ldb, eps, mode, flag, s_piv, s_rank, sh);
+}
+
+template <bool LEAF>
+__global__ void __launch_bounds__(128, 4)
+    k_truncate_ws(PlanD P, PassD X, int p0, int np, int ldv, int ldb, double eps, int mode, double2* ws, size_t ws_stride) {
+    __shared__ int flag, s_piv, s_rank;
+    __shared__ double2 sh[2];
+    double2* base = ws + (size_t)blockIdx.x * ws_stride;
+    for (int i = blockIdx.x; i < np; i += gridDim.x) {
+        truncate_pair<LEAF>(P, X, p0 + i, base, ldv, ldb, eps, mode, flag, s_piv, s_rank, sh);
+        __syncthreads();
+    }
+}
+
+TruncLaunch plan_truncate(const PlanD& P, int np, int maxrowsM, int maxZrows, bool leaf_level, bool force_ws) {
+    TruncLaunch L;
+    L.ldv = odd_ld(max(maxrowsM, 1));
+    L.ldb = odd_ld(max(maxZrows, 1));
+    const size_t bytes = ((leaf_level ? 0 : (size_t)L.ldv * P.k + 6 * P.m * P.m) + (size_t)L.ldb * L.ldv) * sizeof(double2) +
+                         (size_t)L.ldv * (sizeof(double) + 2 * sizeof(int)) + 16;
+    L.use_ws = force_ws || bytes > (size_t)P.smem_optin;
+    if (L.use_ws) {
+        L.smem = 0;
+        L.ws_stride = (bytes + sizeof(double2) - 1) / sizeof(double2);
+        L.grid = min(np, P.num_sms * 4);
+    } else {
+        L.smem = bytes;
+        L.ws_stride = 0;
+        L.grid = np;
+    }
+    return L;
+}
+
+void launch_truncate(const PlanD& P, bool row, int p0, int np, const TruncLaunch& L, bool leaf_level, double eps,
+                     int mode, double2* ws, cudaStream_t s) {
     if (!np) return;
-    int ldv = odd_ld(max(maxrowsM, 1));
-    int ldb = odd_ld(max(maxZrows, 1));
-    size_t sm = ((leaf_level ? 0 : (size_t)ldv * P.k + 6 * P.m * P.m) + (size_t)ldb * ldv) * sizeof(double2) +
-                (size_t)ldv * (sizeof(double) + 2 * sizeof(int)) + 16;
-    if (leaf_level)
-        k_truncate<true><<<np, 128, sm, s>>>(P, row ? P.row : P.col, p0, ldv, ldb, eps, mode);
-    else
-        k_truncate<false><<<np, 128, sm, s>>>(P, row ? P.row : P.col, p0, ldv, ldb, eps, mode);
+    const PassD& X = row ? P.row : P.col;
+    if (L.use_ws) {
+        if (leaf_level)
+            k_truncate_ws<true><<<L.grid, 128, 0, s>>>(P, X, p0, np, L.ldv, L.ldb, eps, mode, ws, L.ws_stride);
+        else
+            k_truncate_ws<false><<<L.grid, 128, 0, s>>>(P, X, p0, np, L.ldv, L.ldb, eps, mode, ws, L.ws_stride);
+    } else if (leaf_level) {
+        k_truncate<true><<<np, 128, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, eps, mode);
+    } else {
+        k_truncate<false><<<np, 128, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, eps, mode);
+    }
 }
 
 // Column pass from the row pass by adjoint symmetry (check_symmetry in
 // dh2_api.cu): for the column pair p = (s,c) and the row pair q = (s,-c), the column-pass
 // matrices are the complex conjugates of the row-pass ones, so k' = k, sigma' = sigma,
 // Q' = conj(Q) (F' = conj(F)) and C' = conj(C).  CTA per column pair.
-__global__ void k_mirror_pass(PlanD P, const int* col2row) {
-    const int p = blockIdx.x;
+__global__ void k_mirror_pass(PlanD P, const int* col2row, int p0) {
+    const int p = p0 + blockIdx.x;
     const int q = col2row[p];
     const PassD& R = P.row;
     const PassD& X = P.col;
@@ -787,42 +753,48 @@ __global__ void k_mirror_pass(PlanD P, const int* col2row) {
     for (int idx = threadIdx.x; idx < ldq * kk; idx += blockDim.x) Qc[idx] = cconj(Qr[idx]);
 }
 
-void launch_mirror_pass(const PlanD& P, const int* col2row, int np, cudaStream_t s) {
-    if (np) k_mirror_pass<<<np, 128, 0, s>>>(P, col2row);
+void launch_mirror_pass(const PlanD& P, const int* col2row, int p0, int np, cudaStream_t s) {
+    if (np) k_mirror_pass<<<np, 128, 0, s>>>(P, col2row, p0);
 }
 
-// Projection (Lemma Projections): T_b = C_tc S_b, S~_b = T_b C'_sc^*.  CTA per block.
-__global__ void k_project(PlanD P, int ldt) {
+// Projection (Lemma Projections): T_b = C_tc S_b, S~_b = T_b C'_sc^*.  CTA per block,
+// rows of C_tc in chunks of <= `chunk` (T chunk x k in shared memory).
+__global__ void k_project(PlanD P, int b0, int ldt, int chunk) {
     extern __shared__ double2 sm[];
-    const int b = blockIdx.x, k = P.k;
+    const int b = b0 + blockIdx.x, k = P.k;
     const int pr = P.blk_prow[b], pc = P.blk_pcol[b];
     const int kt = P.row.rank[pr], ks = P.col.rank[pc];
     const int lt = P.row.kb[pr], ls = P.col.kb[pc];
     const double2* Ct = P.row.C + P.row.C_off[pr];
     const double2* Cs = P.col.C + P.col.C_off[pc];
     const double2* S = P.S + (size_t)b * k * k;
-    double2* T = sm;
-    for (int idx = threadIdx.x; idx < kt * k; idx += blockDim.x) {
-        int a = idx % kt, mu = idx / kt;
-        double2 acc = cmk(0.0, 0.0);
-        for (int nu = 0; nu < k; ++nu) cfma(acc, Ct[a + (size_t)nu * lt], S[nu + (size_t)mu * k]);
-        T[a + (size_t)mu * ldt] = acc;
-    }
-    __syncthreads();
     double2* St = P.St + P.blk_St_off[b];
-    for (int idx = threadIdx.x; idx < kt * ks; idx += blockDim.x) {
-        int a = idx % kt, c = idx / kt;
-        double2 acc = cmk(0.0, 0.0);
-        for (int mu = 0; mu < k; ++mu) cfma_bj(acc, T[a + (size_t)mu * ldt], Cs[c + (size_t)mu * ls]);
-        St[a + (size_t)c * lt] = acc;
+    double2* T = sm;
+    for (int a0 = 0; a0 < kt; a0 += chunk) {
+        const int nb = min(chunk, kt - a0);
+        if (a0) __syncthreads();
+        for (int idx = threadIdx.x; idx < nb * k; idx += blockDim.x) {
+            int a = idx % nb, mu = idx / nb;
+            double2 acc = cmk(0.0, 0.0);
+            for (int nu = 0; nu < k; ++nu) cfma(acc, Ct[a0 + a + (size_t)nu * lt], S[nu + (size_t)mu * k]);
+            T[a + (size_t)mu * ldt] = acc;
+        }
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < nb * ks; idx += blockDim.x) {
+            int a = idx % nb, c = idx / nb;
+            double2 acc = cmk(0.0, 0.0);
+            for (int mu = 0; mu < k; ++mu) cfma_bj(acc, T[a + (size_t)mu * ldt], Cs[c + (size_t)mu * ls]);
+            St[a0 + a + (size_t)c * lt] = acc;
+        }
     }
 }
 
-void launch_project(const PlanD& P, int maxkrow, cudaStream_t s) {
-    if (!P.nblk) return;
-    int ldt = odd_ld(max(maxkrow, 1));
+void launch_project(const PlanD& P, int b0, int nb, int maxkrow, cudaStream_t s) {
+    if (!nb) return;
+    const int chunk = max(1, min(maxkrow, 64));
+    int ldt = odd_ld(chunk);
     size_t sm = (size_t)ldt * P.k * sizeof(double2);
-    k_project<<<P.nblk, 128, sm, s>>>(P, ldt);
+    k_project<<<nb, 128, sm, s>>>(P, b0, ldt, chunk);
 }
 
 // ============================================================== matvec (far field)
@@ -871,9 +843,9 @@ __global__ void k_mv_forward(PlanD P, bool recomp, int p0, const double2* xp, do
 }
 
 // Coupling: yh_tc = sum_{b=(t,s,c)} S_b xh_sc (ORIG) or S~_b xh'_sc (RECOMP).
-__global__ void k_mv_couple(PlanD P, bool recomp, const double2* xh, double2* yh) {
+__global__ void k_mv_couple(PlanD P, bool recomp, int p0, const double2* xh, double2* yh) {
     const PassD& X = P.row;
-    const int p = blockIdx.x, k = P.k;
+    const int p = p0 + blockIdx.x, k = P.k;
     const int kout = recomp ? X.rank[p] : k;
     for (int a = threadIdx.x; a < kout; a += blockDim.x) {
         double2 acc = cmk(0.0, 0.0);
@@ -928,9 +900,10 @@ __global__ void k_mv_backward(PlanD P, bool recomp, int p0, double2* yh) {
 }
 
 // Leaf output: y|_t = sum_{c} B_tc yh_tc over the row pairs of each leaf cluster.
-__global__ void k_mv_leaf_out(PlanD P, bool recomp, const int* lc, const int* lc_ptr, const double2* yh, double2* yp) {
+__global__ void k_mv_leaf_out(PlanD P, bool recomp, const int* lc, const int* lc_ptr, int g0, const double2* yh,
+                              double2* yp) {
     const PassD& X = P.row;
-    const int g = blockIdx.x, k = P.k;
+    const int g = g0 + blockIdx.x, k = P.k;
     const int p_first = lc[lc_ptr[g]];
     const int t = P.bp_t[X.bp[p_first]];
     const int nt = P.c_size[t];
@@ -964,16 +937,33 @@ __global__ void k_permute(const int64_t* perm, const double2* in, double2* out, 
 void launch_mv_forward(const PlanD& P, bool recomp, int p0, int np, const double2* xp, double2* xh, cudaStream_t s) {
     if (np) k_mv_forward<<<np, 64, 0, s>>>(P, recomp, p0, xp, xh);
 }
-void launch_mv_couple(const PlanD& P, bool recomp, const double2* xh, double2* yh, cudaStream_t s) {
-    if (P.row.npairs) k_mv_couple<<<P.row.npairs, 64, 0, s>>>(P, recomp, xh, yh);
+void launch_mv_couple(const PlanD& P, bool recomp, int p0, int np, const double2* xh, double2* yh, cudaStream_t s) {
+    if (np) k_mv_couple<<<np, 64, 0, s>>>(P, recomp, p0, xh, yh);
 }
 void launch_mv_backward(const PlanD& P, bool recomp, int p0, int np, double2* yh, cudaStream_t s) {
     if (np) k_mv_backward<<<np, 64, 0, s>>>(P, recomp, p0, yh);
 }
-void launch_mv_leaf_out(const PlanD& P, bool recomp, const int* lc, const int* lc_ptr, int nlc, const double2* yh,
+void launch_mv_leaf_out(const PlanD& P, bool recomp, const int* lc, const int* lc_ptr, int g0, int nlc, const double2* yh,
                         double2* yp, cudaStream_t s) {
-    if (nlc) k_mv_leaf_out<<<nlc, 64, 0, s>>>(P, recomp, lc, lc_ptr, yh, yp);
+    if (nlc) k_mv_leaf_out<<<nlc, 64, 0, s>>>(P, recomp, lc, lc_ptr, g0, yh, yp);
 }
+// Exchange packing: dst[doff[i] + j] = src[soff[i] + j] for j < len[i], CTA per segment.
+template <typename T>
+__global__ void k_copy_segments(const T* src, T* dst, const int64_t* soff, const int64_t* doff, const int64_t* len) {
+    const int i = blockIdx.x;
+    const T* a = src + soff[i];
+    T* b = dst + doff[i];
+    for (int64_t j = threadIdx.x; j < len[i]; j += blockDim.x) b[j] = a[j];
+}
+void launch_copy_segments(const double2* src, double2* dst, const int64_t* soff, const int64_t* doff, const int64_t* len,
+                          int nseg, cudaStream_t s) {
+    if (nseg) k_copy_segments<double2><<<nseg, 128, 0, s>>>(src, dst, soff, doff, len);
+}
+void launch_copy_segments_i(const int* src, int* dst, const int64_t* soff, const int64_t* doff, const int64_t* len,
+                            int nseg, cudaStream_t s) {
+    if (nseg) k_copy_segments<int><<<nseg, 32, 0, s>>>(src, dst, soff, doff, len);
+}
+
 void launch_permute(const int64_t* perm, const double2* in, double2* out, int n, bool gather, cudaStream_t s) {
     k_permute<<<(n + 255) / 256, 256, 0, s>>>(perm, in, out, n, gather);
 }
@@ -989,8 +979,8 @@ cudaError_t configure_kernels() {
     int dev = 0, optin = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    const void* ks[] = {(const void*)k_leafV, (const void*)k_basis, (const void*)k_block_weights,
-                        (const void*)k_total_weights, (const void*)k_truncate<true>, (const void*)k_truncate<false>,
+    const void* ks[] = {(const void*)k_leafV, (const void*)k_basis<false>, (const void*)k_basis<true>,
+                        (const void*)k_block_weights, (const void*)k_total_weights<false>, (const void*)k_total_weights<true>, (const void*)k_truncate<true>, (const void*)k_truncate<false>,
                         (const void*)k_project};
     for (const void* f : ks) {
         if (e != cudaSuccess) break;

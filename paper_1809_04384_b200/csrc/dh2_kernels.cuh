@@ -37,6 +37,8 @@ struct PassD {
 
 struct PlanD {
     int n, m, k, nclusters;
+    int smem_optin;       // opt-in dynamic shared memory per CTA (bytes), minus a static-smem margin
+    int num_sms;
     double kappa;
     // geometry
     const double* xyz;
@@ -85,22 +87,34 @@ void launch_quad(const PlanD& P, cudaStream_t s);
 void launch_grid(const PlanD& P, cudaStream_t s);
 void launch_leafV(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStream_t s);
 void launch_E(const PlanD& P, const int* bps, int nbps, cudaStream_t s);
-void launch_S(const PlanD& P, cudaStream_t s);
+void launch_S(const PlanD& P, int b0, int nb, cudaStream_t s);
 // recompression (§3.2)
 void launch_basis(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStream_t s);
-void launch_block_weights(const PlanD& P, int mode, const int* mirror, cudaStream_t s);
+void launch_block_weights(const PlanD& P, int b0, int nb, int mode, const int* mirror, cudaStream_t s);
 void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* mirror, cudaStream_t s);
-void launch_truncate(const PlanD& P, bool row, int p0, int np, int maxrowsM, int maxZrows, bool leaf_level, double eps,
-                     int mode, cudaStream_t s);
-void launch_mirror_pass(const PlanD& P, const int* col2row, int np, cudaStream_t s);
-void launch_project(const PlanD& P, int maxkrow, cudaStream_t s);
+struct TruncLaunch {
+    int ldv = 1, ldb = 1, grid = 0;
+    bool use_ws = false;      // working set in a global workspace (persistent grid) instead of smem
+    size_t smem = 0;          // dynamic shared memory per CTA
+    size_t ws_stride = 0;     // workspace per CTA (double2 units); total grid * ws_stride
+};
+TruncLaunch plan_truncate(const PlanD& P, int np, int maxrowsM, int maxZrows, bool leaf_level, bool force_ws);
+void launch_truncate(const PlanD& P, bool row, int p0, int np, const TruncLaunch& L, bool leaf_level, double eps,
+                     int mode, double2* ws, cudaStream_t s);
+void launch_mirror_pass(const PlanD& P, const int* col2row, int p0, int np, cudaStream_t s);
+void launch_project(const PlanD& P, int b0, int nb, int maxkrow, cudaStream_t s);
 // matvec (forward / coupling / backward)
 void launch_mv_forward(const PlanD& P, bool recomp, int p0, int np, const double2* xp, double2* xh,
                        cudaStream_t s);
-void launch_mv_couple(const PlanD& P, bool recomp, const double2* xh, double2* yh, cudaStream_t s);
+void launch_mv_couple(const PlanD& P, bool recomp, int p0, int np, const double2* xh, double2* yh, cudaStream_t s);
 void launch_mv_backward(const PlanD& P, bool recomp, int p0, int np, double2* yh, cudaStream_t s);
-void launch_mv_leaf_out(const PlanD& P, bool recomp, const int* lc, const int* lc_ptr, int nlc, const double2* yh,
+void launch_mv_leaf_out(const PlanD& P, bool recomp, const int* lc, const int* lc_ptr, int g0, int nlc, const double2* yh,
                         double2* yp, cudaStream_t s);
+// exchange packing / unpacking (multi-GPU sharding)
+void launch_copy_segments(const double2* src, double2* dst, const int64_t* soff, const int64_t* doff, const int64_t* len,
+                          int nseg, cudaStream_t s);
+void launch_copy_segments_i(const int* src, int* dst, const int64_t* soff, const int64_t* doff, const int64_t* len,
+                            int nseg, cudaStream_t s);
 void launch_permute(const int64_t* perm, const double2* in, double2* out, int n, bool gather, cudaStream_t s);
 
 }  // namespace dh2

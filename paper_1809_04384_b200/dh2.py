@@ -21,7 +21,8 @@ DH2_HOST_PTRS, DH2_DEVICE_PTRS = 0, 1
 
 # every symbol include/dh2.h declares
 EXPORTED = ["dh2_build_interp", "dh2_setup_device", "dh2_recompress", "dh2_matvec", "dh2_storage",
-            "dh2_set_stream", "dh2_set_option", "dh2_set_profiling", "dh2_get_stats", "dh2_export", "dh2_destroy", "dh2_last_error"]
+            "dh2_set_stream", "dh2_set_option", "dh2_set_profiling", "dh2_get_stats", "dh2_export", "dh2_export_shard",
+            "dh2_nccl_unique_id", "dh2_destroy", "dh2_last_error"]
 
 
 class dh2_mesh(ctypes.Structure):
@@ -75,6 +76,8 @@ def load_library(path=LIB_PATH):
     lib.dh2_set_option.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64]
     lib.dh2_get_stats.argtypes = [vp, ctypes.c_char_p, P(ctypes.c_int64)]
     lib.dh2_export.argtypes = [vp, ctypes.c_char_p, vp, P(ctypes.c_int64)]
+    lib.dh2_export_shard.argtypes = [vp, ctypes.c_int32, ctypes.c_char_p, vp, P(ctypes.c_int64)]
+    lib.dh2_nccl_unique_id.argtypes = [vp]
     lib.dh2_destroy.argtypes = [vp]
     lib.dh2_last_error.argtypes = [vp]
     lib.dh2_last_error.restype = ctypes.c_char_p
@@ -85,10 +88,24 @@ def load_library(path=LIB_PATH):
     return lib
 
 
-class DH2:
-    """One DH^2 matrix on one GPU: dh2_build_interp -> dh2_recompress -> dh2_matvec / dh2_storage."""
+def nccl_unique_id():
+    """128-byte ncclUniqueId (bytes) for dh2_build_interp with world > 1 (rank 0 creates it)."""
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    rc = lib.dh2_nccl_unique_id(buf)
+    if rc != DH2_OK:
+        raise DH2Error(rc, lib.dh2_last_error(None).decode())
+    return buf.raw
 
-    def __init__(self, xyz, tri, kappa, m, leaf, eta1=1.0, eta2=10.0, device=0):
+
+class DH2:
+    """One DH^2 matrix: dh2_build_interp -> dh2_recompress -> dh2_matvec / dh2_storage.
+
+    world > 1 partitions the matrix into `world` subtree shards (include/dh2.h, dh2_dist):
+    with nccl_uid (bytes from nccl_unique_id() on rank 0) this process is shard `rank` of an
+    NCCL job; without it, all shards run in this process on `device` (virtual mode)."""
+
+    def __init__(self, xyz, tri, kappa, m, leaf, eta1=1.0, eta2=10.0, device=0, world=1, rank=0, nccl_uid=None):
         self.lib = load_library()
         self._xyz = np.ascontiguousarray(xyz, dtype=np.float64)
         self._tri = np.ascontiguousarray(tri, dtype=np.int64)
@@ -96,7 +113,9 @@ class DH2:
                         self._xyz.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                         self._tri.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
         prm = dh2_params(float(kappa), int(m), int(leaf), float(eta1), float(eta2), 7)
-        dist = dh2_dist(0, 1, None, int(device))
+        self._uid = ctypes.create_string_buffer(bytes(nccl_uid), 128) if nccl_uid is not None else None
+        dist = dh2_dist(int(rank), int(world), ctypes.cast(self._uid, ctypes.c_void_p) if self._uid is not None else None,
+                        int(device))
         h = ctypes.c_void_p()
         rc = self.lib.dh2_build_interp(ctypes.byref(mesh), ctypes.byref(prm), ctypes.byref(dist), ctypes.byref(h))
         if rc != DH2_OK:
@@ -159,10 +178,28 @@ class DH2:
         self._check(self.lib.dh2_get_stats(self.h, buf, ctypes.byref(ln)))
         return json.loads(buf.value.decode())
 
-    def export(self, name, dtype):
+    def export(self, name, dtype, shard=None):
         nb = ctypes.c_int64(0)
-        self._check(self.lib.dh2_export(self.h, name.encode(), None, ctypes.byref(nb)))
+        if shard is None:
+            call = lambda buf: self.lib.dh2_export(self.h, name.encode(), buf, ctypes.byref(nb))  # noqa: E731
+        else:
+            call = lambda buf: self.lib.dh2_export_shard(self.h, int(shard), name.encode(), buf, ctypes.byref(nb))  # noqa: E731
+        self._check(call(None))
         out = np.empty(nb.value // np.dtype(dtype).itemsize, dtype=dtype)
         if nb.value:
-            self._check(self.lib.dh2_export(self.h, name.encode(), out.ctypes.data, ctypes.byref(nb)))
+            self._check(call(out.ctypes.data))
+        return out
+
+    def exchange_lists(self, shard=None):
+        """Partition exchange items: {kind: [ids per peer]} for kind in xR_send, xR_recv,
+        xC_send, xC_recv (see include/dh2.h, dh2_export_shard)."""
+        out = {}
+        for kind in ("xR_send", "xR_recv", "xC_send", "xC_recv"):
+            a = self.export(kind, np.int32, shard=0 if shard is None else shard)
+            lists, i = [], 0
+            while i < len(a):
+                c = int(a[i])
+                lists.append(a[i + 1:i + 1 + c].tolist())
+                i += 1 + c
+            out[kind] = lists
         return out

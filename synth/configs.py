@@ -2,7 +2,8 @@
 
 C1..C5 are BASELINE.json configs[0..4]; P0..P3 are the tiny
 parity configurations of SURVEY.md §8(c) that exercise nesting (C1 has admissible
-blocks on the leaf level only).  q is the per-face refinement: sphere n = 8 q^2,
+blocks on the leaf level only); P4/P5 run the C4/C5 order m = 5 (k = 125) and eps = 1e-6
+at oracle-friendly sizes.  q is the per-face refinement: sphere n = 8 q^2,
 cube n = 12 q^2.  eta1 = 1 (directions), eta2 = 10 (admissibility) as BASELINE.json
 states.
 """
@@ -13,6 +14,9 @@ CONFIGS = {
     "P1": dict(mesh="sphere", q=8, kappa=4.0, m=3, leaf=8, eta1=1.0, eta2=10.0, eps=1e-4),
     "P2": dict(mesh="sphere", q=16, kappa=8.0, m=3, leaf=16, eta1=1.0, eta2=10.0, eps=1e-4),
     "P3": dict(mesh="cube", q=8, kappa=5.0, m=3, leaf=16, eta1=1.0, eta2=10.0, eps=1e-4),
+    # k = 125 (m = 5) at the C4/C5 tolerance eps = 1e-6: cube (flat boxes) and sphere
+    "P4": dict(mesh="cube", q=8, kappa=5.0, m=5, leaf=16, eta1=1.0, eta2=10.0, eps=1e-6),
+    "P5": dict(mesh="sphere", q=16, kappa=6.0, m=5, leaf=16, eta1=1.0, eta2=10.0, eps=1e-6),
     # BASELINE.json configs
     "C1": dict(mesh="sphere", q=8, kappa=4.0, m=3, leaf=16, eta1=1.0, eta2=10.0, eps=1e-4),
     "C2": dict(mesh="sphere", q=32, kappa=16.0, m=4, leaf=32, eta1=1.0, eta2=10.0, eps=1e-4),

@@ -50,7 +50,7 @@ def test_invalid_arguments(lib):
         DH2(xyz, np.array([[0, 1, 1]]), 1.0, 3, 8, device=-1)  # zero area
     assert e.value.code == DH2_EINVAL
     with pytest.raises(DH2Error) as e:
-        DH2(xyz, np.array([[0, 1, 2]]), 1.0, 5, 8, device=-1)  # k = 125 not in this build
+        DH2(xyz, np.array([[0, 1, 2]]), 1.0, 6, 8, device=-1)  # m = 6 (k = 216) beyond the grid tables
     assert e.value.code == DH2_ENOTIMPL
     h = DH2(xyz, np.array([[0, 1, 2]]), 1.0, 3, 8, device=-1)
     with pytest.raises(DH2Error) as e:

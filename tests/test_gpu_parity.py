@@ -15,7 +15,7 @@ from conftest import oracle_run
 
 pytestmark = pytest.mark.gpu
 
-SMALL = ["P0", "P1", "P2", "P3", "C1"]
+SMALL = ["P0", "P1", "P2", "P3", "P4", "P5", "C1"]
 _GPU = {}
 
 
@@ -24,17 +24,19 @@ _GPU = {}
 CASES = [(n, 1) for n in SMALL + ["C2"]] + [(n, 0) for n in SMALL]
 
 
-def gpu_run(name, eps=None, mode="FROB_BLOCKREL", sym=1):
+def gpu_run(name, eps=None, mode="FROB_BLOCKREL", sym=1, ws=0):
     from paper_1809_04384_b200 import DH2
     from gpu_view import GpuView
-    key = (name, eps, mode, sym)
+    key = (name, eps, mode, sym, ws)
     if key not in _GPU:
         cfg = get_config(name)
         xyz, tri = mesh_for(cfg)
         h = DH2(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"])
         h.set_option("adjoint_symmetry", sym)
+        h.set_option("truncate_workspace", ws)
         h.recompress(cfg["eps"] if eps is None else eps, mode)
         assert h.stats()["adjoint_symmetry"]["used"] == bool(sym)
+        assert (h.stats()["truncate_ws_launches"] > 0) == bool(ws)
         rc = oracle_run(name, eps, mode)
         _GPU[key] = (h, GpuView(h, rc.st), rc)
     return _GPU[key]
@@ -155,6 +157,22 @@ def test_G6_certified_sums(name, sym):
     # (iii) ||G_b - G~_b||^2 = ||G_b||^2 - ||S~_b||^2 summed: global error <= E_row + E_col (weighted)
     err2 = sum(rc.omega[b] ** 2 * (g.normG2[b] - np.linalg.norm(g.St[b]) ** 2) for b in range(len(rc.st.blocks)))
     assert err2 <= (s["E_row"] + s["E_col"]) * (1 + 1e-6) + 1e-12
+
+
+@pytest.mark.parametrize("name", ["P2", "P4"])
+def test_truncate_workspace_path(name):
+    """The global-workspace (persistent grid) truncation used when the working set exceeds
+    shared memory gives the same ranks, singular values and matrix as the shared-memory path."""
+    h, g, rc = gpu_run(name, ws=1)
+    for side in ("row", "col"):
+        go, oo = getattr(g, side), getattr(rc, side)
+        assert go.rank == oo.rank
+        for key, so in oo.sigma.items():
+            n = min(len(go.sigma[key]), len(so))
+            assert np.abs(go.sigma[key][:n] - so[:n]).max(initial=0.0) <= 1e-12 * max(so[0] if len(so) else 0.0, 1e-300)
+    x = seeded_vector(rc.st.n, 1)
+    yo = ops.matvec(rc, x, "orig")
+    assert np.linalg.norm(h.matvec(x, 1) - ops.matvec(rc, x, "recomp")) <= 1e-10 * np.linalg.norm(yo)
 
 
 @pytest.mark.parametrize("mode", ["FROB_CLUSTERREL", "SPEC_BLOCKREL"])

@@ -2,7 +2,8 @@
 """Attribute ncu SASS-level stall samples to CUDA source lines (offline, no GPU).
 
 usage: sass_lines.py <ncu report> <kernel regex> <libdh2.so> [launch index]
-Extracts the cubin from the .so, disassembles the kernel with line info (nvdisasm -g) and
+SRC_DIR overrides the source directory used to print the lines (the sources the .so was
+built from).  Extracts the cubin from the .so, disassembles the kernel with line info (nvdisasm -g) and
 joins it with the per-instruction samples of `ncu -i --page source --print-source sass`.
 """
 import collections
@@ -39,7 +40,7 @@ for cub in glob.glob(os.path.join(tmp, "*.cubin")):
     syms = subprocess.run(["cuobjdump", "-symbols", cub], capture_output=True, text=True).stdout
     for s in re.findall(r"STT_FUNC\s+\S+\s+\S+\s+(\S+)", syms):
         dem = subprocess.run(["cu++filt", s], capture_output=True, text=True).stdout.strip()
-        if dem.split("(")[0] == kname.split("(")[0]:
+        if dem.replace(" ", "") == kname.replace(" ", ""):
             mangled = s
             dis = subprocess.run(["nvdisasm", "-g", "-c", cub], capture_output=True, text=True).stdout
             cur = None
@@ -60,6 +61,7 @@ for cub in glob.glob(os.path.join(tmp, "*.cubin")):
             break
     if mangled:
         break
+print("kernel:", kname, "->", mangled, file=sys.stderr)
 agg = collections.Counter()
 aggi = collections.Counter()
 tot = sum(d[1] for d in data) or 1
@@ -71,7 +73,8 @@ srcs = {}
 for key, v in agg.most_common(30):
     f, l = key
     txt = ""
-    for cand in glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_1809_04384_b200", "csrc", f)):
+    srcdir = os.environ.get("SRC_DIR") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_1809_04384_b200", "csrc")
+    for cand in glob.glob(os.path.join(srcdir, f)):
         srcs.setdefault(cand, open(cand).read().splitlines())
         if 0 < l <= len(srcs[cand]):
             txt = srcs[cand][l - 1].strip()
