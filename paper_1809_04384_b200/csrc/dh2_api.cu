@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <exception>
 #include <map>
 #include <memory>
 #include <tuple>
@@ -170,6 +171,7 @@ struct Shard {
     std::vector<cudaEvent_t> ev_pool;
     int64_t launches_total = 0;
     double host_build_ms = 0.0, host_tables_ms = 0.0;
+    double tab_ms[6] = {0, 0, 0, 0, 0, 0};  // build_tables: basis pairs, blocks, passes, mirror, symmetry, exchange
     double E_row = 0, E_col = 0, far2 = 0;
 
     ~Shard() {
@@ -327,6 +329,13 @@ void build_tables(Shard* C) {
     C->k = k;
     C->m = S.p.m;
     C->nclusters = (int)T.begin.size();
+    using tclk = std::chrono::steady_clock;
+    auto tmark = tclk::now();
+    auto tick = [&](int i) {
+        auto now = tclk::now();
+        C->tab_ms[i] += std::chrono::duration<double, std::milli>(now - tmark).count();
+        tmark = now;
+    };
     assign_owners(C);
     const int me = C->rank, W = C->world;
     const auto& own = C->owner;
@@ -386,6 +395,7 @@ void build_tables(Shard* C) {
             C->bp_R_rows[id] = std::min(rows, k);
         }
     auto r_by_qr = [&](int id) { return !T.is_leaf(C->bp_t[id]) || T.size(C->bp_t[id]) > k; };
+    tick(0);
     // blocks (global ids; own range contiguous after assign_owners)
     const int nb = (int)S.blocks.size();
     C->b_lo = nb;
@@ -447,8 +457,14 @@ void build_tables(Shard* C) {
             eoff += 6LL * C->m * C->m;
         }
     C->E_total = eoff;
-    // passes (global pair ids; per-pair slabs only for the pairs this shard computes or imports)
-    for (int side = 0; side < 2; ++side) {
+    tick(1);
+    // passes (global pair ids; per-pair slabs only for the pairs this shard computes or imports);
+    // the two sides are independent (sd() values are all cached by the basis-pair pass above)
+    C->blk_prow.clear();
+    C->blk_pcol.clear();
+    std::exception_ptr side_err[2];
+#pragma omp parallel for num_threads(2) schedule(static, 1)
+    for (int side = 0; side < 2; ++side) try {
         PassH& X = side == 0 ? C->row : C->col;
         const auto& pairs = side == 0 ? S.row_pairs : S.col_pairs;
         std::unordered_map<uint64_t, int> pid;
@@ -592,7 +608,12 @@ void build_tables(Shard* C) {
         }
         if (!X.lc.empty()) X.lc_ptr.push_back((int)X.lc.size());
         if (X.lc_lo < 0) X.lc_lo = X.lc_hi = 0;
+    } catch (...) {
+        side_err[side] = std::current_exception();
     }
+    for (auto& e : side_err)
+        if (e) std::rethrow_exception(e);
+    tick(2);
     // antipodal mirror b' = (s, t, -c) of every block: S_{b'} = S_b^T exactly (DESIGN §total weights)
     {
         std::unordered_map<uint64_t, int> ts;
@@ -609,7 +630,9 @@ void build_tables(Shard* C) {
             if (neg) C->blk_mirror[b] = it->second; else ++C->mirror_missing;
         }
     }
+    tick(3);
     check_symmetry(C);
+    tick(4);
     if (W > 1 && !C->sym_ok)
         throw NotImpl("sharding needs the adjoint-symmetric structure (" + C->sym_why + ")");
     C->blk_St_off.assign(nb, -1);
@@ -640,6 +663,7 @@ void build_tables(Shard* C) {
             std::sort(l.begin(), l.end());
             l.erase(std::unique(l.begin(), l.end()), l.end());
         }
+    tick(5);
 }
 
 void upload_pass(Shard* C, PassH& X, PassD& D, bool alloc_Z) {
@@ -994,7 +1018,7 @@ void run_project(Shard* C) {
     int maxkrow = 0;
     for (int l = 0; l < (int)C->row.own_lo.size(); ++l)
         for (int p = C->row.own_lo[l]; p < C->row.own_hi[l]; ++p) maxkrow = std::max(maxkrow, C->row.rank[p]);
-    C->timed("project", 1, [&] { launch_project(P, C->b_lo, C->b_hi - C->b_lo, maxkrow, C->stream); });
+    C->timed("project", 1, [&] { launch_project(P, C->b_lo, C->b_hi - C->b_lo, maxkrow, C->d_blk_mirror.p, C->stream); });
     double fl = 0;
     for (int b = C->b_lo; b < C->b_hi; ++b) {
         double kt = C->row.rank[C->blk_prow[b]], ks = C->col.rank[C->blk_pcol[b]];
@@ -1866,7 +1890,9 @@ int dh2_get_stats(const dh2_ctx* C, char* buf, int64_t* len) {
       << ", \"own_blocks\": " << (S0->b_hi - S0->b_lo) << ", \"exchange_bytes\": " << C->exch_bytes
       << ", \"host_build_ms\": " << S0->host_build_ms << ", \"host_phases_ms\": {\"tree\": " << S.ms_tree
       << ", \"dirs\": " << S.ms_dirs << ", \"blocks\": " << S.ms_blocks << ", \"closure\": " << S.ms_closure
-      << ", \"tables\": " << S0->host_tables_ms << "}, \"launches_total\": " << launches
+      << ", \"tables\": " << S0->host_tables_ms << ", \"tables_split\": [" << S0->tab_ms[0] << ", " << S0->tab_ms[1]
+      << ", " << S0->tab_ms[2] << ", " << S0->tab_ms[3] << ", " << S0->tab_ms[4] << ", " << S0->tab_ms[5]
+      << "]}, \"launches_total\": " << launches
       << ", \"E_row\": " << C->E_row << ", \"E_col\": " << C->E_col << ", \"far2\": " << C->far2
       << ", \"device_bytes\": " << devb << ", \"mirror_missing\": " << S0->mirror_missing
       << ", \"truncate_ws_launches\": " << ws

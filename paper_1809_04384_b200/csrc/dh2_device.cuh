@@ -736,6 +736,131 @@ __device__ inline int qrcp_auto(double2* B, int ldb, int M, int N, int* piv, dou
 }
 
 
+// Pivoted QR without column exchanges, for M <= G*E rows: step j picks the remaining physical
+// column pc of largest norm (first on ties) and reflects rows j.. of every remaining column;
+// piv[j] = pc, and column pc holds R[0..j, j] (logical order) above its Householder vector.
+// Every warp selects the pivot and forms the reflector itself from the same shared data, so a
+// step needs one barrier and no serial section; the column norms are double-buffered
+// (nrm, nrm + N) because warps read step j's norms while others write step j+1's.
+// Same R (up to the order of ties) as qrcp_t; stops at the numerical rank like qrcp_t.
+// Requires nrm to hold 2 N doubles.  Returns the steps done.
+template <int G, int E>
+__device__ inline int qrcp_np_t(double2* B, int ldb, int M, int N, int* piv, double* nrm, double rank_rel2) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int gl = tid & (G - 1), gid = tid / G, ng = blockDim.x / G;
+    const unsigned mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+    const int K = min(M, N);
+    __syncthreads();  // B was just written by the caller
+    for (int c = gid; c < N; c += ng) {
+        const double2* bc = B + c * ldb + gl;
+        double s = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+            if (gl + G * e < M) s += cabs2(bc[G * e]);
+        for (int o = G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(mask, s, o);
+        if (gl == 0) nrm[c] = s;
+    }
+    __syncthreads();
+    double total = 0.0;
+    int j = 0, prev_pc = -1;
+    double2 prev_beta = cmk(0.0, 0.0);
+    for (; j < K; ++j) {
+        const double* ncur = nrm + (j & 1) * N;
+        double* nnext = nrm + ((j + 1) & 1) * N;
+        // pivot: every warp, identical reduction order
+        double best = -1.0, rem = 0.0;
+        int bi = N;
+        for (int c = lane; c < N; c += 32) {
+            const double v = ncur[c];
+            if (v >= 0.0) {
+                rem += v;
+                if (v > best) { best = v; bi = c; }
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            rem += __shfl_xor_sync(0xffffffffu, rem, o);
+            if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (j == 0) total = rem;
+        if (tid == 0 && prev_pc >= 0) B[j - 1 + prev_pc * ldb] = prev_beta;
+        if (rank_rel2 > 0.0 && j > 0 && rem <= rank_rel2 * total) break;
+        const int pc = bi;
+        // reflector of column pc, rows j..M-1 (every warp)
+        const double2* colp = B + pc * ldb;
+        double sq = 0.0;
+        for (int i = j + 1 + lane; i < M; i += 32) sq += cabs2(colp[i]);
+        sq = warp_sum(sq);
+        const double2 alpha = colp[j];
+        double tau = 0.0;
+        double2 beta = alpha, u0 = alpha;
+        if (sq > 0.0) {
+            const double aa = sqrt(cabs2(alpha));
+            const double xn = sqrt(sq + aa * aa);
+            const double2 ph = aa > 0.0 ? cscale(alpha, 1.0 / aa) : cmk(1.0, 0.0);
+            beta = cscale(ph, -xn);
+            u0 = cscale(ph, aa + xn);
+            tau = 1.0 / (xn * (xn + aa));
+        }
+        double2 u[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int i = gl + G * e;
+            u[e] = (i > j && i < M) ? colp[i] : (i == j ? u0 : cmk(0.0, 0.0));
+        }
+        for (int c = gid; c < N; c += ng) {
+            if (c == pc || ncur[c] < 0.0) continue;
+            double2* bc = B + c * ldb;
+            double2 x[E];
+            double2 w = cmk(0.0, 0.0);
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int i = gl + G * e;
+                x[e] = (i < M) ? bc[i] : cmk(0.0, 0.0);
+                cfma_cj(w, u[e], x[e]);
+            }
+            for (int o = G >> 1; o > 0; o >>= 1) {
+                w.x += __shfl_xor_sync(mask, w.x, o);
+                w.y += __shfl_xor_sync(mask, w.y, o);
+            }
+            w = cscale(w, tau);
+            double s2 = 0.0;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int i = gl + G * e;
+                if (i >= j && i < M) {
+                    x[e] = csub(x[e], cmul(u[e], w));
+                    bc[i] = x[e];
+                }
+                if (i > j && i < M) s2 += cabs2(x[e]);
+            }
+            for (int o = G >> 1; o > 0; o >>= 1) s2 += __shfl_xor_sync(mask, s2, o);
+            if (gl == 0) nnext[c] = s2;
+        }
+        if (tid == 0) {
+            nnext[pc] = -1.0;
+            piv[j] = pc;
+        }
+        // columns finished earlier stay marked in the next buffer
+        for (int c = tid; c < N; c += blockDim.x)
+            if (ncur[c] < 0.0) nnext[c] = -1.0;
+        prev_pc = pc;
+        prev_beta = beta;
+        __syncthreads();
+    }
+    if (tid == 0 && prev_pc >= 0 && j == K) B[K - 1 + prev_pc * ldb] = prev_beta;
+    __syncthreads();
+    return j;
+}
+
+__device__ inline int qrcp_np_auto(double2* B, int ldb, int M, int N, int* piv, double* nrm, double rank_rel2) {
+    if (M <= 16) return qrcp_np_t<4, 4>(B, ldb, M, N, piv, nrm, rank_rel2);
+    if (M <= 32) return qrcp_np_t<8, 4>(B, ldb, M, N, piv, nrm, rank_rel2);
+    if (M <= 64) return qrcp_np_t<16, 4>(B, ldb, M, N, piv, nrm, rank_rel2);
+    return qrcp_np_t<32, 4>(B, ldb, M, N, piv, nrm, rank_rel2);  // M <= 128
+}
+
 // ------------------------------------------------------------------ FP64 tensor cores (DMMA)
 // D = A B + C for one 8x8x4 f64 tile (mma.sync m8n8k4; SASS DMMA).  Fragments: lane holds
 // A[lane/4][lane%4], B[lane%4][lane/4], C/D[lane/4][2(lane%4)+{0,1}].
@@ -808,6 +933,50 @@ __device__ inline void chunk_gemm_S_dmma(const double2* X, int rx, int i0, int n
         chunk_gemm_S_dmma_t<true>(X, rx, i0, nb, Sg, conj_s, strided, w, k, out, ldo);
     else
         chunk_gemm_S_dmma_t<false>(X, rx, i0, nb, Sg, conj_s, strided, w, k, out, ldo);
+}
+
+// C = A B^H on the FP64 tensor cores: C[i, j] = sum_mu A[i, mu] conj(Bm[j, mu]) for i < na,
+// j < nbm, mu < k (A: na x k, ld lda; Bm: nbm x k, ld ldbm; both column-major, global or shared).
+// Tiles of 8 x 8 per warp task, k padded to a multiple of 4 with zero fragments.  STORE: write
+// C (ld ldo); otherwise return this thread's share of ||C||_F^2 (padded entries are zero).
+template <bool STORE>
+__device__ inline double dmma_abh(const double2* A, int lda, int na, const double2* Bm, int ldbm, int nbm, int k,
+                                  double2* out, int ldo) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int nrt = (na + 7) >> 3, nct = (nbm + 7) >> 3;
+    const int ar = lane >> 2, ac = lane & 3;
+    double part = 0.0;
+    for (int task = warp; task < nrt * nct; task += nw) {
+        const int rt = task % nrt, ct = task / nrt;
+        const int row = rt * 8 + ar, col = ct * 8 + ar;
+        const bool rok = row < na, cok = col < nbm;
+        ZTile t{0.0, 0.0, 0.0, 0.0};
+        const double2* ap = A + row;
+        const double2* bp = Bm + col;
+        int mu = 0;
+        for (; mu + 4 <= k; mu += 4) {
+            const int mm = mu + ac;
+            const double2 a = rok ? ap[(size_t)mm * lda] : cmk(0.0, 0.0);
+            const double2 b = cok ? cconj(bp[(size_t)mm * ldbm]) : cmk(0.0, 0.0);
+            ztile_mma(t, a, b);
+        }
+        if (mu < k) {
+            const int mm = mu + ac;
+            const double2 a = (rok && mm < k) ? ap[(size_t)mm * lda] : cmk(0.0, 0.0);
+            const double2 b = (cok && mm < k) ? cconj(bp[(size_t)mm * ldbm]) : cmk(0.0, 0.0);
+            ztile_mma(t, a, b);
+        }
+        if constexpr (STORE) {
+            const int oc = ct * 8 + 2 * ac;
+            if (rok) {
+                if (oc < nbm) out[row + (size_t)oc * ldo] = cmk(t.r0, t.i0);
+                if (oc + 1 < nbm) out[row + (size_t)(oc + 1) * ldo] = cmk(t.r1, t.i1);
+            }
+        } else {
+            part += (t.r0 * t.r0 + t.i0 * t.i0) + (t.r1 * t.r1 + t.i1 * t.i1);
+        }
+    }
+    return part;
 }
 
 }  // namespace dh2

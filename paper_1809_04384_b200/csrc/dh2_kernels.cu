@@ -80,6 +80,44 @@ __global__ void k_grid(PlanD P) {
     P.grid[t] = g;
 }
 
+// Output stage of k_leafV: thread per (triangle i, z-index jz) accumulates the m^2 entries
+// nu = jx + m jy + m^2 jz over the 7 quadrature points from registers (tensor structure of
+// L_{t,nu} = L_x L_y L_z), writes coalesced along i.
+template <int MM>
+__device__ inline void leafV_out(double2* V, int nt, const double2* ph, const double* L) {
+    for (int task = threadIdx.x; task < nt * MM; task += blockDim.x) {
+        const int i = task % nt, jz = task / nt;
+        double2 acc[MM][MM];
+#pragma unroll
+        for (int a = 0; a < MM; ++a)
+#pragma unroll
+            for (int b = 0; b < MM; ++b) acc[a][b] = cmk(0.0, 0.0);
+        for (int q = 0; q < 7; ++q) {
+            const double* Lq = L + ((i * 7 + q) * 3) * MM;
+            const double2 p = ph[i * 7 + q];
+            double lx[MM], ly[MM];
+#pragma unroll
+            for (int j = 0; j < MM; ++j) {
+                lx[j] = Lq[j];
+                ly[j] = Lq[MM + j];
+            }
+            const double lz = Lq[2 * MM + jz];
+#pragma unroll
+            for (int b = 0; b < MM; ++b)
+#pragma unroll
+                for (int a = 0; a < MM; ++a) {
+                    const double l = lx[a] * ly[b] * lz;
+                    acc[b][a].x = fma(p.x, l, acc[b][a].x);
+                    acc[b][a].y = fma(p.y, l, acc[b][a].y);
+                }
+        }
+#pragma unroll
+        for (int b = 0; b < MM; ++b)
+#pragma unroll
+            for (int a = 0; a < MM; ++a) V[(size_t)(a + MM * b + MM * MM * jz) * nt + i] = acc[b][a];
+    }
+}
+
 // Leaf bases V_tc[i,nu] = sum_q |tau_i| w_q exp(i kappa <x_iq, c>) L_{t,nu}(x_iq)
 // (modified Lagrange polynomials P:270-275).  One CTA per leaf basis pair.
 __global__ void k_leafV(PlanD P, const int* bps) {
@@ -108,18 +146,25 @@ __global__ void k_leafV(PlanD P, const int* bps) {
     }
     __syncthreads();
     double2* V = P.V + P.bp_V_off[bp];
-    for (int idx = threadIdx.x; idx < nt * k; idx += blockDim.x) {
-        int i = idx % nt, nu = idx / nt;
-        int jx = nu % m, jy = (nu / m) % m, jz = nu / (m * m);
-        double2 acc = cmk(0.0, 0.0);
-        for (int q = 0; q < 7; ++q) {
-            const double* Lq = L + ((i * 7 + q) * 3) * m;
-            double l = Lq[jx] * Lq[m + jy] * Lq[2 * m + jz];
-            double2 p = ph[i * 7 + q];
-            acc.x = fma(p.x, l, acc.x);
-            acc.y = fma(p.y, l, acc.y);
-        }
-        V[(size_t)nu * nt + i] = acc;
+    switch (m) {
+        case 2: leafV_out<2>(V, nt, ph, L); break;
+        case 3: leafV_out<3>(V, nt, ph, L); break;
+        case 4: leafV_out<4>(V, nt, ph, L); break;
+        case 5: leafV_out<5>(V, nt, ph, L); break;
+        default:
+            for (int idx = threadIdx.x; idx < nt * k; idx += blockDim.x) {
+                int i = idx % nt, nu = idx / nt;
+                int jx = nu % m, jy = (nu / m) % m, jz = nu / (m * m);
+                double2 acc = cmk(0.0, 0.0);
+                for (int q = 0; q < 7; ++q) {
+                    const double* Lq = L + ((i * 7 + q) * 3) * m;
+                    double l = Lq[jx] * Lq[m + jy] * Lq[2 * m + jz];
+                    double2 p = ph[i * 7 + q];
+                    acc.x = fma(p.x, l, acc.x);
+                    acc.y = fma(p.y, l, acc.y);
+                }
+                V[(size_t)nu * nt + i] = acc;
+            }
     }
 }
 
@@ -191,7 +236,7 @@ void launch_grid(const PlanD& P, cudaStream_t s) { k_grid<<<(P.nclusters + 127) 
 void launch_leafV(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStream_t s) {
     if (!nbps) return;
     size_t sm = (size_t)maxrows * 7 * sizeof(double2) + (size_t)maxrows * 7 * 3 * P.m * sizeof(double);
-    k_leafV<<<nbps, 256, sm, s>>>(P, bps);
+    k_leafV<<<nbps, 128, sm, s>>>(P, bps);
 }
 void launch_E(const PlanD& P, const int* bps, int nbps, cudaStream_t s) {
     if (!nbps) return;
@@ -225,22 +270,26 @@ __host__ __device__ inline size_t r_elems(int k, int ldr) {
     return PK ? (size_t)k * (k + 1) / 2 : (size_t)ldr * k;
 }
 
-// Same as cta_qr_append for nb <= 32 with compile-time lane groups: 16 lanes per column,
-// 2 rows of B per lane (rows gl and gl+16) plus row j of R on lane 0.
-template <bool PK>
-__device__ inline void cta_qr_append32(double2* R, int ldr, double2* B, int ldb, int nb, int k) {
+// Annihilate the nb x k chunk B (nb <= 16 E) into the k x k upper-triangular smem factor R:
+// [R; B] = Q [R'; 0] by k structured Householder reflections, each touching row j of R and the
+// nb rows of B only (the rows of R below j are zero in column j).  Lane groups of 16 own one
+// column at a time, E rows of B per lane (rows gl + 16 e) plus row j of R on lane 0.  One
+// barrier per reflection: every warp forms the reflector itself; the new diagonal beta_j is
+// stored one step later (nobody reads R[j, j] during step j+1).
+template <bool PK, int E>
+__device__ inline void cta_qr_append(double2* R, int ldr, double2* B, int ldb, int nb, int k) {
     constexpr int G = 16;
     const int tid = threadIdx.x, lane = tid & 31;
     const int gl = tid & (G - 1), gid = tid / G, ng = blockDim.x / G;
     const unsigned mask = 0xffffu << (lane & 16);
-    const bool r0 = gl < nb, r1 = gl + G < nb;
     __syncthreads();
     int prev = -1;
     double2 prev_beta = cmk(0.0, 0.0);
     for (int j = 0; j < k; ++j) {
         if (tid == 0 && prev >= 0) R[ridx<PK>(prev, prev, ldr)] = prev_beta;
         const double2* bj = B + j * ldb;
-        double s = (lane < nb) ? cabs2(bj[lane]) : 0.0;
+        double s = 0.0;
+        for (int i = lane; i < nb; i += 32) s += cabs2(bj[i]);
         s = warp_sum(s);
         const double2 alpha = R[ridx<PK>(j, j, ldr)];
         double tau = 0.0;
@@ -254,20 +303,23 @@ __device__ inline void cta_qr_append32(double2* R, int ldr, double2* B, int ldb,
             tau = 1.0 / (xn * (xn + aa));
         }
         if (tau != 0.0) {
-            const double2 ua = r0 ? bj[gl] : cmk(0.0, 0.0);
-            const double2 ub = r1 ? bj[gl + G] : cmk(0.0, 0.0);
+            double2 u[E];
+#pragma unroll
+            for (int e = 0; e < E; ++e) u[e] = (gl + G * e < nb) ? bj[gl + G * e] : cmk(0.0, 0.0);
             for (int c = j + 1 + gid; c < k; c += ng) {
                 double2* bc = B + c * ldb;
-                const double2 xa = r0 ? bc[gl] : cmk(0.0, 0.0);
-                const double2 xb = r1 ? bc[gl + G] : cmk(0.0, 0.0);
+                double2 x[E];
                 double2 rj = cmk(0.0, 0.0);
                 double2 w = cmk(0.0, 0.0);
                 if (gl == 0) {
                     rj = R[ridx<PK>(j, c, ldr)];
                     cfma_cj(w, u0, rj);
                 }
-                cfma_cj(w, ua, xa);
-                cfma_cj(w, ub, xb);
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    x[e] = (gl + G * e < nb) ? bc[gl + G * e] : cmk(0.0, 0.0);
+                    cfma_cj(w, u[e], x[e]);
+                }
 #pragma unroll
                 for (int o = G >> 1; o > 0; o >>= 1) {
                     w.x += __shfl_xor_sync(mask, w.x, o);
@@ -275,8 +327,9 @@ __device__ inline void cta_qr_append32(double2* R, int ldr, double2* B, int ldb,
                 }
                 w = cscale(w, tau);
                 if (gl == 0) R[ridx<PK>(j, c, ldr)] = csub(rj, cmul(u0, w));
-                if (r0) bc[gl] = csub(xa, cmul(ua, w));
-                if (r1) bc[gl + G] = csub(xb, cmul(ub, w));
+#pragma unroll
+                for (int e = 0; e < E; ++e)
+                    if (gl + G * e < nb) bc[gl + G * e] = csub(x[e], cmul(u[e], w));
             }
         }
         prev = j;
@@ -292,12 +345,12 @@ __device__ inline void cta_qr_append32(double2* R, int ldr, double2* B, int ldb,
 // R_tc = R of QR([R_{t1c1} E_{t1c}; R_{t2c2} E_{t2c}]).  Rows are streamed in chunks of <= 32,
 // transformed by the Kronecker-factored E and annihilated into a k x k triangle (structured
 // Householder); if the stack has <= k rows it is the weight itself (P = I) and is written out.
-template <bool PK>
+template <bool PK, int E>
 __global__ void k_basis(PlanD P, const int* bps, int ldr, int ldb) {
     extern __shared__ double2 sm[];
     const int bp = bps[blockIdx.x];
     const int k = P.k, m = P.m;
-    const int CH = 32;
+    constexpr int CH = 16 * E;
     const bool leaf = P.bp_child0[bp] < 0;
     int src_bp[2] = {bp, -1};
     int nsrc = 1, total;
@@ -321,26 +374,35 @@ __global__ void k_basis(PlanD P, const int* bps, int ldr, int ldb) {
     const int out = P.bp_R_rows[bp];
     if (qr)
         for (int idx = threadIdx.x; idx < (int)r_elems<PK>(k, ldr); idx += blockDim.x) R[idx] = cmk(0.0, 0.0);
-    int cur = 0;
+    // rows of the stack are gathered (and transformed by E) into chunks of CH rows across the
+    // sources, each full chunk annihilated into R; without QR they go straight to R_out
+    int fill = 0, cur = 0;
     for (int sidx = 0; sidx < nsrc; ++sidx) {
         const int r = leaf ? total : P.bp_R_rows[src_bp[sidx]];
         const double2* X = leaf ? (P.V + P.bp_V_off[bp]) : (P.R + P.bp_R_off[src_bp[sidx]]);
-        for (int i0 = 0; i0 < r; i0 += CH) {
-            const int nb = min(CH, r - i0);
+        for (int i0 = 0; i0 < r;) {
+            const int nb = qr ? min(CH - fill, r - i0) : min(CH, r - i0);
+            double2* dst = B + fill;
             __syncthreads();
             for (int idx = threadIdx.x; idx < nb * k; idx += blockDim.x)
-                B[idx % nb + (size_t)(idx / nb) * ldb] = X[i0 + idx % nb + (size_t)(idx / nb) * r];
+                dst[idx % nb + (size_t)(idx / nb) * ldb] = X[i0 + idx % nb + (size_t)(idx / nb) * r];
             __syncthreads();
-            if (!leaf) kron_apply(B, ldb, nb, m, Ef + sidx * 3 * m * m, false);
-            if (qr) {
-                cta_qr_append32<PK>(R, ldr, B, ldb, nb, k);
-            } else {
+            if (!leaf) kron_apply(dst, ldb, nb, m, Ef + sidx * 3 * m * m, false);
+            i0 += nb;
+            if (!qr) {
                 for (int idx = threadIdx.x; idx < nb * k; idx += blockDim.x)
                     Rout[cur + idx % nb + (size_t)(idx / nb) * out] = B[idx % nb + (size_t)(idx / nb) * ldb];
                 cur += nb;
+                continue;
+            }
+            fill += nb;
+            if (fill == CH) {
+                cta_qr_append<PK, E>(R, ldr, B, ldb, fill, k);
+                fill = 0;
             }
         }
     }
+    if (qr && fill > 0) cta_qr_append<PK, E>(R, ldr, B, ldb, fill, k);
     if (qr) {
         __syncthreads();
         for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) {
@@ -351,21 +413,23 @@ __global__ void k_basis(PlanD P, const int* bps, int ldr, int ldb) {
 }
 
 // dynamic shared memory of the chunked-Householder kernels; packed R when the square does not fit
-static size_t qr_chunk_smem(const PlanD& P, bool pk, int ldr, int ldb, int nE, bool with_r = true) {
-    const size_t relems = !with_r ? 0 : pk ? (size_t)P.k * (P.k + 1) / 2 : (size_t)ldr * P.k;
-    return (relems + (size_t)ldb * P.k + (size_t)nE * P.m * P.m) * sizeof(double2);
+static size_t qr_chunk_smem(const PlanD& P, bool pk, int ldr, int ldb, int nE, bool with_qr = true) {
+    const size_t relems = !with_qr ? 0 : pk ? (size_t)P.k * (P.k + 1) / 2 : (size_t)ldr * P.k;
+    const size_t belems = (size_t)ldb * P.k;  // chunk (staging buffer without QR)
+    return (relems + belems + (size_t)nE * P.m * P.m) * sizeof(double2);
 }
 
 void launch_basis(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStream_t s) {
     if (!nbps) return;
-    const int ldr = odd_ld(P.k), ldb = odd_ld(32);
     const bool any_qr = maxrows > P.k;
-    const bool pk = qr_chunk_smem(P, false, ldr, ldb, 6) > (size_t)P.smem_optin;
-    const size_t sm = qr_chunk_smem(P, pk, ldr, ldb, 6, any_qr);
-    if (pk)
-        k_basis<true><<<nbps, 256, sm, s>>>(P, bps, ldr, ldb);
-    else
-        k_basis<false><<<nbps, 256, sm, s>>>(P, bps, ldr, ldb);
+    const int ldr = odd_ld(P.k);
+    if (P.k <= 64) {  // 64-row chunks, packed triangle
+        const int ldb = odd_ld(64);
+        k_basis<true, 4><<<nbps, 256, qr_chunk_smem(P, true, ldr, ldb, 6, any_qr), s>>>(P, bps, ldr, ldb);
+    } else {
+        const int ldb = odd_ld(32);
+        k_basis<true, 2><<<nbps, 256, qr_chunk_smem(P, true, ldr, ldb, 6, any_qr), s>>>(P, bps, ldr, ldb);
+    }
 }
 
 // Block weights (DESIGN reading R12): ||G_b||_F^2 = ||R_tc S_b R_sc^*||_F^2 (W = P R, Eq. 18);
@@ -384,23 +448,12 @@ __global__ void __launch_bounds__(256, 3) k_block_weights(PlanD P, int b0, int m
     const double2* Sg = P.S + (size_t)(mb >= 0 ? mb : b) * k * k;
     double2* U = sm;  // chunk x k
     double part = 0.0;
-    const int tj = (rs + 1) / 2;
     for (int i0 = 0; i0 < rt; i0 += chunk) {
         const int nb = min(chunk, rt - i0);
         if (i0) __syncthreads();
         chunk_gemm_S_dmma(Rt, rt, i0, nb, Sg, false, mb < 0, 1.0, k, U, ldu);
         __syncthreads();
-        for (int tile = threadIdx.x; tile < nb * tj; tile += blockDim.x) {
-            const int i = tile % nb, j0 = (tile / nb) * 2;
-            double2 a0 = cmk(0.0, 0.0), a1 = cmk(0.0, 0.0);
-            const bool two = j0 + 1 < rs;
-            for (int nu = 0; nu < k; ++nu) {
-                const double2 u = U[i + (size_t)nu * ldu];
-                cfma_bj(a0, u, Rs[j0 + (size_t)nu * rs]);
-                if (two) cfma_bj(a1, u, Rs[j0 + 1 + (size_t)nu * rs]);
-            }
-            part += cabs2(a0) + cabs2(a1);
-        }
+        part += dmma_abh<false>(U, ldu, nb, Rs, rs, rs, k, nullptr, 0);  // ||U R_sc^*||_F^2, FP64 tensor cores
     }
     part = warp_sum(part);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
@@ -427,12 +480,12 @@ void launch_block_weights(const PlanD& P, int b0, int nb, int mode, const int* m
 // The rows of Z_tc^* are produced in chunks of <= 32 rows and annihilated into the k x k
 // triangle R (structured Householder); if Z_tc^* has <= k rows it is stored as is (P = I).
 // Row pass: rows w_b R_sc S_b^*.  Column pass (adjoint): rows w_b R_tc S_b.
-template <bool PK>
+template <bool PK, int E>
 __global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, const int* mirror, int ldr, int ldb) {
     extern __shared__ double2 sm[];
     const int p = p0 + blockIdx.x;
     const int k = P.k, m = P.m;
-    const int CH = 32;
+    constexpr int CH = 16 * E;
     const int zr = X.Z_rows[p];
     double2* Zg = X.Z + X.Z_off[p];
     // total rows of Z^*
@@ -448,9 +501,21 @@ __global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, const int* m
     double2* Ef = B + (size_t)ldb * k;                // 3 m^2
     if (qr)
         for (int idx = threadIdx.x; idx < (int)r_elems<PK>(k, ldr); idx += blockDim.x) R[idx] = cmk(0.0, 0.0);
-    // without QR (<= k rows, zr == total) the rows of Z^* are the weight itself (P = I) and go
-    // straight to their global slab
-    int cur = 0;
+    // the rows of Z^* are produced into chunks of CH rows across the sources, each full chunk
+    // annihilated into R; without QR (<= k rows, zr == total) they are the weight itself
+    // (P = I) and go straight to the global slab
+    int fill = 0, cur = 0;
+    auto next = [&](int nb) {
+        if (!qr) {
+            cur += nb;
+            return;
+        }
+        fill += nb;
+        if (fill == CH) {
+            cta_qr_append<PK, E>(R, ldr, B, ldb, fill, k);
+            fill = 0;
+        }
+    };
     for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) {
         const int b = X.blk[ib];
         const int obp = row ? P.blk_bpcol[b] : P.blk_bprow[b];
@@ -460,16 +525,14 @@ __global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, const int* m
         const int mb = row ? b : mirror[b];
         const double2* Sg = P.S + (size_t)(mb >= 0 ? mb : b) * k * k;
         const bool strided = !row && mb < 0;
-        for (int i0 = 0; i0 < r; i0 += CH) {
-            const int nb = min(CH, r - i0);
-            double2* dst = qr ? B : Zg + cur;
+        for (int i0 = 0; i0 < r;) {
+            const int nb = qr ? min(CH - fill, r - i0) : min(CH, r - i0);
+            double2* dst = qr ? B + fill : Zg + cur;
             const int ldd = qr ? ldb : zr;
             __syncthreads();
             chunk_gemm_S_dmma(Ro, r, i0, nb, Sg, row, strided, w, k, dst, ldd);  // FP64 tensor cores
-            if (qr)
-                cta_qr_append32<PK>(R, ldr, B, ldb, nb, k);
-            else
-                cur += nb;
+            i0 += nb;
+            next(nb);
         }
     }
     for (int ip = X.par_ptr[p]; ip < X.par_ptr[p + 1]; ++ip) {
@@ -480,21 +543,22 @@ __global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, const int* m
         const double2* Eg = P.E + P.bp_E_off[X.bp[pp]] + ci * 3 * m * m;
         __syncthreads();
         for (int idx = threadIdx.x; idx < 3 * m * m; idx += blockDim.x) Ef[idx] = Eg[idx];
-        for (int i0 = 0; i0 < r; i0 += CH) {
-            const int nb = min(CH, r - i0);
-            double2* dst = qr ? B : Zg + cur;
-            const int ldd = qr ? ldb : zr;
+        for (int i0 = 0; i0 < r;) {
+            const int nb = qr ? min(CH - fill, r - i0) : min(CH, r - i0);
+            double2* dst = B + (qr ? fill : 0);
             __syncthreads();
             for (int idx = threadIdx.x; idx < nb * k; idx += blockDim.x)
-                dst[idx % nb + (size_t)(idx / nb) * ldd] = Zp[i0 + idx % nb + (size_t)(idx / nb) * r];
+                dst[idx % nb + (size_t)(idx / nb) * ldb] = Zp[i0 + idx % nb + (size_t)(idx / nb) * r];
             __syncthreads();
-            kron_apply(dst, ldd, nb, m, Ef, true);  // Zhat_{t+c+} E_{tc+}^*
-            if (qr)
-                cta_qr_append32<PK>(R, ldr, B, ldb, nb, k);
-            else
-                cur += nb;
+            kron_apply(dst, ldb, nb, m, Ef, true);  // Zhat_{t+c+} E_{tc+}^*
+            if (!qr)
+                for (int idx = threadIdx.x; idx < nb * k; idx += blockDim.x)
+                    Zg[cur + idx % nb + (size_t)(idx / nb) * zr] = B[idx % nb + (size_t)(idx / nb) * ldb];
+            i0 += nb;
+            next(nb);
         }
     }
+    if (qr && fill > 0) cta_qr_append<PK, E>(R, ldr, B, ldb, fill, k);
     if (qr) {
         __syncthreads();
         for (int idx = threadIdx.x; idx < zr * k; idx += blockDim.x) {
@@ -506,13 +570,15 @@ __global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, const int* m
 
 void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* mirror, cudaStream_t s) {
     if (!np) return;
-    const int ldr = odd_ld(P.k), ldb = odd_ld(32);
-    const bool pk = qr_chunk_smem(P, false, ldr, ldb, 3) > (size_t)P.smem_optin;
-    const size_t sm = qr_chunk_smem(P, pk, ldr, ldb, 3);
-    if (pk)
-        k_total_weights<true><<<np, 256, sm, s>>>(P, row ? P.row : P.col, row, p0, mirror, ldr, ldb);
-    else
-        k_total_weights<false><<<np, 256, sm, s>>>(P, row ? P.row : P.col, row, p0, mirror, ldr, ldb);
+    const int ldr = odd_ld(P.k);
+    const PassD& X = row ? P.row : P.col;
+    if (P.k <= 64) {  // 64-row chunks, packed triangle
+        const int ldb = odd_ld(64);
+        k_total_weights<true, 4><<<np, 256, qr_chunk_smem(P, true, ldr, ldb, 3), s>>>(P, X, row, p0, mirror, ldr, ldb);
+    } else {
+        const int ldb = odd_ld(32);
+        k_total_weights<true, 2><<<np, 256, qr_chunk_smem(P, true, ldr, ldb, 3), s>>>(P, X, row, p0, mirror, ldr, ldb);
+    }
 }
 
 // Truncation, one CTA per pair of one level (bottom-up):
@@ -572,35 +638,9 @@ __device__ inline void truncate_pair(const PlanD& P, const PassD& X, int p, doub
         }
         return;
     }
-    // B = M^* = Zhat Vt^*  (zr x rowsM), 2 x 4 register tiles
-    {
-        constexpr int TJ = 2, TI = 4;
-        const int tj = (zr + TJ - 1) / TJ, ti = (rowsM + TI - 1) / TI;
-        for (int tile = threadIdx.x; tile < tj * ti; tile += blockDim.x) {
-            const int j0 = (tile % tj) * TJ, i0 = (tile / tj) * TI;
-            double2 acc[TJ][TI];
-#pragma unroll
-            for (int a = 0; a < TJ; ++a)
-#pragma unroll
-                for (int b = 0; b < TI; ++b) acc[a][b] = cmk(0.0, 0.0);
-            for (int nu = 0; nu < k; ++nu) {
-                double2 zv[TJ], vv[TI];
-#pragma unroll
-                for (int a = 0; a < TJ; ++a) zv[a] = (j0 + a < zr) ? Z[j0 + a + nu * zr] : cmk(0.0, 0.0);
-#pragma unroll
-                for (int b = 0; b < TI; ++b) vv[b] = (i0 + b < rowsM) ? Vt[i0 + b + nu * ldvt] : cmk(0.0, 0.0);
-#pragma unroll
-                for (int a = 0; a < TJ; ++a)
-#pragma unroll
-                    for (int b = 0; b < TI; ++b) cfma_bj(acc[a][b], zv[a], vv[b]);
-            }
-#pragma unroll
-            for (int a = 0; a < TJ; ++a)
-#pragma unroll
-                for (int b = 0; b < TI; ++b)
-                    if (j0 + a < zr && i0 + b < rowsM) B[j0 + a + (i0 + b) * ldb] = acc[a][b];
-        }
-    }
+    // B = M^* = Zhat Vt^*  (zr x rowsM) on the FP64 tensor cores
+    dmma_abh<true>(Z, zr, zr, Vt, ldvt, rowsM, k, B, ldb);
+    // pivoted QR, stopped at the numerical rank (trailing ||.||_F <= 1e-15 ||M||_F)
     // pivoted QR, stopped at the numerical rank (trailing ||.||_F <= 1e-15 ||M||_F)
     const int ncol = qrcp_auto(B, ldb, zr, rowsM, piv, nrm, sh, &s_piv, 1e-30);
     zero_lower(B, ldb, ncol, rowsM);  // drop the Householder vectors below the diagonal of R
@@ -669,7 +709,7 @@ __device__ inline void truncate_pair(const PlanD& P, const PassD& X, int p, doub
 // exceeds the opt-in shared memory (large k / ranks), a persistent grid whose CTAs keep their
 // working set in a private global (L2-resident) workspace slab.
 template <bool LEAF>
-__global__ void __launch_bounds__(128, LEAF ? 6 : 4)
+__global__ void __launch_bounds__(128, LEAF ? 5 : 4)
     k_truncate(PlanD P, PassD X, int p0, int ldv, int ldb, double eps, int mode) {
     extern __shared__ double2 smd[];
     __shared__ int flag, s_piv, s_rank;
@@ -758,8 +798,9 @@ void launch_mirror_pass(const PlanD& P, const int* col2row, int p0, int np, cuda
 }
 
 // Projection (Lemma Projections): T_b = C_tc S_b, S~_b = T_b C'_sc^*.  CTA per block,
-// rows of C_tc in chunks of <= `chunk` (T chunk x k in shared memory).
-__global__ void k_project(PlanD P, int b0, int ldt, int chunk) {
+// rows of C_tc in chunks of <= `chunk` (T chunk x k in shared memory); both products on the FP64
+// tensor cores, S_b read coalesced through its antipodal mirror block where that is local.
+__global__ void k_project(PlanD P, int b0, int ldt, int chunk, const int* mirror) {
     extern __shared__ double2 sm[];
     const int b = b0 + blockIdx.x, k = P.k;
     const int pr = P.blk_prow[b], pc = P.blk_pcol[b];
@@ -767,34 +808,25 @@ __global__ void k_project(PlanD P, int b0, int ldt, int chunk) {
     const int lt = P.row.kb[pr], ls = P.col.kb[pc];
     const double2* Ct = P.row.C + P.row.C_off[pr];
     const double2* Cs = P.col.C + P.col.C_off[pc];
-    const double2* S = P.S + (size_t)b * k * k;
+    const int mb = mirror[b];
+    const double2* Sg = P.S + (size_t)(mb >= 0 ? mb : b) * k * k;
     double2* St = P.St + P.blk_St_off[b];
     double2* T = sm;
     for (int a0 = 0; a0 < kt; a0 += chunk) {
         const int nb = min(chunk, kt - a0);
         if (a0) __syncthreads();
-        for (int idx = threadIdx.x; idx < nb * k; idx += blockDim.x) {
-            int a = idx % nb, mu = idx / nb;
-            double2 acc = cmk(0.0, 0.0);
-            for (int nu = 0; nu < k; ++nu) cfma(acc, Ct[a0 + a + (size_t)nu * lt], S[nu + (size_t)mu * k]);
-            T[a + (size_t)mu * ldt] = acc;
-        }
+        chunk_gemm_S_dmma(Ct, lt, a0, nb, Sg, false, mb < 0, 1.0, k, T, ldt);
         __syncthreads();
-        for (int idx = threadIdx.x; idx < nb * ks; idx += blockDim.x) {
-            int a = idx % nb, c = idx / nb;
-            double2 acc = cmk(0.0, 0.0);
-            for (int mu = 0; mu < k; ++mu) cfma_bj(acc, T[a + (size_t)mu * ldt], Cs[c + (size_t)mu * ls]);
-            St[a0 + a + (size_t)c * lt] = acc;
-        }
+        dmma_abh<true>(T, ldt, nb, Cs, ls, ks, k, St + a0, lt);
     }
 }
 
-void launch_project(const PlanD& P, int b0, int nb, int maxkrow, cudaStream_t s) {
+void launch_project(const PlanD& P, int b0, int nb, int maxkrow, const int* mirror, cudaStream_t s) {
     if (!nb) return;
     const int chunk = max(1, min(maxkrow, 64));
     int ldt = odd_ld(chunk);
     size_t sm = (size_t)ldt * P.k * sizeof(double2);
-    k_project<<<nb, 128, sm, s>>>(P, b0, ldt, chunk);
+    k_project<<<nb, 128, sm, s>>>(P, b0, ldt, chunk, mirror);
 }
 
 // ============================================================== matvec (far field)
@@ -979,8 +1011,8 @@ cudaError_t configure_kernels() {
     int dev = 0, optin = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    const void* ks[] = {(const void*)k_leafV, (const void*)k_basis<false>, (const void*)k_basis<true>,
-                        (const void*)k_block_weights, (const void*)k_total_weights<false>, (const void*)k_total_weights<true>, (const void*)k_truncate<true>, (const void*)k_truncate<false>,
+    const void* ks[] = {(const void*)k_leafV, (const void*)k_basis<true, 4>, (const void*)k_basis<true, 2>,
+                        (const void*)k_block_weights, (const void*)k_total_weights<true, 4>, (const void*)k_total_weights<true, 2>, (const void*)k_truncate<true>, (const void*)k_truncate<false>,
                         (const void*)k_project};
     for (const void* f : ks) {
         if (e != cudaSuccess) break;

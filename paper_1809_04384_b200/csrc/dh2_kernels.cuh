@@ -102,7 +102,7 @@ TruncLaunch plan_truncate(const PlanD& P, int np, int maxrowsM, int maxZrows, bo
 void launch_truncate(const PlanD& P, bool row, int p0, int np, const TruncLaunch& L, bool leaf_level, double eps,
                      int mode, double2* ws, cudaStream_t s);
 void launch_mirror_pass(const PlanD& P, const int* col2row, int p0, int np, cudaStream_t s);
-void launch_project(const PlanD& P, int b0, int nb, int maxkrow, cudaStream_t s);
+void launch_project(const PlanD& P, int b0, int nb, int maxkrow, const int* mirror, cudaStream_t s);
 // matvec (forward / coupling / backward)
 void launch_mv_forward(const PlanD& P, bool recomp, int p0, int np, const double2* xp, double2* xh,
                        cudaStream_t s);

@@ -8,14 +8,15 @@
 using namespace dh2;
 
 // op: 0 = cta_qr (R), 1 = cta_qrcp (R, piv), 2 = qrcp_auto (R, piv), 3 = cta_jacobi_rows on the
-// rows of the input, 4 = jacobi_rows_auto on the rows of the input.
+// rows of the input, 4 = jacobi_rows_auto on the rows of the input, 5/6 = 1/2 with the rank stop,
+// 7/8 = qrcp_np_auto (no column exchanges) without / with the rank stop.
 __global__ void k_devtest(int op, const double2* in, double2* out, int* iout, double* dout, int M, int N, int ld) {
     extern __shared__ double2 smem[];
     __shared__ double2 sh[4];
     __shared__ int s_piv, flag;
     double2* A = smem;
     double* nrm = reinterpret_cast<double*>(A + (size_t)ld * N);
-    int* piv = reinterpret_cast<int*>(nrm + N + M);
+    int* piv = reinterpret_cast<int*>(nrm + 2 * N + M);
     const double2* X = in + (size_t)blockIdx.x * M * N;
     for (int idx = threadIdx.x; idx < M * N; idx += blockDim.x) A[idx % M + (idx / M) * ld] = X[idx];
     __syncthreads();
@@ -27,6 +28,8 @@ __global__ void k_devtest(int op, const double2* in, double2* out, int* iout, do
     if (op == 4) res = jacobi_rows_auto(A, ld, M, N, nrm, &flag);
     if (op == 5) res = cta_qrcp(A, ld, M, N, piv, nrm, sh, &s_piv, 1e-30);
     if (op == 6) res = qrcp_auto(A, ld, M, N, piv, nrm, sh, &s_piv, 1e-30);
+    if (op == 7) res = qrcp_np_auto(A, ld, M, N, piv, nrm, 0.0);
+    if (op == 8) res = qrcp_np_auto(A, ld, M, N, piv, nrm, 1e-30);
     __syncthreads();
     double2* Y = out + (size_t)blockIdx.x * M * N;
     for (int idx = threadIdx.x; idx < M * N; idx += blockDim.x) Y[idx] = A[idx % M + (idx / M) * ld];
@@ -38,7 +41,7 @@ __global__ void k_devtest(int op, const double2* in, double2* out, int* iout, do
 extern "C" int devtest_run(int op, const double* in, double* out, int* iout, double* dout, int batch, int M, int N,
                            int threads) {
     int ld = (M | 1);
-    size_t sm = (size_t)ld * N * sizeof(double2) + (size_t)(N + M) * sizeof(double) + (size_t)(N + M) * sizeof(int) + 64;
+    size_t sm = (size_t)ld * N * sizeof(double2) + (size_t)(2 * N + M) * sizeof(double) + (size_t)(N + M) * sizeof(int) + 64;
     double2 *din, *dout2;
     int* di;
     double* dd;

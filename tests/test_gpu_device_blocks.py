@@ -46,16 +46,28 @@ def graded(rng, batch, M, N, decay):
     return U @ S @ V.conj().transpose(0, 2, 1), s
 
 
+def r_factor(out, iout, op, K, N):
+    """R in pivoted (logical) column order: ops 7/8 leave the columns in place and report the
+    pivot order piv[0:steps]; the columns never pivoted follow in increasing order."""
+    if op in (7, 8):
+        steps = iout[0]
+        piv = list(iout[1:1 + steps])
+        piv += [c for c in range(N) if c not in piv]
+        piv = np.array(piv)
+        return np.triu(out[:K][:, piv]), piv
+    piv = iout[1:] if op else np.arange(N)
+    return np.triu(out[:K]), piv
+
+
 @pytest.mark.parametrize("M,N", [(5, 3), (27, 5), (52, 32), (64, 64), (100, 64), (128, 64)])
-@pytest.mark.parametrize("op", [0, 1, 2])
+@pytest.mark.parametrize("op", [0, 1, 2, 7])
 def test_qr_variants(dev, op, M, N):
     rng = np.random.default_rng(M * 100 + N)
     A = rng.normal(size=(6, M, N)) + 1j * rng.normal(size=(6, M, N))
     out, iout, _ = run(dev, op, A)
     K = min(M, N)
     for b in range(6):
-        R = np.triu(out[b][:K])
-        piv = iout[b, 1:] if op else np.arange(N)
+        R, piv = r_factor(out[b], iout[b], op, K, N)
         Ap = A[b][:, piv]
         assert sorted(piv.tolist()) == list(range(N))
         G = Ap.conj().T @ Ap
@@ -84,7 +96,7 @@ def test_jacobi_rows(dev, op, nv, L):
 
 
 @pytest.mark.parametrize("M,N", [(27, 13), (16, 14), (52, 32), (64, 64)])
-@pytest.mark.parametrize("op", [5, 6])
+@pytest.mark.parametrize("op", [5, 6, 8])
 def test_qrcp_rank_stop(dev, op, M, N):
     """With the numerical-rank stop enabled, full-rank graded matrices are factorised completely,
     and an exactly rank-r matrix stops at r with the leading rows exact."""
@@ -99,13 +111,13 @@ def test_qrcp_rank_stop(dev, op, M, N):
     assert np.all(iout[:, 0] <= r + 1), iout[:, 0]
     for b in range(4):
         k = iout[b, 0]
-        R = np.triu(out[b][:k])
-        Bp = B[b][:, iout[b, 1:]]
+        R, piv = r_factor(out[b], iout[b], op, k, N)
+        Bp = B[b][:, piv]
         G = Bp.conj().T @ Bp
         assert np.abs(R.conj().T @ R - G).max() <= 1e-12 * np.abs(G).max()
 
 
-@pytest.mark.parametrize("op", [5, 6])
+@pytest.mark.parametrize("op", [5, 6, 8])
 def test_qrcp_on_oracle_truncation_matrices(dev, op):
     """M^* = Zhat Vhat^* of every non-leaf row pair of P1 (from the oracle): the rank-stopped
     pivoted QR keeps R^*R = (M^* Pi)^*(M^* Pi) up to the dropped trailing block."""
@@ -128,8 +140,7 @@ def test_qrcp_on_oracle_truncation_matrices(dev, op):
         out, iout, _ = run(dev, op, A)
         for b in range(len(As)):
             k = iout[b, 0]
-            R = np.triu(out[b][:k])
-            Ap = A[b][:, iout[b, 1:]]
+            R, piv = r_factor(out[b], iout[b], op, k, N)
             sv = np.linalg.svd(A[b], compute_uv=False)
             svR = np.linalg.svd(R, compute_uv=False)
             n = min(len(sv), len(svR))
