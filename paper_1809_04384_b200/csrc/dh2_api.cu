@@ -78,6 +78,7 @@ struct PassH {
     std::vector<int64_t> Z_off, C_off, Q_off, sig_off;
     std::vector<int> lev_ptr;  // pairs of level l: [lev_ptr[l], lev_ptr[l+1])
     std::vector<int> lc, lc_ptr;  // leaf-cluster groups (matvec output)
+    std::vector<int> bp2p;        // basis pair id -> pair id of this pass (-1 if absent)
     std::vector<int> own_lo, own_hi;  // per level: pairs of this shard [own_lo[l], own_hi[l])
     int lc_lo = 0, lc_hi = 0;         // leaf-cluster groups of this shard
     int64_t Z_total = 0, C_total = 0, Q_total = 0, sig_total = 0;
@@ -129,7 +130,18 @@ struct Shard {
     std::vector<int64_t> dir_off;
     std::vector<double> dirs_flat;
     // basis pairs
-    std::unordered_map<uint64_t, int> bp_id;  // (level-independent) key (t<<32)|c
+    // basis pair lookup: the ids of cluster t are [bp_cl[t], bp_cl[t+1]), sorted by direction
+    std::vector<int> bp_cl;
+    int bp_find(int64_t t, int64_t c) const {
+        auto b = bp_c.begin() + bp_cl[t], e = bp_c.begin() + bp_cl[t + 1];
+        auto it = std::lower_bound(b, e, (int)c);
+        return (it != e && *it == c) ? (int)(it - bp_c.begin()) : -1;
+    }
+    int bp_at(int64_t t, int64_t c) const {
+        const int id = bp_find(t, c);
+        if (id < 0) throw std::logic_error("basis pair missing (closure broken)");
+        return id;
+    }
     std::vector<int> bp_t, bp_dir, bp_sddir, bp_child0, bp_child1, bp_R_rows, bp_level, bp_c;
     std::vector<int64_t> bp_V_off, bp_R_off, bp_E_off;
     std::vector<int> bp_lev_ptr;
@@ -242,8 +254,7 @@ void check_symmetry(Shard* C) {
     C->col2row.clear();
     if (C->mirror_missing) { C->sym_why = "blocks without an antipodal mirror"; return; }
     if (R.bp.size() != X.bp.size()) { C->sym_why = "row and column pair counts differ"; return; }
-    std::unordered_map<uint64_t, int> rowpid;
-    for (size_t q = 0; q < R.bp.size(); ++q) rowpid[key(C->bp_t[R.bp[q]], C->bp_c[R.bp[q]])] = (int)q;
+
     std::vector<std::vector<int64_t>> neg(L + 1);
     for (int l = 0; l <= L; ++l) {
         if (S.basis_pairs[l].empty()) continue;
@@ -261,9 +272,10 @@ void check_symmetry(Shard* C) {
     for (size_t p = 0; p < X.bp.size(); ++p) {
         const int id = X.bp[p];
         const int64_t nc = neg[C->bp_level[id]][C->bp_c[id]];
-        auto it = nc < 0 ? rowpid.end() : rowpid.find(key(C->bp_t[id], nc));
-        if (it == rowpid.end()) { C->sym_why = "column pair without a row pair at -c"; return; }
-        c2r[p] = it->second;
+        const int nid = nc < 0 ? -1 : C->bp_find(C->bp_t[id], nc);
+        const int q = nid < 0 ? -1 : R.bp2p[nid];
+        if (q < 0) { C->sym_why = "column pair without a row pair at -c"; return; }
+        c2r[p] = q;
     }
     for (size_t p = 0; p < X.bp.size(); ++p) {
         const int q = c2r[p];
@@ -353,7 +365,6 @@ void build_tables(Shard* C) {
         C->bp_lev_ptr[l] = (int)C->bp_t.size();
         for (const Pair& pr : S.basis_pairs[l]) {
             int id = (int)C->bp_t.size();
-            C->bp_id[key(pr.t, pr.c)] = id;
             C->bp_t.push_back((int)pr.t);
             C->bp_c.push_back((int)pr.c);
             C->bp_level.push_back(l);
@@ -362,6 +373,13 @@ void build_tables(Shard* C) {
     }
     C->bp_lev_ptr[L + 1] = (int)C->bp_t.size();
     const int nbp = (int)C->bp_t.size();
+    // clusters are numbered level by level (BFS) and pairs sorted by (t, c) within a level, so
+    // the pairs of one cluster are contiguous
+    C->bp_cl.assign(C->nclusters + 1, 0);
+    for (int id = 0; id < nbp; ++id) ++C->bp_cl[C->bp_t[id] + 1];
+    for (int t = 0; t < C->nclusters; ++t) C->bp_cl[t + 1] += C->bp_cl[t];
+    for (int id = 1; id < nbp; ++id)
+        if (C->bp_t[id] < C->bp_t[id - 1]) throw std::logic_error("basis pairs not grouped by cluster");
     C->bp_child0.assign(nbp, -1);
     C->bp_child1.assign(nbp, -1);
     C->bp_sddir.assign(nbp, -1);
@@ -380,11 +398,8 @@ void build_tables(Shard* C) {
         if (!T.is_leaf(t)) {
             int64_t c2 = S.sd(l, C->bp_c[id]);
             C->bp_sddir[id] = (int)(C->dir_off[l + 1] + c2);
-            auto it0 = C->bp_id.find(key(T.child0[t], c2));
-            auto it1 = C->bp_id.find(key(T.child1[t], c2));
-            if (it0 == C->bp_id.end() || it1 == C->bp_id.end()) throw std::logic_error("closure broken");
-            C->bp_child0[id] = it0->second;
-            C->bp_child1[id] = it1->second;
+            C->bp_child0[id] = C->bp_at(T.child0[t], c2);
+            C->bp_child1[id] = C->bp_at(T.child1[t], c2);
         }
     }
     // basis-weight rows, bottom-up (Eq. 18): leaf min(#t, k) (R = V if #t <= k), inner min(r1 + r2, k)
@@ -406,8 +421,8 @@ void build_tables(Shard* C) {
         C->blk_t.push_back((int)B.t);
         C->blk_s.push_back((int)B.s);
         C->blk_dir.push_back((int)(C->dir_off[l] + B.c));
-        C->blk_bprow.push_back(C->bp_id.at(key(B.t, B.c)));
-        C->blk_bpcol.push_back(C->bp_id.at(key(B.s, B.c)));
+        C->blk_bprow.push_back(C->bp_at(B.t, B.c));
+        C->blk_bpcol.push_back(C->bp_at(B.s, B.c));
         if (own[B.t] == me) {
             C->b_lo = std::min(C->b_lo, b);
             C->b_hi = std::max(C->b_hi, b + 1);
@@ -467,13 +482,14 @@ void build_tables(Shard* C) {
     for (int side = 0; side < 2; ++side) try {
         PassH& X = side == 0 ? C->row : C->col;
         const auto& pairs = side == 0 ? S.row_pairs : S.col_pairs;
-        std::unordered_map<uint64_t, int> pid;
+        X.bp2p.assign(nbp, -1);
         X.lev_ptr.assign(L + 2, 0);
         for (int l = 0; l <= L; ++l) {
             X.lev_ptr[l] = (int)X.bp.size();
             for (const Pair& pr : pairs[l]) {
-                pid[key(pr.t, pr.c)] = (int)X.bp.size();
-                X.bp.push_back(C->bp_id.at(key(pr.t, pr.c)));
+                const int id = C->bp_at(pr.t, pr.c);
+                X.bp2p[id] = (int)X.bp.size();
+                X.bp.push_back(id);
             }
         }
         X.lev_ptr[L + 1] = (int)X.bp.size();
@@ -484,17 +500,17 @@ void build_tables(Shard* C) {
             int id = X.bp[p];
             int t = C->bp_t[id];
             if (!T.is_leaf(t)) {
-                int l = C->bp_level[id];
-                int64_t c2 = S.sd(l, C->bp_c[id]);
-                X.child0[p] = pid.at(key(T.child0[t], c2));
-                X.child1[p] = pid.at(key(T.child1[t], c2));
+                X.child0[p] = X.bp2p[C->bp_child0[id]];
+                X.child1[p] = X.bp2p[C->bp_child1[id]];
+                if (X.child0[p] < 0 || X.child1[p] < 0) throw std::logic_error("pass closure broken");
             }
         }
         // blocks CSR (blocks sorted by (t,s) per owner: per pair sorted by the other cluster)
         std::vector<std::vector<int>> bl(np);
         for (int b = 0; b < nb; ++b) {
             const Block& B = S.blocks[b];
-            int p = pid.at(key(side == 0 ? B.t : B.s, B.c));
+            int p = X.bp2p[side == 0 ? C->blk_bprow[b] : C->blk_bpcol[b]];
+            if (p < 0) throw std::logic_error("block pair missing from the pass");
             bl[p].push_back(b);
             if (side == 0)
                 C->blk_prow.push_back(p);

@@ -554,12 +554,18 @@ __device__ inline int jacobi_rows_t(double2* R, int ldr, int nv, int len, double
                 const double al = nrm[p], be = nrm[q];
                 const double g2 = cabs2(ga);
                 if (g2 > tol2 * (al * be) && al > 0.0 && be > 0.0) {
-                    const double ig = rsqrt(g2);
+                    // rotation by the smaller angle theta with tan(2 theta) = 2|g|/(be - al), from
+                    // two dependent rsqrt only: with d = be - al, r = sqrt(d^2 + 4|g|^2),
+                    // c^2 = (1 + |d|/r)/2 and t = tan(theta) = sign(d) |g| / (r c^2)
+                    const double ig = rsqrt(g2);  // 1/|g| (independent chain)
                     const double gm = g2 * ig;
-                    const double zeta = 0.5 * (be - al) * ig;
-                    const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-                    const double c = rsqrt(fma(t, t, 1.0));
-                    const double sn = c * t;
+                    const double d = be - al;
+                    const double ir = rsqrt(fma(d, d, 4.0 * g2));
+                    const double c2 = fma(0.5 * fabs(d), ir, 0.5);
+                    const double ic = rsqrt(c2);
+                    const double c = c2 * ic;
+                    const double t = (d >= 0.0 ? gm : -gm) * ir * (ic * ic);
+                    const double sn = t * c;
                     const double2 ec = cmk(ga.x * ig, ga.y * ig);
 #pragma unroll
                     for (int e = 0; e < E; ++e) {

@@ -236,6 +236,26 @@ std::vector<std::vector<Pair>> Structure::closure(bool row) {
         std::sort(v.begin(), v.end());
         v.erase(std::unique(v.begin(), v.end()), v.end());
         if (l == T.depth) break;
+        // sd_l of every direction used on this level, computed in parallel into the cache
+        // (D(l), D(l+1) and the cache are materialised first: nearest() then only reads)
+        if (!v.empty()) {
+            D(l);
+            D(l + 1);
+            std::vector<int64_t>& cache = sd_cache[l];
+            if (cache.size() < D(l).size() / 3) cache.resize(D(l).size() / 3, -1);
+            std::vector<int64_t> todo;
+            for (auto& pr : v)
+                if (!T.is_leaf(pr.t) && cache[pr.c] < 0 && (todo.empty() || todo.back() != pr.c)) todo.push_back(pr.c);
+            std::sort(todo.begin(), todo.end());
+            todo.erase(std::unique(todo.begin(), todo.end()), todo.end());
+            const std::vector<double>& Dl = D(l);
+#pragma omp parallel for schedule(dynamic, 16)
+            for (int64_t i = 0; i < (int64_t)todo.size(); ++i) {
+                const int64_t c = todo[i];
+                double y[3] = {Dl[3 * c], Dl[3 * c + 1], Dl[3 * c + 2]};
+                cache[c] = nearest(l + 1, y);
+            }
+        }
         for (auto& pr : v) {
             if (T.is_leaf(pr.t)) continue;
             int64_t c2 = sd(l, pr.c);
