@@ -109,6 +109,21 @@ __device__ __forceinline__ void lagrange_axis(const GridD& g, int a, int m, cons
     }
 }
 
+// ------------------------------------------------------------------ asynchronous staging
+// dst (nb x k, ld ldd, shared) <- src rows [i0, i0 + nb) of a column-major global matrix (ld lds)
+// with 16-byte cp.async copies (many loads in flight per thread); the caller waits with
+// cp_async_wait_all() and a barrier.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ inline void stage_rows(double2* dst, int ldd, const double2* src, int lds, int i0, int nb, int k) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int nu = warp; nu < k; nu += nw)
+        for (int i = lane; i < nb; i += 32) cp_async16(dst + i + (size_t)nu * ldd, src + i0 + i + (size_t)nu * lds);
+}
+
 // ------------------------------------------------------------------ CTA-cooperative kernels
 
 // In-place X <- X * E or X <- X * E^* for the Kronecker-structured transfer matrix
@@ -307,7 +322,8 @@ __device__ inline int cta_jacobi(double2* W, int ld, int m, int n, int* flag) {
 // are recomputed exactly after every step (no downdating).  On return piv[j] = original
 // column placed at position j, R = upper trapezoid of B[0:min(M,N), :] in pivoted order.
 // If rank_rel2 > 0 the factorisation stops at the first step j whose trailing block has
-// ||B[j:, j:]||_F^2 <= rank_rel2 * ||B||_F^2 (numerical rank); returns the steps done.
+// ||B[j:, j:]||_F^2 <= rank_rel2 * (largest column norm of B)^2 <= rank_rel2 * sigma_1(B)^2
+// (numerical rank); returns the steps done.
 __device__ inline int cta_qrcp(double2* B, int ldb, int M, int N, int* piv, double* nrm, double2* sh, int* s_piv,
                                double rank_rel2) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
@@ -339,8 +355,8 @@ __device__ inline int cta_qrcp(double2* B, int ldb, int M, int N, int* piv, doub
                 if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
             }
             if (lane == 0) {
-                if (j == 0) s_total = rem;
-                *s_piv = (rank_rel2 > 0.0 && rem <= rank_rel2 * s_total) ? -1 : bi;
+                if (j == 0) s_total = best;
+                *s_piv = (rank_rel2 > 0.0 && j > 0 && rem <= rank_rel2 * s_total) ? -1 : bi;
             }
         }
         __syncthreads();
@@ -650,7 +666,7 @@ __device__ inline int qrcp_t(double2* B, int ldb, int M, int N, int* piv, double
             const int pc = (rank_rel2 > 0.0 && j > 0 && rem <= rank_rel2 * s_total) ? -1 : bi;
             // swap columns j <-> pc (warp 0) and form the Householder vector of column j
             if (lane == 0) {
-                if (j == 0) s_total = rem;
+                if (j == 0) s_total = best;
                 *s_piv = pc;
             }
             if (pc >= 0) {
@@ -892,7 +908,7 @@ __device__ __forceinline__ void ztile_mma(ZTile& t, double2 a, double2 b) {
 // if conj_s) or Sg[mu + nu k] if strided.  k is padded to a multiple of 32 with zero fragments
 // (k = 125 for m = 5).  Each warp owns one 8-row tile and four 8-column tiles, reusing its A
 // fragment across them.
-template <bool FULL>
+template <bool FULL, bool UNROLL>
 __device__ inline void chunk_gemm_S_dmma_t(const double2* X, int rx, int i0, int nb, const double2* Sg, bool conj_s,
                                            bool strided, double w, int k, double2* out, int ldo) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -908,6 +924,7 @@ __device__ inline void chunk_gemm_S_dmma_t(const double2* X, int rx, int i0, int
 #pragma unroll
         for (int q = 0; q < 4; ++q) t[q] = ZTile{0.0, 0.0, 0.0, 0.0};
         const double2* xa = X + i0 + row;
+#pragma unroll(UNROLL ? 4 : 1)
         for (int mu = 0; mu < k; mu += 4) {
             const int mm = mu + ac;
             const bool mok = full || mm < k;
@@ -933,12 +950,14 @@ __device__ inline void chunk_gemm_S_dmma_t(const double2* X, int rx, int i0, int
     }
 }
 
+// UNROLL: unroll the k loop 4x (more loads in flight; more registers)
+template <bool UNROLL = false>
 __device__ inline void chunk_gemm_S_dmma(const double2* X, int rx, int i0, int nb, const double2* Sg, bool conj_s,
                                          bool strided, double w, int k, double2* out, int ldo) {
     if ((k & 31) == 0)
-        chunk_gemm_S_dmma_t<true>(X, rx, i0, nb, Sg, conj_s, strided, w, k, out, ldo);
+        chunk_gemm_S_dmma_t<true, UNROLL>(X, rx, i0, nb, Sg, conj_s, strided, w, k, out, ldo);
     else
-        chunk_gemm_S_dmma_t<false>(X, rx, i0, nb, Sg, conj_s, strided, w, k, out, ldo);
+        chunk_gemm_S_dmma_t<false, UNROLL>(X, rx, i0, nb, Sg, conj_s, strided, w, k, out, ldo);
 }
 
 // C = A B^H on the FP64 tensor cores: C[i, j] = sum_mu A[i, mu] conj(Bm[j, mu]) for i < na,
@@ -960,6 +979,7 @@ __device__ inline double dmma_abh(const double2* A, int lda, int na, const doubl
         const double2* ap = A + row;
         const double2* bp = Bm + col;
         int mu = 0;
+#pragma unroll 4
         for (; mu + 4 <= k; mu += 4) {
             const int mm = mu + ac;
             const double2 a = rok ? ap[(size_t)mm * lda] : cmk(0.0, 0.0);

@@ -384,8 +384,8 @@ __global__ void k_basis(PlanD P, const int* bps, int ldr, int ldb) {
             const int nb = qr ? min(CH - fill, r - i0) : min(CH, r - i0);
             double2* dst = B + fill;
             __syncthreads();
-            for (int idx = threadIdx.x; idx < nb * k; idx += blockDim.x)
-                dst[idx % nb + (size_t)(idx / nb) * ldb] = X[i0 + idx % nb + (size_t)(idx / nb) * r];
+            stage_rows(dst, ldb, X, r, i0, nb, k);
+            cp_async_wait_all();
             __syncthreads();
             if (!leaf) kron_apply(dst, ldb, nb, m, Ef + sidx * 3 * m * m, false);
             i0 += nb;
@@ -641,8 +641,10 @@ __device__ inline void truncate_pair(const PlanD& P, const PassD& X, int p, doub
     // B = M^* = Zhat Vt^*  (zr x rowsM) on the FP64 tensor cores
     dmma_abh<true>(Z, zr, zr, Vt, ldvt, rowsM, k, B, ldb);
     // pivoted QR, stopped at the numerical rank (trailing ||.||_F <= 1e-15 ||M||_F)
-    // pivoted QR, stopped at the numerical rank (trailing ||.||_F <= 1e-15 ||M||_F)
-    const int ncol = qrcp_auto(B, ldb, zr, rowsM, piv, nrm, sh, &s_piv, 1e-30);
+    // pivoted QR, stopped once the trailing block has ||R22||_F <= 1e-13 max_j ||M^*(:, j)|| <=
+    // 1e-13 sigma_1: every singular value dropped with it is below the parity tolerance
+    // 1e-12 sigma_1 (DESIGN §6 G3), and its share of any tail sum is < 1e-26 sigma_1^2
+    const int ncol = qrcp_auto(B, ldb, zr, rowsM, piv, nrm, sh, &s_piv, 1e-26);
     zero_lower(B, ldb, ncol, rowsM);  // drop the Householder vectors below the diagonal of R
     __syncthreads();
     const int nsw = jacobi_rows_auto(B, ldb, ncol, rowsM, nrm, &flag);
@@ -815,7 +817,7 @@ __global__ void k_project(PlanD P, int b0, int ldt, int chunk, const int* mirror
     for (int a0 = 0; a0 < kt; a0 += chunk) {
         const int nb = min(chunk, kt - a0);
         if (a0) __syncthreads();
-        chunk_gemm_S_dmma(Ct, lt, a0, nb, Sg, false, mb < 0, 1.0, k, T, ldt);
+        chunk_gemm_S_dmma<true>(Ct, lt, a0, nb, Sg, false, mb < 0, 1.0, k, T, ldt);
         __syncthreads();
         dmma_abh<true>(T, ldt, nb, Cs, ls, ks, k, St + a0, lt);
     }

@@ -26,10 +26,10 @@ __global__ void k_devtest(int op, const double2* in, double2* out, int* iout, do
     if (op == 2) res = qrcp_auto(A, ld, M, N, piv, nrm, sh, &s_piv, 0.0);
     if (op == 3) res = cta_jacobi_rows(A, ld, M, N, nrm, &flag);
     if (op == 4) res = jacobi_rows_auto(A, ld, M, N, nrm, &flag);
-    if (op == 5) res = cta_qrcp(A, ld, M, N, piv, nrm, sh, &s_piv, 1e-30);
-    if (op == 6) res = qrcp_auto(A, ld, M, N, piv, nrm, sh, &s_piv, 1e-30);
+    if (op == 5) res = cta_qrcp(A, ld, M, N, piv, nrm, sh, &s_piv, 1e-26);
+    if (op == 6) res = qrcp_auto(A, ld, M, N, piv, nrm, sh, &s_piv, 1e-26);
     if (op == 7) res = qrcp_np_auto(A, ld, M, N, piv, nrm, 0.0);
-    if (op == 8) res = qrcp_np_auto(A, ld, M, N, piv, nrm, 1e-30);
+    if (op == 8) res = qrcp_np_auto(A, ld, M, N, piv, nrm, 1e-26);
     __syncthreads();
     double2* Y = out + (size_t)blockIdx.x * M * N;
     for (int idx = threadIdx.x; idx < M * N; idx += blockDim.x) Y[idx] = A[idx % M + (idx / M) * ld];

@@ -98,13 +98,17 @@ def test_jacobi_rows(dev, op, nv, L):
 @pytest.mark.parametrize("M,N", [(27, 13), (16, 14), (52, 32), (64, 64)])
 @pytest.mark.parametrize("op", [5, 6, 8])
 def test_qrcp_rank_stop(dev, op, M, N):
-    """With the numerical-rank stop enabled, full-rank graded matrices are factorised completely,
-    and an exactly rank-r matrix stops at r with the leading rows exact."""
+    """With the numerical-rank stop (trailing ||R22||_F^2 <= 1e-26 max column norm^2, the
+    truncation's threshold), a graded matrix is factorised at least while the singular-value tail
+    exceeds 1e-13 sigma_1 (||R22||_F^2 >= sum_{j > i} sigma_j^2), and an exactly rank-r matrix
+    stops at r or r + 1 with the leading rows exact."""
     rng = np.random.default_rng(7)
     A, s = graded(rng, 4, M, N, 0.6)
     out, iout, _ = run(dev, op, A)
     K = min(M, N)
-    assert np.all(iout[:, 0] == K), iout[:, 0]
+    tail2 = np.cumsum((s * s)[::-1])[::-1]  # tail2[i] = sum_{j >= i} sigma_j^2
+    need = int(np.sum(tail2 > 1e-26 * s[0] ** 2))
+    assert np.all((iout[:, 0] >= need) & (iout[:, 0] <= K)), (iout[:, 0], need)
     r = 5
     B = A[:, :, :r] @ (rng.normal(size=(4, r, N)) + 1j * rng.normal(size=(4, r, N)))
     out, iout, _ = run(dev, op, B)
@@ -144,8 +148,8 @@ def test_qrcp_on_oracle_truncation_matrices(dev, op):
             sv = np.linalg.svd(A[b], compute_uv=False)
             svR = np.linalg.svd(R, compute_uv=False)
             n = min(len(sv), len(svR))
-            assert np.abs(sv[:n] - svR[:n]).max() <= 1e-13 * sv[0], (M, N, k, sv, svR)
-            assert np.all(sv[n:] <= 1e-14 * sv[0]), (M, N, k, sv)
+            assert np.abs(sv[:n] - svR[:n]).max() <= 2e-13 * sv[0], (M, N, k, sv, svR)  # Weyl: dropped block <= 1e-13 sigma_1
+            assert np.all(sv[n:] <= 1e-13 * sv[0]), (M, N, k, sv)
 
 
 @pytest.mark.parametrize("nb", [1, 8, 13, 32, 64])
