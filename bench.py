@@ -263,24 +263,31 @@ def main():
         bo = xh.nbytes
         h.close()
         torch.cuda.synchronize()
-        tt = []
+        tt, parts = [], []
         for i in range(args.e2e_steps + 1):
             barrier()
             t0 = time.perf_counter()
             g = make()
+            ta = time.perf_counter()
             g.recompress(cfg["eps"])
+            tb = time.perf_counter()
             yh = g.matvec(xh, 1)
             t1 = time.perf_counter()
+            hb = g.stats()["host_build_ms"]
             g.close()
             if i > 0:
                 tt.append(t1 - t0)
+                parts.append((ta - t0, hb * 1e-3, tb - ta, t1 - tb))
         te = float(np.mean(tt))
+        pm = np.mean(np.array(parts), axis=0)
         if world > 1:
             t = torch.tensor([te], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
         e2e = {"value": n / te / 1e6, "unit": "Mdof/s", "h2d_bytes_per_step": int(bi),
-               "d2h_bytes_per_step": int(bo), "seconds_per_step": te}
+               "d2h_bytes_per_step": int(bo), "seconds_per_step": te,
+               "breakdown_s": {"build_interp": pm[0], "of_which_host_structure": pm[1], "recompress": pm[2],
+                               "matvec": pm[3]}}
         del yh
 
     if rank == 0:

@@ -1910,7 +1910,9 @@ int dh2_get_stats(const dh2_ctx* C, char* buf, int64_t* len) {
       << ", " << S0->tab_ms[2] << ", " << S0->tab_ms[3] << ", " << S0->tab_ms[4] << ", " << S0->tab_ms[5]
       << "]}, \"launches_total\": " << launches
       << ", \"E_row\": " << C->E_row << ", \"E_col\": " << C->E_col << ", \"far2\": " << C->far2
-      << ", \"device_bytes\": " << devb << ", \"mirror_missing\": " << S0->mirror_missing
+      << ", \"device_bytes\": " << devb << ", \"shard_device_bytes\": [";
+    for (size_t i = 0; i < C->sh.size(); ++i) o << (i ? ", " : "") << plan_bytes(C->sh[i].get());
+    o << "], \"mirror_missing\": " << S0->mirror_missing
       << ", \"truncate_ws_launches\": " << ws
       << ", \"adjoint_symmetry\": {\"available\": " << (S0->sym_ok ? "true" : "false") << ", \"enabled\": " << S0->sym_opt
       << ", \"used\": " << (S0->sym_used ? "true" : "false") << ", \"why_not\": \"" << S0->sym_why << "\"}"
