@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <exception>
 #include <map>
 #include <memory>
@@ -206,6 +207,7 @@ struct Shard {
         return e;
     }
     // run `f` (which launches `nl` kernels) under the timing class `cls`
+    bool debug_sync = std::getenv("DH2_DEBUG_SYNC") != nullptr;
     template <typename F>
     void timed(const std::string& cls, int nl, F&& f) {
         if (profiling) {
@@ -218,7 +220,8 @@ struct Shard {
             f();
         }
         cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) throw CudaError("launch of kernel class '" + cls + "': " + cudaGetErrorString(e));
+        if (e == cudaSuccess && debug_sync) e = cudaStreamSynchronize(stream);  // DH2_DEBUG_SYNC=1
+        if (e != cudaSuccess) throw CudaError("kernel class '" + cls + "': " + cudaGetErrorString(e));
         kstat[cls].launches += nl;
         launches_total += nl;
     }
@@ -1011,6 +1014,10 @@ void run_weights_truncate(Shard* C, double eps, int mode) {
             C->timed(std::string(row ? "truncate_row@" : "truncate_col@") + std::to_string(l), 1, [&] { launch_truncate(P, row, p0, np, TL, all_leaf, eps, mode, C->d_ws.p, s); });
             CK(cudaMemcpyAsync(X.rank.data() + p0, X.d_rank.p + p0, np * sizeof(int), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
+            for (int p = p0; p < p0 + np; ++p)
+                if (X.rank[p] < 0)
+                    throw CudaError("non-finite singular values in the truncation of level " + std::to_string(l) +
+                                    " (pair " + std::to_string(p) + "): non-finite input from an earlier phase");
             double fl = 0;
             for (int p = p0; p < p0 + np; ++p) {
                 double rows = X.child0[p] < 0 ? (double)T.size(C->bp_t[X.bp[p]]) : X.rank[X.child0[p]] + X.rank[X.child1[p]];

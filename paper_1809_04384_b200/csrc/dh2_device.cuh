@@ -7,6 +7,10 @@
 namespace dh2 {
 
 constexpr int MMAX = 5;  // maximal Chebyshev order per axis supported by the grid tables
+// Householder reflectors are formed only for columns with sum of squares above HH_TINY: below it
+// tau = 1/(xn (xn + |alpha|)) can overflow (xn < 1e-154), and the column (norm < 1e-150) is
+// numerically zero at every scale of this problem; it is left in place (beta = alpha).
+constexpr double HH_TINY = 1e-300;
 
 struct GridD {
     double mid[3];
@@ -226,7 +230,7 @@ __device__ inline void cta_qr(double2* A, int lda, int M, int N, double2* sh /* 
                 double2 alpha = colj[j];
                 double tau = 0.0;
                 double2 beta = alpha;
-                if (s > 0.0) {
+                if (s > HH_TINY) {  // tiny columns are left as they are (1/(xn (xn + aa)) would overflow)
                     double aa = sqrt(cabs2(alpha));
                     double xn = sqrt(s + aa * aa);
                     double2 ph = aa > 0.0 ? cscale(alpha, 1.0 / aa) : cmk(1.0, 0.0);
@@ -383,7 +387,7 @@ __device__ inline int cta_qrcp(double2* B, int ldb, int M, int N, int* piv, doub
                 double2 alpha = colj[j];
                 double tau = 0.0;
                 double2 beta = alpha;
-                if (s > 0.0) {
+                if (s > HH_TINY) {  // tiny columns are left as they are (1/(xn (xn + aa)) would overflow)
                     double aa = sqrt(cabs2(alpha));
                     double xn = sqrt(s + aa * aa);
                     double2 ph = aa > 0.0 ? cscale(alpha, 1.0 / aa) : cmk(1.0, 0.0);
@@ -690,7 +694,7 @@ __device__ inline int qrcp_t(double2* B, int ldb, int M, int N, int* piv, double
                     const double2 alpha = colj[j];
                     double tau = 0.0;
                     double2 beta = alpha;
-                    if (s > 0.0) {
+                    if (s > HH_TINY) {  // tiny columns are left as they are (1/(xn (xn + aa)) would overflow)
                         const double aa = sqrt(cabs2(alpha));
                         const double xn = sqrt(s + aa * aa);
                         const double2 ph = aa > 0.0 ? cscale(alpha, 1.0 / aa) : cmk(1.0, 0.0);
@@ -817,7 +821,7 @@ __device__ inline int qrcp_np_t(double2* B, int ldb, int M, int N, int* piv, dou
         const double2 alpha = colp[j];
         double tau = 0.0;
         double2 beta = alpha, u0 = alpha;
-        if (sq > 0.0) {
+        if (sq > HH_TINY) {  // see cta_qr_append
             const double aa = sqrt(cabs2(alpha));
             const double xn = sqrt(sq + aa * aa);
             const double2 ph = aa > 0.0 ? cscale(alpha, 1.0 / aa) : cmk(1.0, 0.0);

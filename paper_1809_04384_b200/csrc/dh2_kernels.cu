@@ -294,7 +294,7 @@ __device__ inline void cta_qr_append(double2* R, int ldr, double2* B, int ldb, i
         const double2 alpha = R[ridx<PK>(j, j, ldr)];
         double tau = 0.0;
         double2 beta = alpha, u0 = cmk(0.0, 0.0);
-        if (s > 0.0) {
+        if (s > HH_TINY) {  // tiny columns are left as they are (1/(xn (xn + aa)) would overflow)
             const double aa = sqrt(cabs2(alpha));
             const double xn = sqrt(s + aa * aa);
             const double2 ph = aa > 0.0 ? cscale(alpha, 1.0 / aa) : cmk(1.0, 0.0);
@@ -640,7 +640,6 @@ __device__ inline void truncate_pair(const PlanD& P, const PassD& X, int p, doub
     }
     // B = M^* = Zhat Vt^*  (zr x rowsM) on the FP64 tensor cores
     dmma_abh<true>(Z, zr, zr, Vt, ldvt, rowsM, k, B, ldb);
-    // pivoted QR, stopped at the numerical rank (trailing ||.||_F <= 1e-15 ||M||_F)
     // pivoted QR, stopped once the trailing block has ||R22||_F <= 1e-13 max_j ||M^*(:, j)|| <=
     // 1e-13 sigma_1: every singular value dropped with it is below the parity tolerance
     // 1e-12 sigma_1 (DESIGN §6 G3), and its share of any tail sum is < 1e-26 sigma_1^2
@@ -650,11 +649,12 @@ __device__ inline void truncate_pair(const PlanD& P, const PassD& X, int p, doub
     const int nsw = jacobi_rows_auto(B, ldb, ncol, rowsM, nrm, &flag);
     if (threadIdx.x == 0) X.sweeps[p] = nsw;
     // singular values = norms of the rows of R; order by decreasing value (ties: lower index)
+    // (keys with NaN mapped to -1 so that ord is always a permutation; such a pair is flagged below)
     for (int j = threadIdx.x; j < ncol; j += blockDim.x) {
         int pos = 0;
-        const double sj = nrm[j];
+        const double sj = nrm[j] == nrm[j] ? nrm[j] : -1.0;
         for (int i = 0; i < ncol; ++i) {
-            const double si = nrm[i];
+            const double si = nrm[i] == nrm[i] ? nrm[i] : -1.0;
             pos += (si > sj) || (si == sj && i < j);
         }
         ord[pos] = j;
@@ -682,8 +682,11 @@ __device__ inline void truncate_pair(const PlanD& P, const PassD& X, int p, doub
             }
         }
         if (kk > kb) kk = kb;
+        bool finite = true;
+        for (int a = 0; a < ncol; ++a) finite = finite && isfinite(so[a]);
+        if (!finite) kk = 0;  // non-finite input: no output, rank -1 reported to the host
         s_rank = kk;
-        X.rank[p] = kk;
+        X.rank[p] = finite ? kk : -1;
         X.nsig[p] = ncol;
         X.disc[p] = disc;
     }

@@ -17,12 +17,19 @@ CONFIGS = {
     # k = 125 (m = 5) at the C4/C5 tolerance eps = 1e-6: cube (flat boxes) and sphere
     "P4": dict(mesh="cube", q=8, kappa=5.0, m=5, leaf=16, eta1=1.0, eta2=10.0, eps=1e-6),
     "P5": dict(mesh="sphere", q=16, kappa=6.0, m=5, leaf=16, eta1=1.0, eta2=10.0, eps=1e-6),
+    # the C5 leaf shape (cube, flat leaves of 48 triangles) at k = 125
+    "P6": dict(mesh="cube", q=8, kappa=5.0, m=5, leaf=64, eta1=1.0, eta2=10.0, eps=1e-6),
+    "P7": dict(mesh="cube", q=16, kappa=14.0, m=5, leaf=64, eta1=1.0, eta2=10.0, eps=1e-6),
     # BASELINE.json configs
     "C1": dict(mesh="sphere", q=8, kappa=4.0, m=3, leaf=16, eta1=1.0, eta2=10.0, eps=1e-4),
     "C2": dict(mesh="sphere", q=32, kappa=16.0, m=4, leaf=32, eta1=1.0, eta2=10.0, eps=1e-4),
     "C3": dict(mesh="sphere", q=64, kappa=32.0, m=4, leaf=32, eta1=1.0, eta2=10.0, eps=1e-5),
     "C4": dict(mesh="sphere", q=128, kappa=64.0, m=5, leaf=64, eta1=1.0, eta2=10.0, eps=1e-6),
     "C5": dict(mesh="cube", q=128, kappa=115.0, m=5, leaf=64, eta1=1.0, eta2=10.0, eps=1e-6),
+    # C4 / C5 scaled down to one GPU's memory (same order m = 5, leaf 64, eps = 1e-6 and kappa h ~ 0.9):
+    # the full C4/C5 need the partitioned or memory-lean path
+    "C4s": dict(mesh="sphere", q=32, kappa=16.0, m=5, leaf=64, eta1=1.0, eta2=10.0, eps=1e-6),
+    "C5s": dict(mesh="cube", q=32, kappa=29.0, m=5, leaf=64, eta1=1.0, eta2=10.0, eps=1e-6),
 }
 
 

@@ -1,7 +1,10 @@
-"""C3 (BASELINE configs[2]: sphere n = 32768, kappa = 32, m = 4, eps = 1e-5) at full size on the
-GPU, checked on seeded samples of outputs that the oracle computes one by one (oracle/lazy.py:
-the same §3.2 formulas evaluated on the dependency cone of each sampled pair), plus
-properties that hold at any size."""
+"""Configurations too large for the eager oracle, at full size on the GPU: C3 (BASELINE configs[2]:
+sphere n = 32768, kappa = 32, m = 4, eps = 1e-5) and the one-GPU scale-downs of C4 / C5 at their
+order m = 5 (k = 125), leaf 64 and eps = 1e-6 (C4s: sphere n = 8192; C5s: cube n = 12288, flat
+boxes, truncations above the leaves large enough for the global-workspace kernel).  Checked on
+seeded samples of outputs that the oracle computes one by one (oracle/lazy.py: the same §3.2
+formulas evaluated on the dependency cone of each sampled pair), plus properties that hold at
+any size."""
 import numpy as np
 import pytest
 
@@ -10,12 +13,12 @@ from synth import get_config, mesh_for
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def c3():
+@pytest.fixture(scope="module", params=["C3", "C4s", "C5s"])
+def c3(request):
     from paper_1809_04384_b200 import DH2
     from oracle.structure import DH2Structure
     from oracle.lazy import LazyRecompression
-    cfg = get_config("C3")
+    cfg = get_config(request.param)
     xyz, tri = mesh_for(cfg)
     h = DH2(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"])
     h.recompress(cfg["eps"])
@@ -69,7 +72,7 @@ def test_c3_sampled_pairs(c3, side):
             G0 = Zo.conj().T @ Zo
             assert np.abs(Zg.conj().T @ Zg - G0).max() <= 1e-11 * np.abs(G0).max()
             checked += 1
-    assert checked >= 50
+    assert checked >= min(50, 12 * sum(1 for l in range(len(lev_ptr) - 1) if lev_ptr[l + 1] > lev_ptr[l]))
 
 
 def test_c3_sampled_basis_weights_and_block_norms(c3):
