@@ -19,6 +19,7 @@ CONFIGS = {
     "P5": dict(mesh="sphere", q=16, kappa=6.0, m=5, leaf=16, eta1=1.0, eta2=10.0, eps=1e-6),
     # the C5 leaf shape (cube, flat leaves of 48 triangles) at k = 125
     "P6": dict(mesh="cube", q=8, kappa=5.0, m=5, leaf=64, eta1=1.0, eta2=10.0, eps=1e-6),
+    # three active levels of that shape: regression case of DESIGN reading N2 (numerically zero columns)
     "P7": dict(mesh="cube", q=16, kappa=14.0, m=5, leaf=64, eta1=1.0, eta2=10.0, eps=1e-6),
     # BASELINE.json configs
     "C1": dict(mesh="sphere", q=8, kappa=4.0, m=3, leaf=16, eta1=1.0, eta2=10.0, eps=1e-4),
