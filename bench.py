@@ -186,7 +186,13 @@ def main():
                    world=args.shards)
 
     n = cfg["n"]
-    h = make()
+    try:
+        h = make()
+    except Exception as e:  # e.g. DH2_ENOMEM: the full-materialisation plan exceeds the GPU (C4/C5)
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "config": {"workload": workload_desc(cfg), "n": n},
+                              "unavailable": str(e).splitlines()[0]}), flush=True)
+        return
     stream = torch.cuda.current_stream()
     h.set_stream(stream.cuda_stream)
     x = torch.from_numpy(seeded_vector(n, 1)).to("cuda")
