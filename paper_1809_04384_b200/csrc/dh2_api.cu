@@ -158,6 +158,8 @@ struct Shard {
     bool sym_ok = false;     // structure admits it (checked in build_tables)
     int sym_opt = 1;         // dh2_set_option("adjoint_symmetry")
     int force_ws = 0;        // dh2_set_option("truncate_workspace")
+    int split_trunc = 1;     // dh2_set_option("truncate_split"): warp-register Jacobi for leaves <= 32
+    DevBuf<char> d_tscr;     // scratch of the split truncation
     DevBuf<double2> d_ws;    // truncation workspace (persistent grid), grown on demand
     int64_t ws_launches = 0; // truncation launches that used the workspace
     bool sym_used = false;   // the last dh2_recompress derived the column pass from the row pass
@@ -1003,6 +1005,16 @@ void run_weights_truncate(Shard* C, double eps, int mode) {
             if (any_leaf && !all_leaf)  // median-split trees never mix leaves and inner clusters on a level
                 throw NotImpl("a tree level mixing leaf and non-leaf clusters is not supported by k_truncate");
             const TruncLaunch TL = plan_truncate(P, np, maxrows, maxz, all_leaf, C->force_ws != 0);
+            const bool split = C->split_trunc && all_leaf && maxrows <= 32 && !TL.use_ws;
+            if (split) {
+                const size_t need = trunc_split_scratch_bytes(np);
+                if (C->d_tscr.n < need) {
+                    CK(cudaStreamSynchronize(s));
+                    C->d_tscr.alloc(need);
+                }
+                C->timed(std::string(row ? "truncate_row@" : "truncate_col@") + std::to_string(l), 3,
+                         [&] { launch_truncate_split(P, row, p0, np, TL, eps, mode, C->d_tscr.p, s); });
+            }
             if (TL.use_ws) {
                 const size_t need = (size_t)TL.grid * TL.ws_stride;
                 if (C->d_ws.n < need) {
@@ -1011,7 +1023,8 @@ void run_weights_truncate(Shard* C, double eps, int mode) {
                 }
                 ++C->ws_launches;
             }
-            C->timed(std::string(row ? "truncate_row@" : "truncate_col@") + std::to_string(l), 1, [&] { launch_truncate(P, row, p0, np, TL, all_leaf, eps, mode, C->d_ws.p, s); });
+            if (!split)
+                C->timed(std::string(row ? "truncate_row@" : "truncate_col@") + std::to_string(l), 1, [&] { launch_truncate(P, row, p0, np, TL, all_leaf, eps, mode, C->d_ws.p, s); });
             CK(cudaMemcpyAsync(X.rank.data() + p0, X.d_rank.p + p0, np * sizeof(int), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             for (int p = p0; p < p0 + np; ++p)
@@ -1866,6 +1879,11 @@ int dh2_set_option(dh2_ctx* X, const char* name, int64_t value) {
     if (nm == "truncate_workspace") {  // 1: force the global-workspace truncation path (tests)
         if (value != 0 && value != 1) return fail(X, DH2_EINVAL, "truncate_workspace must be 0 or 1");
         for (auto& S : X->sh) S->force_ws = (int)value;
+        return DH2_OK;
+    }
+    if (nm == "truncate_split") {  // 0: the one-kernel truncation also for leaves <= 32 (tests)
+        if (value != 0 && value != 1) return fail(X, DH2_EINVAL, "truncate_split must be 0 or 1");
+        for (auto& S : X->sh) S->split_trunc = (int)value;
         return DH2_OK;
     }
     if (nm == "adjoint_symmetry") {

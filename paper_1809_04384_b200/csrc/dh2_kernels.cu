@@ -588,23 +588,25 @@ void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* m
 //   Jacobi: high relative accuracy, few sweeps; no Gram matrix is formed, DESIGN reading Q13);
 //   rank k_tc by the rule of `mode`, Q = first k_tc vectors (leaf: Q_tc, non-leaf:
 //   Qhat = [F_{t1c}; F_{t2c}]), C_tc = Q^* V_tc or Qhat^* Vhat (Eq. 19).
+// Truncation prologue: M^* = Zhat Vt^* (leaf Vt = V_tc; above the leaves
+// Vt = Vhat = [C_{t1c1} E_{t1c}; C_{t2c2} E_{t2c}] built here) and its pivoted QR, stopped at the
+// numerical rank.  On return the rows 0..ncol-1 of B hold R (zero below the pivoted diagonal), piv
+// the pivot order; returns ncol, or -1 if the pair is empty (rank 0 already recorded).
 template <bool LEAF>
-__device__ inline void truncate_pair(const PlanD& P, const PassD& X, int p, double2* sm, int ldv, int ldb, double eps,
-                                     int mode, int& flag, int& s_piv, int& s_rank, double2* sh) {
+__device__ inline int truncate_prologue(const PlanD& P, const PassD& X, int p, double2* sm, int ldv, int ldb,
+                                        double2*& B, double*& nrm, int*& piv, int*& ord, int& rowsM,
+                                        const double2*& Vt, int& ldvt, int& s_piv, double2* sh) {
     const int k = P.k, m = P.m;
     const int bp = X.bp[p];
     constexpr bool leaf = LEAF;  // one instance per kind of level (all pairs of a level are alike)
     const int zr = X.Z_rows[p];
     const double2* Z = X.Z + X.Z_off[p];
     double2* Vs = sm;                                  // non-leaf Vhat (rowsM x k, ld ldv)
-    double2* B = Vs + (leaf ? 0 : (size_t)ldv * k);    // M^* (zr x rowsM, ld ldb)
+    B = Vs + (leaf ? 0 : (size_t)ldv * k);             // M^* (zr x rowsM, ld ldb)
     double2* Ef = B + (size_t)ldb * ldv;               // 6 m^2 (non-leaf)
-    double* nrm = reinterpret_cast<double*>(Ef + (leaf ? 0 : 6 * m * m));  // ldv
-    int* piv = reinterpret_cast<int*>(nrm + ldv);      // ldv
-    int* ord = piv + ldv;                              // ldv
-    int rowsM;
-    const double2* Vt;
-    int ldvt;
+    nrm = reinterpret_cast<double*>(Ef + (leaf ? 0 : 6 * m * m));  // ldv
+    piv = reinterpret_cast<int*>(nrm + ldv);           // ldv
+    ord = piv + ldv;                                   // ldv
     if constexpr (leaf) {
         rowsM = P.c_size[P.bp_t[bp]];
         Vt = P.V + P.bp_V_off[bp];
@@ -626,17 +628,14 @@ __device__ inline void truncate_pair(const PlanD& P, const PassD& X, int p, doub
         Vt = Vs;
         ldvt = ldv;
     }
-    const int ldq = leaf ? rowsM : X.rowsb[p];
-    double2* Qg = X.Q + X.Q_off[p];
-    double2* Cg = X.C + X.C_off[p];
-    const int kb = X.kb[p];
     if (rowsM == 0 || zr == 0) {
         if (threadIdx.x == 0) {
             X.rank[p] = 0;
             X.nsig[p] = 0;
             X.disc[p] = 0.0;
+            X.sweeps[p] = 0;
         }
-        return;
+        return -1;
     }
     // B = M^* = Zhat Vt^*  (zr x rowsM) on the FP64 tensor cores
     dmma_abh<true>(Z, zr, zr, Vt, ldvt, rowsM, k, B, ldb);
@@ -646,8 +645,18 @@ __device__ inline void truncate_pair(const PlanD& P, const PassD& X, int p, doub
     const int ncol = qrcp_auto(B, ldb, zr, rowsM, piv, nrm, sh, &s_piv, 1e-26);
     zero_lower(B, ldb, ncol, rowsM);  // drop the Householder vectors below the diagonal of R
     __syncthreads();
-    const int nsw = jacobi_rows_auto(B, ldb, ncol, rowsM, nrm, &flag);
-    if (threadIdx.x == 0) X.sweeps[p] = nsw;
+    return ncol;
+}
+
+// Truncation epilogue: singular values sigma_a = ||row ord[a] of R|| (rows of R
+// mutually orthogonal after the Jacobi), rank by the rule of `mode`, Q / Qhat = [F1; F2] and
+// C = Q^* Vt from the rows of R, the pivot order piv and Vt (rowsM x k, ld ldvt).
+__device__ inline void truncate_epilogue(const PassD& X, int p, int k, const double2* B, int ldb, int ncol, int rowsM,
+                                         const int* piv, const double* nrm, int* ord, const double2* Vt, int ldvt,
+                                         int ldq, double eps, int mode, int& s_rank) {
+    double2* Qg = X.Q + X.Q_off[p];
+    double2* Cg = X.C + X.C_off[p];
+    const int kb = X.kb[p];
     // singular values = norms of the rows of R; order by decreasing value (ties: lower index)
     // (keys with NaN mapped to -1 so that ord is always a permutation; such a pair is flagged below)
     for (int j = threadIdx.x; j < ncol; j += blockDim.x) {
@@ -713,6 +722,22 @@ __device__ inline void truncate_pair(const PlanD& P, const PassD& X, int p, doub
 // Truncation kernels: one CTA per pair with the working set in shared memory, or, when it
 // exceeds the opt-in shared memory (large k / ranks), a persistent grid whose CTAs keep their
 // working set in a private global (L2-resident) workspace slab.
+
+template <bool LEAF>
+__device__ inline void truncate_pair(const PlanD& P, const PassD& X, int p, double2* sm, int ldv, int ldb, double eps,
+                                     int mode, int& flag, int& s_piv, int& s_rank, double2* sh) {
+    double2* B;
+    double* nrm;
+    int *piv, *ord;
+    int rowsM, ldvt;
+    const double2* Vt;
+    const int ncol = truncate_prologue<LEAF>(P, X, p, sm, ldv, ldb, B, nrm, piv, ord, rowsM, Vt, ldvt, s_piv, sh);
+    if (ncol < 0) return;
+    const int nsw = jacobi_rows_auto(B, ldb, ncol, rowsM, nrm, &flag);
+    if (threadIdx.x == 0) X.sweeps[p] = nsw;
+    truncate_epilogue(X, p, P.k, B, ldb, ncol, rowsM, piv, nrm, ord, Vt, ldvt, LEAF ? rowsM : X.rowsb[p], eps, mode, s_rank);
+}
+
 template <bool LEAF>
 __global__ void __launch_bounds__(128, LEAF ? 5 : 4)
     k_truncate(PlanD P, PassD X, int p0, int ldv, int ldb, double eps, int mode) {
@@ -732,6 +757,212 @@ __global__ void __launch_bounds__(128, 4)
         truncate_pair<LEAF>(P, X, p0 + i, base, ldv, ldb, eps, mode, flag, s_piv, s_rank, sh);
         __syncthreads();
     }
+}
+
+// ------------------------------------------------------------------ leaf truncation, split path
+// For leaf levels with #t <= 32 (C2, C3): (1) k_trunc_qr: M^* and its pivoted QR per CTA as above,
+// R written to a scratch slab (32 x 32, row r = vector r, element-major) with the pivot order;
+// (2) k_jacobi_w32: the one-sided Jacobi on the rows of R with one WARP per pair and the matrix in
+// registers (lane = element, 32 slots = vectors): same rotation formulas, tolerance and norm
+// updates as jacobi_rows_t, round-robin by the circle method (pairs = slots (2i, 2i+1), a fixed
+// slot permutation after every round), no shared-memory traffic and no block barriers;
+// (3) k_trunc_epi: ordering, rank rule, Q and C from the scratch (truncate_epilogue).
+
+// circle-method tournament on 32 slots: slot <-> position, one step of the rotation
+__host__ __device__ constexpr int jw_pos(int s) { return (s & 1) ? 31 - (s >> 1) : (s >> 1); }
+__host__ __device__ constexpr int jw_slot(int pos) { return pos < 16 ? 2 * pos : 2 * (31 - pos) + 1; }
+__host__ __device__ constexpr int jw_next(int pos) { return pos == 0 ? 0 : (pos == 31 ? 1 : pos + 1); }
+__host__ __device__ constexpr int jw_prev(int pos) { return pos == 0 ? 0 : (pos == 1 ? 31 : pos - 1); }
+
+// v[0..31] per lane -> lane l returns sum over the warp of v[l] (recursive halving, 31 shuffles)
+__device__ __forceinline__ double reduce_scatter32(double (&v)[32], int lane) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < o; ++i) {
+            const double send = up ? v[i] : v[i + o];
+            const double keep = up ? v[i + o] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    return v[0];
+}
+
+// v[0..15] per lane -> lanes l and l^16 return the sum over the warp of v[l & 15]
+__device__ __forceinline__ double reduce_scatter16(double (&v)[16], int lane) {
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < o; ++i) {
+            const double send = up ? v[i] : v[i + o];
+            const double keep = up ? v[i + o] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+}
+
+__global__ void __launch_bounds__(128, 5) k_trunc_qr(PlanD P, PassD X, int p0, int ldv, int ldb, double2* sR, int* sPiv,
+                                                    int* sMeta) {
+    extern __shared__ double2 smd[];
+    __shared__ int s_piv;
+    __shared__ double2 sh[2];
+    const int i = blockIdx.x, p = p0 + i;
+    double2* B;
+    double* nrm;
+    int *piv, *ord;
+    int rowsM, ldvt;
+    const double2* Vt;
+    const int ncol = truncate_prologue<true>(P, X, p, smd, ldv, ldb, B, nrm, piv, ord, rowsM, Vt, ldvt, s_piv, sh);
+    if (threadIdx.x == 0) {
+        sMeta[2 * i] = ncol;  // -1: empty pair, already recorded
+        sMeta[2 * i + 1] = rowsM;
+    }
+    if (ncol < 0) return;
+    double2* R = sR + (size_t)i * 1024;
+    for (int idx = threadIdx.x; idx < 1024; idx += blockDim.x) {
+        const int r = idx >> 5, j = idx & 31;
+        R[idx] = (r < ncol && j < rowsM) ? B[r + (size_t)j * ldb] : cmk(0.0, 0.0);
+    }
+    for (int j = threadIdx.x; j < 32; j += blockDim.x) sPiv[i * 32 + j] = j < rowsM ? piv[j] : 0;
+}
+
+__global__ void __launch_bounds__(128, 3) k_jacobi_w32(PassD X, int p0, int np, double2* sR, double* sN, const int* sMeta) {
+    __shared__ double4 prm[4][16];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int i = blockIdx.x * 4 + w;
+    if (i >= np) return;  // whole warp
+    const int ncol = sMeta[2 * i], len = sMeta[2 * i + 1];
+    if (ncol < 0) return;
+    constexpr unsigned FULL = 0xffffffffu;
+    double2 x[32];  // lane = element c of the row vectors of R: x[r] = R[r, c]
+    double2* R = sR + (size_t)i * 1024;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) x[r] = R[r * 32 + lane];
+    const double tol = fmax((double)len, 1.0) * 2.220446049250313e-16;
+    const double tol2 = tol * tol;
+    auto norms = [&]() {
+        double v[32];
+#pragma unroll
+        for (int r = 0; r < 32; ++r) v[r] = cabs2(x[r]);
+        return reduce_scatter32(v, lane);
+    };
+    double nr = 0.0;
+    int sweep = 0;
+#pragma unroll 1
+    for (; sweep < 60 && ncol > 1; ++sweep) {
+        nr = norms();
+        bool any = false;
+#pragma unroll 1
+        for (int round = 0; round < 31; ++round) {
+            // a conj(b) of the slot pairs (2q, 2q+1), this lane's element; pairs 0-7 and 8-15 are
+            // reduced separately (16 values each) so that lane 2q / 2q+1 ends with Re / Im of g_q
+            double mine;
+            {
+                double d[16];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const double2 a = x[2 * q], b = x[2 * q + 1];
+                    d[2 * q] = fma(a.x, b.x, a.y * b.y);
+                    d[2 * q + 1] = fma(a.y, b.x, -(a.x * b.y));
+                }
+                const double lo = reduce_scatter16(d, lane);
+#pragma unroll
+                for (int q = 8; q < 16; ++q) {
+                    const double2 a = x[2 * q], b = x[2 * q + 1];
+                    d[2 * q - 16] = fma(a.x, b.x, a.y * b.y);
+                    d[2 * q - 15] = fma(a.y, b.x, -(a.x * b.y));
+                }
+                const double hi = reduce_scatter16(d, lane);
+                mine = (lane & 16) ? hi : lo;
+            }
+            const double other = __shfl_xor_sync(FULL, mine, 1);
+            const double2 ga = (lane & 1) ? cmk(other, mine) : cmk(mine, other);
+            const double nother = __shfl_xor_sync(FULL, nr, 1);
+            const double al = (lane & 1) ? nother : nr, be = (lane & 1) ? nr : nother;
+            const double g2 = cabs2(ga);
+            double c = 1.0, sn = 0.0;
+            double2 ec = cmk(1.0, 0.0);
+            if (g2 > tol2 * (al * be) && al > 0.0 && be > 0.0) {  // as jacobi_rows_t
+                const double ig = rsqrt(g2);
+                const double gm = g2 * ig;
+                const double dd = be - al;
+                const double ir = rsqrt(fma(dd, dd, 4.0 * g2));
+                const double c2 = fma(0.5 * fabs(dd), ir, 0.5);
+                const double ic = rsqrt(c2);
+                c = c2 * ic;
+                const double t = (dd >= 0.0 ? gm : -gm) * ir * (ic * ic);
+                sn = t * c;
+                ec = cmk(ga.x * ig, ga.y * ig);
+                nr = (lane & 1) ? be + t * gm : al - t * gm;
+                any = true;
+            }
+            if (!(lane & 1)) prm[w][lane >> 1] = make_double4(c, sn, ec.x, ec.y);
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const double4 pr = prm[w][q];
+                const double2 a = x[2 * q];
+                const double2 bb = cmul(cmk(pr.z, pr.w), x[2 * q + 1]);
+                x[2 * q] = cmk(pr.x * a.x - pr.y * bb.x, pr.x * a.y - pr.y * bb.y);
+                x[2 * q + 1] = cmk(pr.y * a.x + pr.x * bb.x, pr.y * a.y + pr.x * bb.y);
+                if ((q & 3) == 3) __syncwarp();  // keeps the parameter loads from being hoisted (registers)
+            }
+            {  // positions 1..31 advance by one (31 wraps to 1), position 0 stays: one register cycle
+                const double2 tmp = x[jw_slot(31)];
+#pragma unroll
+                for (int pos = 31; pos >= 2; --pos) x[jw_slot(pos)] = x[jw_slot(pos - 1)];
+                x[jw_slot(1)] = tmp;
+            }
+            nr = __shfl_sync(FULL, nr, jw_slot(jw_prev(jw_pos(lane))));
+        }
+        if (!__any_sync(FULL, any)) break;  // a full sweep without rotation: converged
+    }
+    nr = norms();
+#pragma unroll
+    for (int r = 0; r < 32; ++r) R[r * 32 + lane] = x[r];
+    sN[i * 32 + lane] = nr;
+    if (lane == 0) X.sweeps[p0 + i] = sweep;
+}
+
+__global__ void __launch_bounds__(128) k_trunc_epi(PlanD P, PassD X, int p0, const double2* sR, const double* sN,
+                                                  const int* sPiv, const int* sMeta, double eps, int mode) {
+    __shared__ double2 B[32 * 33];
+    __shared__ double nrm[32];
+    __shared__ int piv[32], ord[32];
+    __shared__ int s_rank;
+    const int i = blockIdx.x, p = p0 + i;
+    const int ncol = sMeta[2 * i], rowsM = sMeta[2 * i + 1];
+    if (ncol < 0) return;
+    for (int idx = threadIdx.x; idx < 1024; idx += blockDim.x) {
+        const int r = idx >> 5, j = idx & 31;
+        B[r + j * 33] = sR[(size_t)i * 1024 + idx];
+    }
+    if (threadIdx.x < 32) {
+        nrm[threadIdx.x] = sN[i * 32 + threadIdx.x];
+        piv[threadIdx.x] = sPiv[i * 32 + threadIdx.x];
+    }
+    __syncthreads();
+    const int bp = X.bp[p];
+    const double2* Vt = P.V + P.bp_V_off[bp];
+    truncate_epilogue(X, p, P.k, B, 33, ncol, rowsM, piv, nrm, ord, Vt, rowsM, rowsM, eps, mode, s_rank);
+}
+
+size_t trunc_split_scratch_bytes(int np) { return (size_t)np * (1024 * sizeof(double2) + 32 * sizeof(double) + 34 * sizeof(int)); }
+
+void launch_truncate_split(const PlanD& P, bool row, int p0, int np, const TruncLaunch& L, double eps, int mode,
+                           void* scratch, cudaStream_t s) {
+    if (!np) return;
+    const PassD& X = row ? P.row : P.col;
+    double2* sR = reinterpret_cast<double2*>(scratch);
+    double* sN = reinterpret_cast<double*>(sR + (size_t)np * 1024);
+    int* sPiv = reinterpret_cast<int*>(sN + (size_t)np * 32);
+    int* sMeta = sPiv + (size_t)np * 32;
+    k_trunc_qr<<<np, 128, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, sR, sPiv, sMeta);
+    k_jacobi_w32<<<(np + 3) / 4, 128, 0, s>>>(X, p0, np, sR, sN, sMeta);
+    k_trunc_epi<<<np, 128, 0, s>>>(P, X, p0, sR, sN, sPiv, sMeta, eps, mode);
 }
 
 TruncLaunch plan_truncate(const PlanD& P, int np, int maxrowsM, int maxZrows, bool leaf_level, bool force_ws) {
@@ -1017,7 +1248,7 @@ cudaError_t configure_kernels() {
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     const void* ks[] = {(const void*)k_leafV, (const void*)k_basis<true, 4>, (const void*)k_basis<true, 2>,
-                        (const void*)k_block_weights, (const void*)k_total_weights<true, 4>, (const void*)k_total_weights<true, 2>, (const void*)k_truncate<true>, (const void*)k_truncate<false>,
+                        (const void*)k_block_weights, (const void*)k_total_weights<true, 4>, (const void*)k_total_weights<true, 2>, (const void*)k_truncate<true>, (const void*)k_truncate<false>, (const void*)k_trunc_qr,
                         (const void*)k_project};
     for (const void* f : ks) {
         if (e != cudaSuccess) break;

@@ -101,6 +101,10 @@ struct TruncLaunch {
 TruncLaunch plan_truncate(const PlanD& P, int np, int maxrowsM, int maxZrows, bool leaf_level, bool force_ws);
 void launch_truncate(const PlanD& P, bool row, int p0, int np, const TruncLaunch& L, bool leaf_level, double eps,
                      int mode, double2* ws, cudaStream_t s);
+// leaf levels with #t <= 32: pivoted QR per CTA, register-resident warp Jacobi, epilogue
+size_t trunc_split_scratch_bytes(int np);
+void launch_truncate_split(const PlanD& P, bool row, int p0, int np, const TruncLaunch& L, double eps, int mode,
+                           void* scratch, cudaStream_t s);
 void launch_mirror_pass(const PlanD& P, const int* col2row, int p0, int np, cudaStream_t s);
 void launch_project(const PlanD& P, int b0, int nb, int maxkrow, const int* mirror, cudaStream_t s);
 // matvec (forward / coupling / backward)
