@@ -24,16 +24,17 @@ _GPU = {}
 CASES = [(n, 1) for n in SMALL + ["C2"]] + [(n, 0) for n in SMALL]
 
 
-def gpu_run(name, eps=None, mode="FROB_BLOCKREL", sym=1, ws=0):
+def gpu_run(name, eps=None, mode="FROB_BLOCKREL", sym=1, ws=0, split=1):
     from paper_1809_04384_b200 import DH2
     from gpu_view import GpuView
-    key = (name, eps, mode, sym, ws)
+    key = (name, eps, mode, sym, ws, split)
     if key not in _GPU:
         cfg = get_config(name)
         xyz, tri = mesh_for(cfg)
         h = DH2(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"])
         h.set_option("adjoint_symmetry", sym)
         h.set_option("truncate_workspace", ws)
+        h.set_option("truncate_split", split)
         h.recompress(cfg["eps"] if eps is None else eps, mode)
         assert h.stats()["adjoint_symmetry"]["used"] == bool(sym)
         assert (h.stats()["truncate_ws_launches"] > 0) == bool(ws)
@@ -159,11 +160,13 @@ def test_G6_certified_sums(name, sym):
     assert err2 <= (s["E_row"] + s["E_col"]) * (1 + 1e-6) + 1e-12
 
 
-@pytest.mark.parametrize("name", ["P2", "P4"])
-def test_truncate_workspace_path(name):
-    """The global-workspace (persistent grid) truncation used when the working set exceeds
-    shared memory gives the same ranks, singular values and matrix as the shared-memory path."""
-    h, g, rc = gpu_run(name, ws=1)
+@pytest.mark.parametrize("name,ws,split", [("P2", 1, 1), ("P4", 1, 1), ("P1", 0, 0), ("P2", 0, 0), ("C1", 0, 0)])
+def test_truncate_paths(name, ws, split):
+    """The other truncation kernels give the same ranks, singular values and matrix: the
+    global-workspace persistent grid (used when the working set exceeds shared memory) and the
+    one-kernel shared-memory truncation (replaced by the split QR / warp-Jacobi / epilogue
+    kernels on leaf levels with #t <= 32)."""
+    h, g, rc = gpu_run(name, ws=ws, split=split)
     for side in ("row", "col"):
         go, oo = getattr(g, side), getattr(rc, side)
         assert go.rank == oo.rank
