@@ -120,6 +120,7 @@ __device__ inline void leafV_out(double2* V, int nt, const double2* ph, const do
 
 // Leaf bases V_tc[i,nu] = sum_q |tau_i| w_q exp(i kappa <x_iq, c>) L_{t,nu}(x_iq)
 // (modified Lagrange polynomials P:270-275).  One CTA per leaf basis pair.
+template <int MM>  // Chebyshev order m (0: runtime m, generic output loop); one register budget per m
 __global__ void k_leafV(PlanD P, const int* bps) {
     extern __shared__ double2 sm[];
     const int bp = bps[blockIdx.x];
@@ -146,25 +147,22 @@ __global__ void k_leafV(PlanD P, const int* bps) {
     }
     __syncthreads();
     double2* V = P.V + P.bp_V_off[bp];
-    switch (m) {
-        case 2: leafV_out<2>(V, nt, ph, L); break;
-        case 3: leafV_out<3>(V, nt, ph, L); break;
-        case 4: leafV_out<4>(V, nt, ph, L); break;
-        case 5: leafV_out<5>(V, nt, ph, L); break;
-        default:
-            for (int idx = threadIdx.x; idx < nt * k; idx += blockDim.x) {
-                int i = idx % nt, nu = idx / nt;
-                int jx = nu % m, jy = (nu / m) % m, jz = nu / (m * m);
-                double2 acc = cmk(0.0, 0.0);
-                for (int q = 0; q < 7; ++q) {
-                    const double* Lq = L + ((i * 7 + q) * 3) * m;
-                    double l = Lq[jx] * Lq[m + jy] * Lq[2 * m + jz];
-                    double2 p = ph[i * 7 + q];
-                    acc.x = fma(p.x, l, acc.x);
-                    acc.y = fma(p.y, l, acc.y);
-                }
-                V[(size_t)nu * nt + i] = acc;
+    if constexpr (MM > 0) {
+        leafV_out<MM>(V, nt, ph, L);
+    } else {
+        for (int idx = threadIdx.x; idx < nt * k; idx += blockDim.x) {
+            int i = idx % nt, nu = idx / nt;
+            int jx = nu % m, jy = (nu / m) % m, jz = nu / (m * m);
+            double2 acc = cmk(0.0, 0.0);
+            for (int q = 0; q < 7; ++q) {
+                const double* Lq = L + ((i * 7 + q) * 3) * m;
+                double l = Lq[jx] * Lq[m + jy] * Lq[2 * m + jz];
+                double2 p = ph[i * 7 + q];
+                acc.x = fma(p.x, l, acc.x);
+                acc.y = fma(p.y, l, acc.y);
             }
+            V[(size_t)nu * nt + i] = acc;
+        }
     }
 }
 
@@ -236,7 +234,13 @@ void launch_grid(const PlanD& P, cudaStream_t s) { k_grid<<<(P.nclusters + 127) 
 void launch_leafV(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStream_t s) {
     if (!nbps) return;
     size_t sm = (size_t)maxrows * 7 * sizeof(double2) + (size_t)maxrows * 7 * 3 * P.m * sizeof(double);
-    k_leafV<<<nbps, 128, sm, s>>>(P, bps);
+    switch (P.m) {
+        case 2: k_leafV<2><<<nbps, 128, sm, s>>>(P, bps); break;
+        case 3: k_leafV<3><<<nbps, 128, sm, s>>>(P, bps); break;
+        case 4: k_leafV<4><<<nbps, 128, sm, s>>>(P, bps); break;
+        case 5: k_leafV<5><<<nbps, 128, sm, s>>>(P, bps); break;
+        default: k_leafV<0><<<nbps, 128, sm, s>>>(P, bps); break;
+    }
 }
 void launch_E(const PlanD& P, const int* bps, int nbps, cudaStream_t s) {
     if (!nbps) return;
@@ -1247,7 +1251,8 @@ cudaError_t configure_kernels() {
     int dev = 0, optin = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    const void* ks[] = {(const void*)k_leafV, (const void*)k_basis<true, 4>, (const void*)k_basis<true, 2>,
+    const void* ks[] = {(const void*)k_leafV<0>, (const void*)k_leafV<2>, (const void*)k_leafV<3>, (const void*)k_leafV<4>,
+                        (const void*)k_leafV<5>, (const void*)k_basis<true, 4>, (const void*)k_basis<true, 2>,
                         (const void*)k_block_weights, (const void*)k_total_weights<true, 4>, (const void*)k_total_weights<true, 2>, (const void*)k_truncate<true>, (const void*)k_truncate<false>, (const void*)k_trunc_qr,
                         (const void*)k_project};
     for (const void* f : ks) {
