@@ -76,7 +76,14 @@ struct DevBuf {
 
 struct PassH {
     std::vector<int> bp, child0, child1, Z_rows, blk_ptr, blk, par_ptr, par, par_child, rowsb, kb;
-    std::vector<int64_t> Z_off, C_off, Q_off, sig_off;
+    std::vector<int64_t> Z_off, C_off, Q_off, sig_off;  // active offsets (column pass: aliases, see below)
+    // column pass of an adjoint-symmetric structure: C', Q', sigma' of an own pair are read as the
+    // conjugate of the row results at (s,-c) in the row pools (no copies); imported C' of the
+    // partition sit after the row C pool.  *_own: compact offsets of a separate column storage
+    // (used when two passes are requested).
+    bool alias = false;
+    std::vector<int64_t> C_off_own, Q_off_own, sig_off_own, C_off_alias, Q_off_alias, sig_off_alias;
+    int64_t C_imp_total = 0, C_extra = 0;
     std::vector<int> lev_ptr;  // pairs of level l: [lev_ptr[l], lev_ptr[l+1])
     std::vector<int> lc, lc_ptr;  // leaf-cluster groups (matvec output)
     std::vector<int> bp2p;        // basis pair id -> pair id of this pass (-1 if absent)
@@ -653,6 +660,34 @@ void build_tables(Shard* C) {
     }
     tick(3);
     check_symmetry(C);
+    if (C->sym_ok) {
+        PassH &R = C->row, &X = C->col;
+        const int np = (int)X.bp.size();
+        X.C_off_own = X.C_off;
+        X.Q_off_own = X.Q_off;
+        X.sig_off_own = X.sig_off;
+        X.C_off_alias.assign(np, -1);
+        X.Q_off_alias.assign(np, -1);
+        X.sig_off_alias.assign(np, -1);
+        X.C_imp_total = 0;
+        for (int p = 0; p < np; ++p) {
+            if (X.C_off[p] < 0) continue;
+            if (X.Q_off[p] >= 0) {  // own pair: the row pair at -c
+                const int q = C->col2row[p];
+                X.C_off_alias[p] = R.C_off[q];
+                X.Q_off_alias[p] = R.Q_off[q];
+                X.sig_off_alias[p] = R.sig_off[q];
+            } else {  // imported C' (partition), after the row C pool
+                X.C_off_alias[p] = R.C_total + X.C_imp_total;
+                X.C_imp_total += (int64_t)X.kb[p] * k;
+            }
+        }
+        R.C_extra = X.C_imp_total;
+        X.alias = true;
+        X.C_off = X.C_off_alias;
+        X.Q_off = X.Q_off_alias;
+        X.sig_off = X.sig_off_alias;
+    }
     tick(4);
     if (W > 1 && !C->sym_ok)
         throw NotImpl("sharding needs the adjoint-symmetric structure (" + C->sym_why + ")");
@@ -712,9 +747,11 @@ void upload_pass(Shard* C, PassH& X, PassD& D, bool alloc_Z) {
     X.d_disc.alloc(np);
     X.d_sweeps.alloc(np);
     if (alloc_Z) X.d_Z.alloc(X.Z_total);
-    X.d_C.alloc(X.C_total);
-    X.d_Q.alloc(X.Q_total);
-    X.d_sigma.alloc(X.sig_total);
+    if (!X.alias) {  // (aliased column factors live in the row pools)
+        X.d_C.alloc(X.C_total + X.C_extra);
+        X.d_Q.alloc(X.Q_total);
+        X.d_sigma.alloc(X.sig_total);
+    }
     D.npairs = (int)np;
     D.bp = X.d_bp.p;
     D.child0 = X.d_child0.p;
@@ -746,7 +783,11 @@ size_t plan_bytes(const Shard* C) {
     b += (size_t)C->VR_total * 16 + (size_t)C->E_total * 16 + (size_t)(C->b_hi - C->b_lo) * C->k * C->k * 16;
     b += (size_t)C->St_total * 16;
     for (const PassH* X : {&C->row, &C->col})
-        b += (size_t)((X == &C->col && C->sym_ok ? 0 : X->Z_total) + X->C_total + X->Q_total) * 16 + (size_t)X->sig_total * 8;
+        if (X->alias)
+            b += 0;  // column factors read from the row pools (imports counted in row C_extra)
+        else
+            b += (size_t)((X == &C->col && C->sym_ok ? 0 : X->Z_total) + X->C_total + X->C_extra + X->Q_total) * 16 +
+                 (size_t)X->sig_total * 8;
     b += (size_t)C->n * 7 * 32 + (size_t)C->nclusters * sizeof(GridD);
     return b;
 }
@@ -864,6 +905,12 @@ void upload_all(Shard* C, const double* xyz, int64_t nv, const int64_t* tri) {
     P.normG2 = C->d_normG2.p;
     upload_pass(C, C->row, P.row, true);
     upload_pass(C, C->col, P.col, !C->sym_ok);  // column Zhat only when two passes can run
+    if (C->col.alias) {
+        P.col.C = P.row.C;
+        P.col.Q = P.row.Q;
+        P.col.sigma = P.row.sigma;
+    }
+    P.col_conj = C->col.alias ? 1 : 0;
     if (C->sym_ok) C->d_col2row.upload(C->col2row, s);
 }
 
@@ -902,6 +949,42 @@ void run_setup(Shard* C) {
 inline double qr_flops(double M, double N) {
     double K = std::min(M, N);
     return 8.0 * (M * N * K - (M + N) * K * K / 2.0 + K * K * K / 3.0);
+}
+
+// Column factors aliased to the conjugate row factors (adjoint symmetry) or in their own storage
+// (two passes requested on a symmetric structure; one shard).
+void set_col_alias(Shard* C, bool alias) {
+    PassH& X = C->col;
+    PlanD& P = C->P;
+    cudaStream_t s = C->stream;
+    CK(cudaStreamSynchronize(s));
+    if (alias) {
+        X.C_off = X.C_off_alias;
+        X.Q_off = X.Q_off_alias;
+        X.sig_off = X.sig_off_alias;
+        P.col.C = P.row.C;
+        P.col.Q = P.row.Q;
+        P.col.sigma = P.row.sigma;
+    } else {
+        if (C->world > 1) throw NotImpl("sharded recompression needs adjoint_symmetry = 1");
+        X.C_off = X.C_off_own;
+        X.Q_off = X.Q_off_own;
+        X.sig_off = X.sig_off_own;
+        if (!X.d_C.p && X.C_total) X.d_C.alloc(X.C_total);
+        if (!X.d_Q.p && X.Q_total) X.d_Q.alloc(X.Q_total);
+        if (!X.d_sigma.p && X.sig_total) X.d_sigma.alloc(X.sig_total);
+        P.col.C = X.d_C.p;
+        P.col.Q = X.d_Q.p;
+        P.col.sigma = X.d_sigma.p;
+    }
+    X.d_C_off.upload(X.C_off, s);
+    X.d_Q_off.upload(X.Q_off, s);
+    X.d_sig_off.upload(X.sig_off, s);
+    P.col.C_off = X.d_C_off.p;
+    P.col.Q_off = X.d_Q_off.p;
+    P.col.sig_off = X.d_sig_off.p;
+    P.col_conj = alias ? 1 : 0;
+    X.alias = alias;
 }
 
 // Phase b: basis weights of this shard's basis pairs, bottom-up (Eq. 18).
@@ -952,6 +1035,7 @@ void run_weights_truncate(Shard* C, double eps, int mode) {
         C->col.d_Z.alloc(C->col.Z_total);
         C->P.col.Z = C->col.d_Z.p;
     }
+    if (C->sym_ok && C->col.alias != sym) set_col_alias(C, sym);
     C->sym_used = sym;
     for (int side = 0; side < 2; ++side) {
         PassH& X = side == 0 ? C->row : C->col;
@@ -1204,6 +1288,7 @@ void export_shard(const Shard* C, const char* name, void* buf, int64_t* nbytes) 
         }
         static thread_local std::vector<double2> tmpz;
         ExportItem it{nullptr, 0, false, 1};
+        bool conj_out = false;
         auto pairs_arr = [&](const std::vector<std::vector<Pair>>& P) {
             tmp64.clear();
             for (size_t l = 0; l < P.size(); ++l)
@@ -1262,7 +1347,15 @@ void export_shard(const Shard* C, const char* name, void* buf, int64_t* nbytes) 
                 it = hv(tmpz);
                 sliced = false;  // tmpz holds exactly the requested range
             } else if (base == "Z") it = dv(X->d_Z);
-            else if (base == "C") it = dv(X->d_C);
+            else if (X == &C->col && X->alias && (base == "C" || base == "Q" || base == "sigma")) {
+                // aliased column factors: conjugates of the row storage at (s,-c) (offsets C_off_col, ...)
+                if (base == "sigma") {
+                    it = dv(C->row.d_sigma);
+                } else {
+                    it = dv(base == "C" ? C->row.d_C : C->row.d_Q);
+                    conj_out = true;
+                }
+            } else if (base == "C") it = dv(X->d_C);
             else if (base == "Q") it = dv(X->d_Q);
             else if (base == "sigma") it = dv(X->d_sigma);
             else if (base == "rank") it = dv(X->d_rank);
@@ -1343,6 +1436,10 @@ void export_shard(const Shard* C, const char* name, void* buf, int64_t* nbytes) 
             CK(cudaMemcpy(buf, it.p, it.bytes, cudaMemcpyDeviceToHost));
         } else {
             std::memcpy(buf, it.p, it.bytes);
+        }
+        if (conj_out) {
+            double2* z = static_cast<double2*>(buf);
+            for (size_t i = 0; i < it.bytes / sizeof(double2); ++i) z[i].y = -z[i].y;
         }
         *nbytes = (int64_t)it.bytes;
         (void)tmpd;
@@ -1491,7 +1588,7 @@ void upload_seg(dh2_ctx::Seg& g, const std::vector<int64_t>& so, const std::vect
     g.n = (int)so.size();
 }
 
-double2* pool2(Shard* S, XKind kind) { return kind == X_R ? S->d_VR.p : kind == X_C ? S->col.d_C.p : S->d_xh.p; }
+double2* pool2(Shard* S, XKind kind) { return kind == X_R ? S->d_VR.p : kind == X_C ? S->P.col.C : S->d_xh.p; }
 
 // one exchange of `kind` among all shards (virtual) or with all peers (NCCL)
 void exchange(dh2_ctx* X, XKind kind) {

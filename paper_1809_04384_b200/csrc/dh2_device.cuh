@@ -968,7 +968,7 @@ __device__ inline void chunk_gemm_S_dmma(const double2* X, int rx, int i0, int n
 // j < nbm, mu < k (A: na x k, ld lda; Bm: nbm x k, ld ldbm; both column-major, global or shared).
 // Tiles of 8 x 8 per warp task, k padded to a multiple of 4 with zero fragments.  STORE: write
 // C (ld ldo); otherwise return this thread's share of ||C||_F^2 (padded entries are zero).
-template <bool STORE>
+template <bool STORE, bool BCONJ = false>  // BCONJ: Bm is stored conjugated (C = A Bm^T of the stored data)
 __device__ inline double dmma_abh(const double2* A, int lda, int na, const double2* Bm, int ldbm, int nbm, int k,
                                   double2* out, int ldo) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -987,13 +987,14 @@ __device__ inline double dmma_abh(const double2* A, int lda, int na, const doubl
         for (; mu + 4 <= k; mu += 4) {
             const int mm = mu + ac;
             const double2 a = rok ? ap[(size_t)mm * lda] : cmk(0.0, 0.0);
-            const double2 b = cok ? cconj(bp[(size_t)mm * ldbm]) : cmk(0.0, 0.0);
+            const double2 b = cok ? (BCONJ ? bp[(size_t)mm * ldbm] : cconj(bp[(size_t)mm * ldbm])) : cmk(0.0, 0.0);
             ztile_mma(t, a, b);
         }
         if (mu < k) {
             const int mm = mu + ac;
             const double2 a = (rok && mm < k) ? ap[(size_t)mm * lda] : cmk(0.0, 0.0);
-            const double2 b = (cok && mm < k) ? cconj(bp[(size_t)mm * ldbm]) : cmk(0.0, 0.0);
+            const double2 b = (cok && mm < k) ? (BCONJ ? bp[(size_t)mm * ldbm] : cconj(bp[(size_t)mm * ldbm]))
+                                              : cmk(0.0, 0.0);
             ztile_mma(t, a, b);
         }
         if constexpr (STORE) {

@@ -1013,28 +1013,16 @@ __global__ void k_mirror_pass(PlanD P, const int* col2row, int p0) {
     const int q = col2row[p];
     const PassD& R = P.row;
     const PassD& X = P.col;
-    const int kk = R.rank[q], ns = R.nsig[q], kb = X.kb[p];
-    if (threadIdx.x == 0) {
-        X.rank[p] = kk;
-        X.nsig[p] = ns;
+    if (threadIdx.x == 0) {  // the factors themselves are read conjugated from the row storage (P.col_conj)
+        X.rank[p] = R.rank[q];
+        X.nsig[p] = R.nsig[q];
         X.disc[p] = R.disc[q];
         X.sweeps[p] = R.sweeps[q];
     }
-    for (int i = threadIdx.x; i < ns; i += blockDim.x) X.sigma[X.sig_off[p] + i] = R.sigma[R.sig_off[q] + i];
-    const double2* Cr = R.C + R.C_off[q];
-    double2* Cc = X.C + X.C_off[p];
-    for (int idx = threadIdx.x; idx < kk * P.k; idx += blockDim.x) {
-        const int a = idx % kk, nu = idx / kk;
-        Cc[a + (size_t)nu * kb] = cconj(Cr[a + (size_t)nu * kb]);
-    }
-    const int ldq = X.child0[p] < 0 ? P.c_size[P.bp_t[X.bp[p]]] : X.rowsb[p];
-    const double2* Qr = R.Q + R.Q_off[q];
-    double2* Qc = X.Q + X.Q_off[p];
-    for (int idx = threadIdx.x; idx < ldq * kk; idx += blockDim.x) Qc[idx] = cconj(Qr[idx]);
 }
 
 void launch_mirror_pass(const PlanD& P, const int* col2row, int p0, int np, cudaStream_t s) {
-    if (np) k_mirror_pass<<<np, 128, 0, s>>>(P, col2row, p0);
+    if (np) k_mirror_pass<<<np, 32, 0, s>>>(P, col2row, p0);
 }
 
 // Projection (Lemma Projections): T_b = C_tc S_b, S~_b = T_b C'_sc^*.  CTA per block,
@@ -1057,7 +1045,10 @@ __global__ void k_project(PlanD P, int b0, int ldt, int chunk, const int* mirror
         if (a0) __syncthreads();
         chunk_gemm_S_dmma<true>(Ct, lt, a0, nb, Sg, false, mb < 0, 1.0, k, T, ldt);
         __syncthreads();
-        dmma_abh<true>(T, ldt, nb, Cs, ls, ks, k, St + a0, lt);
+        if (P.col_conj)  // C'_sc stored as the row C at (s,-c): C' = conj(stored)
+            dmma_abh<true, true>(T, ldt, nb, Cs, ls, ks, k, St + a0, lt);
+        else
+            dmma_abh<true, false>(T, ldt, nb, Cs, ls, ks, k, St + a0, lt);
     }
 }
 
@@ -1085,7 +1076,10 @@ __global__ void k_mv_forward(PlanD P, bool recomp, int p0, const double2* xp, do
             const int nt = P.c_size[t];
             const double2* x = xp + P.c_begin[t];
             const double2* B = recomp ? (X.Q + X.Q_off[p]) : (P.V + P.bp_V_off[bp]);
-            for (int i = 0; i < nt; ++i) cfma_cj(acc, B[i + (size_t)a * nt], x[i]);
+            if (recomp && P.col_conj)  // Q' stored as the row Q at (s,-c): conj(Q') = stored
+                for (int i = 0; i < nt; ++i) cfma(acc, B[i + (size_t)a * nt], x[i]);
+            else
+                for (int i = 0; i < nt; ++i) cfma_cj(acc, B[i + (size_t)a * nt], x[i]);
         } else {
             const int ch[2] = {X.child0[p], X.child1[p]};
             if (recomp) {
@@ -1094,7 +1088,10 @@ __global__ void k_mv_forward(PlanD P, bool recomp, int p0, const double2* xp, do
                 int off = 0;
                 for (int c = 0; c < 2; ++c) {
                     const int kc = X.rank[ch[c]];
-                    for (int r = 0; r < kc; ++r) cfma_cj(acc, F[off + r + (size_t)a * ldf], xh[(size_t)ch[c] * k + r]);
+                    if (P.col_conj)
+                        for (int r = 0; r < kc; ++r) cfma(acc, F[off + r + (size_t)a * ldf], xh[(size_t)ch[c] * k + r]);
+                    else
+                        for (int r = 0; r < kc; ++r) cfma_cj(acc, F[off + r + (size_t)a * ldf], xh[(size_t)ch[c] * k + r]);
                     off += kc;
                 }
             } else {

@@ -39,6 +39,7 @@ struct PlanD {
     int n, m, k, nclusters;
     int smem_optin;       // opt-in dynamic shared memory per CTA (bytes), minus a static-smem margin
     int num_sms;
+    int col_conj;         // 1: column factors C', Q' are stored as the row factors at -c (read conjugated)
     double kappa;
     // geometry
     const double* xyz;
