@@ -31,6 +31,9 @@ CONFIGS = {
     # the full C4/C5 need the partitioned or memory-lean path
     "C4s": dict(mesh="sphere", q=32, kappa=16.0, m=5, leaf=64, eta1=1.0, eta2=10.0, eps=1e-6),
     "C5s": dict(mesh="cube", q=32, kappa=29.0, m=5, leaf=64, eta1=1.0, eta2=10.0, eps=1e-6),
+    # the largest scale-downs that fit one GPU (155 / 96 GB device plans)
+    "C4q": dict(mesh="sphere", q=64, kappa=32.0, m=5, leaf=64, eta1=1.0, eta2=10.0, eps=1e-6),
+    "C5q": dict(mesh="cube", q=48, kappa=43.0, m=5, leaf=64, eta1=1.0, eta2=10.0, eps=1e-6),
 }
 
 

@@ -1,7 +1,8 @@
 """Configurations too large for the eager oracle, at full size on the GPU: C3 (BASELINE configs[2]:
 sphere n = 32768, kappa = 32, m = 4, eps = 1e-5) and the one-GPU scale-downs of C4 / C5 at their
-order m = 5 (k = 125), leaf 64 and eps = 1e-6 (C4s: sphere n = 8192; C5s: cube n = 12288, flat
-boxes, truncations above the leaves large enough for the global-workspace kernel).  Checked on
+order m = 5 (k = 125), leaf 64, eps = 1e-6 and kappa h ~ 0.9 (C4s: sphere n = 8192; C5s: cube
+n = 12288, flat boxes, truncations above the leaves large enough for the global-workspace kernel;
+C4q: sphere n = 32768, kappa = 32, 155 GB of device data; C5q: cube n = 27648, kappa = 43).  Checked on
 seeded samples of outputs that the oracle computes one by one (oracle/lazy.py: the same §3.2
 formulas evaluated on the dependency cone of each sampled pair), plus properties that hold at
 any size."""
@@ -13,7 +14,7 @@ from synth import get_config, mesh_for
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module", params=["C3", "C4s", "C5s"])
+@pytest.fixture(scope="module", params=["C3", "C4s", "C5s", "C4q", "C5q"])
 def c3(request):
     from paper_1809_04384_b200 import DH2
     from oracle.structure import DH2Structure
