@@ -808,6 +808,19 @@ __device__ __forceinline__ double reduce_scatter16(double (&v)[16], int lane) {
     return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
 }
 
+// v[0..31] per lane -> lane l returns sum over the warp of v[l], through a padded 32 x 33 shared
+// buffer of the warp (fewer instructions than the shuffle reduce-scatter; fixed summation order)
+__device__ __forceinline__ double transpose_sum32(const double (&v)[32], double* buf, int lane) {
+#pragma unroll
+    for (int e = 0; e < 32; ++e) buf[lane * 33 + e] = v[e];
+    __syncwarp();
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) s += buf[r * 33 + lane];
+    __syncwarp();
+    return s;
+}
+
 __global__ void __launch_bounds__(128, 5) k_trunc_qr(PlanD P, PassD X, int p0, int ldv, int ldb, double2* sR, int* sPiv,
                                                     int* sMeta) {
     extern __shared__ double2 smd[];
@@ -835,6 +848,7 @@ __global__ void __launch_bounds__(128, 5) k_trunc_qr(PlanD P, PassD X, int p0, i
 
 __global__ void __launch_bounds__(128, 3) k_jacobi_w32(PassD X, int p0, int np, double2* sR, double* sN, const int* sMeta) {
     __shared__ double4 prm[4][16];
+    __shared__ double tsum[4][32 * 33];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int i = blockIdx.x * 4 + w;
     if (i >= np) return;  // whole warp
@@ -847,11 +861,12 @@ __global__ void __launch_bounds__(128, 3) k_jacobi_w32(PassD X, int p0, int np, 
     for (int r = 0; r < 32; ++r) x[r] = R[r * 32 + lane];
     const double tol = fmax((double)len, 1.0) * 2.220446049250313e-16;
     const double tol2 = tol * tol;
+    double* tbuf = tsum[w];
     auto norms = [&]() {
         double v[32];
 #pragma unroll
         for (int r = 0; r < 32; ++r) v[r] = cabs2(x[r]);
-        return reduce_scatter32(v, lane);
+        return transpose_sum32(v, tbuf, lane);
     };
     double nr = 0.0;
     int sweep = 0;
@@ -865,22 +880,14 @@ __global__ void __launch_bounds__(128, 3) k_jacobi_w32(PassD X, int p0, int np, 
             // reduced separately (16 values each) so that lane 2q / 2q+1 ends with Re / Im of g_q
             double mine;
             {
-                double d[16];
+                double d[32];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
+                for (int q = 0; q < 16; ++q) {
                     const double2 a = x[2 * q], b = x[2 * q + 1];
                     d[2 * q] = fma(a.x, b.x, a.y * b.y);
                     d[2 * q + 1] = fma(a.y, b.x, -(a.x * b.y));
                 }
-                const double lo = reduce_scatter16(d, lane);
-#pragma unroll
-                for (int q = 8; q < 16; ++q) {
-                    const double2 a = x[2 * q], b = x[2 * q + 1];
-                    d[2 * q - 16] = fma(a.x, b.x, a.y * b.y);
-                    d[2 * q - 15] = fma(a.y, b.x, -(a.x * b.y));
-                }
-                const double hi = reduce_scatter16(d, lane);
-                mine = (lane & 16) ? hi : lo;
+                mine = transpose_sum32(d, tbuf, lane);
             }
             const double other = __shfl_xor_sync(FULL, mine, 1);
             const double2 ga = (lane & 1) ? cmk(other, mine) : cmk(mine, other);
