@@ -432,7 +432,7 @@ void launch_basis(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStr
         k_basis<true, 4><<<nbps, 256, qr_chunk_smem(P, true, ldr, ldb, 6, any_qr), s>>>(P, bps, ldr, ldb);
     } else {
         const int ldb = odd_ld(32);
-        k_basis<true, 2><<<nbps, 256, qr_chunk_smem(P, true, ldr, ldb, 6, any_qr), s>>>(P, bps, ldr, ldb);
+        k_basis<true, 2><<<nbps, 512, qr_chunk_smem(P, true, ldr, ldb, 6, any_qr), s>>>(P, bps, ldr, ldb);
     }
 }
 
@@ -581,7 +581,7 @@ void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* m
         k_total_weights<true, 4><<<np, 256, qr_chunk_smem(P, true, ldr, ldb, 3), s>>>(P, X, row, p0, mirror, ldr, ldb);
     } else {
         const int ldb = odd_ld(32);
-        k_total_weights<true, 2><<<np, 256, qr_chunk_smem(P, true, ldr, ldb, 3), s>>>(P, X, row, p0, mirror, ldr, ldb);
+        k_total_weights<true, 2><<<np, 512, qr_chunk_smem(P, true, ldr, ldb, 3), s>>>(P, X, row, p0, mirror, ldr, ldb);
     }
 }
 
@@ -597,8 +597,8 @@ void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* m
 // numerical rank.  On return the rows 0..ncol-1 of B hold R (zero below the pivoted diagonal), piv
 // the pivot order; returns ncol, or -1 if the pair is empty (rank 0 already recorded).
 template <bool LEAF>
-__device__ inline int truncate_prologue(const PlanD& P, const PassD& X, int p, double2* sm, int ldv, int ldb,
-                                        double2*& B, double*& nrm, int*& piv, int*& ord, int& rowsM,
+__device__ inline int truncate_prologue(const PlanD& P, const PassD& X, int p, double2* sm, int ldv, int ldb, bool append,
+                                        double2*& B, int& ldB, double*& nrm, int*& piv, int*& ord, int& rowsM,
                                         const double2*& Vt, int& ldvt, int& s_piv, double2* sh) {
     const int k = P.k, m = P.m;
     const int bp = X.bp[p];
@@ -607,7 +607,13 @@ __device__ inline int truncate_prologue(const PlanD& P, const PassD& X, int p, d
     const double2* Z = X.Z + X.Z_off[p];
     double2* Vs = sm;                                  // non-leaf Vhat (rowsM x k, ld ldv)
     B = Vs + (leaf ? 0 : (size_t)ldv * k);             // M^* (zr x rowsM, ld ldb)
-    double2* Ef = B + (size_t)ldb * ldv;               // 6 m^2 (non-leaf)
+    ldB = ldb;
+    double2* chunk = nullptr;
+    if (leaf && append) {  // tall M^*: its R factor (rowsM x rowsM, ld ldv) from streamed 32-row chunks
+        ldB = ldv;
+        chunk = B + (size_t)ldv * ldv;                 // 32 x rowsM, ld 33
+    }
+    double2* Ef = (leaf && append) ? chunk + (size_t)33 * ldv : B + (size_t)ldb * ldv;  // 6 m^2 (non-leaf)
     nrm = reinterpret_cast<double*>(Ef + (leaf ? 0 : 6 * m * m));  // ldv
     piv = reinterpret_cast<int*>(nrm + ldv);           // ldv
     ord = piv + ldv;                                   // ldv
@@ -641,13 +647,29 @@ __device__ inline int truncate_prologue(const PlanD& P, const PassD& X, int p, d
         }
         return -1;
     }
-    // B = M^* = Zhat Vt^*  (zr x rowsM) on the FP64 tensor cores
-    dmma_abh<true>(Z, zr, zr, Vt, ldvt, rowsM, k, B, ldb);
+    int Mq = zr;  // rows of the matrix the pivoted QR runs on
+    if (leaf && append) {
+        // M^* has more rows than columns: annihilate its row chunks (M^* chunk = Zhat chunk V^* on
+        // the FP64 tensor cores) into the triangle R0 (structured Householder); the pivoted QR of R0
+        // has the pivots, the R factor and the trailing norms of the pivoted QR of M^* (same
+        // column norms), in rowsM instead of zr rows of shared memory
+        for (int idx = threadIdx.x; idx < ldv * rowsM; idx += blockDim.x) B[idx] = cmk(0.0, 0.0);
+        for (int r0 = 0; r0 < zr; r0 += 32) {
+            const int nb = min(32, zr - r0);
+            __syncthreads();
+            dmma_abh<true>(Z + r0, zr, nb, Vt, ldvt, rowsM, k, chunk, 33);
+            cta_qr_append<false, 2>(B, ldv, chunk, 33, nb, rowsM);
+        }
+        Mq = min(zr, rowsM);
+    } else {
+        // B = M^* = Zhat Vt^*  (zr x rowsM) on the FP64 tensor cores
+        dmma_abh<true>(Z, zr, zr, Vt, ldvt, rowsM, k, B, ldb);
+    }
     // pivoted QR, stopped once the trailing block has ||R22||_F <= 1e-13 max_j ||M^*(:, j)|| <=
     // 1e-13 sigma_1: every singular value dropped with it is below the parity tolerance
     // 1e-12 sigma_1 (DESIGN §6 G3), and its share of any tail sum is < 1e-26 sigma_1^2
-    const int ncol = qrcp_auto(B, ldb, zr, rowsM, piv, nrm, sh, &s_piv, 1e-26);
-    zero_lower(B, ldb, ncol, rowsM);  // drop the Householder vectors below the diagonal of R
+    const int ncol = qrcp_auto(B, ldB, Mq, rowsM, piv, nrm, sh, &s_piv, 1e-26);
+    zero_lower(B, ldB, ncol, rowsM);  // drop the Householder vectors below the diagonal of R
     __syncthreads();
     return ncol;
 }
@@ -728,37 +750,38 @@ __device__ inline void truncate_epilogue(const PassD& X, int p, int k, const dou
 // working set in a private global (L2-resident) workspace slab.
 
 template <bool LEAF>
-__device__ inline void truncate_pair(const PlanD& P, const PassD& X, int p, double2* sm, int ldv, int ldb, double eps,
-                                     int mode, int& flag, int& s_piv, int& s_rank, double2* sh) {
+__device__ inline void truncate_pair(const PlanD& P, const PassD& X, int p, double2* sm, int ldv, int ldb, bool append,
+                                     double eps, int mode, int& flag, int& s_piv, int& s_rank, double2* sh) {
     double2* B;
     double* nrm;
     int *piv, *ord;
-    int rowsM, ldvt;
+    int rowsM, ldvt, ldB;
     const double2* Vt;
-    const int ncol = truncate_prologue<LEAF>(P, X, p, sm, ldv, ldb, B, nrm, piv, ord, rowsM, Vt, ldvt, s_piv, sh);
+    const int ncol = truncate_prologue<LEAF>(P, X, p, sm, ldv, ldb, append, B, ldB, nrm, piv, ord, rowsM, Vt, ldvt, s_piv, sh);
     if (ncol < 0) return;
-    const int nsw = jacobi_rows_auto(B, ldb, ncol, rowsM, nrm, &flag);
+    const int nsw = jacobi_rows_auto(B, ldB, ncol, rowsM, nrm, &flag);
     if (threadIdx.x == 0) X.sweeps[p] = nsw;
-    truncate_epilogue(X, p, P.k, B, ldb, ncol, rowsM, piv, nrm, ord, Vt, ldvt, LEAF ? rowsM : X.rowsb[p], eps, mode, s_rank);
+    truncate_epilogue(X, p, P.k, B, ldB, ncol, rowsM, piv, nrm, ord, Vt, ldvt, LEAF ? rowsM : X.rowsb[p], eps, mode, s_rank);
 }
 
 template <bool LEAF>
 __global__ void __launch_bounds__(128, LEAF ? 5 : 4)
-    k_truncate(PlanD P, PassD X, int p0, int ldv, int ldb, double eps, int mode) {
+    k_truncate(PlanD P, PassD X, int p0, int ldv, int ldb, bool append, double eps, int mode) {
     extern __shared__ double2 smd[];
     __shared__ int flag, s_piv, s_rank;
     __shared__ double2 sh[2];
-    truncate_pair<LEAF>(P, X, p0 + blockIdx.x, smd, ldv, ldb, eps, mode, flag, s_piv, s_rank, sh);
+    truncate_pair<LEAF>(P, X, p0 + blockIdx.x, smd, ldv, ldb, append, eps, mode, flag, s_piv, s_rank, sh);
 }
 
 template <bool LEAF>
 __global__ void __launch_bounds__(128, 4)
-    k_truncate_ws(PlanD P, PassD X, int p0, int np, int ldv, int ldb, double eps, int mode, double2* ws, size_t ws_stride) {
+    k_truncate_ws(PlanD P, PassD X, int p0, int np, int ldv, int ldb, bool append, double eps, int mode, double2* ws,
+                  size_t ws_stride) {
     __shared__ int flag, s_piv, s_rank;
     __shared__ double2 sh[2];
     double2* base = ws + (size_t)blockIdx.x * ws_stride;
     for (int i = blockIdx.x; i < np; i += gridDim.x) {
-        truncate_pair<LEAF>(P, X, p0 + i, base, ldv, ldb, eps, mode, flag, s_piv, s_rank, sh);
+        truncate_pair<LEAF>(P, X, p0 + i, base, ldv, ldb, append, eps, mode, flag, s_piv, s_rank, sh);
         __syncthreads();
     }
 }
@@ -821,8 +844,8 @@ __device__ __forceinline__ double transpose_sum32(const double (&v)[32], double*
     return s;
 }
 
-__global__ void __launch_bounds__(128, 5) k_trunc_qr(PlanD P, PassD X, int p0, int ldv, int ldb, double2* sR, int* sPiv,
-                                                    int* sMeta) {
+__global__ void __launch_bounds__(128, 5) k_trunc_qr(PlanD P, PassD X, int p0, int ldv, int ldb, bool append, double2* sR,
+                                                    int* sPiv, int* sMeta) {
     extern __shared__ double2 smd[];
     __shared__ int s_piv;
     __shared__ double2 sh[2];
@@ -830,9 +853,9 @@ __global__ void __launch_bounds__(128, 5) k_trunc_qr(PlanD P, PassD X, int p0, i
     double2* B;
     double* nrm;
     int *piv, *ord;
-    int rowsM, ldvt;
+    int rowsM, ldvt, ldB;
     const double2* Vt;
-    const int ncol = truncate_prologue<true>(P, X, p, smd, ldv, ldb, B, nrm, piv, ord, rowsM, Vt, ldvt, s_piv, sh);
+    const int ncol = truncate_prologue<true>(P, X, p, smd, ldv, ldb, append, B, ldB, nrm, piv, ord, rowsM, Vt, ldvt, s_piv, sh);
     if (threadIdx.x == 0) {
         sMeta[2 * i] = ncol;  // -1: empty pair, already recorded
         sMeta[2 * i + 1] = rowsM;
@@ -841,7 +864,7 @@ __global__ void __launch_bounds__(128, 5) k_trunc_qr(PlanD P, PassD X, int p0, i
     double2* R = sR + (size_t)i * 1024;
     for (int idx = threadIdx.x; idx < 1024; idx += blockDim.x) {
         const int r = idx >> 5, j = idx & 31;
-        R[idx] = (r < ncol && j < rowsM) ? B[r + (size_t)j * ldb] : cmk(0.0, 0.0);
+        R[idx] = (r < ncol && j < rowsM) ? B[r + (size_t)j * ldB] : cmk(0.0, 0.0);
     }
     for (int j = threadIdx.x; j < 32; j += blockDim.x) sPiv[i * 32 + j] = j < rowsM ? piv[j] : 0;
 }
@@ -971,7 +994,7 @@ void launch_truncate_split(const PlanD& P, bool row, int p0, int np, const Trunc
     double* sN = reinterpret_cast<double*>(sR + (size_t)np * 1024);
     int* sPiv = reinterpret_cast<int*>(sN + (size_t)np * 32);
     int* sMeta = sPiv + (size_t)np * 32;
-    k_trunc_qr<<<np, 128, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, sR, sPiv, sMeta);
+    k_trunc_qr<<<np, 128, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, L.append, sR, sPiv, sMeta);
     k_jacobi_w32<<<(np + 3) / 4, 128, 0, s>>>(X, p0, np, sR, sN, sMeta);
     k_trunc_epi<<<np, 128, 0, s>>>(P, X, p0, sR, sN, sPiv, sMeta, eps, mode);
 }
@@ -980,8 +1003,14 @@ TruncLaunch plan_truncate(const PlanD& P, int np, int maxrowsM, int maxZrows, bo
     TruncLaunch L;
     L.ldv = odd_ld(max(maxrowsM, 1));
     L.ldb = odd_ld(max(maxZrows, 1));
-    const size_t bytes = ((leaf_level ? 0 : (size_t)L.ldv * P.k + 6 * P.m * P.m) + (size_t)L.ldb * L.ldv) * sizeof(double2) +
-                         (size_t)L.ldv * (sizeof(double) + 2 * sizeof(int)) + 16;
+    // tall M^* (zr > #t) at a leaf level: reduce it to its R factor by streamed chunks when that
+    // fits more CTAs per SM (C4 leaves of 64: 130 -> 102 KB, 1 -> 2 CTAs; not for C2 or C5)
+    const size_t extra = (size_t)L.ldv * (sizeof(double) + 2 * sizeof(int)) + 16;
+    const size_t bytes_d = ((leaf_level ? 0 : (size_t)L.ldv * P.k + 6 * P.m * P.m) + (size_t)L.ldb * L.ldv) * sizeof(double2) + extra;
+    const size_t bytes_a = (size_t)(L.ldv + 33) * L.ldv * sizeof(double2) + extra;
+    auto ctas = [&](size_t b) { return b > (size_t)P.smem_optin ? 0 : (int)((size_t)(228 * 1024) / (b + 1024)); };
+    L.append = leaf_level && maxZrows > maxrowsM && maxrowsM > 32 && ctas(bytes_a) > ctas(bytes_d);
+    const size_t bytes = L.append ? bytes_a : bytes_d;
     L.use_ws = force_ws || bytes > (size_t)P.smem_optin;
     if (L.use_ws) {
         L.smem = 0;
@@ -1001,13 +1030,13 @@ void launch_truncate(const PlanD& P, bool row, int p0, int np, const TruncLaunch
     const PassD& X = row ? P.row : P.col;
     if (L.use_ws) {
         if (leaf_level)
-            k_truncate_ws<true><<<L.grid, 128, 0, s>>>(P, X, p0, np, L.ldv, L.ldb, eps, mode, ws, L.ws_stride);
+            k_truncate_ws<true><<<L.grid, 128, 0, s>>>(P, X, p0, np, L.ldv, L.ldb, L.append, eps, mode, ws, L.ws_stride);
         else
-            k_truncate_ws<false><<<L.grid, 128, 0, s>>>(P, X, p0, np, L.ldv, L.ldb, eps, mode, ws, L.ws_stride);
+            k_truncate_ws<false><<<L.grid, 128, 0, s>>>(P, X, p0, np, L.ldv, L.ldb, L.append, eps, mode, ws, L.ws_stride);
     } else if (leaf_level) {
-        k_truncate<true><<<np, 128, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, eps, mode);
+        k_truncate<true><<<np, 128, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, L.append, eps, mode);
     } else {
-        k_truncate<false><<<np, 128, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, eps, mode);
+        k_truncate<false><<<np, 128, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, L.append, eps, mode);
     }
 }
 

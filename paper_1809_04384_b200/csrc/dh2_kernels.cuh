@@ -96,6 +96,7 @@ void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* m
 struct TruncLaunch {
     int ldv = 1, ldb = 1, grid = 0;
     bool use_ws = false;      // working set in a global workspace (persistent grid) instead of smem
+    bool append = false;      // leaf level with zr > #t: M^* reduced to its R factor by streamed chunks
     size_t smem = 0;          // dynamic shared memory per CTA
     size_t ws_stride = 0;     // workspace per CTA (double2 units); total grid * ws_stride
 };
