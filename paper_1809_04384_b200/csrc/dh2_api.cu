@@ -53,6 +53,30 @@ struct NoMem : std::runtime_error {
         if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));       \
     } while (0)
 
+// Device memory comes from the device's stream-ordered pool, which keeps freed memory reserved
+// (release threshold = max): a new context in the same process reuses it instead of paying
+// cudaMalloc/cudaFree of many GB again.  Allocation and release are ordered on the legacy stream
+// and completed before use; every context synchronises its streams before it frees.
+inline void pool_setup(int dev) {
+    static int done_dev = -1;
+    if (done_dev == dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done_dev = dev;
+}
+// bytes the pool holds in reserve (freed by earlier contexts), usable by a new plan
+inline size_t pool_reusable(int dev) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return 0;
+    uint64_t res = 0, used = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    return res > used ? (size_t)(res - used) : 0;
+}
+
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
@@ -60,14 +84,17 @@ struct DevBuf {
     void alloc(size_t cnt) {
         free();
         n = cnt;
-        if (cnt) CK(cudaMalloc(&p, cnt * sizeof(T)));
+        if (cnt) {
+            CK(cudaMallocAsync(reinterpret_cast<void**>(&p), cnt * sizeof(T), 0));
+            CK(cudaStreamSynchronize(0));
+        }
     }
     void upload(const std::vector<T>& v, cudaStream_t s) {
         alloc(v.size());
         if (n) CK(cudaMemcpyAsync(p, v.data(), n * sizeof(T), cudaMemcpyHostToDevice, s));
     }
     void free() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, 0);
         p = nullptr;
         n = 0;
     }
@@ -797,6 +824,7 @@ void upload_all(Shard* C, const double* xyz, int64_t nv, const int64_t* tri) {
     const ClusterTree& T = C->st.ct;
     size_t freeb = 0, totb = 0;
     CK(cudaMemGetInfo(&freeb, &totb));
+    freeb += pool_reusable(C->device);
     size_t need = plan_bytes(C);
     if (need + (size_t)256 * 1024 * 1024 > freeb)
         throw NoMem("device memory plan needs " + std::to_string(need >> 20) + " MiB, free " + std::to_string(freeb >> 20) + " MiB");
@@ -1856,6 +1884,7 @@ int dh2_build_interp(const dh2_mesh* mesh, const dh2_params* params, const dh2_d
             X->comm = comm;
         }
         CK(configure_kernels());
+        pool_setup(X->device);
         int optin = 0, nsm = 0;
         CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, X->device));
         CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, X->device));
