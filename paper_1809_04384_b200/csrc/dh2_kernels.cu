@@ -801,49 +801,6 @@ __host__ __device__ constexpr int jw_slot(int pos) { return pos < 16 ? 2 * pos :
 __host__ __device__ constexpr int jw_next(int pos) { return pos == 0 ? 0 : (pos == 31 ? 1 : pos + 1); }
 __host__ __device__ constexpr int jw_prev(int pos) { return pos == 0 ? 0 : (pos == 1 ? 31 : pos - 1); }
 
-// v[0..31] per lane -> lane l returns sum over the warp of v[l] (recursive halving, 31 shuffles)
-__device__ __forceinline__ double reduce_scatter32(double (&v)[32], int lane) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-        const bool up = (lane & o) != 0;
-#pragma unroll
-        for (int i = 0; i < o; ++i) {
-            const double send = up ? v[i] : v[i + o];
-            const double keep = up ? v[i + o] : v[i];
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-        }
-    }
-    return v[0];
-}
-
-// v[0..15] per lane -> lanes l and l^16 return the sum over the warp of v[l & 15]
-__device__ __forceinline__ double reduce_scatter16(double (&v)[16], int lane) {
-#pragma unroll
-    for (int o = 8; o >= 1; o >>= 1) {
-        const bool up = (lane & o) != 0;
-#pragma unroll
-        for (int i = 0; i < o; ++i) {
-            const double send = up ? v[i] : v[i + o];
-            const double keep = up ? v[i + o] : v[i];
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-        }
-    }
-    return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
-}
-
-// v[0..31] per lane -> lane l returns sum over the warp of v[l], through a padded 32 x 33 shared
-// buffer of the warp (fewer instructions than the shuffle reduce-scatter; fixed summation order)
-__device__ __forceinline__ double transpose_sum32(const double (&v)[32], double* buf, int lane) {
-#pragma unroll
-    for (int e = 0; e < 32; ++e) buf[lane * 33 + e] = v[e];
-    __syncwarp();
-    double s = 0.0;
-#pragma unroll
-    for (int r = 0; r < 32; ++r) s += buf[r * 33 + lane];
-    __syncwarp();
-    return s;
-}
-
 __global__ void __launch_bounds__(128, 5) k_trunc_qr(PlanD P, PassD X, int p0, int ldv, int ldb, bool append, double2* sR,
                                                     int* sPiv, int* sMeta) {
     extern __shared__ double2 smd[];
@@ -886,10 +843,14 @@ __global__ void __launch_bounds__(128, 3) k_jacobi_w32(PassD X, int p0, int np, 
     const double tol2 = tol * tol;
     double* tbuf = tsum[w];
     auto norms = [&]() {
-        double v[32];
 #pragma unroll
-        for (int r = 0; r < 32; ++r) v[r] = cabs2(x[r]);
-        return transpose_sum32(v, tbuf, lane);
+        for (int r = 0; r < 32; ++r) tbuf[lane * 33 + r] = cabs2(x[r]);
+        __syncwarp();
+        double v = 0.0;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) v += tbuf[r * 33 + lane];
+        __syncwarp();
+        return v;
     };
     double nr = 0.0;
     int sweep = 0;
@@ -902,15 +863,18 @@ __global__ void __launch_bounds__(128, 3) k_jacobi_w32(PassD X, int p0, int np, 
             // a conj(b) of the slot pairs (2q, 2q+1), this lane's element; pairs 0-7 and 8-15 are
             // reduced separately (16 values each) so that lane 2q / 2q+1 ends with Re / Im of g_q
             double mine;
-            {
-                double d[32];
+            {  // a conj(b) partials straight into the transpose buffer, then column sums
 #pragma unroll
                 for (int q = 0; q < 16; ++q) {
                     const double2 a = x[2 * q], b = x[2 * q + 1];
-                    d[2 * q] = fma(a.x, b.x, a.y * b.y);
-                    d[2 * q + 1] = fma(a.y, b.x, -(a.x * b.y));
+                    tbuf[lane * 33 + 2 * q] = fma(a.x, b.x, a.y * b.y);
+                    tbuf[lane * 33 + 2 * q + 1] = fma(a.y, b.x, -(a.x * b.y));
                 }
-                mine = transpose_sum32(d, tbuf, lane);
+                __syncwarp();
+                mine = 0.0;
+#pragma unroll
+                for (int r = 0; r < 32; ++r) mine += tbuf[r * 33 + lane];
+                __syncwarp();
             }
             const double other = __shfl_xor_sync(FULL, mine, 1);
             const double2 ga = (lane & 1) ? cmk(other, mine) : cmk(mine, other);
