@@ -1169,28 +1169,42 @@ __global__ void k_mv_backward(PlanD P, bool recomp, int p0, double2* yh) {
 }
 
 // Leaf output: y|_t = sum_{c} B_tc yh_tc over the row pairs of each leaf cluster.
-__global__ void k_mv_leaf_out(PlanD P, bool recomp, const int* lc, const int* lc_ptr, int g0, const double2* yh,
-                              double2* yp) {
+// Leaf output: y|_t = sum_c B_tc yh_tc over the row pairs of each leaf cluster.  CTA per leaf
+// cluster, 256 threads = (row i, pair slice): the pairs are split into blockDim/nt slices summed
+// separately, then added in slice order (fixed order: deterministic).
+__global__ void __launch_bounds__(256) k_mv_leaf_out(PlanD P, bool recomp, const int* lc, const int* lc_ptr, int g0,
+                                                     const double2* yh, double2* yp) {
+    __shared__ double2 part[256];
     const PassD& X = P.row;
     const int g = g0 + blockIdx.x, k = P.k;
-    const int p_first = lc[lc_ptr[g]];
-    const int t = P.bp_t[X.bp[p_first]];
+    const int q0 = lc_ptr[g], q1 = lc_ptr[g + 1];
+    const int t = P.bp_t[X.bp[lc[q0]]];
     const int nt = P.c_size[t];
-    for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+    const int ns = max(1, (int)blockDim.x / max(nt, 1));  // pair slices
+    for (int i0 = 0; i0 < nt; i0 += blockDim.x / ns) {
+        const int i = i0 + threadIdx.x % (blockDim.x / ns), sl = threadIdx.x / (blockDim.x / ns);
         double2 acc = cmk(0.0, 0.0);
-        for (int q = lc_ptr[g]; q < lc_ptr[g + 1]; ++q) {
-            const int p = lc[q];
-            const double2* v = yh + (size_t)p * k;
-            if (recomp) {
-                const double2* Q = X.Q + X.Q_off[p];
-                const int kp = X.rank[p];
-                for (int a = 0; a < kp; ++a) cfma(acc, Q[i + (size_t)a * nt], v[a]);
-            } else {
-                const double2* V = P.V + P.bp_V_off[X.bp[p]];
-                for (int a = 0; a < k; ++a) cfma(acc, V[i + (size_t)a * nt], v[a]);
+        if (i < nt && sl < ns)
+            for (int q = q0 + sl; q < q1; q += ns) {
+                const int p = lc[q];
+                const double2* v = yh + (size_t)p * k;
+                if (recomp) {
+                    const double2* Q = X.Q + X.Q_off[p];
+                    const int kp = X.rank[p];
+                    for (int a = 0; a < kp; ++a) cfma(acc, Q[i + (size_t)a * nt], v[a]);
+                } else {
+                    const double2* V = P.V + P.bp_V_off[X.bp[p]];
+                    for (int a = 0; a < k; ++a) cfma(acc, V[i + (size_t)a * nt], v[a]);
+                }
             }
+        part[threadIdx.x] = acc;
+        __syncthreads();
+        if (threadIdx.x < blockDim.x / ns && i < nt) {
+            double2 sum = cmk(0.0, 0.0);
+            for (int r = 0; r < ns; ++r) sum = cadd(sum, part[r * (blockDim.x / ns) + threadIdx.x]);
+            yp[P.c_begin[t] + i] = sum;
         }
-        yp[P.c_begin[t] + i] = acc;
+        __syncthreads();
     }
 }
 
@@ -1214,7 +1228,7 @@ void launch_mv_backward(const PlanD& P, bool recomp, int p0, int np, double2* yh
 }
 void launch_mv_leaf_out(const PlanD& P, bool recomp, const int* lc, const int* lc_ptr, int g0, int nlc, const double2* yh,
                         double2* yp, cudaStream_t s) {
-    if (nlc) k_mv_leaf_out<<<nlc, 64, 0, s>>>(P, recomp, lc, lc_ptr, g0, yh, yp);
+    if (nlc) k_mv_leaf_out<<<nlc, 256, 0, s>>>(P, recomp, lc, lc_ptr, g0, yh, yp);
 }
 // Exchange packing: dst[doff[i] + j] = src[soff[i] + j] for j < len[i], CTA per segment.
 template <typename T>
