@@ -801,7 +801,7 @@ __host__ __device__ constexpr int jw_slot(int pos) { return pos < 16 ? 2 * pos :
 __host__ __device__ constexpr int jw_next(int pos) { return pos == 0 ? 0 : (pos == 31 ? 1 : pos + 1); }
 __host__ __device__ constexpr int jw_prev(int pos) { return pos == 0 ? 0 : (pos == 1 ? 31 : pos - 1); }
 
-__global__ void __launch_bounds__(128, 5) k_trunc_qr(PlanD P, PassD X, int p0, int ldv, int ldb, bool append, double2* sR,
+__global__ void __launch_bounds__(128, 6) k_trunc_qr(PlanD P, PassD X, int p0, int ldv, int ldb, bool append, double2* sR,
                                                     int* sPiv, int* sMeta) {
     extern __shared__ double2 smd[];
     __shared__ int s_piv;
