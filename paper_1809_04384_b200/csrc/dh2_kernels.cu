@@ -765,7 +765,7 @@ __device__ inline void truncate_pair(const PlanD& P, const PassD& X, int p, doub
 }
 
 template <bool LEAF>
-__global__ void __launch_bounds__(128, LEAF ? 5 : 4)
+__global__ void __launch_bounds__(128, 5)
     k_truncate(PlanD P, PassD X, int p0, int ldv, int ldb, bool append, double eps, int mode) {
     extern __shared__ double2 smd[];
     __shared__ int flag, s_piv, s_rank;
