@@ -1028,7 +1028,7 @@ void launch_mirror_pass(const PlanD& P, const int* col2row, int p0, int np, cuda
 // Projection (Lemma Projections): T_b = C_tc S_b, S~_b = T_b C'_sc^*.  CTA per block,
 // rows of C_tc in chunks of <= `chunk` (T chunk x k in shared memory); both products on the FP64
 // tensor cores, S_b read coalesced through its antipodal mirror block where that is local.
-__global__ void k_project(PlanD P, int b0, int ldt, int chunk, const int* mirror) {
+__global__ void __launch_bounds__(128, 4) k_project(PlanD P, int b0, int ldt, int chunk, const int* mirror) {
     extern __shared__ double2 sm[];
     const int b = b0 + blockIdx.x, k = P.k;
     const int pr = P.blk_prow[b], pc = P.blk_pcol[b];
