@@ -1683,6 +1683,9 @@ void exchange(dh2_ctx* X, XKind kind) {
     dh2_ctx::Seg* in = build(false);
     const bool ints = kind == X_RANK;
     const size_t esz = ints ? sizeof(int) : sizeof(double2);
+    const bool grow = ints ? (X->isend.n < (size_t)out->total || X->irecv.n < (size_t)in->total)
+                           : (X->sendbuf.n < (size_t)out->total || X->recvbuf.n < (size_t)in->total);
+    if (grow) CK(cudaStreamSynchronize(s));  // earlier sends/receives may still use the old buffers
     if (ints) {
         if (X->isend.n < (size_t)out->total) X->isend.alloc(out->total);
         if (X->irecv.n < (size_t)in->total) X->irecv.alloc(in->total);
