@@ -150,6 +150,8 @@ def main():
     ap.add_argument("--sample-frac", type=float, default=0.125)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shards", type=int, default=1, help="virtual shards on one GPU (single process)")
+    ap.add_argument("--option", action="append", default=[], metavar="NAME=VALUE",
+                    help="dh2_set_option before recompress (A/B of kernel variants)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -176,6 +178,13 @@ def main():
             dist.barrier()
 
     def make():
+        h = make_ctx()
+        for o in args.option:
+            k, v = o.split("=")
+            h.set_option(k, int(v))
+        return h
+
+    def make_ctx():
         """collective: one shard per rank (NCCL), or args.shards virtual shards on this GPU"""
         if world > 1:
             obj = [nccl_unique_id() if rank == 0 else None]

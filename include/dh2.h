@@ -165,6 +165,16 @@ int dh2_set_stream(dh2_ctx* ctx, void* cuda_stream);
  *     matrices of (s,-c): Zhat', sigma', k', Q', F', C' follow by conjugation.  Used only if
  *     dh2_build_interp verified that correspondence on the whole structure (stats key
  *     "adjoint_symmetry"); otherwise, or with value 0, both passes run.
+ *   "truncate_workspace" (0 | 1, default 0): force the global-workspace truncation kernel.
+ *   "truncate_split" (0 | 1, default 1): leaf levels with #t <= 32 truncate in three kernels
+ *     (pivoted QR, warp-level one-sided Jacobi, epilogue) instead of one CTA per pair.
+ *   "fuse_leaf_weights" (0 | 1, default 0): on those leaf levels (k <= 64) fold the total
+ *     weights into the truncation's QR kernel: the rows of the stack whose R factor is Zhat_tc
+ *     are multiplied by V_tc^* and reduced directly, Zhat_tc is never formed (stats
+ *     "fused_leaf_levels_row/col"; export "Z" is not defined on those levels).
+ *   "fuse_direct_rows" (0..64, default 64): fused stacks up to this height form M^* directly,
+ *     taller ones are reduced by Householder appends (stats "fused_append_pairs").
+ *   All variants give the same ranks, singular values and matrices up to rounding (tests).
  * Errors: DH2_EINVAL for an unknown name or value. */
 int dh2_set_option(dh2_ctx* ctx, const char* name, int64_t value);
 

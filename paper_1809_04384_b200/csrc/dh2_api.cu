@@ -193,6 +193,10 @@ struct Shard {
     int sym_opt = 1;         // dh2_set_option("adjoint_symmetry")
     int force_ws = 0;        // dh2_set_option("truncate_workspace")
     int split_trunc = 1;     // dh2_set_option("truncate_split"): warp-register Jacobi for leaves <= 32
+    int fuse_leaf = 0;       // dh2_set_option("fuse_leaf_weights"): leaf Zhat folded into the split QR
+    std::vector<int> fused_levels[2];  // levels of the last recompress whose Zhat was fused (row, col)
+    int64_t fused_append = 0;          // fused pairs whose stack (> fuse_direct rows) took the QR-append mode
+    int fuse_direct = 64;              // dh2_set_option("fuse_direct_rows")
     DevBuf<char> d_tscr;     // scratch of the split truncation
     DevBuf<double2> d_ws;    // truncation workspace (persistent grid), grown on demand
     int64_t ws_launches = 0; // truncation launches that used the workspace
@@ -1065,6 +1069,9 @@ void run_weights_truncate(Shard* C, double eps, int mode) {
     }
     if (C->sym_ok && C->col.alias != sym) set_col_alias(C, sym);
     C->sym_used = sym;
+    C->fused_levels[0].clear();
+    C->fused_levels[1].clear();
+    C->fused_append = 0;
     for (int side = 0; side < 2; ++side) {
         PassH& X = side == 0 ? C->row : C->col;
         const bool row = side == 0;
@@ -1082,12 +1089,35 @@ void run_weights_truncate(Shard* C, double eps, int mode) {
                 }
             }
             C->kstat["mirror_col"].bytes += by;
+            C->fused_levels[1] = C->fused_levels[0];  // column Zhat mirrors the row Zhat
             continue;
+        }
+        // leaf levels truncated by the split path with k <= 64 fold their total weights into the
+        // split QR (k_trunc_zqr): Zhat of such a level is never formed
+        auto level_kind = [&](int l, bool& all_leaf, bool& any_leaf) {
+            all_leaf = true;
+            any_leaf = false;
+            for (int p = X.own_lo[l]; p < X.own_hi[l]; ++p) {
+                all_leaf = all_leaf && X.child0[p] < 0;
+                any_leaf = any_leaf || X.child0[p] < 0;
+            }
+        };
+        std::vector<char> fused(L + 1, 0);
+        for (int l = 0; l <= L; ++l) {
+            const int np = X.own_hi[l] - X.own_lo[l];
+            bool all_leaf, any_leaf;
+            level_kind(l, all_leaf, any_leaf);
+            if (!np || !all_leaf || !C->fuse_leaf || !C->split_trunc || k > 64 || X.lev_max_leafrows[l] > 32) continue;
+            const TruncLaunch TL = plan_truncate(P, np, X.lev_max_leafrows[l], X.lev_max_zrows[l], true, C->force_ws != 0);
+            if (TL.use_ws) continue;
+            fused[l] = 1;
+            C->fused_levels[side].push_back(l);
+            for (int p = X.own_lo[l]; p < X.own_hi[l]; ++p) C->fused_append += X.total_rows[p] > C->fuse_direct;
         }
         // total weights, top-down
         for (int l = 0; l <= L; ++l) {
             int p0 = X.own_lo[l], np = X.own_hi[l] - p0;
-            if (!np) continue;
+            if (!np || fused[l]) continue;
             C->timed(std::string(row ? "total_weights_row@" : "total_weights_col@") + std::to_string(l), 1, [&] { launch_total_weights(P, row, p0, np, C->d_blk_mirror.p, s); });
             double fl = 0;
             for (int p = p0; p < p0 + np; ++p) {
@@ -1109,11 +1139,8 @@ void run_weights_truncate(Shard* C, double eps, int mode) {
             for (int p = p0; p < p0 + np; ++p)
                 if (X.child0[p] >= 0) maxrows = std::max(maxrows, X.rank[X.child0[p]] + X.rank[X.child1[p]]);
             int maxz = X.lev_max_zrows[l];
-            bool all_leaf = true, any_leaf = false;
-            for (int p = p0; p < p0 + np; ++p) {
-                all_leaf = all_leaf && X.child0[p] < 0;
-                any_leaf = any_leaf || X.child0[p] < 0;
-            }
+            bool all_leaf, any_leaf;
+            level_kind(l, all_leaf, any_leaf);
             if (any_leaf && !all_leaf)  // median-split trees never mix leaves and inner clusters on a level
                 throw NotImpl("a tree level mixing leaf and non-leaf clusters is not supported by k_truncate");
             const TruncLaunch TL = plan_truncate(P, np, maxrows, maxz, all_leaf, C->force_ws != 0);
@@ -1125,7 +1152,7 @@ void run_weights_truncate(Shard* C, double eps, int mode) {
                     C->d_tscr.alloc(need);
                 }
                 C->timed(std::string(row ? "truncate_row@" : "truncate_col@") + std::to_string(l), 3,
-                         [&] { launch_truncate_split(P, row, p0, np, TL, eps, mode, C->d_tscr.p, s); });
+                         [&] { launch_truncate_split(P, row, p0, np, TL, eps, mode, C->d_tscr.p, fused[l] != 0, C->fuse_direct, C->d_blk_mirror.p, s); });
             }
             if (TL.use_ws) {
                 const size_t need = (size_t)TL.grid * TL.ws_stride;
@@ -1148,7 +1175,18 @@ void run_weights_truncate(Shard* C, double eps, int mode) {
                 double rows = X.child0[p] < 0 ? (double)T.size(C->bp_t[X.bp[p]]) : X.rank[X.child0[p]] + X.rank[X.child1[p]];
                 double zr = X.Z_rows[p];
                 if (X.child0[p] >= 0) fl += 8.0 * 3 * rows * k * m;
-                fl += 8.0 * rows * zr * k;  // M
+                if (fused[l]) {  // stack rows (as total weights), stack V^*, structured QR appends
+                    const double tot = X.total_rows[p];
+                    for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) {
+                        int b = X.blk[ib];
+                        fl += 8.0 * C->bp_R_rows[row ? C->blk_bpcol[b] : C->blk_bprow[b]] * (double)k * k;
+                    }
+                    for (int ip = X.par_ptr[p]; ip < X.par_ptr[p + 1]; ++ip) fl += 8.0 * 3 * X.Z_rows[X.par[ip]] * (double)k * m;
+                    fl += 8.0 * tot * rows * k + 8.0 * tot * rows * rows;
+                    zr = std::min(tot, rows);
+                } else {
+                    fl += 8.0 * rows * zr * k;  // M
+                }
                 double n = std::min(rows, zr);
                 if (rows < zr) fl += qr_flops(zr, rows);
                 fl += 8.0 * 10.0 * rows * n * n;  // SVD, C_svd = 10 model (DESIGN §flop model)
@@ -2010,6 +2048,16 @@ int dh2_set_option(dh2_ctx* X, const char* name, int64_t value) {
         for (auto& S : X->sh) S->force_ws = (int)value;
         return DH2_OK;
     }
+    if (nm == "fuse_leaf_weights") {  // 1: leaf Zhat folded into the split QR (k_trunc_zqr), not stored
+        if (value != 0 && value != 1) return fail(X, DH2_EINVAL, "fuse_leaf_weights must be 0 or 1");
+        for (auto& S : X->sh) S->fuse_leaf = (int)value;
+        return DH2_OK;
+    }
+    if (nm == "fuse_direct_rows") {  // fused leaf QR: stacks up to this height form M^* directly (tests: 0)
+        if (value < 0 || value > 64) return fail(X, DH2_EINVAL, "fuse_direct_rows must be in [0, 64]");
+        for (auto& S : X->sh) S->fuse_direct = (int)value;
+        return DH2_OK;
+    }
     if (nm == "truncate_split") {  // 0: the one-kernel truncation also for leaves <= 32 (tests)
         if (value != 0 && value != 1) return fail(X, DH2_EINVAL, "truncate_split must be 0 or 1");
         for (auto& S : X->sh) S->split_trunc = (int)value;
@@ -2067,7 +2115,13 @@ int dh2_get_stats(const dh2_ctx* C, char* buf, int64_t* len) {
       << ", \"device_bytes\": " << devb << ", \"shard_device_bytes\": [";
     for (size_t i = 0; i < C->sh.size(); ++i) o << (i ? ", " : "") << plan_bytes(C->sh[i].get());
     o << "], \"mirror_missing\": " << S0->mirror_missing
-      << ", \"truncate_ws_launches\": " << ws
+      << ", \"truncate_ws_launches\": " << ws;
+    for (int side = 0; side < 2; ++side) {
+        o << (side ? ", \"fused_leaf_levels_col\": [" : ", \"fused_leaf_levels_row\": [");
+        for (size_t i = 0; i < S0->fused_levels[side].size(); ++i) o << (i ? ", " : "") << S0->fused_levels[side][i];
+        o << "]";
+    }
+    o << ", \"fused_append_pairs\": " << S0->fused_append
       << ", \"adjoint_symmetry\": {\"available\": " << (S0->sym_ok ? "true" : "false") << ", \"enabled\": " << S0->sym_opt
       << ", \"used\": " << (S0->sym_used ? "true" : "false") << ", \"why_not\": \"" << S0->sym_why << "\"}"
       << ", \"kernels\": {";

@@ -826,6 +826,127 @@ __global__ void __launch_bounds__(128, 6) k_trunc_qr(PlanD P, PassD X, int p0, i
     for (int j = threadIdx.x; j < 32; j += blockDim.x) sPiv[i * 32 + j] = j < rowsM ? piv[j] : 0;
 }
 
+// (1') leaf total weights fused into (1) (k <= 64): the rows of the stack whose R factor is Zhat_tc
+// (omega_b R_sc S_b^*, Zhat_{t+c+} E_{tc+}^*, as in k_total_weights) are streamed in
+// chunks of 32, each chunk multiplied by V_tc^* on the FP64 tensor cores and annihilated into a
+// #t x #t triangle R0.  Zhat^* Zhat = Stack^* Stack, so R0^* R0 = V Zhat^* Zhat V^* = M M^*: R0 has
+// the column norms, pivots and R factor of the pivoted QR of M^* = Zhat V^* (the append mode
+// above with Zhat's own QR folded in), and the leaf Zhat is never formed or stored.
+__global__ void __launch_bounds__(256, 3) k_trunc_zqr(PlanD P, PassD X, bool row, int p0, const int* mirror,
+                                                    int direct_max, double2* sR, int* sPiv, int* sMeta) {
+    extern __shared__ double2 smd[];
+    __shared__ int s_piv;
+    __shared__ double2 sh[2];
+    constexpr int CH = 32, LD = 33;
+    const int i = blockIdx.x, p = p0 + i;
+    const int k = P.k, m = P.m;
+    const int bp = X.bp[p];
+    const int rowsM = P.c_size[P.bp_t[bp]];
+    const double2* Vt = P.V + P.bp_V_off[bp];  // rowsM x k, ld rowsM
+    const int zr = X.Z_rows[p];
+    if (rowsM == 0 || zr == 0) {
+        if (threadIdx.x == 0) {
+            X.rank[p] = 0;
+            X.nsig[p] = 0;
+            X.disc[p] = 0.0;
+            X.sweeps[p] = 0;
+            sMeta[2 * i] = -1;
+            sMeta[2 * i + 1] = rowsM;
+        }
+        return;
+    }
+    // stack height; with <= direct_max (<= 64) rows M^* = Stack V^* itself is formed (Zhat = Stack, P = I) and the
+    // pivoted QR runs on it directly, as k_trunc_qr does on Zhat V^*
+    int total = 0;
+    for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) {
+        const int b = X.blk[ib];
+        total += P.bp_R_rows[row ? P.blk_bpcol[b] : P.blk_bprow[b]];
+    }
+    for (int ip = X.par_ptr[p]; ip < X.par_ptr[p + 1]; ++ip) total += X.Z_rows[X.par[ip]];
+    const bool direct = total <= direct_max;
+    double2* B = smd;                          // CH x k stack chunk, ld LD
+    double2* Pm = B + (size_t)LD * k;          // CH x rowsM product chunk, ld LD
+    double2* R0 = Pm + (size_t)LD * 32;        // rowsM x rowsM triangle, ld LD
+    double2* Md = Pm;                          // direct: M^* (total x rowsM, ld 65) over Pm and R0
+    constexpr int LDM = 65;
+    double2* Ef = R0 + (size_t)LD * 32;        // 3 m^2
+    double* nrm = reinterpret_cast<double*>(Ef + 3 * m * m);  // 2 x 32
+    int* piv = reinterpret_cast<int*>(nrm + 64);              // 32
+    if (!direct)
+        for (int idx = threadIdx.x; idx < LD * 32; idx += blockDim.x) R0[idx] = cmk(0.0, 0.0);
+    int fill = 0, done = 0;
+    auto flush = [&]() {
+        __syncthreads();
+        if (direct) {
+            dmma_abh<true>(B, LD, fill, Vt, rowsM, rowsM, k, Md + done, LDM);  // rows of Stack V^*
+        } else {
+            dmma_abh<true>(B, LD, fill, Vt, rowsM, rowsM, k, Pm, LD);  // chunk V^*
+            cta_qr_append<false, 2>(R0, LD, Pm, LD, fill, rowsM);
+        }
+        done += fill;
+        fill = 0;
+    };
+    for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) {
+        const int b = X.blk[ib];
+        const int obp = row ? P.blk_bpcol[b] : P.blk_bprow[b];
+        const int r = P.bp_R_rows[obp];
+        const double2* Ro = P.R + P.bp_R_off[obp];
+        const double w = P.omega[b];
+        const int mb = row ? b : mirror[b];
+        const double2* Sg = P.S + (size_t)(mb >= 0 ? mb : b) * k * k;
+        const bool strided = !row && mb < 0;
+        for (int i0 = 0; i0 < r;) {
+            const int nb = min(CH - fill, r - i0);
+            __syncthreads();
+            chunk_gemm_S_dmma(Ro, r, i0, nb, Sg, row, strided, w, k, B + fill, LD);
+            i0 += nb;
+            fill += nb;
+            if (fill == CH) flush();
+        }
+    }
+    for (int ip = X.par_ptr[p]; ip < X.par_ptr[p + 1]; ++ip) {
+        const int pp = X.par[ip];
+        const int ci = X.par_child[ip];
+        const int r = X.Z_rows[pp];
+        const double2* Zp = X.Z + X.Z_off[pp];
+        const double2* Eg = P.E + P.bp_E_off[X.bp[pp]] + ci * 3 * m * m;
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < 3 * m * m; idx += blockDim.x) Ef[idx] = Eg[idx];
+        for (int i0 = 0; i0 < r;) {
+            const int nb = min(CH - fill, r - i0);
+            double2* dst = B + fill;
+            __syncthreads();
+            for (int idx = threadIdx.x; idx < nb * k; idx += blockDim.x)
+                dst[idx % nb + (size_t)(idx / nb) * LD] = Zp[i0 + idx % nb + (size_t)(idx / nb) * r];
+            __syncthreads();
+            kron_apply(dst, LD, nb, m, Ef, true);  // Zhat_{t+c+} E_{tc+}^*
+            i0 += nb;
+            fill += nb;
+            if (fill == CH) flush();
+        }
+    }
+    if (fill > 0) flush();
+    double2* Rf = direct ? Md : R0;
+    const int ldf = direct ? LDM : LD;
+    const int ncol = qrcp_auto(Rf, ldf, direct ? total : min(total, rowsM), rowsM, piv, nrm, sh, &s_piv, 1e-26);
+    zero_lower(Rf, ldf, ncol, rowsM);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        sMeta[2 * i] = ncol;
+        sMeta[2 * i + 1] = rowsM;
+    }
+    double2* R = sR + (size_t)i * 1024;
+    for (int idx = threadIdx.x; idx < 1024; idx += blockDim.x) {
+        const int r = idx >> 5, j = idx & 31;
+        R[idx] = (r < ncol && j < rowsM) ? Rf[r + (size_t)j * ldf] : cmk(0.0, 0.0);
+    }
+    for (int j = threadIdx.x; j < 32; j += blockDim.x) sPiv[i * 32 + j] = j < rowsM ? piv[j] : 0;
+}
+
+size_t trunc_zqr_smem(const PlanD& P) {
+    return ((size_t)33 * P.k + 2 * 33 * 32 + 3 * P.m * P.m) * sizeof(double2) + 64 * sizeof(double) + 32 * sizeof(int);
+}
+
 __global__ void __launch_bounds__(128, 3) k_jacobi_w32(PassD X, int p0, int np, double2* sR, double* sN, const int* sMeta) {
     __shared__ double4 prm[4][16];
     __shared__ double tsum[4][32 * 33];
@@ -951,14 +1072,17 @@ __global__ void __launch_bounds__(128) k_trunc_epi(PlanD P, PassD X, int p0, con
 size_t trunc_split_scratch_bytes(int np) { return (size_t)np * (1024 * sizeof(double2) + 32 * sizeof(double) + 34 * sizeof(int)); }
 
 void launch_truncate_split(const PlanD& P, bool row, int p0, int np, const TruncLaunch& L, double eps, int mode,
-                           void* scratch, cudaStream_t s) {
+                           void* scratch, bool fused, int fuse_direct, const int* mirror, cudaStream_t s) {
     if (!np) return;
     const PassD& X = row ? P.row : P.col;
     double2* sR = reinterpret_cast<double2*>(scratch);
     double* sN = reinterpret_cast<double*>(sR + (size_t)np * 1024);
     int* sPiv = reinterpret_cast<int*>(sN + (size_t)np * 32);
     int* sMeta = sPiv + (size_t)np * 32;
-    k_trunc_qr<<<np, 128, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, L.append, sR, sPiv, sMeta);
+    if (fused)
+        k_trunc_zqr<<<np, 256, trunc_zqr_smem(P), s>>>(P, X, row, p0, mirror, fuse_direct, sR, sPiv, sMeta);
+    else
+        k_trunc_qr<<<np, 128, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, L.append, sR, sPiv, sMeta);
     k_jacobi_w32<<<(np + 3) / 4, 128, 0, s>>>(X, p0, np, sR, sN, sMeta);
     k_trunc_epi<<<np, 128, 0, s>>>(P, X, p0, sR, sN, sPiv, sMeta, eps, mode);
 }
@@ -1264,7 +1388,7 @@ cudaError_t configure_kernels() {
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     const void* ks[] = {(const void*)k_leafV<0>, (const void*)k_leafV<2>, (const void*)k_leafV<3>, (const void*)k_leafV<4>,
                         (const void*)k_leafV<5>, (const void*)k_basis<true, 4>, (const void*)k_basis<true, 2>,
-                        (const void*)k_block_weights, (const void*)k_total_weights<true, 4>, (const void*)k_total_weights<true, 2>, (const void*)k_truncate<true>, (const void*)k_truncate<false>, (const void*)k_trunc_qr,
+                        (const void*)k_block_weights, (const void*)k_total_weights<true, 4>, (const void*)k_total_weights<true, 2>, (const void*)k_truncate<true>, (const void*)k_truncate<false>, (const void*)k_trunc_qr, (const void*)k_trunc_zqr,
                         (const void*)k_project};
     for (const void* f : ks) {
         if (e != cudaSuccess) break;

@@ -105,8 +105,11 @@ void launch_truncate(const PlanD& P, bool row, int p0, int np, const TruncLaunch
                      int mode, double2* ws, cudaStream_t s);
 // leaf levels with #t <= 32: pivoted QR per CTA, register-resident warp Jacobi, epilogue
 size_t trunc_split_scratch_bytes(int np);
+// fused: leaf total weights folded into the QR kernel (k_trunc_zqr, k <= 64; the level's Zhat is
+// not formed; stacks of <= fuse_direct rows form M^* directly, taller ones are QR-appended;
+// mirror as for launch_total_weights)
 void launch_truncate_split(const PlanD& P, bool row, int p0, int np, const TruncLaunch& L, double eps, int mode,
-                           void* scratch, cudaStream_t s);
+                           void* scratch, bool fused, int fuse_direct, const int* mirror, cudaStream_t s);
 void launch_mirror_pass(const PlanD& P, const int* col2row, int p0, int np, cudaStream_t s);
 void launch_project(const PlanD& P, int b0, int nb, int maxkrow, const int* mirror, cudaStream_t s);
 // matvec (forward / coupling / backward)

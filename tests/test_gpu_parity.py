@@ -24,10 +24,10 @@ _GPU = {}
 CASES = [(n, 1) for n in SMALL + ["C2"]] + [(n, 0) for n in SMALL]
 
 
-def gpu_run(name, eps=None, mode="FROB_BLOCKREL", sym=1, ws=0, split=1):
+def gpu_run(name, eps=None, mode="FROB_BLOCKREL", sym=1, ws=0, split=1, fuse=0, direct=64):
     from paper_1809_04384_b200 import DH2
     from gpu_view import GpuView
-    key = (name, eps, mode, sym, ws, split)
+    key = (name, eps, mode, sym, ws, split, fuse, direct)
     if key not in _GPU:
         cfg = get_config(name)
         xyz, tri = mesh_for(cfg)
@@ -35,9 +35,13 @@ def gpu_run(name, eps=None, mode="FROB_BLOCKREL", sym=1, ws=0, split=1):
         h.set_option("adjoint_symmetry", sym)
         h.set_option("truncate_workspace", ws)
         h.set_option("truncate_split", split)
+        h.set_option("fuse_leaf_weights", fuse)
+        h.set_option("fuse_direct_rows", direct)
         h.recompress(cfg["eps"] if eps is None else eps, mode)
         assert h.stats()["adjoint_symmetry"]["used"] == bool(sym)
         assert (h.stats()["truncate_ws_launches"] > 0) == bool(ws)
+        if not fuse:
+            assert h.stats()["fused_leaf_levels_row"] == []
         rc = oracle_run(name, eps, mode)
         _GPU[key] = (h, GpuView(h, rc.st), rc)
     return _GPU[key]
@@ -69,7 +73,9 @@ def test_G1_setup_entrywise(name):
 
 @pytest.mark.parametrize("name,sym", CASES)
 def test_G2_weight_grams(name, sym):
-    """R^*R per basis pair <= 1e-12 ||R||^2; Zhat^*Zhat per pair <= 1e-11 ||Zhat||^2."""
+    """R^*R per basis pair <= 1e-12 ||R||^2; Zhat^*Zhat per pair <= 1e-11 ||Zhat||^2 (with the
+    leaf total weights formed: fuse_leaf_weights = 0; the fused path never stores leaf Zhat and is
+    pinned by the singular values, ranks and matrices of the other tests)."""
     h, g, rc = gpu_run(name, sym=sym)
     st = rc.st
     for l in st.active_levels:
@@ -160,13 +166,19 @@ def test_G6_certified_sums(name, sym):
     assert err2 <= (s["E_row"] + s["E_col"]) * (1 + 1e-6) + 1e-12
 
 
-@pytest.mark.parametrize("name,ws,split", [("P2", 1, 1), ("P4", 1, 1), ("P1", 0, 0), ("P2", 0, 0), ("C1", 0, 0)])
-def test_truncate_paths(name, ws, split):
+@pytest.mark.parametrize("name,ws,split,fuse", [("P2", 1, 1, 0), ("P4", 1, 1, 0), ("P1", 0, 0, 0), ("P2", 0, 0, 0),
+                                               ("C1", 0, 0, 0), ("P1", 0, 1, 1), ("P2", 0, 1, 1), ("P4", 0, 1, 1),
+                                               ("C1", 0, 1, 1), ("P2", 0, 1, 2), ("C1", 0, 1, 2)])
+def test_truncate_paths(name, ws, split, fuse):
     """The other truncation kernels give the same ranks, singular values and matrix: the
     global-workspace persistent grid (used when the working set exceeds shared memory) and the
     one-kernel shared-memory truncation (replaced by the split QR / warp-Jacobi / epilogue
-    kernels on leaf levels with #t <= 32)."""
-    h, g, rc = gpu_run(name, ws=ws, split=split)
+    kernels on leaf levels with #t <= 32), and the split path with the leaf total weights formed
+    and stored (default) or folded into its QR kernel (fuse_leaf_weights = 1: stacks of <= 64 rows
+    form M^* directly; fuse = 2 here: fuse_direct_rows = 0, every stack takes the QR-append mode)."""
+    h, g, rc = gpu_run(name, ws=ws, split=split, fuse=min(fuse, 1), direct=0 if fuse == 2 else 64)
+    if fuse == 2:
+        assert h.stats()["fused_append_pairs"] > 0
     for side in ("row", "col"):
         go, oo = getattr(g, side), getattr(rc, side)
         assert go.rank == oo.rank

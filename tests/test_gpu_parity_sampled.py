@@ -51,6 +51,7 @@ def test_c3_sampled_pairs(c3, side):
     rank = h.export("rank_" + side, np.int32)
     z_off = h.export("Z_off_" + side, np.int64)
     z_rows = h.export("Z_rows_" + side, np.int32)
+    fused = set(h.stats()["fused_leaf_levels_" + side])
     rng = np.random.default_rng(11 if side == "row" else 12)
     checked = 0
     for l in range(len(lev_ptr) - 1):
@@ -67,6 +68,9 @@ def test_c3_sampled_pairs(c3, side):
             assert np.abs(sg[:n] - so[:n]).max(initial=0.0) <= 1e-12 * s1, (side, l, t, c)
             assert np.all(so[n:] <= 1e-12 * s1)
             assert rank[p] == tr["rank"], (side, l, t, c)
+            if l in fused:  # leaf Zhat folded into the truncation QR, never stored
+                checked += 1
+                continue
             zr = int(z_rows[p])
             Zg = _slice(h, "Z_" + side, z_off[p], zr * k, np.complex128).reshape(k, zr).T
             Zo = lz.Zhat(side, t, c)
