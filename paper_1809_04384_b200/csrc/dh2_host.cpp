@@ -2,6 +2,7 @@
 #include "dh2_host.h"
 
 #include <algorithm>
+#include <iterator>
 #include <chrono>
 #include <cmath>
 #include <numeric>
@@ -66,11 +67,17 @@ void Structure::build_tree(const double* xyz, const int64_t* tri, int64_t nt) {
             int axis = 0;
             for (int a = 1; a < 3; ++a)
                 if (ext[a] > ext[axis]) axis = a;
-            std::sort(T.perm.begin() + b, T.perm.begin() + e, [&](int64_t i, int64_t j) {
+            auto key_less = [&](int64_t i, int64_t j) {
                 double ki = cen[3 * i + axis], kj = cen[3 * j + axis];
                 return ki < kj || (ki == kj && i < j);
-            });
+            };
+            // median split: the key order is total (ties by index), so partitioning at the median
+            // gives the halves of the sorted order; a half that becomes a leaf keeps the sorted
+            // order (the order of a cluster that is split again is irrelevant: it is re-partitioned)
             int64_t half = (cnt + 1) / 2;
+            std::nth_element(T.perm.begin() + b, T.perm.begin() + b + half, T.perm.begin() + e, key_less);
+            if (half <= p.leaf) std::sort(T.perm.begin() + b, T.perm.begin() + b + half, key_less);
+            if (cnt - half <= p.leaf) std::sort(T.perm.begin() + b + half, T.perm.begin() + e, key_less);
             int64_t c0 = (int64_t)T.begin.size();
             int64_t rng[2][2] = {{b, b + half}, {b + half, e}};
             for (auto& r : rng) {
@@ -126,8 +133,45 @@ const std::vector<double>& Structure::D(int l) {
                     }
         }
     }
+    build_tiles(l);
     dirs_ready[l] = 1;
     return out;
+}
+
+// Search index of D_l for nearest(): the m x m squares of each face grouped in T x T tiles
+// (T ~ sqrt m), each with the mean of its directions and the largest distance to one of them.
+void Structure::build_tiles(int l) {
+    if ((int)tiles.size() <= l) tiles.resize(l + 1);
+    DirTiles& X = tiles[l];
+    X = DirTiles{};
+    const int md = mdir[l];
+    if (md < 4) return;  // <= 54 directions: exhaustive search
+    const std::vector<double>& Dl = dirs[l];
+    const int T = std::max(2, (int)std::lround(std::sqrt((double)md)));
+    const int nt = (md + T - 1) / T;
+    X.ptr.push_back(0);
+    for (int f = 0; f < 6; ++f)
+        for (int tu = 0; tu < nt; ++tu)
+            for (int tv = 0; tv < nt; ++tv) {
+                double cen[3] = {0.0, 0.0, 0.0};
+                const size_t first = X.member.size();
+                for (int iu = tu * T; iu < std::min(md, (tu + 1) * T); ++iu)
+                    for (int iv = tv * T; iv < std::min(md, (tv + 1) * T); ++iv) {
+                        const int64_t c = ((int64_t)f * md + iu) * md + iv;  // order of D(l)
+                        X.member.push_back(c);
+                        for (int a = 0; a < 3; ++a) cen[a] += Dl[3 * c + a];
+                    }
+                const double cnt = (double)(X.member.size() - first);
+                double r = 0.0;
+                for (int a = 0; a < 3; ++a) cen[a] /= cnt;
+                for (size_t i = first; i < X.member.size(); ++i) {
+                    const int64_t c = X.member[i];
+                    r = std::max(r, norm3(Dl[3 * c] - cen[0], Dl[3 * c + 1] - cen[1], Dl[3 * c + 2] - cen[2]));
+                }
+                X.centre.insert(X.centre.end(), cen, cen + 3);
+                X.radius.push_back(r);
+                X.ptr.push_back((int64_t)X.member.size());
+            }
 }
 
 // Best approximation of y in D_l with the symmetric tie rule (DESIGN reading Q4):
@@ -139,10 +183,37 @@ int64_t Structure::nearest(int l, const double y[3]) {
     static const double wr[3] = {1.0, std::sqrt(2.0), std::sqrt(3.0)};
     const double wn = norm3(wr[0], wr[1], wr[2]);
     const double w[3] = {wr[0] / wn, wr[1] / wn, wr[2] / wn};
-    double mn = INFINITY;
-    for (int64_t c = 0; c < nd; ++c) {
+    auto dist2 = [&](int64_t c) {
         double d0 = y[0] - Dl[3 * c], d1 = y[1] - Dl[3 * c + 1], d2 = y[2] - Dl[3 * c + 2];
-        double dd = (d0 * d0 + d1 * d1) + d2 * d2;
+        return (d0 * d0 + d1 * d1) + d2 * d2;
+    };
+    // Candidate set: every direction (exhaustive), or, with the tile index, the members of every
+    // tile that can hold a direction within sqrt(U + 1e-12) of y, U = the smallest distance^2 in
+    // the tile whose centre is nearest to y (triangle inequality |y - c| >= |y - centre| - radius,
+    // with a 1e-7 margin for rounding).  That set contains the minimiser and every direction of
+    // the tie window below, so mn, the window and the choice are those of the exhaustive search.
+    std::vector<int64_t> cand;
+    const DirTiles* X = (int)tiles.size() > l && !tiles[l].ptr.empty() ? &tiles[l] : nullptr;
+    if (X) {
+        const int64_t ntl = (int64_t)X->radius.size();
+        std::vector<double> e(ntl);
+        int64_t tb = 0;
+        for (int64_t i = 0; i < ntl; ++i) {
+            e[i] = norm3(y[0] - X->centre[3 * i], y[1] - X->centre[3 * i + 1], y[2] - X->centre[3 * i + 2]);
+            if (e[i] < e[tb]) tb = i;
+        }
+        double U = INFINITY;
+        for (int64_t q = X->ptr[tb]; q < X->ptr[tb + 1]; ++q) U = std::min(U, dist2(X->member[q]));
+        const double rad = std::sqrt(U + 1e-12) + 1e-7;
+        for (int64_t i = 0; i < ntl; ++i)
+            if (e[i] - X->radius[i] <= rad) cand.insert(cand.end(), X->member.begin() + X->ptr[i], X->member.begin() + X->ptr[i + 1]);
+        std::sort(cand.begin(), cand.end());
+    }
+    const int64_t ncand = X ? (int64_t)cand.size() : nd;
+    auto at = [&](int64_t i) { return X ? cand[i] : i; };
+    double mn = INFINITY;
+    for (int64_t i = 0; i < ncand; ++i) {
+        double dd = dist2(at(i));
         if (dd < mn) mn = dd;
     }
     const double thr = mn + 1e-12;
@@ -150,9 +221,9 @@ int64_t Structure::nearest(int l, const double y[3]) {
     const double s = yw >= 0.0 ? 1.0 : -1.0;
     int64_t best = -1;
     double bscore = -INFINITY;
-    for (int64_t c = 0; c < nd; ++c) {
-        double d0 = y[0] - Dl[3 * c], d1 = y[1] - Dl[3 * c + 1], d2 = y[2] - Dl[3 * c + 2];
-        double dd = (d0 * d0 + d1 * d1) + d2 * d2;
+    for (int64_t i = 0; i < ncand; ++i) {
+        const int64_t c = at(i);
+        double dd = dist2(c);
         if (dd <= thr) {
             double sc = s * ((Dl[3 * c] * w[0] + Dl[3 * c + 1] * w[1]) + Dl[3 * c + 2] * w[2]);
             if (best < 0 || sc > bscore) {
@@ -223,6 +294,34 @@ void Structure::build_blocks() {
     std::sort(near.begin(), near.end());
 }
 
+// Sort by (t, c) and drop duplicates: counting sort by cluster (a level's clusters are a
+// contiguous BFS range), then each cluster's few directions.
+static void sort_unique_pairs(std::vector<Pair>& v) {
+    if (v.empty()) return;
+    int64_t t0 = v[0].t, t1 = v[0].t;
+    for (auto& pr : v) {
+        t0 = std::min(t0, pr.t);
+        t1 = std::max(t1, pr.t);
+    }
+    std::vector<int64_t> cnt(t1 - t0 + 2, 0);
+    for (auto& pr : v) ++cnt[pr.t - t0 + 1];
+    for (size_t i = 1; i < cnt.size(); ++i) cnt[i] += cnt[i - 1];
+    std::vector<Pair> out(v.size());
+    {
+        std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+        for (auto& pr : v) out[pos[pr.t - t0]++] = pr;
+    }
+    size_t w = 0;
+    for (size_t g = 0; g + 1 < cnt.size(); ++g) {
+        auto a = out.begin() + cnt[g], b = out.begin() + cnt[g + 1];
+        std::sort(a, b);
+        for (auto it = a; it != b; ++it)
+            if (w == 0 || !(out[w - 1] == *it)) out[w++] = *it;
+    }
+    out.resize(w);
+    v.swap(out);
+}
+
 // Active pairs: (t, c_b) of every admissible block plus the closure (t', sd_t(c)).
 std::vector<std::vector<Pair>> Structure::closure(bool row) {
     ClusterTree& T = ct;
@@ -233,8 +332,7 @@ std::vector<std::vector<Pair>> Structure::closure(bool row) {
     }
     for (int l = 0; l <= T.depth; ++l) {
         auto& v = pairs[l];
-        std::sort(v.begin(), v.end());
-        v.erase(std::unique(v.begin(), v.end()), v.end());
+        sort_unique_pairs(v);
         if (l == T.depth) break;
         // sd_l of every direction used on this level, computed in parallel into the cache
         // (D(l), D(l+1) and the cache are materialised first: nearest() then only reads)
@@ -291,6 +389,7 @@ void Structure::build(const double* xyz, int64_t nv, const int64_t* tri, int64_t
     dirs.assign(L + 1, {});
     dirs_ready.assign(L + 1, 0);
     sd_cache.assign(L + 1, {});
+    tiles.assign(L + 1, {});
     auto t2 = clk::now();
     ms_dirs = ms(t1, t2);
     build_blocks();
@@ -300,11 +399,9 @@ void Structure::build(const double* xyz, int64_t nv, const int64_t* tri, int64_t
     col_pairs = closure(false);
     basis_pairs.assign(L + 1, {});
     for (int l = 0; l <= L; ++l) {
-        auto& v = basis_pairs[l];
-        v = row_pairs[l];
-        v.insert(v.end(), col_pairs[l].begin(), col_pairs[l].end());
-        std::sort(v.begin(), v.end());
-        v.erase(std::unique(v.begin(), v.end()), v.end());
+        auto& v = basis_pairs[l];  // union of the two sorted, duplicate-free lists
+        v.reserve(row_pairs[l].size() + col_pairs[l].size());
+        std::set_union(row_pairs[l].begin(), row_pairs[l].end(), col_pairs[l].begin(), col_pairs[l].end(), std::back_inserter(v));
         if (!v.empty() && first_level < 0) first_level = l;
     }
     // make sure every level that hosts pairs has its direction set materialised

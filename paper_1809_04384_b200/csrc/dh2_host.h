@@ -49,6 +49,13 @@ struct Structure {
     std::vector<std::vector<double>> dirs;  // 3 per direction; generated lazily (empty if unused)
     std::vector<char> dirs_ready;
     std::vector<std::vector<int64_t>> sd_cache;  // per level, -1 = not computed
+    // per level: the directions grouped by tiles of adjacent face squares (search index of
+    // nearest(); built with D(l); empty for small sets, which are searched exhaustively)
+    struct DirTiles {
+        std::vector<double> centre, radius;    // per tile: centre (3), max distance to a member
+        std::vector<int64_t> ptr, member;      // members of tile i: member[ptr[i] .. ptr[i+1])
+    };
+    std::vector<DirTiles> tiles;
     std::vector<Block> blocks;                   // admissible leaves L+, sorted by (t, s)
     std::vector<std::pair<int64_t, int64_t>> near;  // inadmissible leaves L-
     std::vector<std::vector<Pair>> row_pairs, col_pairs, basis_pairs;  // per level, sorted
@@ -63,6 +70,7 @@ struct Structure {
    private:
     void build_tree(const double* xyz, const int64_t* tri, int64_t nt);
     void build_blocks();
+    void build_tiles(int level);
     std::vector<std::vector<Pair>> closure(bool row);
 };
 
