@@ -192,21 +192,27 @@ int64_t Structure::nearest(int l, const double y[3]) {
     // the tile whose centre is nearest to y (triangle inequality |y - c| >= |y - centre| - radius,
     // with a 1e-7 margin for rounding).  That set contains the minimiser and every direction of
     // the tie window below, so mn, the window and the choice are those of the exhaustive search.
-    std::vector<int64_t> cand;
+    thread_local std::vector<int64_t> cand;
+    thread_local std::vector<double> e;
+    cand.clear();
     const DirTiles* X = (int)tiles.size() > l && !tiles[l].ptr.empty() ? &tiles[l] : nullptr;
     if (X) {
         const int64_t ntl = (int64_t)X->radius.size();
-        std::vector<double> e(ntl);
+        e.resize(ntl);  // squared distances to the tile centres
         int64_t tb = 0;
         for (int64_t i = 0; i < ntl; ++i) {
-            e[i] = norm3(y[0] - X->centre[3 * i], y[1] - X->centre[3 * i + 1], y[2] - X->centre[3 * i + 2]);
+            const double d0 = y[0] - X->centre[3 * i], d1 = y[1] - X->centre[3 * i + 1], d2 = y[2] - X->centre[3 * i + 2];
+            e[i] = (d0 * d0 + d1 * d1) + d2 * d2;
             if (e[i] < e[tb]) tb = i;
         }
         double U = INFINITY;
         for (int64_t q = X->ptr[tb]; q < X->ptr[tb + 1]; ++q) U = std::min(U, dist2(X->member[q]));
         const double rad = std::sqrt(U + 1e-12) + 1e-7;
-        for (int64_t i = 0; i < ntl; ++i)
-            if (e[i] - X->radius[i] <= rad) cand.insert(cand.end(), X->member.begin() + X->ptr[i], X->member.begin() + X->ptr[i + 1]);
+        for (int64_t i = 0; i < ntl; ++i) {
+            const double lim = rad + X->radius[i];  // |y - centre| <= rad + radius
+            if (e[i] <= lim * lim * (1.0 + 1e-12))
+                cand.insert(cand.end(), X->member.begin() + X->ptr[i], X->member.begin() + X->ptr[i + 1]);
+        }
         std::sort(cand.begin(), cand.end());
     }
     const int64_t ncand = X ? (int64_t)cand.size() : nd;
