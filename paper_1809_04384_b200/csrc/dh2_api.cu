@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <numeric>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -320,6 +321,7 @@ void check_symmetry(Shard* C) {
         if (q < 0) { C->sym_why = "column pair without a row pair at -c"; return; }
         c2r[p] = q;
     }
+    std::vector<int> a, b, pa, pb;  // scratch, reused across pairs
     for (size_t p = 0; p < X.bp.size(); ++p) {
         const int q = c2r[p];
         if (X.Z_rows[p] != R.Z_rows[q] || X.total_rows[p] != R.total_rows[q] || X.kb[p] != R.kb[q] ||
@@ -328,13 +330,15 @@ void check_symmetry(Shard* C) {
         if (X.child0[p] >= 0 && (c2r[X.child0[p]] != R.child0[q] || c2r[X.child1[p]] != R.child1[q])) {
             C->sym_why = "children differ"; return;
         }
-        std::vector<int> a, b;
+        a.clear();
+        b.clear();
         for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) a.push_back(C->blk_mirror[X.blk[ib]]);
         for (int ib = R.blk_ptr[q]; ib < R.blk_ptr[q + 1]; ++ib) b.push_back(R.blk[ib]);
         std::sort(a.begin(), a.end());
         std::sort(b.begin(), b.end());
         if (a != b) { C->sym_why = "block sets differ"; return; }
-        std::vector<int> pa, pb;
+        pa.clear();
+        pb.clear();
         for (int ip = X.par_ptr[p]; ip < X.par_ptr[p + 1]; ++ip) pa.push_back(c2r[X.par[ip]] * 2 + X.par_child[ip]);
         for (int ip = R.par_ptr[q]; ip < R.par_ptr[q + 1]; ++ip) pb.push_back(R.par[ip] * 2 + R.par_child[ip]);
         std::sort(pa.begin(), pa.end());
@@ -549,39 +553,46 @@ void build_tables(Shard* C) {
             }
         }
         // blocks CSR (blocks sorted by (t,s) per owner: per pair sorted by the other cluster)
-        std::vector<std::vector<int>> bl(np);
+        // (counting sort into the CSR, then each pair's few blocks by the other cluster)
+        std::vector<int>& bpp = side == 0 ? C->blk_prow : C->blk_pcol;
+        bpp.resize(nb);
+        X.blk_ptr.assign(np + 1, 0);
         for (int b = 0; b < nb; ++b) {
-            const Block& B = S.blocks[b];
             int p = X.bp2p[side == 0 ? C->blk_bprow[b] : C->blk_bpcol[b]];
             if (p < 0) throw std::logic_error("block pair missing from the pass");
-            bl[p].push_back(b);
-            if (side == 0)
-                C->blk_prow.push_back(p);
-            else
-                C->blk_pcol.push_back(p);
+            bpp[b] = p;
+            ++X.blk_ptr[p + 1];
         }
-        for (auto& v : bl) std::sort(v.begin(), v.end(), [&](int a, int b) {
-            const Block &A = S.blocks[a], &B = S.blocks[b];
-            return side == 0 ? (A.s < B.s || (A.s == B.s && a < b)) : (A.t < B.t || (A.t == B.t && a < b));
-        });
-        X.blk_ptr.assign(np + 1, 0);
-        for (int p = 0; p < np; ++p) {
-            X.blk_ptr[p + 1] = X.blk_ptr[p] + (int)bl[p].size();
-            X.blk.insert(X.blk.end(), bl[p].begin(), bl[p].end());
+        for (int p = 0; p < np; ++p) X.blk_ptr[p + 1] += X.blk_ptr[p];
+        X.blk.assign(nb, 0);
+        {
+            std::vector<int> pos(X.blk_ptr.begin(), X.blk_ptr.end() - 1);
+            for (int b = 0; b < nb; ++b) X.blk[pos[bpp[b]]++] = b;
         }
-        // parents CSR: (t+, c+) -> children (t_i, sd(c+))
-        std::vector<std::vector<std::pair<int, int>>> pl(np);
-        for (int p = 0; p < np; ++p) {
-            if (X.child0[p] < 0) continue;
-            pl[X.child0[p]].push_back({p, 0});
-            pl[X.child1[p]].push_back({p, 1});
-        }
+        for (int p = 0; p < np; ++p)
+            std::sort(X.blk.begin() + X.blk_ptr[p], X.blk.begin() + X.blk_ptr[p + 1], [&](int a, int b) {
+                const Block &A = S.blocks[a], &B = S.blocks[b];
+                return side == 0 ? (A.s < B.s || (A.s == B.s && a < b)) : (A.t < B.t || (A.t == B.t && a < b));
+            });
+        // parents CSR: (t+, c+) -> children (t_i, sd(c+)), parents in increasing order
         X.par_ptr.assign(np + 1, 0);
         for (int p = 0; p < np; ++p) {
-            X.par_ptr[p + 1] = X.par_ptr[p] + (int)pl[p].size();
-            for (auto& q : pl[p]) {
-                X.par.push_back(q.first);
-                X.par_child.push_back(q.second);
+            if (X.child0[p] < 0) continue;
+            ++X.par_ptr[X.child0[p] + 1];
+            ++X.par_ptr[X.child1[p] + 1];
+        }
+        for (int p = 0; p < np; ++p) X.par_ptr[p + 1] += X.par_ptr[p];
+        X.par.assign(X.par_ptr[np], 0);
+        X.par_child.assign(X.par_ptr[np], 0);
+        {
+            std::vector<int> pos(X.par_ptr.begin(), X.par_ptr.end() - 1);
+            for (int p = 0; p < np; ++p) {
+                if (X.child0[p] < 0) continue;
+                for (int ci = 0; ci < 2; ++ci) {
+                    const int q = pos[ci ? X.child1[p] : X.child0[p]]++;
+                    X.par[q] = p;
+                    X.par_child[q] = ci;
+                }
             }
         }
         // Zhat rows, top-down
@@ -675,18 +686,27 @@ void build_tables(Shard* C) {
     tick(2);
     // antipodal mirror b' = (s, t, -c) of every block: S_{b'} = S_b^T exactly (DESIGN §total weights)
     {
-        std::unordered_map<uint64_t, int> ts;
-        for (int b = 0; b < nb; ++b) ts[key(S.blocks[b].t, S.blocks[b].s)] = b;
+        // block ids ordered by (t, s) (the structure's order unless re-ordered by owner)
+        std::vector<int> ord(nb);
+        std::iota(ord.begin(), ord.end(), 0);
+        auto ts_less = [&](int a, int b) {
+            const Block &A = S.blocks[a], &B = S.blocks[b];
+            return A.t < B.t || (A.t == B.t && A.s < B.s);
+        };
+        if (!std::is_sorted(ord.begin(), ord.end(), ts_less)) std::sort(ord.begin(), ord.end(), ts_less);
         C->blk_mirror.assign(nb, -1);
         for (int b = 0; b < nb; ++b) {
             const Block& B = S.blocks[b];
-            auto it = ts.find(key(B.s, B.t));
-            if (it == ts.end()) { ++C->mirror_missing; continue; }
+            auto it = std::lower_bound(ord.begin(), ord.end(), 0, [&](int a, int) {
+                const Block& A = S.blocks[a];
+                return A.t < B.s || (A.t == B.s && A.s < B.t);
+            });
+            if (it == ord.end() || S.blocks[*it].t != B.s || S.blocks[*it].s != B.t) { ++C->mirror_missing; continue; }
             int l = (int)T.level[B.t];
             const auto& D = S.D(l);
-            int64_t c2 = S.blocks[it->second].c;
+            int64_t c2 = S.blocks[*it].c;
             bool neg = D[3 * c2] == -D[3 * B.c] && D[3 * c2 + 1] == -D[3 * B.c + 1] && D[3 * c2 + 2] == -D[3 * B.c + 2];
-            if (neg) C->blk_mirror[b] = it->second; else ++C->mirror_missing;
+            if (neg) C->blk_mirror[b] = *it; else ++C->mirror_missing;
         }
     }
     tick(3);

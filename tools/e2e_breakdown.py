@@ -20,3 +20,4 @@ for it in range(3):
     t4 = time.perf_counter()
     print("iter %d build %.1f ms (host structure %.1f ms) recompress %.1f ms matvec %.1f ms destroy %.1f ms total %.1f ms"
           % (it, 1e3 * (t1 - t0), s["host_build_ms"], 1e3 * (t2 - t1), 1e3 * (t3 - t2), 1e3 * (t4 - t3), 1e3 * (t4 - t0)))
+    print("   host phases ms", {k: round(v, 2) if isinstance(v, float) else v for k, v in s["host_phases_ms"].items()})
