@@ -17,6 +17,7 @@ time per step).  The timed region is bracketed by barriers + synchronisation.
 --shards P (single process) runs the same partition in the virtual mode on one GPU.
 """
 import argparse
+import threading
 import json
 import os
 import statistics
@@ -43,6 +44,8 @@ def workload_desc(cfg):
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
+    """nvidia-smi in loop mode (every 50 ms) on a reader thread; start() returns once the first
+    sample arrived, begin()/end() bracket the timed region and only samples inside it count."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
@@ -50,23 +53,47 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.lines = []
+        self.t0 = self.t1 = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.monotonic(), line))
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+        deadline = time.monotonic() + 10.0
+        while not self.lines and time.monotonic() < deadline and self.proc.poll() is None:
+            time.sleep(0.01)
+
+    def begin(self):
+        self.t0 = time.monotonic()
+
+    def end(self):
+        self.t1 = time.monotonic()
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
-        out, _ = self.proc.communicate(timeout=10)
+        try:
+            self.proc.wait(timeout=10)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=5)
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
+        for t, line in self.lines:
+            if self.t0 is None or self.t1 is None or not (self.t0 <= t <= self.t1):
+                continue
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 7:
                 continue
@@ -142,11 +169,11 @@ def run_reference(args, cfg, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--sample-frac", type=float, default=0.125)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shards", type=int, default=1, help="virtual shards on one GPU (single process)")
@@ -218,9 +245,10 @@ def main():
     h.set_profiling(True)
     s0 = h.stats()
     sampler = ClockSampler(local)
+    sampler.start()
     barrier()
     torch.cuda.synchronize()
-    sampler.start()
+    sampler.begin()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
@@ -228,6 +256,7 @@ def main():
         step()
     ev1.record(stream)
     torch.cuda.synchronize()
+    sampler.end()
     barrier()
     clocks = sampler.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
@@ -290,6 +319,8 @@ def main():
             t1 = time.perf_counter()
             hb = g.stats()["host_build_ms"]
             g.close()
+            print("e2e iter %d: build %.1f ms (host %.1f) recompress %.1f ms matvec %.1f ms" %
+                  (i, 1e3 * (ta - t0), hb, 1e3 * (tb - ta), 1e3 * (t1 - tb)), file=sys.stderr)
             if i > 0:
                 tt.append(t1 - t0)
                 parts.append((ta - t0, hb * 1e-3, tb - ta, t1 - tb))
