@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <numeric>
 #include <chrono>
 #include <cmath>
@@ -321,29 +322,52 @@ void check_symmetry(Shard* C) {
         if (q < 0) { C->sym_why = "column pair without a row pair at -c"; return; }
         c2r[p] = q;
     }
-    std::vector<int> a, b, pa, pb;  // scratch, reused across pairs
-    for (size_t p = 0; p < X.bp.size(); ++p) {
-        const int q = c2r[p];
-        if (X.Z_rows[p] != R.Z_rows[q] || X.total_rows[p] != R.total_rows[q] || X.kb[p] != R.kb[q] ||
-            X.rowsb[p] != R.rowsb[q]) { C->sym_why = "bounds differ"; return; }
-        if ((X.child0[p] < 0) != (R.child0[q] < 0)) { C->sym_why = "leaf mismatch"; return; }
-        if (X.child0[p] >= 0 && (c2r[X.child0[p]] != R.child0[q] || c2r[X.child1[p]] != R.child1[q])) {
-            C->sym_why = "children differ"; return;
+    // per-pair comparisons in parallel (read-only); the first failing pair in index order names the reason
+    const int64_t npairs = (int64_t)X.bp.size();
+    std::vector<const char*> why(npairs, nullptr);
+    std::atomic<bool> bad{false};
+#pragma omp parallel
+    {
+        std::vector<int> a, b, pa, pb;  // scratch, reused across pairs
+#pragma omp for schedule(dynamic, 512)
+        for (int64_t p = 0; p < npairs; ++p) {
+            if (bad.load(std::memory_order_relaxed)) continue;
+            const int q = c2r[p];
+            const char* w = nullptr;
+            if (X.Z_rows[p] != R.Z_rows[q] || X.total_rows[p] != R.total_rows[q] || X.kb[p] != R.kb[q] ||
+                X.rowsb[p] != R.rowsb[q])
+                w = "bounds differ";
+            else if ((X.child0[p] < 0) != (R.child0[q] < 0))
+                w = "leaf mismatch";
+            else if (X.child0[p] >= 0 && (c2r[X.child0[p]] != R.child0[q] || c2r[X.child1[p]] != R.child1[q]))
+                w = "children differ";
+            if (!w) {
+                a.clear();
+                b.clear();
+                for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) a.push_back(C->blk_mirror[X.blk[ib]]);
+                for (int ib = R.blk_ptr[q]; ib < R.blk_ptr[q + 1]; ++ib) b.push_back(R.blk[ib]);
+                std::sort(a.begin(), a.end());
+                std::sort(b.begin(), b.end());
+                if (a != b) w = "block sets differ";
+            }
+            if (!w) {
+                pa.clear();
+                pb.clear();
+                for (int ip = X.par_ptr[p]; ip < X.par_ptr[p + 1]; ++ip) pa.push_back(c2r[X.par[ip]] * 2 + X.par_child[ip]);
+                for (int ip = R.par_ptr[q]; ip < R.par_ptr[q + 1]; ++ip) pb.push_back(R.par[ip] * 2 + R.par_child[ip]);
+                std::sort(pa.begin(), pa.end());
+                std::sort(pb.begin(), pb.end());
+                if (pa != pb) w = "parents differ";
+            }
+            if (w) {
+                why[p] = w;
+                bad.store(true, std::memory_order_relaxed);
+            }
         }
-        a.clear();
-        b.clear();
-        for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) a.push_back(C->blk_mirror[X.blk[ib]]);
-        for (int ib = R.blk_ptr[q]; ib < R.blk_ptr[q + 1]; ++ib) b.push_back(R.blk[ib]);
-        std::sort(a.begin(), a.end());
-        std::sort(b.begin(), b.end());
-        if (a != b) { C->sym_why = "block sets differ"; return; }
-        pa.clear();
-        pb.clear();
-        for (int ip = X.par_ptr[p]; ip < X.par_ptr[p + 1]; ++ip) pa.push_back(c2r[X.par[ip]] * 2 + X.par_child[ip]);
-        for (int ip = R.par_ptr[q]; ip < R.par_ptr[q + 1]; ++ip) pb.push_back(R.par[ip] * 2 + R.par_child[ip]);
-        std::sort(pa.begin(), pa.end());
-        std::sort(pb.begin(), pb.end());
-        if (pa != pb) { C->sym_why = "parents differ"; return; }
+    }
+    if (bad.load()) {
+        for (int64_t p = 0; p < npairs; ++p)
+            if (why[p]) { C->sym_why = why[p]; return; }
     }
     C->col2row.swap(c2r);
     C->sym_ok = true;
