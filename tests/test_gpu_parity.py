@@ -136,7 +136,7 @@ def test_G4_matvec(name, sym):
         assert np.linalg.norm(yrg - yr) <= 1e-10 * ref
 
 
-@pytest.mark.parametrize("name,sym", [c for c in CASES if c[0] in SMALL])
+@pytest.mark.parametrize("name,sym", [c for c in CASES if c[0] in SMALL] + [("C2", 1)])
 def test_G5_dense_blocks(name, sym):
     """Every block densely expanded from both factor sets:
     sqrt(sum_b ||G~_b^gpu - G~_b^orc||^2) <= 1e-10 ||G_far||_F; GPU bases orthonormal."""
@@ -219,3 +219,17 @@ def test_edge_cases():
     h.recompress(cfg["eps"])
     st = h.storage(1)
     assert st["kb_per_dof_matrix"] < h.storage(0)["kb_per_dof_matrix"]
+
+
+@pytest.mark.parametrize("name,sym", CASES)
+def test_storage_recomp_matches_oracle(name, sym):
+    """dh2_storage for both matrices equals the oracle's count (itself pinned
+    to the coefficients the oracle's arrays hold, tests/test_oracle_recompress.py): the ranks are
+    identical (G3), so every byte count must agree exactly."""
+    h, g, rc = gpu_run(name, sym=sym)
+    for which, key in ((0, "orig"), (1, "recomp")):
+        mine, ref = h.storage(which), ops.storage(rc, key)
+        for f in ("n", "row_basis_bytes", "col_basis_bytes", "coupling_bytes", "nearfield_bytes", "max_rank"):
+            assert mine[f] == ref[f], (which, f, mine[f], ref[f])
+        for f in ("kb_per_dof_basis", "kb_per_dof_matrix", "mean_rank"):
+            assert mine[f] == pytest.approx(ref[f], rel=1e-13), (which, f)

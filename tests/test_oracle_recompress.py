@@ -203,3 +203,40 @@ def test_storage_hand_count():
                                         + rep["nearfield_bytes"]) / st.n / 1024.0
     rr = ops.storage(rc, "recomp")
     assert rr["kb_per_dof_matrix"] < rep["kb_per_dof_matrix"]
+
+
+@pytest.mark.parametrize("name", ["C1", "P1", "P2"])
+def test_storage_recomp_counts_stored_coefficients(name):
+    """storage('recomp') (16 B per complex coefficient, 1 KB = 1024 B) equals
+    the number of coefficients the recompressed matrix actually holds: the leaf matrices Q_tc, the
+    transfer blocks F_{t'c} and the couplings S~_b, counted from the arrays themselves (their
+    shapes), not from the rank formula.  Ranks: the column counts of those arrays."""
+    rc = oracle_run(name)
+    st, ct = rc.st, rc.st.ct
+    rep = ops.storage(rc, "recomp")
+    side_bytes, cols = [], []
+    for res, pairs in ((rc.row, st.row_pairs), (rc.col, st.col_pairs)):
+        tot = 0
+        for l in range(ct.depth + 1):
+            for (t, c) in pairs[l]:
+                if ct.is_leaf(t):
+                    Q = res.Q[(t, c)]
+                    assert Q.shape[0] == ct.size(t)
+                    tot += Q.size
+                    cols.append(Q.shape[1])
+                else:
+                    F = res.F[(t, c)]
+                    assert len(F) == 2 and F[0].shape[1] == F[1].shape[1]
+                    tot += F[0].size + F[1].size
+                    cols.append(F[0].shape[1])
+        side_bytes.append(16.0 * tot)
+    coup = 16.0 * sum(rc.St[b].size for b in range(len(st.blocks)))
+    near = 16.0 * sum(ct.size(int(t)) * ct.size(int(s)) for t, s in st.near)
+    assert rep["row_basis_bytes"] == side_bytes[0]
+    assert rep["col_basis_bytes"] == side_bytes[1]
+    assert rep["coupling_bytes"] == coup
+    assert rep["nearfield_bytes"] == near
+    assert rep["kb_per_dof_matrix"] == pytest.approx((sum(side_bytes) + coup + near) / st.n / 1024.0, rel=1e-15)
+    assert rep["max_rank"] == max(cols)
+    assert rep["mean_rank"] == pytest.approx(np.mean(cols), rel=1e-14)
+    assert 0 < rep["kb_per_dof_matrix"] < ops.storage(rc, "orig")["kb_per_dof_matrix"]
