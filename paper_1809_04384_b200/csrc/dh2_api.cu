@@ -25,6 +25,7 @@
 #include "../../include/dh2.h"
 #include "dh2_host.h"
 #include "dh2_kernels.cuh"
+#include "dh2_shard.h"
 
 namespace dh2 {
 cudaError_t configure_kernels();
@@ -36,249 +37,7 @@ namespace {
 
 std::string g_last_error;
 
-struct CudaError : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
-struct StateError : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
-struct NotImpl : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
-struct NoMem : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
-
-#define CK(x)                                                                                          \
-    do {                                                                                               \
-        cudaError_t e_ = (x);                                                                          \
-        if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));       \
-    } while (0)
-
-// Device memory comes from the device's stream-ordered pool, which keeps freed memory reserved
-// (release threshold = max): a new context in the same process reuses it instead of paying
-// cudaMalloc/cudaFree of many GB again.  Allocation and release are ordered on the legacy stream
-// and completed before use; every context synchronises its streams before it frees.
-inline void pool_setup(int dev) {
-    static int done_dev = -1;
-    if (done_dev == dev) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    done_dev = dev;
-}
-// bytes the pool holds in reserve (freed by earlier contexts), usable by a new plan
-inline size_t pool_reusable(int dev) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return 0;
-    uint64_t res = 0, used = 0;
-    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
-    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
-    return res > used ? (size_t)(res - used) : 0;
-}
-
-template <typename T>
-struct DevBuf {
-    T* p = nullptr;
-    size_t n = 0;
-    void alloc(size_t cnt) {
-        free();
-        n = cnt;
-        if (cnt) {
-            CK(cudaMallocAsync(reinterpret_cast<void**>(&p), cnt * sizeof(T), 0));
-            CK(cudaStreamSynchronize(0));
-        }
-    }
-    void upload(const std::vector<T>& v, cudaStream_t s) {
-        alloc(v.size());
-        if (n) CK(cudaMemcpyAsync(p, v.data(), n * sizeof(T), cudaMemcpyHostToDevice, s));
-    }
-    void free() {
-        if (p) cudaFreeAsync(p, 0);
-        p = nullptr;
-        n = 0;
-    }
-    ~DevBuf() { free(); }
-};
-
-struct PassH {
-    std::vector<int> bp, child0, child1, Z_rows, blk_ptr, blk, par_ptr, par, par_child, rowsb, kb;
-    std::vector<int64_t> Z_off, C_off, Q_off, sig_off;  // active offsets (column pass: aliases, see below)
-    // column pass of an adjoint-symmetric structure: C', Q', sigma' of an own pair are read as the
-    // conjugate of the row results at (s,-c) in the row pools (no copies); imported C' of the
-    // partition sit after the row C pool.  *_own: compact offsets of a separate column storage
-    // (used when two passes are requested).
-    bool alias = false;
-    std::vector<int64_t> C_off_own, Q_off_own, sig_off_own, C_off_alias, Q_off_alias, sig_off_alias;
-    int64_t C_imp_total = 0, C_extra = 0;
-    std::vector<int> lev_ptr;  // pairs of level l: [lev_ptr[l], lev_ptr[l+1])
-    std::vector<int> lc, lc_ptr;  // leaf-cluster groups (matvec output)
-    std::vector<int> bp2p;        // basis pair id -> pair id of this pass (-1 if absent)
-    std::vector<int> own_lo, own_hi;  // per level: pairs of this shard [own_lo[l], own_hi[l])
-    int lc_lo = 0, lc_hi = 0;         // leaf-cluster groups of this shard
-    int64_t Z_total = 0, C_total = 0, Q_total = 0, sig_total = 0;
-    int max_total_rows_level(int l) const { return lev_max_total[l]; }
-    std::vector<int> lev_max_total, lev_max_zrows, lev_max_leafrows;
-    std::vector<int> total_rows;
-    // device
-    DevBuf<int> d_bp, d_child0, d_child1, d_Z_rows, d_blk_ptr, d_blk, d_par_ptr, d_par, d_par_child, d_rowsb, d_kb,
-        d_rank, d_nsig, d_lc, d_lc_ptr, d_sweeps;
-    DevBuf<int64_t> d_Z_off, d_C_off, d_Q_off, d_sig_off;
-    DevBuf<double2> d_Z, d_C, d_Q;
-    DevBuf<double> d_sigma, d_disc;
-    std::vector<int> rank;  // host copy after recompression
-    std::vector<double> disc;
-};
-
-struct KStat {
-    int64_t launches = 0;
-    double ms = 0.0;
-    double flops = 0.0;
-    double bytes = 0.0;
-};
-
 }  // namespace
-
-struct Shard {
-    Structure st;
-    // sharding: shard `rank` of `world` owns the subtree of the rank-th cluster on
-    // the cut level log2(world) -- its row/column pairs, and the blocks (t,s,c) with t in it.
-    // world == 1 owns everything.
-    int rank = 0, world = 1, cut = 0;
-    std::vector<int> owner;          // per cluster, -1 above the cut
-    std::vector<char> bp_own;        // basis pair computed by this shard
-    int b_lo = 0, b_hi = 0;          // own blocks [b_lo, b_hi) (blocks sorted by owner of t)
-    int64_t pos_lo = 0, pos_hi = 0;  // own range of cluster-ordered positions
-    // exchange items per peer, in the same order on both sides (host-computed, replicated)
-    std::vector<std::vector<int>> R_send, R_recv;  // basis pair ids: R_sc computed by QR (non-leaf)
-    std::vector<std::vector<int>> C_send, C_recv;  // column pair ids: C'_sc, k'_sc, xh'_sc
-    int n = 0, k = 0, m = 0, nclusters = 0;
-    int device = 0;
-    cudaStream_t own_stream = nullptr;
-    cudaStream_t stream = nullptr;
-    bool profiling = false;
-    bool recompressed = false;
-    std::string err;
-    double eps = 0.0;
-    int mode = 0;
-    // directions
-    std::vector<int64_t> dir_off;
-    std::vector<double> dirs_flat;
-    // basis pairs
-    // basis pair lookup: the ids of cluster t are [bp_cl[t], bp_cl[t+1]), sorted by direction
-    std::vector<int> bp_cl;
-    int bp_find(int64_t t, int64_t c) const {
-        auto b = bp_c.begin() + bp_cl[t], e = bp_c.begin() + bp_cl[t + 1];
-        auto it = std::lower_bound(b, e, (int)c);
-        return (it != e && *it == c) ? (int)(it - bp_c.begin()) : -1;
-    }
-    int bp_at(int64_t t, int64_t c) const {
-        const int id = bp_find(t, c);
-        if (id < 0) throw std::logic_error("basis pair missing (closure broken)");
-        return id;
-    }
-    std::vector<int> bp_t, bp_dir, bp_sddir, bp_child0, bp_child1, bp_R_rows, bp_level, bp_c;
-    std::vector<int64_t> bp_V_off, bp_R_off, bp_E_off;
-    std::vector<int> bp_lev_ptr;
-    int64_t VR_total = 0, E_total = 0;
-    std::vector<std::vector<int>> leafV_lists, basis_lists, E_lists;  // per level
-    std::vector<int> basis_maxrows;
-    int max_leaf = 0;
-    // blocks
-    std::vector<int> blk_t, blk_s, blk_dir, blk_bprow, blk_bpcol, blk_prow, blk_pcol, blk_mirror;
-    int64_t mirror_missing = 0;
-    // adjoint symmetry: column pair p = (s,c) <-> row pair col2row[p] = (s,-c)
-    std::vector<int> col2row;
-    bool sym_ok = false;     // structure admits it (checked in build_tables)
-    int sym_opt = 1;         // dh2_set_option("adjoint_symmetry")
-    int force_ws = 0;        // dh2_set_option("truncate_workspace")
-    int split_trunc = 1;     // dh2_set_option("truncate_split"): warp-register Jacobi for leaves <= 32
-    int fuse_leaf = 0;       // dh2_set_option("fuse_leaf_weights"): leaf Zhat folded into the split QR
-    std::vector<int> fused_levels[2];  // levels of the last recompress whose Zhat was fused (row, col)
-    int64_t fused_append = 0;          // fused pairs whose stack (> fuse_direct rows) took the QR-append mode
-    int fuse_direct = 64;              // dh2_set_option("fuse_direct_rows")
-    DevBuf<char> d_tscr;     // scratch of the split truncation
-    DevBuf<double2> d_ws;    // truncation workspace (persistent grid), grown on demand
-    int64_t ws_launches = 0; // truncation launches that used the workspace
-    bool sym_used = false;   // the last dh2_recompress derived the column pass from the row pass
-    std::string sym_why;     // why sym_ok is false
-    DevBuf<int> d_col2row;
-    std::vector<int64_t> blk_St_off;
-    int64_t St_total = 0;
-    PassH row, col;
-    // device
-    DevBuf<double> d_xyz, d_c_lo, d_c_hi, d_dirs, d_omega, d_normG2;
-    DevBuf<int64_t> d_tri, d_perm, d_c_begin, d_bp_V_off, d_bp_R_off, d_bp_E_off, d_blk_St_off;
-    DevBuf<int> d_blk_mirror;
-    DevBuf<int> d_c_size, d_bp_t, d_bp_dir, d_bp_sddir, d_bp_child0, d_bp_child1, d_bp_R_rows, d_blk_t, d_blk_s,
-        d_blk_dir, d_blk_bprow, d_blk_bpcol, d_blk_prow, d_blk_pcol;
-    std::vector<std::unique_ptr<DevBuf<int>>> d_lists;
-    std::vector<const int*> d_leafV_list, d_basis_list, d_E_list;
-    DevBuf<double4> d_qp;
-    DevBuf<GridD> d_grid;
-    DevBuf<double2> d_VR, d_E, d_S, d_St, d_x, d_y, d_xp, d_yp, d_xh, d_yh;
-    PlanD P{};
-    // stats
-    std::map<std::string, KStat> kstat;
-    std::vector<std::tuple<std::string, cudaEvent_t, cudaEvent_t>> pending;
-    std::vector<cudaEvent_t> ev_pool;
-    int64_t launches_total = 0;
-    double host_build_ms = 0.0, host_tables_ms = 0.0;
-    double tab_ms[6] = {0, 0, 0, 0, 0, 0};  // build_tables: basis pairs, blocks, passes, mirror, symmetry, exchange
-    double E_row = 0, E_col = 0, far2 = 0;
-
-    ~Shard() {
-        for (auto& e : ev_pool) cudaEventDestroy(e);
-        for (auto& p : pending) {
-            cudaEventDestroy(std::get<1>(p));
-            cudaEventDestroy(std::get<2>(p));
-        }
-        if (own_stream) cudaStreamDestroy(own_stream);
-    }
-
-    cudaEvent_t ev() {
-        cudaEvent_t e;
-        if (!ev_pool.empty()) {
-            e = ev_pool.back();
-            ev_pool.pop_back();
-        } else {
-            CK(cudaEventCreate(&e));
-        }
-        return e;
-    }
-    // run `f` (which launches `nl` kernels) under the timing class `cls`
-    bool debug_sync = std::getenv("DH2_DEBUG_SYNC") != nullptr;
-    template <typename F>
-    void timed(const std::string& cls, int nl, F&& f) {
-        if (profiling) {
-            cudaEvent_t a = ev(), b = ev();
-            CK(cudaEventRecord(a, stream));
-            f();
-            CK(cudaEventRecord(b, stream));
-            pending.emplace_back(cls, a, b);
-        } else {
-            f();
-        }
-        cudaError_t e = cudaGetLastError();
-        if (e == cudaSuccess && debug_sync) e = cudaStreamSynchronize(stream);  // DH2_DEBUG_SYNC=1
-        if (e != cudaSuccess) throw CudaError("kernel class '" + cls + "': " + cudaGetErrorString(e));
-        kstat[cls].launches += nl;
-        launches_total += nl;
-    }
-    void finish() {
-        CK(cudaStreamSynchronize(stream));
-        for (auto& p : pending) {
-            float ms = 0.f;
-            CK(cudaEventElapsedTime(&ms, std::get<1>(p), std::get<2>(p)));
-            kstat[std::get<0>(p)].ms += ms;
-            ev_pool.push_back(std::get<1>(p));
-            ev_pool.push_back(std::get<2>(p));
-        }
-        pending.clear();
-    }
-};
 
 namespace {
 
@@ -473,6 +232,24 @@ void build_tables(Shard* C) {
             C->bp_child1[id] = C->bp_at(T.child1[t], c2);
         }
     }
+    // (t,-c) of every basis pair (antipodal direction sets, DESIGN R2/R4)
+    C->bp_neg.assign(nbp, -1);
+    for (int l = 0; l <= L; ++l) {
+        if (S.basis_pairs[l].empty()) continue;
+        const auto& D = S.D(l);
+        const int nd = (int)D.size() / 3;
+        std::map<std::tuple<double, double, double>, int> idx;
+        for (int c = 0; c < nd; ++c) idx[{D[3 * c] + 0.0, D[3 * c + 1] + 0.0, D[3 * c + 2] + 0.0}] = c;
+        std::vector<int> neg(nd, -1);
+        for (int c = 0; c < nd; ++c) {
+            auto it = idx.find({-D[3 * c] + 0.0, -D[3 * c + 1] + 0.0, -D[3 * c + 2] + 0.0});
+            if (it != idx.end()) neg[c] = it->second;
+        }
+        for (int id = C->bp_lev_ptr[l]; id < C->bp_lev_ptr[l + 1]; ++id) {
+            const int nc = neg[C->bp_c[id]];
+            C->bp_neg[id] = nc < 0 ? -1 : C->bp_find(C->bp_t[id], nc);
+        }
+    }
     // basis-weight rows, bottom-up (Eq. 18): leaf min(#t, k) (R = V if #t <= k), inner min(r1 + r2, k)
     for (int l = L; l >= 0; --l)
         for (int id = C->bp_lev_ptr[l]; id < C->bp_lev_ptr[l + 1]; ++id) {
@@ -494,6 +271,7 @@ void build_tables(Shard* C) {
         C->blk_dir.push_back((int)(C->dir_off[l] + B.c));
         C->blk_bprow.push_back(C->bp_at(B.t, B.c));
         C->blk_bpcol.push_back(C->bp_at(B.s, B.c));
+        C->blk_bpcs.push_back(C->bp_neg[C->blk_bpcol.back()]);
         if (own[B.t] == me) {
             C->b_lo = std::min(C->b_lo, b);
             C->b_hi = std::max(C->b_hi, b + 1);
@@ -505,7 +283,10 @@ void build_tables(Shard* C) {
     // basis pairs needed here: own ones, plus the column pairs of own blocks owned elsewhere
     // (imported: R received if computed by QR, else R = V regenerated from the replicated mesh)
     std::vector<char> need(C->bp_own.begin(), C->bp_own.end());
-    for (int b = C->b_lo; b < C->b_hi; ++b) need[C->blk_bpcol[b]] = 1;
+    for (int b = C->b_lo; b < C->b_hi; ++b) {
+        need[C->blk_bpcol[b]] = 1;
+        if (C->blk_bpcs[b] >= 0) need[C->blk_bpcs[b]] = 1;  // column side under the adjoint symmetry
+    }
     int64_t off = 0;
     for (int id = 0; id < nbp; ++id) {
         if (!need[id]) continue;
@@ -762,6 +543,24 @@ void build_tables(Shard* C) {
         X.C_off = X.C_off_alias;
         X.Q_off = X.Q_off_alias;
         X.sig_off = X.sig_off_alias;
+        // row basis pairs only (own), plus the (s,-c) of own blocks whose column cluster is elsewhere
+        std::vector<char> need_sym(nbp, 0);
+        for (int id = 0; id < nbp; ++id) need_sym[id] = C->bp_own[id] && R.bp2p[id] >= 0;
+        for (int b = C->b_lo; b < C->b_hi; ++b) {
+            if (C->blk_bpcs[b] < 0) throw std::logic_error("column pair without (s,-c) on a symmetric structure");
+            need_sym[C->blk_bpcs[b]] = 1;
+        }
+        C->leafV_lists_sym.assign(L + 1, {});
+        C->basis_lists_sym.assign(L + 1, {});
+        C->E_lists_sym.assign(L + 1, {});
+        for (int l = 0; l <= L; ++l) {
+            for (int id : C->leafV_lists[l])
+                if (need_sym[id]) C->leafV_lists_sym[l].push_back(id);
+            for (int id : C->basis_lists[l])
+                if (R.bp2p[id] >= 0) C->basis_lists_sym[l].push_back(id);
+            for (int id : C->E_lists[l])
+                if (R.bp2p[id] >= 0) C->E_lists_sym[l].push_back(id);
+        }
     }
     tick(4);
     if (W > 1 && !C->sym_ok)
@@ -780,7 +579,7 @@ void build_tables(Shard* C) {
     for (int b = 0; b < nb; ++b) {
         const int rt = own[C->blk_t[b]], rs = own[C->blk_s[b]];
         if (rt == rs || (rt != me && rs != me)) continue;
-        const int bp = C->blk_bpcol[b], p = C->blk_pcol[b];
+        const int bp = C->blk_bpcs[b], p = C->blk_pcol[b];  // R of (s,-c): the column side is its conjugate
         if (rs == me) {
             if (r_by_qr(bp)) C->R_send[rt].push_back(bp);
             C->C_send[rt].push_back(p);
@@ -821,10 +620,12 @@ void upload_pass(Shard* C, PassH& X, PassD& D, bool alloc_Z) {
     X.d_nsig.alloc(np);
     X.d_disc.alloc(np);
     X.d_sweeps.alloc(np);
-    if (alloc_Z) X.d_Z.alloc(X.Z_total);
+    if (alloc_Z && !C->lean.on) X.d_Z.alloc(X.Z_total);
     if (!X.alias) {  // (aliased column factors live in the row pools)
-        X.d_C.alloc(X.C_total + X.C_extra);
-        X.d_Q.alloc(X.Q_total);
+        if (!C->lean.on) {  // lean plan: C, Q in growable pools (lean_alloc)
+            X.d_C.alloc(X.C_total + X.C_extra);
+            X.d_Q.alloc(X.Q_total);
+        }
         X.d_sigma.alloc(X.sig_total);
     }
     D.npairs = (int)np;
@@ -854,6 +655,7 @@ void upload_pass(Shard* C, PassH& X, PassD& D, bool alloc_Z) {
 }
 
 size_t plan_bytes(const Shard* C) {
+    if (C->lean.on) return (size_t)lean_bytes(C);
     size_t b = 0;
     b += (size_t)C->VR_total * 16 + (size_t)C->E_total * 16 + (size_t)(C->b_hi - C->b_lo) * C->k * C->k * 16;
     b += (size_t)C->St_total * 16;
@@ -867,17 +669,42 @@ size_t plan_bytes(const Shard* C) {
     return b;
 }
 
-void upload_all(Shard* C, const double* xyz, int64_t nv, const int64_t* tri) {
-    cudaStream_t s = C->stream;
-    const ClusterTree& T = C->st.ct;
+// The full plan materialises V, S and every factor; when it does not fit (or when forced), the
+// memory-lean chunked plan is used instead (dh2_lean.cu), with the smallest number of chunks whose
+// estimate fits.
+void choose_plan(Shard* C) {
     size_t freeb = 0, totb = 0;
     CK(cudaMemGetInfo(&freeb, &totb));
     freeb += pool_reusable(C->device);
-    size_t need = plan_bytes(C);
-    if (need + (size_t)256 * 1024 * 1024 > freeb)
-        throw NoMem("device memory plan needs " + std::to_string(need >> 20) + " MiB, free " + std::to_string(freeb >> 20) + " MiB");
-    C->d_xyz.upload(std::vector<double>(xyz, xyz + 3 * nv), s);
-    C->d_tri.upload(std::vector<int64_t>(tri, tri + 3 * C->n), s);
+    const size_t margin = (size_t)2 << 30;
+    if (C->lean.on) {
+        if ((size_t)lean_bytes(C) + margin > freeb)
+            throw NoMem("lean device memory plan needs " + std::to_string((size_t)lean_bytes(C) >> 20) + " MiB, free " +
+                        std::to_string(freeb >> 20) + " MiB");
+        return;
+    }
+    const size_t need = plan_bytes(C);
+    if (need + (size_t)256 * 1024 * 1024 <= freeb) return;
+    const std::string full = "device memory plan needs " + std::to_string(need >> 20) + " MiB, free " + std::to_string(freeb >> 20) + " MiB";
+    if (!C->sym_ok || C->world > 1) throw NoMem(full + " (the memory-lean plan needs one shard and the adjoint symmetry)");
+    const int ntop = (int)C->st.ct.levels[std::max(0, C->st.first_level)].size();
+    for (int G = 1;; G *= 2) {
+        lean_plan(C, G);
+        if ((size_t)lean_bytes(C) + margin <= freeb) return;
+        if (G >= ntop) break;
+    }
+    throw NoMem(full + "; the memory-lean plan needs " + std::to_string((size_t)lean_bytes(C) >> 20) + " MiB with " +
+                std::to_string(C->lean.G) + " chunks");
+}
+
+void upload_all(Shard* C, const double* xyz, int64_t nv, const int64_t* tri) {
+    cudaStream_t s = C->stream;
+    const ClusterTree& T = C->st.ct;
+    choose_plan(C);
+    if (xyz) {  // (a re-layout keeps the device mesh)
+        C->d_xyz.upload(std::vector<double>(xyz, xyz + 3 * nv), s);
+        C->d_tri.upload(std::vector<int64_t>(tri, tri + 3 * C->n), s);
+    }
     C->d_perm.upload(T.perm, s);
     C->d_c_lo.upload(T.lo, s);
     C->d_c_hi.upload(T.hi, s);
@@ -920,14 +747,22 @@ void upload_all(Shard* C, const double* xyz, int64_t nv, const int64_t* tri) {
         C->d_leafV_list.push_back(up_list(C->leafV_lists[l]));
         C->d_basis_list.push_back(up_list(C->basis_lists[l]));
         C->d_E_list.push_back(up_list(C->E_lists[l]));
+        if (C->sym_ok) {
+            C->d_leafV_list_sym.push_back(up_list(C->leafV_lists_sym[l]));
+            C->d_basis_list_sym.push_back(up_list(C->basis_lists_sym[l]));
+            C->d_E_list_sym.push_back(up_list(C->E_lists_sym[l]));
+        }
     }
+    C->d_blk_bpcs.upload(C->blk_bpcs, s);
     C->d_qp.alloc((size_t)C->n * 7);
     C->d_grid.alloc(C->nclusters);
     C->d_VR.alloc(C->VR_total);
     C->d_E.alloc(C->E_total);
     const size_t nb = C->st.blocks.size();
-    C->d_S.alloc((size_t)(C->b_hi - C->b_lo) * C->k * C->k);  // own blocks only
-    C->d_St.alloc(C->St_total);
+    if (!C->lean.on) {  // (lean: S per chunk, S~ once the ranks are known)
+        C->d_S.alloc((size_t)(C->b_hi - C->b_lo) * C->k * C->k);  // own blocks only
+        C->d_St.alloc(C->St_total);
+    }
     C->d_omega.alloc(nb);
     C->d_normG2.alloc(nb);
     C->d_xp.alloc(C->n);
@@ -972,10 +807,17 @@ void upload_all(Shard* C, const double* xyz, int64_t nv, const int64_t* tri) {
     P.blk_dir = C->d_blk_dir.p;
     P.blk_bprow = C->d_blk_bprow.p;
     P.blk_bpcol = C->d_blk_bpcol.p;
+    P.blk_bpcs = C->d_blk_bpcs.p;
     P.blk_prow = C->d_blk_prow.p;
     P.blk_pcol = C->d_blk_pcol.p;
     P.blk_St_off = C->d_blk_St_off.p;
-    P.S = C->d_S.p - (ptrdiff_t)C->b_lo * C->k * C->k;  // indexed by global block id
+    {  // S slots: own blocks in order (slot b - b_lo)
+        std::vector<int> slot(nb, 0);
+        for (int b = C->b_lo; b < C->b_hi; ++b) slot[b] = b - C->b_lo;
+        C->d_blk_slot.upload(slot, s);
+    }
+    P.blk_slot = C->d_blk_slot.p;
+    P.S = C->d_S.p;
     P.St = C->d_St.p;
     P.omega = C->d_omega.p;
     P.normG2 = C->d_normG2.p;
@@ -988,6 +830,10 @@ void upload_all(Shard* C, const double* xyz, int64_t nv, const int64_t* tri) {
     }
     P.col_conj = C->col.alias ? 1 : 0;
     if (C->sym_ok) C->d_col2row.upload(C->col2row, s);
+    P.col2row = C->d_col2row.p;
+    // set-up of the row basis pairs only when the column side can be read by conjugation
+    P.sym = (C->sym_ok && C->sym_opt) ? 1 : 0;
+    if (C->lean.on) lean_alloc(C);
 }
 
 // Device set-up (§2): quadrature points, grids, leaf V, E factors, S.
@@ -998,22 +844,28 @@ void run_setup(Shard* C) {
     const int k = C->k;
     C->timed("setup_quad", 2, [&] { launch_quad(P, s); });
     C->timed("setup_grid", 1, [&] { launch_grid(P, s); });
+    // adjoint symmetry: V and E of the row basis pairs only (the column side is read conjugated)
+    const bool sym = P.sym && !C->col_data;
+    C->sym_setup = sym;
     for (int l = 0; l <= L; ++l) {
-        int nl = (int)C->leafV_lists[l].size();
+        const auto& lv = sym ? C->leafV_lists_sym[l] : C->leafV_lists[l];
+        int nl = C->lean.on ? 0 : (int)lv.size();  // lean plan: leaf V per chunk inside the recompression
         if (nl) {
-            C->timed("setup_leafV", 1, [&] { launch_leafV(P, C->d_leafV_list[l], nl, C->max_leaf, s); });
+            C->timed("setup_leafV", 1, [&] { launch_leafV(P, sym ? C->d_leafV_list_sym[l] : C->d_leafV_list[l], nl, C->max_leaf, s); });
             double ent = 0;
-            for (int id : C->leafV_lists[l]) ent += (double)C->st.ct.size(C->bp_t[id]) * k;
+            for (int id : lv) ent += (double)C->st.ct.size(C->bp_t[id]) * k;
             auto& st = C->kstat["setup_leafV"];
             st.flops += ent * 7 * 6;
             st.bytes += ent * 16 + ent / k * 7 * 32;
         }
-        int ne = (int)C->E_lists[l].size();
+        int ne = (int)(sym ? C->E_lists_sym[l] : C->E_lists[l]).size();
         if (ne) {
-            C->timed("setup_E", 1, [&] { launch_E(P, C->d_E_list[l], ne, s); });
+            C->timed("setup_E", 1, [&] { launch_E(P, sym ? C->d_E_list_sym[l] : C->d_E_list[l], ne, s); });
             C->kstat["setup_E"].bytes += (double)ne * 6 * C->m * C->m * 16;
         }
     }
+    if (!sym) C->col_data = true;
+    if (C->lean.on) return;  // S_b per chunk inside the recompression
     const int nb = C->b_hi - C->b_lo;
     C->timed("setup_S", 1, [&] { launch_S(P, C->b_lo, nb, s); });
     auto& st = C->kstat["setup_S"];
@@ -1069,12 +921,14 @@ void run_basis(Shard* C) {
     cudaStream_t s = C->stream;
     const ClusterTree& T = C->st.ct;
     const int L = T.depth, k = C->k, m = C->m;
+    const bool sym = P.sym != 0;  // row basis pairs only (adjoint symmetry)
     for (int l = L; l >= 0; --l) {
-        int nb = (int)C->basis_lists[l].size();
+        const auto& lst = sym ? C->basis_lists_sym[l] : C->basis_lists[l];
+        int nb = (int)lst.size();
         if (!nb) continue;
-        C->timed("basis@" + std::to_string(l), 1, [&] { launch_basis(P, C->d_basis_list[l], nb, C->basis_maxrows[l], s); });
+        C->timed("basis@" + std::to_string(l), 1, [&] { launch_basis(P, sym ? C->d_basis_list_sym[l] : C->d_basis_list[l], nb, C->basis_maxrows[l], s); });
         double fl = 0;
-        for (int id : C->basis_lists[l]) {
+        for (int id : lst) {
             int rows;
             if (C->bp_child0[id] < 0)
                 rows = (int)T.size(C->bp_t[id]);
@@ -1088,6 +942,72 @@ void run_basis(Shard* C) {
         C->kstat["basis@" + std::to_string(l)].flops += fl;
     }
 }
+
+}  // namespace
+
+namespace dh2 {
+// Truncation of the pairs [p0, p0 + np) of level l (all leaves or all inner pairs): kernel choice
+// (split warp-Jacobi path for leaves <= 32, shared-memory CTA per pair, or the global-workspace
+// persistent grid), rank read-back (sizes the next level) and the executed-flop model.
+void truncate_level(Shard* C, PassH& X, bool row, int l, int p0, int np, int maxrows, int maxz, bool all_leaf, bool fused,
+                    double eps, int mode) {
+    const PlanD& P = C->P;
+    cudaStream_t s = C->stream;
+    const ClusterTree& T = C->st.ct;
+    const int k = C->k, m = C->m;
+    const TruncLaunch TL = plan_truncate(P, np, maxrows, maxz, all_leaf, C->force_ws != 0);
+    const bool split = C->split_trunc && all_leaf && maxrows <= 32 && !TL.use_ws;
+    const std::string cls = std::string(row ? "truncate_row@" : "truncate_col@") + std::to_string(l);
+    if (split) {
+        const size_t need = trunc_split_scratch_bytes(np);
+        if (C->d_tscr.n < need) {
+            CK(cudaStreamSynchronize(s));
+            C->d_tscr.alloc(need);
+        }
+        C->timed(cls, 3, [&] { launch_truncate_split(P, row, p0, np, TL, eps, mode, C->d_tscr.p, fused, C->fuse_direct, C->d_blk_mirror.p, s); });
+    }
+    if (TL.use_ws) {
+        const size_t need = (size_t)TL.grid * TL.ws_stride;
+        if (C->d_ws.n < need) {
+            CK(cudaStreamSynchronize(s));
+            C->d_ws.alloc(need);
+        }
+        ++C->ws_launches;
+    }
+    if (!split) C->timed(cls, 1, [&] { launch_truncate(P, row, p0, np, TL, all_leaf, eps, mode, C->d_ws.p, s); });
+    CK(cudaMemcpyAsync(X.rank.data() + p0, X.d_rank.p + p0, np * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int p = p0; p < p0 + np; ++p)
+        if (X.rank[p] < 0)
+            throw CudaError("non-finite singular values in the truncation of level " + std::to_string(l) + " (pair " +
+                            std::to_string(p) + "): non-finite input from an earlier phase");
+    double fl = 0;
+    for (int p = p0; p < p0 + np; ++p) {
+        double rows = X.child0[p] < 0 ? (double)T.size(C->bp_t[X.bp[p]]) : X.rank[X.child0[p]] + X.rank[X.child1[p]];
+        double zr = X.Z_rows[p];
+        if (X.child0[p] >= 0) fl += 8.0 * 3 * rows * k * m;
+        if (fused) {  // stack rows (as total weights), stack V^*, structured QR appends
+            const double tot = X.total_rows[p];
+            for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) {
+                int b = X.blk[ib];
+                fl += 8.0 * C->bp_R_rows[row ? C->blk_bpcol[b] : C->blk_bprow[b]] * (double)k * k;
+            }
+            for (int ip = X.par_ptr[p]; ip < X.par_ptr[p + 1]; ++ip) fl += 8.0 * 3 * X.Z_rows[X.par[ip]] * (double)k * m;
+            fl += 8.0 * tot * rows * k + 8.0 * tot * rows * rows;
+            zr = std::min(tot, rows);
+        } else {
+            fl += 8.0 * rows * zr * k;  // M
+        }
+        double n = std::min(rows, zr);
+        if (rows < zr) fl += qr_flops(zr, rows);
+        fl += 8.0 * 10.0 * rows * n * n;  // SVD, C_svd = 10 model (DESIGN §flop model)
+        fl += 8.0 * X.rank[p] * rows * k;  // C
+    }
+    C->kstat[cls].flops += fl;
+}
+}  // namespace dh2
+
+namespace {
 
 // Phases c-e: block weights, total weights (top-down) and truncation (bottom-up) of the row
 // pass over this shard's pairs; the column pass by adjoint symmetry (or a second pass, 1 shard).
@@ -1182,61 +1102,11 @@ void run_weights_truncate(Shard* C, double eps, int mode) {
             int maxrows = X.lev_max_leafrows[l];
             for (int p = p0; p < p0 + np; ++p)
                 if (X.child0[p] >= 0) maxrows = std::max(maxrows, X.rank[X.child0[p]] + X.rank[X.child1[p]]);
-            int maxz = X.lev_max_zrows[l];
             bool all_leaf, any_leaf;
             level_kind(l, all_leaf, any_leaf);
             if (any_leaf && !all_leaf)  // median-split trees never mix leaves and inner clusters on a level
                 throw NotImpl("a tree level mixing leaf and non-leaf clusters is not supported by k_truncate");
-            const TruncLaunch TL = plan_truncate(P, np, maxrows, maxz, all_leaf, C->force_ws != 0);
-            const bool split = C->split_trunc && all_leaf && maxrows <= 32 && !TL.use_ws;
-            if (split) {
-                const size_t need = trunc_split_scratch_bytes(np);
-                if (C->d_tscr.n < need) {
-                    CK(cudaStreamSynchronize(s));
-                    C->d_tscr.alloc(need);
-                }
-                C->timed(std::string(row ? "truncate_row@" : "truncate_col@") + std::to_string(l), 3,
-                         [&] { launch_truncate_split(P, row, p0, np, TL, eps, mode, C->d_tscr.p, fused[l] != 0, C->fuse_direct, C->d_blk_mirror.p, s); });
-            }
-            if (TL.use_ws) {
-                const size_t need = (size_t)TL.grid * TL.ws_stride;
-                if (C->d_ws.n < need) {
-                    CK(cudaStreamSynchronize(s));
-                    C->d_ws.alloc(need);
-                }
-                ++C->ws_launches;
-            }
-            if (!split)
-                C->timed(std::string(row ? "truncate_row@" : "truncate_col@") + std::to_string(l), 1, [&] { launch_truncate(P, row, p0, np, TL, all_leaf, eps, mode, C->d_ws.p, s); });
-            CK(cudaMemcpyAsync(X.rank.data() + p0, X.d_rank.p + p0, np * sizeof(int), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            for (int p = p0; p < p0 + np; ++p)
-                if (X.rank[p] < 0)
-                    throw CudaError("non-finite singular values in the truncation of level " + std::to_string(l) +
-                                    " (pair " + std::to_string(p) + "): non-finite input from an earlier phase");
-            double fl = 0;
-            for (int p = p0; p < p0 + np; ++p) {
-                double rows = X.child0[p] < 0 ? (double)T.size(C->bp_t[X.bp[p]]) : X.rank[X.child0[p]] + X.rank[X.child1[p]];
-                double zr = X.Z_rows[p];
-                if (X.child0[p] >= 0) fl += 8.0 * 3 * rows * k * m;
-                if (fused[l]) {  // stack rows (as total weights), stack V^*, structured QR appends
-                    const double tot = X.total_rows[p];
-                    for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) {
-                        int b = X.blk[ib];
-                        fl += 8.0 * C->bp_R_rows[row ? C->blk_bpcol[b] : C->blk_bprow[b]] * (double)k * k;
-                    }
-                    for (int ip = X.par_ptr[p]; ip < X.par_ptr[p + 1]; ++ip) fl += 8.0 * 3 * X.Z_rows[X.par[ip]] * (double)k * m;
-                    fl += 8.0 * tot * rows * k + 8.0 * tot * rows * rows;
-                    zr = std::min(tot, rows);
-                } else {
-                    fl += 8.0 * rows * zr * k;  // M
-                }
-                double n = std::min(rows, zr);
-                if (rows < zr) fl += qr_flops(zr, rows);
-                fl += 8.0 * 10.0 * rows * n * n;  // SVD, C_svd = 10 model (DESIGN §flop model)
-                fl += 8.0 * X.rank[p] * rows * k;  // C
-            }
-            C->kstat[std::string(row ? "truncate_row@" : "truncate_col@") + std::to_string(l)].flops += fl;
+            truncate_level(C, X, row, l, p0, np, maxrows, X.lev_max_zrows[l], all_leaf, fused[l] != 0, eps, mode);
         }
     }
 }
@@ -1424,7 +1294,11 @@ void export_shard(const Shard* C, const char* name, void* buf, int64_t* nbytes) 
             else if (base == "child1") it = hv(X->child1);
             else if (base == "Z_rows") it = hv(X->Z_rows);
             else if (base == "Z_off") it = hv(X->Z_off);
-            else if (base == "kb") it = hv(X->kb);
+            else if (C->lean.on && X == &C->row && (base == "kb" || base == "rowsb" || base == "C_off" || base == "Q_off")) {
+                // lean plan: the current layout (compact after the truncation)
+                const LeanState& Ln = C->lean;
+                it = base == "kb" ? hv(Ln.kb_cur) : base == "rowsb" ? hv(Ln.rowsb_cur) : base == "C_off" ? hv(Ln.C_off_cur) : hv(Ln.Q_off_cur);
+            } else if (base == "kb") it = hv(X->kb);
             else if (base == "rowsb") it = hv(X->rowsb);
             else if (base == "C_off") it = hv(X->C_off);
             else if (base == "Q_off") it = hv(X->Q_off);
@@ -1457,7 +1331,14 @@ void export_shard(const Shard* C, const char* name, void* buf, int64_t* nbytes) 
                 it = hv(tmpz);
                 sliced = false;  // tmpz holds exactly the requested range
             } else if (base == "Z") it = dv(X->d_Z);
-            else if (X == &C->col && X->alias && (base == "C" || base == "Q" || base == "sigma")) {
+            else if (C->lean.on && (base == "C" || base == "Q")) {
+                // lean plan: compact Q/F and the persistent C (direct pairs) at the start of the pools
+                const LeanState& Ln = C->lean;
+                const bool q = base == "Q";
+                it = {q ? Ln.Qpool.ptr() : Ln.Cpool.ptr(), (size_t)(q ? Ln.Q_used : Ln.C_used) * sizeof(double2), true,
+                      sizeof(double2)};
+                conj_out = X == &C->col;
+            } else if (X == &C->col && X->alias && (base == "C" || base == "Q" || base == "sigma")) {
                 // aliased column factors: conjugates of the row storage at (s,-c) (offsets C_off_col, ...)
                 if (base == "sigma") {
                     it = dv(C->row.d_sigma);
@@ -1508,6 +1389,8 @@ void export_shard(const Shard* C, const char* name, void* buf, int64_t* nbytes) 
         else if (nm == "blk_prow") it = hv(C->blk_prow);
         else if (nm == "blk_pcol") it = hv(C->blk_pcol);
         else if (nm == "blk_mirror") it = hv(C->blk_mirror);
+        else if (nm == "bp_neg") it = hv(C->bp_neg);
+        else if (nm == "blk_bpcs") it = hv(C->blk_bpcs);
         else if (nm == "owner") {
             tmp32.assign(C->owner.begin(), C->owner.end());
             it = hv(tmp32);
@@ -1847,6 +1730,26 @@ void finish_all(dh2_ctx* X) {
 void require_device(const dh2_ctx* X) { require_device(X->sh[0].get()); }
 
 void do_recompress(dh2_ctx* X, double eps, int mode) {
+    if (X->sh.size() == 1 && X->sh[0]->lean.on && X->world == 1) {  // memory-lean chunked plan
+        Shard* S = X->sh[0].get();
+        lean_recompress(S, eps, mode);
+        S->finish();
+        double v[3];
+        local_sums(S, v);
+        X->E_row = v[0];
+        X->E_col = v[1];
+        X->far2 = v[2];
+        return;
+    }
+    for (auto& S : X->sh) {
+        // adjoint symmetry: row basis pairs only; the two-pass mode needs the column-only V/E too
+        const bool sym = S->sym_ok && S->sym_opt;
+        if (!sym && !S->col_data) {
+            S->P.sym = 0;
+            run_setup(S.get());
+        }
+        S->P.sym = sym ? 1 : 0;
+    }
     for (auto& S : X->sh) run_basis(S.get());
     exchange(X, X_R);  // R_sc of column pairs referenced across shards (after phase b)
     for (auto& S : X->sh) run_weights_truncate(S.get(), eps, mode);
@@ -1876,6 +1779,8 @@ void do_recompress(dh2_ctx* X, double eps, int mode) {
 }
 
 void do_matvec(dh2_ctx* X, bool recomp, const double2* x, double2* y) {
+    if (!recomp && X->sh[0]->lean.on)
+        throw NotImpl("ORIG matvec on the memory-lean plan (V and S are not resident)");
     for (auto& S : X->sh) run_mv_forward(S.get(), recomp, x);
     exchange(X, X_XH);  // xh'_sc of column pairs referenced across shards
     for (auto& S : X->sh) run_mv_rest(S.get(), recomp);
@@ -2016,6 +1921,10 @@ int dh2_recompress(dh2_ctx* X, double eps, int32_t mode) {
             S->mode = mode;
         }
         X->exch_bytes = 0;
+        // a failure part-way leaves the factors inconsistent: RECOMP is unavailable until a
+        // recompression completes
+        for (auto& S : X->sh) S->recompressed = false;
+        X->recompressed = false;
         do_recompress(X, eps, mode);
         for (auto& S : X->sh) S->recompressed = true;
         X->recompressed = true;
@@ -2107,8 +2016,36 @@ int dh2_set_option(dh2_ctx* X, const char* name, int64_t value) {
         for (auto& S : X->sh) S->split_trunc = (int)value;
         return DH2_OK;
     }
+    if (nm == "lean_chunks") {  // > 0: re-lay the context out on the memory-lean chunked plan with that many chunks
+        if (value < 1 || value > (1 << 20)) return fail(X, DH2_EINVAL, "lean_chunks must be >= 1");
+        return guarded(X, [&] {
+            if (X->sh.size() != 1 || X->world != 1) throw NotImpl("the memory-lean plan runs on one shard");
+            Shard* S = X->sh[0].get();
+            require_device(S);
+            if (!S->sym_ok || !S->sym_opt) throw NotImpl("the memory-lean plan needs adjoint_symmetry = 1");
+            CK(cudaSetDevice(S->device));
+            CK(cudaStreamSynchronize(S->stream));
+            // release the full plan's pools, then lay out and set up the lean plan
+            S->d_VR.free();
+            S->d_E.free();
+            S->d_S.free();
+            S->d_St.free();
+            for (PassH* P : {&S->row, &S->col}) {
+                P->d_Z.free();
+                P->d_C.free();
+                P->d_Q.free();
+            }
+            lean_plan(S, (int)value);
+            upload_all(S, nullptr, 0, nullptr);
+            run_setup(S);
+            S->finish();
+            S->recompressed = false;
+            X->recompressed = false;
+        });
+    }
     if (nm == "adjoint_symmetry") {
         if (value != 0 && value != 1) return fail(X, DH2_EINVAL, "adjoint_symmetry must be 0 or 1");
+        if (value == 0 && X->sh[0]->lean.on) return fail(X, DH2_ENOTIMPL, "the memory-lean plan needs adjoint_symmetry = 1");
         if (value == 0 && X->world > 1) return fail(X, DH2_ENOTIMPL, "sharded recompression needs adjoint_symmetry = 1");
         for (auto& S : X->sh) S->sym_opt = (int)value;
         return DH2_OK;
@@ -2160,6 +2097,15 @@ int dh2_get_stats(const dh2_ctx* C, char* buf, int64_t* len) {
     for (size_t i = 0; i < C->sh.size(); ++i) o << (i ? ", " : "") << plan_bytes(C->sh[i].get());
     o << "], \"mirror_missing\": " << S0->mirror_missing
       << ", \"truncate_ws_launches\": " << ws;
+    {
+        const LeanState& Ln = S0->lean;
+        o << ", \"lean\": {\"on\": " << (Ln.on ? "true" : "false") << ", \"chunks\": " << Ln.G << ", \"l0\": " << Ln.l0
+          << ", \"VR_persist_bytes\": " << 16.0 * Ln.VR_persist << ", \"VR_scratch_bytes\": " << 16.0 * Ln.VR_scratch
+          << ", \"Z_scratch_bytes\": " << 16.0 * Ln.Z_scratch << ", \"S_slots\": " << Ln.S_slots
+          << ", \"C_pool_mapped\": " << Ln.Cpool.mapped_bytes() << ", \"Q_pool_mapped\": " << Ln.Qpool.mapped_bytes()
+          << ", \"C_compact_bytes\": " << 16.0 * Ln.C_used << ", \"Q_compact_bytes\": " << 16.0 * Ln.Q_used
+          << ", \"compact_items\": " << Ln.compact_items << ", \"device_used_peak\": " << Ln.peak_bytes << "}";
+    }
     for (int side = 0; side < 2; ++side) {
         o << (side ? ", \"fused_leaf_levels_col\": [" : ", \"fused_leaf_levels_row\": [");
         for (size_t i = 0; i < S0->fused_levels[side].size(); ++i) o << (i ? ", " : "") << S0->fused_levels[side][i];
@@ -2167,7 +2113,8 @@ int dh2_get_stats(const dh2_ctx* C, char* buf, int64_t* len) {
     }
     o << ", \"fused_append_pairs\": " << S0->fused_append
       << ", \"adjoint_symmetry\": {\"available\": " << (S0->sym_ok ? "true" : "false") << ", \"enabled\": " << S0->sym_opt
-      << ", \"used\": " << (S0->sym_used ? "true" : "false") << ", \"why_not\": \"" << S0->sym_why << "\"}"
+      << ", \"used\": " << (S0->sym_used ? "true" : "false") << ", \"row_only_setup\": " << (S0->sym_setup ? "true" : "false")
+      << ", \"why_not\": \"" << S0->sym_why << "\"}"
       << ", \"kernels\": {";
     bool first = true;
     for (auto& kv : ks) {

@@ -914,11 +914,12 @@ __device__ __forceinline__ void ztile_mma(ZTile& t, double2 a, double2 b) {
 // fragment across them.
 template <bool FULL, bool UNROLL>
 __device__ inline void chunk_gemm_S_dmma_t(const double2* X, int rx, int i0, int nb, const double2* Sg, bool conj_s,
-                                           bool strided, double w, int k, double2* out, int ldo) {
+                                           bool strided, double w, int k, double2* out, int ldo, bool conj_x) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int nrt = (nb + 7) >> 3, nct4 = (k + 31) >> 5;
     const int ar = lane >> 2, ac = lane & 3;
     const double sgn = conj_s ? -1.0 : 1.0;
+    const double sgx = conj_x ? -1.0 : 1.0;
     constexpr bool full = FULL;
     for (int task = warp; task < nrt * nct4; task += nw) {
         const int rt = task % nrt, cq = task / nrt;
@@ -932,7 +933,8 @@ __device__ inline void chunk_gemm_S_dmma_t(const double2* X, int rx, int i0, int
         for (int mu = 0; mu < k; mu += 4) {
             const int mm = mu + ac;
             const bool mok = full || mm < k;
-            const double2 a = (rok && mok) ? xa[mm * rx] : cmk(0.0, 0.0);
+            double2 a = (rok && mok) ? xa[mm * rx] : cmk(0.0, 0.0);
+            a.y *= sgx;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int nu = (cq * 4 + q) * 8 + ar;
@@ -954,14 +956,15 @@ __device__ inline void chunk_gemm_S_dmma_t(const double2* X, int rx, int i0, int
     }
 }
 
-// UNROLL: unroll the k loop 4x (more loads in flight; more registers)
+// UNROLL: unroll the k loop 4x (more loads in flight; more registers).  conj_x: X is stored
+// conjugated (the column side read from the row basis pair at -c, adjoint symmetry).
 template <bool UNROLL = false>
 __device__ inline void chunk_gemm_S_dmma(const double2* X, int rx, int i0, int nb, const double2* Sg, bool conj_s,
-                                         bool strided, double w, int k, double2* out, int ldo) {
+                                         bool strided, double w, int k, double2* out, int ldo, bool conj_x = false) {
     if ((k & 31) == 0)
-        chunk_gemm_S_dmma_t<true, UNROLL>(X, rx, i0, nb, Sg, conj_s, strided, w, k, out, ldo);
+        chunk_gemm_S_dmma_t<true, UNROLL>(X, rx, i0, nb, Sg, conj_s, strided, w, k, out, ldo, conj_x);
     else
-        chunk_gemm_S_dmma_t<false, UNROLL>(X, rx, i0, nb, Sg, conj_s, strided, w, k, out, ldo);
+        chunk_gemm_S_dmma_t<false, UNROLL>(X, rx, i0, nb, Sg, conj_s, strided, w, k, out, ldo, conj_x);
 }
 
 // C = A B^H on the FP64 tensor cores: C[i, j] = sum_mu A[i, mu] conj(Bm[j, mu]) for i < na,

@@ -198,8 +198,8 @@ __global__ void k_E(PlanD P, const int* bps, int nbps) {
 
 // Coupling matrices S_b[nu,mu] = g_c(xi_{t,nu}, xi_{s,mu})
 //   = exp(i kappa (r - <xi_t - xi_s, c>)) / (4 pi r).  CTA per block.
-__global__ void k_S(PlanD P, int b0) {
-    const int b = b0 + blockIdx.x;
+__global__ void k_S(PlanD P, int b0, const int* blist) {
+    const int b = blist ? blist[blockIdx.x] : b0 + blockIdx.x;
     const int m = P.m, k = P.k;
     __shared__ GridD gt, gs;
     __shared__ double c[3];
@@ -209,7 +209,7 @@ __global__ void k_S(PlanD P, int b0) {
         for (int a = 0; a < 3; ++a) c[a] = P.dirs[3 * P.blk_dir[b] + a];
     }
     __syncthreads();
-    double2* S = P.S + (size_t)b * k * k;
+    double2* S = P.S + (size_t)P.blk_slot[b] * k * k;
     const double inv4pi = 1.0 / (4.0 * M_PI);
     for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) {
         int nu = idx % k, mu = idx / k;
@@ -247,9 +247,9 @@ void launch_E(const PlanD& P, const int* bps, int nbps, cudaStream_t s) {
     int tot = nbps * 6 * P.m * P.m;
     k_E<<<(tot + 255) / 256, 256, 0, s>>>(P, bps, nbps);
 }
-void launch_S(const PlanD& P, int b0, int nb, cudaStream_t s) {
+void launch_S(const PlanD& P, int b0, int nb, cudaStream_t s, const int* blist) {
     if (!nb) return;
-    k_S<<<nb, 256, 0, s>>>(P, b0);
+    k_S<<<nb, 256, 0, s>>>(P, b0, blist);
 }
 
 // ============================================================== recompression (§3.2)
@@ -440,16 +440,17 @@ void launch_basis(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStr
 // w_b = 1/||G_b||_F for the block-relative modes, 1 for FROB_CLUSTERREL.  CTA per block:
 // U = R_tc S_b on the FP64 tensor cores (S read coalesced through the mirror block), in chunks
 // of <= 64 rows of R_tc, then ||U R_sc^*||_F^2 with a fixed-order reduction.
-__global__ void __launch_bounds__(256, 3) k_block_weights(PlanD P, int b0, int mode, int ldu, int chunk, const int* mirror) {
+__global__ void __launch_bounds__(256, 3) k_block_weights(PlanD P, int b0, int mode, int ldu, int chunk, const int* mirror,
+                                                         const int* blist) {
     extern __shared__ double2 sm[];
     __shared__ double red[32];
-    const int b = b0 + blockIdx.x, k = P.k;
-    const int bt = P.blk_bprow[b], bs = P.blk_bpcol[b];
+    const int b = blist ? blist[blockIdx.x] : b0 + blockIdx.x, k = P.k;
+    const int bt = P.blk_bprow[b], bs = P.sym ? P.blk_bpcs[b] : P.blk_bpcol[b];  // sym: R_sc = conj R_{s,-c}
     const int rt = P.bp_R_rows[bt], rs = P.bp_R_rows[bs];
     const double2* Rt = P.R + P.bp_R_off[bt];
     const double2* Rs = P.R + P.bp_R_off[bs];
     const int mb = mirror[b];
-    const double2* Sg = P.S + (size_t)(mb >= 0 ? mb : b) * k * k;
+    const double2* Sg = P.S + (size_t)P.blk_slot[mb >= 0 ? mb : b] * k * k;
     double2* U = sm;  // chunk x k
     double part = 0.0;
     for (int i0 = 0; i0 < rt; i0 += chunk) {
@@ -457,7 +458,9 @@ __global__ void __launch_bounds__(256, 3) k_block_weights(PlanD P, int b0, int m
         if (i0) __syncthreads();
         chunk_gemm_S_dmma(Rt, rt, i0, nb, Sg, false, mb < 0, 1.0, k, U, ldu);
         __syncthreads();
-        part += dmma_abh<false>(U, ldu, nb, Rs, rs, rs, k, nullptr, 0);  // ||U R_sc^*||_F^2, FP64 tensor cores
+        // ||U R_sc^*||_F^2 on the FP64 tensor cores (sym: R_sc^* = (conj R_{s,-c})^* = R_{s,-c}^T)
+        part += P.sym ? dmma_abh<false, true>(U, ldu, nb, Rs, rs, rs, k, nullptr, 0)
+                      : dmma_abh<false, false>(U, ldu, nb, Rs, rs, rs, k, nullptr, 0);
     }
     part = warp_sum(part);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
@@ -470,12 +473,12 @@ __global__ void __launch_bounds__(256, 3) k_block_weights(PlanD P, int b0, int m
     }
 }
 
-void launch_block_weights(const PlanD& P, int b0, int nb, int mode, const int* mirror, cudaStream_t s) {
+void launch_block_weights(const PlanD& P, int b0, int nb, int mode, const int* mirror, cudaStream_t s, const int* blist) {
     if (!nb) return;
     const int chunk = P.k <= 64 ? 64 : 32;
     const int ldu = odd_ld(chunk);
     size_t sm = (size_t)ldu * P.k * sizeof(double2);
-    k_block_weights<<<nb, 256, sm, s>>>(P, b0, mode, ldu, chunk, mirror);
+    k_block_weights<<<nb, 256, sm, s>>>(P, b0, mode, ldu, chunk, mirror, blist);
 }
 
 // Total weights, one CTA per pair of one level (top-down):
@@ -522,19 +525,20 @@ __global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, const int* m
     };
     for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) {
         const int b = X.blk[ib];
-        const int obp = row ? P.blk_bpcol[b] : P.blk_bprow[b];
+        const bool cj = row && P.sym;  // R_sc = conj R_{s,-c} (adjoint symmetry)
+        const int obp = row ? (cj ? P.blk_bpcs[b] : P.blk_bpcol[b]) : P.blk_bprow[b];
         const int r = P.bp_R_rows[obp];
         const double2* Ro = P.R + P.bp_R_off[obp];
         const double w = P.omega[b];
         const int mb = row ? b : mirror[b];
-        const double2* Sg = P.S + (size_t)(mb >= 0 ? mb : b) * k * k;
+        const double2* Sg = P.S + (size_t)P.blk_slot[mb >= 0 ? mb : b] * k * k;
         const bool strided = !row && mb < 0;
         for (int i0 = 0; i0 < r;) {
             const int nb = qr ? min(CH - fill, r - i0) : min(CH, r - i0);
             double2* dst = qr ? B + fill : Zg + cur;
             const int ldd = qr ? ldb : zr;
             __syncthreads();
-            chunk_gemm_S_dmma(Ro, r, i0, nb, Sg, row, strided, w, k, dst, ldd);  // FP64 tensor cores
+            chunk_gemm_S_dmma(Ro, r, i0, nb, Sg, row, strided, w, k, dst, ldd, cj);  // FP64 tensor cores
             i0 += nb;
             next(nb);
         }
@@ -888,17 +892,18 @@ __global__ void __launch_bounds__(256, 3) k_trunc_zqr(PlanD P, PassD X, bool row
     };
     for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) {
         const int b = X.blk[ib];
-        const int obp = row ? P.blk_bpcol[b] : P.blk_bprow[b];
+        const bool cj = row && P.sym;  // R_sc = conj R_{s,-c} (adjoint symmetry)
+        const int obp = row ? (cj ? P.blk_bpcs[b] : P.blk_bpcol[b]) : P.blk_bprow[b];
         const int r = P.bp_R_rows[obp];
         const double2* Ro = P.R + P.bp_R_off[obp];
         const double w = P.omega[b];
         const int mb = row ? b : mirror[b];
-        const double2* Sg = P.S + (size_t)(mb >= 0 ? mb : b) * k * k;
+        const double2* Sg = P.S + (size_t)P.blk_slot[mb >= 0 ? mb : b] * k * k;
         const bool strided = !row && mb < 0;
         for (int i0 = 0; i0 < r;) {
             const int nb = min(CH - fill, r - i0);
             __syncthreads();
-            chunk_gemm_S_dmma(Ro, r, i0, nb, Sg, row, strided, w, k, B + fill, LD);
+            chunk_gemm_S_dmma(Ro, r, i0, nb, Sg, row, strided, w, k, B + fill, LD, cj);
             i0 += nb;
             fill += nb;
             if (fill == CH) flush();
@@ -1152,16 +1157,16 @@ void launch_mirror_pass(const PlanD& P, const int* col2row, int p0, int np, cuda
 // Projection (Lemma Projections): T_b = C_tc S_b, S~_b = T_b C'_sc^*.  CTA per block,
 // rows of C_tc in chunks of <= `chunk` (T chunk x k in shared memory); both products on the FP64
 // tensor cores, S_b read coalesced through its antipodal mirror block where that is local.
-__global__ void __launch_bounds__(128, 4) k_project(PlanD P, int b0, int ldt, int chunk, const int* mirror) {
+__global__ void __launch_bounds__(128, 4) k_project(PlanD P, int b0, int ldt, int chunk, const int* mirror, const int* blist) {
     extern __shared__ double2 sm[];
-    const int b = b0 + blockIdx.x, k = P.k;
+    const int b = blist ? blist[blockIdx.x] : b0 + blockIdx.x, k = P.k;
     const int pr = P.blk_prow[b], pc = P.blk_pcol[b];
     const int kt = P.row.rank[pr], ks = P.col.rank[pc];
     const int lt = P.row.kb[pr], ls = P.col.kb[pc];
     const double2* Ct = P.row.C + P.row.C_off[pr];
     const double2* Cs = P.col.C + P.col.C_off[pc];
     const int mb = mirror[b];
-    const double2* Sg = P.S + (size_t)(mb >= 0 ? mb : b) * k * k;
+    const double2* Sg = P.S + (size_t)P.blk_slot[mb >= 0 ? mb : b] * k * k;
     double2* St = P.St + P.blk_St_off[b];
     double2* T = sm;
     for (int a0 = 0; a0 < kt; a0 += chunk) {
@@ -1176,12 +1181,12 @@ __global__ void __launch_bounds__(128, 4) k_project(PlanD P, int b0, int ldt, in
     }
 }
 
-void launch_project(const PlanD& P, int b0, int nb, int maxkrow, const int* mirror, cudaStream_t s) {
+void launch_project(const PlanD& P, int b0, int nb, int maxkrow, const int* mirror, cudaStream_t s, const int* blist) {
     if (!nb) return;
     const int chunk = max(1, min(maxkrow, 64));
     int ldt = odd_ld(chunk);
     size_t sm = (size_t)ldt * P.k * sizeof(double2);
-    k_project<<<nb, 128, sm, s>>>(P, b0, ldt, chunk, mirror);
+    k_project<<<nb, 128, sm, s>>>(P, b0, ldt, chunk, mirror, blist);
 }
 
 // ============================================================== matvec (far field)
@@ -1190,7 +1195,9 @@ void launch_project(const PlanD& P, int b0, int nb, int maxkrow, const int* mirr
 __global__ void k_mv_forward(PlanD P, bool recomp, int p0, const double2* xp, double2* xh) {
     const PassD& X = P.col;
     const int p = p0 + blockIdx.x, k = P.k, m = P.m;
-    const int bp = X.bp[p];
+    // sym: V_sc and E of the column pair are the conjugates of those of the row pair (s,-c)
+    const bool vcj = !recomp && P.sym;
+    const int bp = vcj ? P.row.bp[P.col2row[p]] : X.bp[p];
     const bool leaf = X.child0[p] < 0;
     const int kout = recomp ? X.rank[p] : k;
     for (int a = threadIdx.x; a < kout; a += blockDim.x) {
@@ -1200,7 +1207,7 @@ __global__ void k_mv_forward(PlanD P, bool recomp, int p0, const double2* xp, do
             const int nt = P.c_size[t];
             const double2* x = xp + P.c_begin[t];
             const double2* B = recomp ? (X.Q + X.Q_off[p]) : (P.V + P.bp_V_off[bp]);
-            if (recomp && P.col_conj)  // Q' stored as the row Q at (s,-c): conj(Q') = stored
+            if ((recomp && P.col_conj) || vcj)  // Q' (V) stored as the row Q (V) at (s,-c): conj(Q') = stored
                 for (int i = 0; i < nt; ++i) cfma(acc, B[i + (size_t)a * nt], x[i]);
             else
                 for (int i = 0; i < nt; ++i) cfma_cj(acc, B[i + (size_t)a * nt], x[i]);
@@ -1226,7 +1233,10 @@ __global__ void k_mv_forward(PlanD P, bool recomp, int p0, const double2* xp, do
                     for (int nup = 0; nup < k; ++nup) {
                         int px = nup % m, py = (nup / m) % m, pz = nup / (m * m);
                         double2 e = cmul(cmul(F[px * m + jx], F[m * m + py * m + jy]), F[2 * m * m + pz * m + jz]);
-                        cfma_cj(acc, e, xh[(size_t)ch[c] * k + nup]);
+                        if (vcj)  // E_{s'c} = conj E_{s',-c}
+                            cfma(acc, e, xh[(size_t)ch[c] * k + nup]);
+                        else
+                            cfma_cj(acc, e, xh[(size_t)ch[c] * k + nup]);
                     }
                 }
             }
@@ -1252,7 +1262,7 @@ __global__ void k_mv_couple(PlanD P, bool recomp, int p0, const double2* xh, dou
                 const int lt = X.kb[p];
                 for (int c = 0; c < ks; ++c) cfma(acc, St[a + (size_t)c * lt], x[c]);
             } else {
-                const double2* S = P.S + (size_t)b * k * k;
+                const double2* S = P.S + (size_t)P.blk_slot[b] * k * k;
                 for (int c = 0; c < k; ++c) cfma(acc, S[a + (size_t)c * k], x[c]);
             }
         }
@@ -1369,6 +1379,24 @@ void launch_copy_segments(const double2* src, double2* dst, const int64_t* soff,
 void launch_copy_segments_i(const int* src, int* dst, const int64_t* soff, const int64_t* doff, const int64_t* len,
                             int nseg, cudaStream_t s) {
     if (nseg) k_copy_segments<int><<<nseg, 32, 0, s>>>(src, dst, soff, doff, len);
+}
+
+// Compaction of truncation outputs (memory-lean path): item i copies the rows x cols matrix at
+// src + soff[i] (leading dimension lds[i]) to dst + doff[i] with leading dimension rows[i].  CTA per item.
+__global__ void k_copy_mat(const double2* src, double2* dst, const int64_t* soff, const int64_t* doff, const int* rows,
+                           const int* cols, const int* lds) {
+    const int i = blockIdx.x;
+    const int r = rows[i], c = cols[i], ld = lds[i];
+    const double2* a = src + soff[i];
+    double2* b = dst + doff[i];
+    for (int idx = threadIdx.x; idx < r * c; idx += blockDim.x) {
+        const int x = idx % r, y = idx / r;
+        b[idx] = a[x + (size_t)y * ld];
+    }
+}
+void launch_copy_mat(const double2* src, double2* dst, const int64_t* soff, const int64_t* doff, const int* rows,
+                     const int* cols, const int* lds, int n, cudaStream_t s) {
+    if (n) k_copy_mat<<<n, 128, 0, s>>>(src, dst, soff, doff, rows, cols, lds);
 }
 
 void launch_permute(const int64_t* perm, const double2* in, double2* out, int n, bool gather, cudaStream_t s) {

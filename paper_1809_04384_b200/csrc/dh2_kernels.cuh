@@ -40,6 +40,9 @@ struct PlanD {
     int smem_optin;       // opt-in dynamic shared memory per CTA (bytes), minus a static-smem margin
     int num_sms;
     int col_conj;         // 1: column factors C', Q' are stored as the row factors at -c (read conjugated)
+    int sym;              // 1: only row basis pairs have V/R/E; the column side of a block (t,s,c) reads
+                          //    the row basis pair (s,-c) conjugated (blk_bpcs; matvec: col2row)
+    const int* col2row;   // column pair (s,c) -> row pair (s,-c) (adjoint-symmetric structures)
     double kappa;
     // geometry
     const double* xyz;
@@ -73,10 +76,12 @@ struct PlanD {
     const int* blk_dir;
     const int* blk_bprow;
     const int* blk_bpcol;
+    const int* blk_bpcs;  // basis pair id of (s,-c)
     const int* blk_prow;  // row-pass pair id of (t,c)
     const int* blk_pcol;  // col-pass pair id of (s,c)
     const int64_t* blk_St_off;  // kb_row x kb_col slab, ld kb_row
-    double2* S;           // nblk * k * k
+    const int* blk_slot;  // slot of block b in S (full plan: b - b_lo; lean plan: position in its chunk)
+    double2* S;           // slots * k * k
     double2* St;
     double* omega;
     double* normG2;
@@ -88,10 +93,11 @@ void launch_quad(const PlanD& P, cudaStream_t s);
 void launch_grid(const PlanD& P, cudaStream_t s);
 void launch_leafV(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStream_t s);
 void launch_E(const PlanD& P, const int* bps, int nbps, cudaStream_t s);
-void launch_S(const PlanD& P, int b0, int nb, cudaStream_t s);
+void launch_S(const PlanD& P, int b0, int nb, cudaStream_t s, const int* blist = nullptr);
 // recompression (§3.2)
 void launch_basis(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStream_t s);
-void launch_block_weights(const PlanD& P, int b0, int nb, int mode, const int* mirror, cudaStream_t s);
+void launch_block_weights(const PlanD& P, int b0, int nb, int mode, const int* mirror, cudaStream_t s,
+                          const int* blist = nullptr);
 void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* mirror, cudaStream_t s);
 struct TruncLaunch {
     int ldv = 1, ldb = 1, grid = 0;
@@ -111,7 +117,8 @@ size_t trunc_split_scratch_bytes(int np);
 void launch_truncate_split(const PlanD& P, bool row, int p0, int np, const TruncLaunch& L, double eps, int mode,
                            void* scratch, bool fused, int fuse_direct, const int* mirror, cudaStream_t s);
 void launch_mirror_pass(const PlanD& P, const int* col2row, int p0, int np, cudaStream_t s);
-void launch_project(const PlanD& P, int b0, int nb, int maxkrow, const int* mirror, cudaStream_t s);
+void launch_project(const PlanD& P, int b0, int nb, int maxkrow, const int* mirror, cudaStream_t s,
+                    const int* blist = nullptr);
 // matvec (forward / coupling / backward)
 void launch_mv_forward(const PlanD& P, bool recomp, int p0, int np, const double2* xp, double2* xh,
                        cudaStream_t s);
@@ -125,5 +132,7 @@ void launch_copy_segments(const double2* src, double2* dst, const int64_t* soff,
 void launch_copy_segments_i(const int* src, int* dst, const int64_t* soff, const int64_t* doff, const int64_t* len,
                             int nseg, cudaStream_t s);
 void launch_permute(const int64_t* perm, const double2* in, double2* out, int n, bool gather, cudaStream_t s);
+void launch_copy_mat(const double2* src, double2* dst, const int64_t* soff, const int64_t* doff, const int* rows,
+                     const int* cols, const int* lds, int n, cudaStream_t s);
 
 }  // namespace dh2

@@ -28,6 +28,16 @@ class GpuView:
         self.R_off = h.export("bp_R_off", np.int64)
         self.R_rows = h.export("bp_R_rows", np.int32)
         self.E_off = h.export("bp_E_off", np.int64)
+        # adjoint symmetry: only ROW basis pairs are set up / weighted; a column-only pair (t,c) is
+        # the conjugate of the row pair (t,-c)
+        self.bp_neg = h.export("bp_neg", np.int32)
+        rp = h.export("row_pairs", np.int64).reshape(-1, 3)
+        self.is_row = np.zeros(len(bp), bool)
+        for _, t, c in rp:
+            self.is_row[self.bp_id[(int(t), int(c))]] = True
+        sym = h.stats()["adjoint_symmetry"]
+        self.sym_ve = bool(sym.get("row_only_setup", False))
+        self.sym_r = bool(sym["used"])
         self.Eall = h.export("E", np.complex128)
         self.S_all = h.export("S", np.complex128)
         if recompressed:
@@ -45,20 +55,30 @@ class GpuView:
                 self.St[b] = _cm(St, St_off[b], kt, ks, self.row.kb[prow[b]])
         del k
 
-    def V(self, t, c):
+    def _mirror(self, t, c, flag):
+        """(basis pair id holding the data, conjugate?) for (t,c)."""
         i = self.bp_id[(t, c)]
+        if flag and not self.is_row[i]:
+            return int(self.bp_neg[i]), True
+        return i, False
+
+    def V(self, t, c):
+        i, cj = self._mirror(t, c, self.sym_ve)
         rows = self.st.ct.size(t)
-        return _cm(self.VR, self.V_off[i], rows, self.k)
+        v = _cm(self.VR, self.V_off[i], rows, self.k)
+        return v.conj() if cj else v
 
     def R(self, t, c):
-        i = self.bp_id[(t, c)]
-        return _cm(self.VR, self.R_off[i], int(self.R_rows[i]), self.k)
+        i, cj = self._mirror(t, c, self.sym_r)
+        r = _cm(self.VR, self.R_off[i], int(self.R_rows[i]), self.k)
+        return r.conj() if cj else r
 
     def E_factors(self, t, c, child):
-        i = self.bp_id[(t, c)]
+        i, cj = self._mirror(t, c, self.sym_ve)
         m = self.st.m
         off = self.E_off[i] + child * 3 * m * m
-        return [self.Eall[off + a * m * m: off + (a + 1) * m * m].reshape(m, m) for a in range(3)]
+        f = [self.Eall[off + a * m * m: off + (a + 1) * m * m].reshape(m, m) for a in range(3)]
+        return [x.conj() for x in f] if cj else f
 
     def E_dense(self, t, c, child):
         ex, ey, ez = self.E_factors(t, c, child)

@@ -86,11 +86,18 @@ def test_c3_sampled_basis_weights_and_block_norms(c3):
     bp = h.export("basis_pairs", np.int64).reshape(-1, 3)
     R_off = h.export("bp_R_off", np.int64)
     R_rows = h.export("bp_R_rows", np.int32)
+    bp_neg = h.export("bp_neg", np.int32)
+    rows = {(int(t), int(c)) for _, t, c in h.export("row_pairs", np.int64).reshape(-1, 3)}
+    sym = h.stats()["adjoint_symmetry"]["used"]
     rng = np.random.default_rng(5)
     for i in rng.choice(len(bp), size=60, replace=False):
         _, t, c = (int(v) for v in bp[i])
-        r = int(R_rows[i])
-        Rg = _slice(h, "VR", R_off[i], r * k, np.complex128).reshape(k, r).T
+        # adjoint symmetry: a column-only basis pair's weight is the conjugate of (t,-c)'s
+        j = int(bp_neg[i]) if sym and (t, c) not in rows else int(i)
+        r = int(R_rows[j])
+        Rg = _slice(h, "VR", R_off[j], r * k, np.complex128).reshape(k, r).T
+        if j != i:
+            Rg = Rg.conj()
         Ro = lz.R(t, c)
         G0 = Ro.conj().T @ Ro
         assert np.abs(Rg.conj().T @ Rg - G0).max() <= 1e-12 * np.abs(G0).max()
