@@ -688,9 +688,9 @@ void choose_plan(Shard* C) {
     const std::string full = "device memory plan needs " + std::to_string(need >> 20) + " MiB, free " + std::to_string(freeb >> 20) + " MiB";
     if (!C->sym_ok || C->world > 1) throw NoMem(full + " (the memory-lean plan needs one shard and the adjoint symmetry)");
     const int ntop = (int)C->st.ct.levels[std::max(0, C->st.first_level)].size();
-    for (int G = 1;; G *= 2) {
+    for (int G = 1;; G *= 2) {  // (the estimate guesses the ranks: keep 15 % in reserve)
         lean_plan(C, G);
-        if ((size_t)lean_bytes(C) + margin <= freeb) return;
+        if ((size_t)lean_bytes(C) + margin <= (size_t)(0.85 * freeb)) return;
         if (G >= ntop) break;
     }
     throw NoMem(full + "; the memory-lean plan needs " + std::to_string((size_t)lean_bytes(C) >> 20) + " MiB with " +
@@ -1390,6 +1390,18 @@ void export_shard(const Shard* C, const char* name, void* buf, int64_t* nbytes) 
         else if (nm == "blk_pcol") it = hv(C->blk_pcol);
         else if (nm == "blk_mirror") it = hv(C->blk_mirror);
         else if (nm == "bp_neg") it = hv(C->bp_neg);
+        else if (nm == "lean_p_lo") it = hv(C->lean.p_lo);
+        else if (nm == "lean_p_hi") it = hv(C->lean.p_hi);
+        else if (nm == "lean_blk_ptr") it = hv(C->lean.blk_ptr);
+        else if (nm == "lean_blk") it = hv(C->lean.blk);
+        else if (nm == "lean_qr_ptr") it = hv(C->lean.qr_ptr);
+        else if (nm == "lean_qr") it = hv(C->lean.qr);
+        else if (nm == "lean_lvd") it = hv(C->lean.lvd);
+        else if (nm == "lean_lvb") it = hv(C->lean.lvb);
+        else if (nm == "lean_keep") it = hv(C->lean.keep);
+        else if (nm == "lean_keepC") it = hv(C->lean.keepC);
+        else if (nm == "lean_slot") it = hv(C->lean_slot);
+        else if (nm == "lean_mirror") it = hv(C->lean_mirror);
         else if (nm == "blk_bpcs") it = hv(C->blk_bpcs);
         else if (nm == "owner") {
             tmp32.assign(C->owner.begin(), C->owner.end());
@@ -2021,7 +2033,10 @@ int dh2_set_option(dh2_ctx* X, const char* name, int64_t value) {
         return guarded(X, [&] {
             if (X->sh.size() != 1 || X->world != 1) throw NotImpl("the memory-lean plan runs on one shard");
             Shard* S = X->sh[0].get();
-            require_device(S);
+            if (S->device == DH2_DEVICE_NONE) {  // structure-only context: the host plan alone (tests)
+                lean_plan(S, (int)value);
+                return;
+            }
             if (!S->sym_ok || !S->sym_opt) throw NotImpl("the memory-lean plan needs adjoint_symmetry = 1");
             CK(cudaSetDevice(S->device));
             CK(cudaStreamSynchronize(S->stream));
