@@ -1,14 +1,16 @@
 #!/usr/bin/env python
-"""Benchmark of the B200 DH^2 hot path (BASELINE.json metric, workload configs[1] = C2).
+"""Benchmark of the B200 DH^2 hot path (BASELINE.json metric) on the largest BASELINE workload that
+runs on one GPU: configs[3] = C4 (sphere, n = 131072, kappa = 64, m = 5, k = 125, eps = 1e-6; the
+paper's own 131,072-triangle timing case), on the memory-lean chunked plan.
 
 A step = one pass of the whole hot path of SURVEY §8(a) over the resident input:
-device set-up (quadrature, grids, leaf V, transfer factors E, couplings S), the hybrid
-recompression (basis weights, block weights, total weights and truncation for rows and
-columns, projection) and one far-field matvec of the recompressed matrix.
-value = n / device time per step (Mdof/s); e2e = the same through the C ABI from HOST
-buffers (mesh in, x in, y out), host structure build and all copies included.
+device set-up (quadrature, grids, transfer factors E; leaf V and S_b are generated inside the
+recompression on the lean plan), the hybrid recompression (basis weights, block weights, total
+weights and truncation, the column pass by adjoint symmetry, projection) and one far-field matvec
+of the recompressed matrix.  value = n / device time per step (Mdof/s); e2e = the same through the
+C ABI from HOST buffers (mesh in, x in, y out), host structure build and all copies included.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
 
 Under torchrun (N > 1) the matrix is partitioned into N subtree shards, one per GPU, with
 NCCL exchanges of the cross-shard factors (include/dh2.h dh2_dist):
@@ -33,7 +35,26 @@ sys.path.insert(0, ROOT)
 from synth import get_config, mesh_for, seeded_vector  # noqa: E402
 
 METRIC = "DH2 recompression Mdof/s"
-FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 148 SMs x 64 DFMA/clk x 2 flop x max SM clock
+
+
+def fp64_peak():
+    """Measured FP64 tensor-core (DMMA m8n8k4) throughput on this pool's B200, sustained for 4 s
+    (tools/fp64_peak.py -> profiles/r02_fp64_peak.json; MEASURED_PEAKS.json has no FP64 entry)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r02_fp64_peak.json")))
+        return d["dmma_m8n8k4"]["sustained_tflops"], ("measured: DMMA m8n8k4 sustained %.2f TF/s (DFMA %.2f, cuBLAS ZGEMM "
+                                                      "%.2f), profiles/r02_fp64_peak.json" % (
+                                                          d["dmma_m8n8k4"]["sustained_tflops"], d["dfma"]["sustained_tflops"],
+                                                          d["cublas_zgemm"]["sustained_tflops"]))
+    except Exception:
+        return 148 * 64 * 2 * 1.965e9 / 1e12, "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (no measurement found)"
+
+
+def hbm_peak():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"], "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 def workload_desc(cfg):
@@ -110,29 +131,36 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- oracle legs
-def oracle_sample(cfg, frac=0.125, seed=0):
-    """Time the oracle (as it stands) on a bounded sample of the workload: the full §3.2
-    pipeline on the sub-matrix made of a seeded random `frac` of the admissible blocks
-    (pairs re-closed over them).  Returns (seconds, work units sample, work units full)."""
-    from oracle.structure import DH2Structure
+# The oracle (oracle/, as it stands) on the host cores: one process per core, each with one BLAS
+# thread, forked after the oracle's host structure is built once (copy-on-write); process i runs
+# the full §3.2 pipeline on its own seeded sample of the workload -- the sub-matrix made of a
+# random fraction of the admissible blocks, pairs re-closed over them.  A "step" is one such batch
+# over all cores; its wall time is measured, nothing is extrapolated: value = the work the batch
+# did, expressed in DoF of the full matrix (n x sample work units / full work units; units = basis
+# + row + column pairs + blocks), per second of wall time.
+_ORC = {}
+
+
+def _units(s):
+    return (sum(len(p) for p in s.basis_pairs) + sum(len(p) for p in s.row_pairs)
+            + sum(len(p) for p in s.col_pairs) + len(s.blocks))
+
+
+def _oracle_worker(args):
+    import copy
     from oracle.recompress import Recompression
-
-    xyz, tri = mesh_for(cfg)
-    st = DH2Structure(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"])
-
-    def units(s):
-        return (sum(len(p) for p in s.basis_pairs) + sum(len(p) for p in s.row_pairs)
-                + sum(len(p) for p in s.col_pairs) + len(s.blocks))
-
-    full = units(st)
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)  # one BLAS thread per process
+    seed, frac = args
+    st0, eps = _ORC["st"], _ORC["eps"]
+    st = copy.copy(st0)
     rng = np.random.default_rng(seed)
-    keep = np.sort(rng.choice(len(st.blocks), size=max(1, int(frac * len(st.blocks))), replace=False))
-    st.blocks = st.blocks[keep]
+    keep = np.sort(rng.choice(len(st0.blocks), size=max(1, int(frac * len(st0.blocks))), replace=False))
+    st.blocks = st0.blocks[keep]
     st._build_pairs()
-    samp = units(st)
     t0 = time.perf_counter()
-    Recompression(st, cfg["eps"]).run()
-    return time.perf_counter() - t0, samp, full
+    Recompression(st, eps).run()
+    return _units(st), time.perf_counter() - t0
 
 
 def cpu_cores():
@@ -142,25 +170,77 @@ def cpu_cores():
         return os.cpu_count()
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+class OracleBench:
+    """Builds the oracle structure once, then times batches of parallel samples."""
+
+    def __init__(self, cfg, frac):
+        for v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ[v] = "1"
+        from oracle.structure import DH2Structure
+        xyz, tri = mesh_for(cfg)
+        t0 = time.perf_counter()
+        st = DH2Structure(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"])
+        self.structure_s = time.perf_counter() - t0
+        _ORC["st"], _ORC["eps"] = st, cfg["eps"]
+        self.full = _units(st)
+        self.n = int(tri.shape[0])
+        self.frac = frac
+        self.cores = cpu_cores()
+        import multiprocessing as mp
+        self.pool = mp.get_context("fork").Pool(self.cores)
+
+    def batch(self, step):
+        t0 = time.perf_counter()
+        res = self.pool.map(_oracle_worker, [(1000 * step + i, self.frac) for i in range(self.cores)])
+        wall = time.perf_counter() - t0
+        work = sum(u for u, _ in res)
+        return wall, work, [t for _, t in res]
+
+    def close(self):
+        self.pool.terminate()
+
+    def describe(self, work, wall):
+        return ("oracle/ (numpy/scipy, as it stands) on %d host processes x 1 BLAS thread (%s): each runs the full "
+                "§3.2 pipeline on its own seeded sample of %.2g of the admissible blocks (pairs re-closed); the batch "
+                "did %d of the %d work units of the full matrix in %.1f s wall; value = n x done/full units / wall"
+                % (self.cores, cpu_model(), self.frac, work, self.full, wall))
+
+
+def default_frac(cfg):
+    # ~5-15 s of CPU work per process for every configuration
+    return {"C1": 0.5, "C2": 0.02, "C3": 0.003}.get(cfg["name"], 0.0005)
+
+
 def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    times = []
+    ob = OracleBench(cfg, args.sample_frac or default_frac(cfg))
+    walls, works = [], []
     for i in range(args.warmup + args.steps):
-        sec, samp, full = oracle_sample(cfg, args.sample_frac, seed=i)
+        wall, work, _ = ob.batch(i)
         if i >= args.warmup:
-            times.append(sec * full / samp)
-    t = float(np.mean(times))
-    n = cfg["n"]
-    val = n / t / 1e6
+            walls.append(wall)
+            works.append(work)
+    ob.close()
+    wall = float(np.mean(walls))
+    val = ob.n * float(np.mean(works)) / ob.full / wall / 1e6
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "Mdof/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_desc(cfg), "n": n},
-            "cpu_baseline": {"value": val, "unit": "Mdof/s", "cores": 1, "kind": "oracle",
-                             "sample": "full §3.2 oracle pipeline on a seeded %.3g fraction of the admissible blocks of "
-                                       "the same matrix, extrapolated by work units (pairs+blocks)" % args.sample_frac},
+            "config": {"workload": workload_desc(cfg), "n": ob.n},
+            "cpu_baseline": {"value": val, "unit": "Mdof/s", "cores": ob.cores, "kind": "oracle",
+                             "sample": ob.describe(int(np.mean(works)), wall),
+                             "oracle_structure_s": ob.structure_s},
             "e2e": {"value": val, "unit": "Mdof/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -169,12 +249,12 @@ def run_reference(args, cfg, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C4")
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--sample-frac", type=float, default=0.125)
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--sample-frac", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shards", type=int, default=1, help="virtual shards on one GPU (single process)")
     ap.add_argument("--option", action="append", default=[], metavar="NAME=VALUE",
@@ -283,18 +363,35 @@ def main():
     dom = max(kern.items(), key=lambda kv: kv[1]["ms"])
     dname, d = dom
     achieved = d["flops"] / (d["ms"] * 1e-3) / 1e12 if d["ms"] > 0 else 0.0
+    peak, peak_src = fp64_peak()
     traffic = None
     try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(dname)
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        tr = tr.get(cfg["name"], {}).get(dname) if cfg["name"] in tr else None
         traffic = tr["bytes_per_launch"] if tr else None
     except Exception:
         traffic = None
-    roof = {"kernel": dname, "bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-            "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-            "traffic_note": "DRAM bytes of one full-capture launch (largest level) from profiles/ncu_traffic.json",
-            "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (no FP64 entry in MEASURED_PEAKS.json)",
+    roof = {"kernel": dname, "bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "traffic_note": "DRAM bytes per launch of this class from an ncu --set full capture (profiles/ncu_traffic.json)",
+            "peak_source": peak_src,
+            "flops_model": "algorithmic flops of the executed work per DESIGN §8 (Kronecker E, k_new-dependent SVD model "
+                           "C_svd = 10), summed over the class's launches in the timed steps",
             "share_of_step": d["ms"] / (ms * args.steps) if ms > 0 else None,
             "avg_launch_ms": d["ms"] / max(d["launches"], 1)}
+    # the HBM-bound passes: leaf V / S_b writes and the compressed matvec's reads
+    hbm, hbm_src = hbm_peak()
+    st1 = h.storage(1)
+    mv_bytes = 2.0 * st1["row_basis_bytes"] + st1["coupling_bytes"] + 16.0 * 4 * n  # Q/F read twice (fwd + bwd), S~, x/y
+    hb = {}
+    for cls in ("setup_leafV", "setup_S", "matvec"):
+        v = kern.get(cls)
+        if not v or v["ms"] <= 0:
+            continue
+        by = v["bytes"] if cls != "matvec" else mv_bytes * args.steps
+        hb[cls] = {"GBps": by / (v["ms"] * 1e-3) / 1e9, "frac_of_hbm": by / (v["ms"] * 1e-3) / 1e9 / hbm,
+                   "bytes_per_step": by / args.steps}
+    roof["hbm_passes"] = {"peak_GBps": hbm, "peak_source": hbm_src, "passes": hb}
     phases = {cls: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
                     "tflops": (v["flops"] / (v["ms"] * 1e-3) / 1e12) if v["ms"] > 0 else 0.0}
               for cls, v in sorted(kern.items())}
@@ -339,14 +436,11 @@ def main():
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-            sec, samp, full = oracle_sample(cfg, args.sample_frac)
-            tfull = sec * full / samp
-            cpu = {"value": n / tfull / 1e6, "unit": "Mdof/s", "cores": 1, "kind": "oracle",
-                   "sample": "full §3.2 oracle pipeline on a seeded %.3g fraction of the admissible blocks "
-                             "(%d of %d work units, %.1f s), extrapolated by work units" % (
-                                 args.sample_frac, samp, full, sec),
-                   "host_cores_available": cpu_cores()}
+            ob = OracleBench(cfg, args.sample_frac or default_frac(cfg))
+            wall, work, per = ob.batch(0)
+            ob.close()
+            cpu = {"value": n * work / ob.full / wall / 1e6, "unit": "Mdof/s", "cores": ob.cores, "kind": "oracle",
+                   "sample": ob.describe(work, wall), "oracle_structure_s": ob.structure_s}
         line = {"metric": METRIC, "value": value, "unit": "Mdof/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",

@@ -1013,4 +1013,248 @@ __device__ inline double dmma_abh(const double2* A, int lda, int na, const doubl
     return part;
 }
 
+// Upper-triangular k x k factor R in shared memory: dense column-major (ld ldr) or packed by
+// columns (R[i, c] at i + c(c+1)/2, 8 k(k+1) bytes; used when the dense square does not fit,
+// e.g. k = 125: 126 KB packed instead of 250 KB).
+template <bool PK>
+__device__ __forceinline__ int ridx(int i, int c, int ldr) {
+    return PK ? i + ((c * (c + 1)) >> 1) : i + c * ldr;
+}
+template <bool PK>
+__host__ __device__ inline size_t r_elems(int k, int ldr) {
+    return PK ? (size_t)k * (k + 1) / 2 : (size_t)ldr * k;
+}
+
+// Annihilate the nb x k chunk B (nb <= 16 E) into the k x k upper-triangular smem factor R:
+// [R; B] = Q [R'; 0] by k structured Householder reflections, each touching row j of R and the
+// nb rows of B only (the rows of R below j are zero in column j).  Lane groups of 16 own one
+// column at a time, E rows of B per lane (rows gl + 16 e) plus row j of R on lane 0.  One
+// barrier per reflection: every warp forms the reflector itself; the new diagonal beta_j is
+// stored one step later (nobody reads R[j, j] during step j+1).
+template <bool PK, int E>
+__device__ inline void cta_qr_append(double2* R, int ldr, double2* B, int ldb, int nb, int k) {
+    constexpr int G = 16;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int gl = tid & (G - 1), gid = tid / G, ng = blockDim.x / G;
+    const unsigned mask = 0xffffu << (lane & 16);
+    __syncthreads();
+    int prev = -1;
+    double2 prev_beta = cmk(0.0, 0.0);
+    for (int j = 0; j < k; ++j) {
+        if (tid == 0 && prev >= 0) R[ridx<PK>(prev, prev, ldr)] = prev_beta;
+        const double2* bj = B + j * ldb;
+        double s = 0.0;
+        for (int i = lane; i < nb; i += 32) s += cabs2(bj[i]);
+        s = warp_sum(s);
+        const double2 alpha = R[ridx<PK>(j, j, ldr)];
+        double tau = 0.0;
+        double2 beta = alpha, u0 = cmk(0.0, 0.0);
+        if (s > HH_TINY) {  // tiny columns are left as they are (1/(xn (xn + aa)) would overflow)
+            const double aa = sqrt(cabs2(alpha));
+            const double xn = sqrt(s + aa * aa);
+            const double2 ph = aa > 0.0 ? cscale(alpha, 1.0 / aa) : cmk(1.0, 0.0);
+            beta = cscale(ph, -xn);
+            u0 = cscale(ph, aa + xn);
+            tau = 1.0 / (xn * (xn + aa));
+        }
+        if (tau != 0.0) {
+            double2 u[E];
+#pragma unroll
+            for (int e = 0; e < E; ++e) u[e] = (gl + G * e < nb) ? bj[gl + G * e] : cmk(0.0, 0.0);
+            for (int c = j + 1 + gid; c < k; c += ng) {
+                double2* bc = B + c * ldb;
+                double2 x[E];
+                double2 rj = cmk(0.0, 0.0);
+                double2 w = cmk(0.0, 0.0);
+                if (gl == 0) {
+                    rj = R[ridx<PK>(j, c, ldr)];
+                    cfma_cj(w, u0, rj);
+                }
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    x[e] = (gl + G * e < nb) ? bc[gl + G * e] : cmk(0.0, 0.0);
+                    cfma_cj(w, u[e], x[e]);
+                }
+#pragma unroll
+                for (int o = G >> 1; o > 0; o >>= 1) {
+                    w.x += __shfl_xor_sync(mask, w.x, o);
+                    w.y += __shfl_xor_sync(mask, w.y, o);
+                }
+                w = cscale(w, tau);
+                if (gl == 0) R[ridx<PK>(j, c, ldr)] = csub(rj, cmul(u0, w));
+#pragma unroll
+                for (int e = 0; e < E; ++e)
+                    if (gl + G * e < nb) bc[gl + G * e] = csub(x[e], cmul(u[e], w));
+            }
+        }
+        prev = j;
+        prev_beta = beta;
+        __syncthreads();
+    }
+    if (tid == 0 && prev >= 0) R[ridx<PK>(prev, prev, ldr)] = prev_beta;
+    __syncthreads();
+}
+
+
+// Blocked form of cta_qr_append (compact WY, panels of 8 columns): [R; B] = Q [R'; 0] with the same
+// structured reflectors H_j = I - tau_j u_j u_j^*, u_j = [u0_j e_j; b_j] (row j of R and the nb <= 32
+// rows of B).  Warp 0 factorises a panel of 8 columns in registers (lane = row of B: warp-synchronous,
+// no block barrier per reflection) and builds T (8 x 8 upper triangular, H_1...H_8 = I - V T V^*);
+// then every warp applies (H_1...H_8)^* = I - V T^* V^* to 8-column tiles of the trailing matrix on
+// the FP64 tensor cores: W = D^* R_p + U^* B_c (DMMA, K = nb), W2 = T^* W, R_p -= D W2, B_c -= U W2
+// (DMMA, K = 8) -- two block barriers per panel instead of one per column.
+struct WyPanel {
+    double2 u0[8];
+    double tau[8];
+    double2 T[64];  // T[i + 8 j]
+};
+
+template <bool PK>
+__device__ inline void cta_qr_append_wy(double2* R, int ldr, double2* B, int ldb, int nb, int k, WyPanel* wp) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const unsigned FULL = 0xffffffffu;
+    __syncthreads();
+    for (int j0 = 0; j0 < k; j0 += 8) {
+        const int P = min(8, k - j0);
+        if (warp == 0) {
+            double2 b[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) b[c] = (lane < nb && c < P) ? B[lane + (size_t)(j0 + c) * ldb] : cmk(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (j >= P) break;
+                double s = 0.0;
+                {
+                    double v = cabs2(b[j]);
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+                    s = v;
+                }
+                const double2 alpha = R[ridx<PK>(j0 + j, j0 + j, ldr)];
+                double tau = 0.0;
+                double2 beta = alpha, u0 = cmk(0.0, 0.0);
+                if (s > HH_TINY) {  // as cta_qr_append: tiny columns are left in place
+                    const double aa = sqrt(cabs2(alpha));
+                    const double xn = sqrt(s + aa * aa);
+                    const double2 ph = aa > 0.0 ? cscale(alpha, 1.0 / aa) : cmk(1.0, 0.0);
+                    beta = cscale(ph, -xn);
+                    u0 = cscale(ph, aa + xn);
+                    tau = 1.0 / (xn * (xn + aa));
+                }
+                // one batched reduction: b_j^* b_c for the panel columns c > j, and the Gram entries
+                // z_i = b_i^* b_j (i < j) of the reflector vectors for T
+                double2 dv[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    dv[c] = cmk(0.0, 0.0);
+                    if (c > j && c < P) cfma_cj(dv[c], b[j], b[c]);
+                    if (c < j) cfma_cj(dv[c], b[c], b[j]);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        if (c == j || c >= P) continue;
+                        dv[c].x += __shfl_xor_sync(FULL, dv[c].x, o);
+                        dv[c].y += __shfl_xor_sync(FULL, dv[c].y, o);
+                    }
+                if (tau != 0.0) {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        if (c <= j || c >= P) continue;
+                        const double2 rjc = R[ridx<PK>(j0 + j, j0 + c, ldr)];
+                        double2 w = dv[c];
+                        cfma_cj(w, u0, rjc);
+                        w = cscale(w, tau);
+                        if (lane == 0) R[ridx<PK>(j0 + j, j0 + c, ldr)] = csub(rjc, cmul(u0, w));
+                        b[c] = csub(b[c], cmul(b[j], w));
+                    }
+                }
+                // T(0:j, j) = -tau_j T(0:j, 0:j) z (lane i computes row i), T(j, j) = tau_j
+                if (lane < j) {
+                    double2 acc = cmk(0.0, 0.0);
+#pragma unroll
+                    for (int m = 0; m < 8; ++m)
+                        if (m >= lane && m < j) cfma(acc, wp->T[lane + 8 * m], dv[m]);
+                    wp->T[lane + 8 * j] = cscale(acc, -tau);
+                }
+                if (lane == 0) {
+                    wp->T[j + 8 * j] = cmk(tau, 0.0);
+                    wp->u0[j] = u0;
+                    wp->tau[j] = tau;
+                    R[ridx<PK>(j0 + j, j0 + j, ldr)] = beta;
+                }
+                __syncwarp();
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                if (lane < nb && c < P) B[lane + (size_t)(j0 + c) * ldb] = b[c];  // reflector vectors u_B
+        }
+        __syncthreads();
+        // trailing columns [j0 + 8, k) in tiles of 8 per warp
+        const int cf = j0 + 8;
+        const int ntile = cf < k ? (k - cf + 7) >> 3 : 0;
+        const int ar = lane >> 2, ac = lane & 3;
+        for (int tile = warp; tile < ntile; tile += nw) {
+            const int c0 = cf + tile * 8;
+            // W = U^* B_c  (8 x 8, K = nb)
+            ZTile t{0.0, 0.0, 0.0, 0.0};
+            for (int r0 = 0; r0 < nb; r0 += 4) {
+                const int r = r0 + ac;
+                const double2 a = (r < nb && ar < P) ? cconj(B[r + (size_t)(j0 + ar) * ldb]) : cmk(0.0, 0.0);
+                const double2 bb = (r < nb && c0 + ar < k) ? B[r + (size_t)(c0 + ar) * ldb] : cmk(0.0, 0.0);
+                ztile_mma(t, a, bb);
+            }
+            // + D^* R_p: lane holds W[ar][2ac], W[ar][2ac+1]
+            const int n0 = c0 + 2 * ac, n1 = n0 + 1;
+            double2 w0 = cmk(t.r0, t.i0), w1 = cmk(t.r1, t.i1);
+            if (ar < P) {
+                const double2 u0 = wp->u0[ar];
+                if (n0 < k) cfma_cj(w0, u0, R[ridx<PK>(j0 + ar, n0, ldr)]);
+                if (n1 < k) cfma_cj(w1, u0, R[ridx<PK>(j0 + ar, n1, ldr)]);
+            }
+            // W2 = T^* W: W2[i][n] = sum_{j <= i} conj(T[j][i]) W[j][n]; W[j][n] lives in lane 4 j + ac
+            double2 v0 = cmk(0.0, 0.0), v1 = cmk(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int src = 4 * j + ac;
+                const double2 x0 = cmk(__shfl_sync(FULL, w0.x, src), __shfl_sync(FULL, w0.y, src));
+                const double2 x1 = cmk(__shfl_sync(FULL, w1.x, src), __shfl_sync(FULL, w1.y, src));
+                if (j <= ar && ar < P && j < P) {
+                    const double2 tj = wp->T[j + 8 * ar];
+                    cfma_cj(v0, tj, x0);
+                    cfma_cj(v1, tj, x1);
+                }
+            }
+            // R_p -= D W2
+            if (ar < P) {
+                const double2 u0 = wp->u0[ar];
+                if (n0 < k) R[ridx<PK>(j0 + ar, n0, ldr)] = csub(R[ridx<PK>(j0 + ar, n0, ldr)], cmul(u0, v0));
+                if (n1 < k) R[ridx<PK>(j0 + ar, n1, ldr)] = csub(R[ridx<PK>(j0 + ar, n1, ldr)], cmul(u0, v1));
+            }
+            // B_c -= U W2  (nb x 8, K = 8): B operand W2[i][n], i = 4 kk + ac, n = ar, held by lane 4 i + (ar >> 1)
+            for (int rt = 0; rt < nb; rt += 8) {
+                ZTile o{0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int kk = 0; kk < 2; ++kk) {
+                    const int i = 4 * kk + ac;
+                    const int src = 4 * i + (ar >> 1);
+                    const double e0 = __shfl_sync(FULL, v0.x, src), e1 = __shfl_sync(FULL, v0.y, src);
+                    const double f0 = __shfl_sync(FULL, v1.x, src), f1 = __shfl_sync(FULL, v1.y, src);
+                    const double2 bb = (ar & 1) ? cmk(f0, f1) : cmk(e0, e1);
+                    const int r = rt + ar;
+                    const double2 a = (r < nb && i < P) ? B[r + (size_t)(j0 + i) * ldb] : cmk(0.0, 0.0);
+                    ztile_mma(o, a, bb);
+                }
+                const int r = rt + ar;
+                if (r < nb) {
+                    if (n0 < k) B[r + (size_t)n0 * ldb] = csub(B[r + (size_t)n0 * ldb], cmk(o.r0, o.i0));
+                    if (n1 < k) B[r + (size_t)n1 * ldb] = csub(B[r + (size_t)n1 * ldb], cmk(o.r1, o.i1));
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
 }  // namespace dh2

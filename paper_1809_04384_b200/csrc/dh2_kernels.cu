@@ -262,86 +262,14 @@ __device__ inline void zero_lower(double2* A, int lda, int rows, int cols) {
 }
 
 
-// Upper-triangular k x k factor R in shared memory: dense column-major (ld ldr) or packed by
-// columns (R[i, c] at i + c(c+1)/2, 8 k(k+1) bytes; used when the dense square does not fit,
-// e.g. k = 125: 126 KB packed instead of 250 KB).
-template <bool PK>
-__device__ __forceinline__ int ridx(int i, int c, int ldr) {
-    return PK ? i + ((c * (c + 1)) >> 1) : i + c * ldr;
-}
-template <bool PK>
-__host__ __device__ inline size_t r_elems(int k, int ldr) {
-    return PK ? (size_t)k * (k + 1) / 2 : (size_t)ldr * k;
-}
-
-// Annihilate the nb x k chunk B (nb <= 16 E) into the k x k upper-triangular smem factor R:
-// [R; B] = Q [R'; 0] by k structured Householder reflections, each touching row j of R and the
-// nb rows of B only (the rows of R below j are zero in column j).  Lane groups of 16 own one
-// column at a time, E rows of B per lane (rows gl + 16 e) plus row j of R on lane 0.  One
-// barrier per reflection: every warp forms the reflector itself; the new diagonal beta_j is
-// stored one step later (nobody reads R[j, j] during step j+1).
+// Chunk append into the triangle: the blocked compact-WY form (chunks of <= 32 rows, option
+// "qr_wy", default on) or the column-by-column one.
 template <bool PK, int E>
-__device__ inline void cta_qr_append(double2* R, int ldr, double2* B, int ldb, int nb, int k) {
-    constexpr int G = 16;
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int gl = tid & (G - 1), gid = tid / G, ng = blockDim.x / G;
-    const unsigned mask = 0xffffu << (lane & 16);
-    __syncthreads();
-    int prev = -1;
-    double2 prev_beta = cmk(0.0, 0.0);
-    for (int j = 0; j < k; ++j) {
-        if (tid == 0 && prev >= 0) R[ridx<PK>(prev, prev, ldr)] = prev_beta;
-        const double2* bj = B + j * ldb;
-        double s = 0.0;
-        for (int i = lane; i < nb; i += 32) s += cabs2(bj[i]);
-        s = warp_sum(s);
-        const double2 alpha = R[ridx<PK>(j, j, ldr)];
-        double tau = 0.0;
-        double2 beta = alpha, u0 = cmk(0.0, 0.0);
-        if (s > HH_TINY) {  // tiny columns are left as they are (1/(xn (xn + aa)) would overflow)
-            const double aa = sqrt(cabs2(alpha));
-            const double xn = sqrt(s + aa * aa);
-            const double2 ph = aa > 0.0 ? cscale(alpha, 1.0 / aa) : cmk(1.0, 0.0);
-            beta = cscale(ph, -xn);
-            u0 = cscale(ph, aa + xn);
-            tau = 1.0 / (xn * (xn + aa));
-        }
-        if (tau != 0.0) {
-            double2 u[E];
-#pragma unroll
-            for (int e = 0; e < E; ++e) u[e] = (gl + G * e < nb) ? bj[gl + G * e] : cmk(0.0, 0.0);
-            for (int c = j + 1 + gid; c < k; c += ng) {
-                double2* bc = B + c * ldb;
-                double2 x[E];
-                double2 rj = cmk(0.0, 0.0);
-                double2 w = cmk(0.0, 0.0);
-                if (gl == 0) {
-                    rj = R[ridx<PK>(j, c, ldr)];
-                    cfma_cj(w, u0, rj);
-                }
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    x[e] = (gl + G * e < nb) ? bc[gl + G * e] : cmk(0.0, 0.0);
-                    cfma_cj(w, u[e], x[e]);
-                }
-#pragma unroll
-                for (int o = G >> 1; o > 0; o >>= 1) {
-                    w.x += __shfl_xor_sync(mask, w.x, o);
-                    w.y += __shfl_xor_sync(mask, w.y, o);
-                }
-                w = cscale(w, tau);
-                if (gl == 0) R[ridx<PK>(j, c, ldr)] = csub(rj, cmul(u0, w));
-#pragma unroll
-                for (int e = 0; e < E; ++e)
-                    if (gl + G * e < nb) bc[gl + G * e] = csub(x[e], cmul(u[e], w));
-            }
-        }
-        prev = j;
-        prev_beta = beta;
-        __syncthreads();
-    }
-    if (tid == 0 && prev >= 0) R[ridx<PK>(prev, prev, ldr)] = prev_beta;
-    __syncthreads();
+__device__ __forceinline__ void qr_append(const PlanD& P, double2* R, int ldr, double2* B, int ldb, int nb, int k, WyPanel* wp) {
+    if (E == 2 && P.qr_wy)
+        cta_qr_append_wy<PK>(R, ldr, B, ldb, nb, k, wp);
+    else
+        cta_qr_append<PK, E>(R, ldr, B, ldb, nb, k);
 }
 
 // Basis weights (Eq. 18; [BO10, Alg. 16] generalised to directions), one CTA per
@@ -352,6 +280,7 @@ __device__ inline void cta_qr_append(double2* R, int ldr, double2* B, int ldb, i
 template <bool PK, int E>
 __global__ void k_basis(PlanD P, const int* bps, int ldr, int ldb) {
     extern __shared__ double2 sm[];
+    __shared__ WyPanel wp;
     const int bp = bps[blockIdx.x];
     const int k = P.k, m = P.m;
     constexpr int CH = 16 * E;
@@ -401,12 +330,12 @@ __global__ void k_basis(PlanD P, const int* bps, int ldr, int ldb) {
             }
             fill += nb;
             if (fill == CH) {
-                cta_qr_append<PK, E>(R, ldr, B, ldb, fill, k);
+                qr_append<PK, E>(P, R, ldr, B, ldb, fill, k, &wp);
                 fill = 0;
             }
         }
     }
-    if (qr && fill > 0) cta_qr_append<PK, E>(R, ldr, B, ldb, fill, k);
+    if (qr && fill > 0) qr_append<PK, E>(P, R, ldr, B, ldb, fill, k, &wp);
     if (qr) {
         __syncthreads();
         for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) {
@@ -490,6 +419,7 @@ void launch_block_weights(const PlanD& P, int b0, int nb, int mode, const int* m
 template <bool PK, int E>
 __global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, const int* mirror, int ldr, int ldb) {
     extern __shared__ double2 sm[];
+    __shared__ WyPanel wp;
     const int p = p0 + blockIdx.x;
     const int k = P.k, m = P.m;
     constexpr int CH = 16 * E;
@@ -519,7 +449,7 @@ __global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, const int* m
         }
         fill += nb;
         if (fill == CH) {
-            cta_qr_append<PK, E>(R, ldr, B, ldb, fill, k);
+            qr_append<PK, E>(P, R, ldr, B, ldb, fill, k, &wp);
             fill = 0;
         }
     };
@@ -566,7 +496,7 @@ __global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, const int* m
             next(nb);
         }
     }
-    if (qr && fill > 0) cta_qr_append<PK, E>(R, ldr, B, ldb, fill, k);
+    if (qr && fill > 0) qr_append<PK, E>(P, R, ldr, B, ldb, fill, k, &wp);
     if (qr) {
         __syncthreads();
         for (int idx = threadIdx.x; idx < zr * k; idx += blockDim.x) {

@@ -82,3 +82,46 @@ extern "C" int devtest_gemm(const double* X, const double* S, double* out, int n
     cudaFree(dout);
     return e == cudaSuccess ? 0 : -2;
 }
+
+// R factor of A (M x N, column-major) by 32-row chunks appended into an N x N triangle:
+// mode 0 = cta_qr_append (dense R), 1 = cta_qr_append_wy (dense), 2 / 3 = the same on the packed R.
+__global__ void k_devappend(int mode, const double2* A, double2* Rout, int M, int N) {
+    extern __shared__ double2 smem[];
+    __shared__ WyPanel wp;
+    const bool pk = mode >= 2;
+    const int ldr = N | 1, ldb = 33;
+    double2* R = smem;
+    const size_t relems = pk ? (size_t)N * (N + 1) / 2 : (size_t)ldr * N;
+    double2* B = R + relems;
+    for (size_t i = threadIdx.x; i < relems; i += blockDim.x) R[i] = cmk(0.0, 0.0);
+    for (int r0 = 0; r0 < M; r0 += 32) {
+        const int nb = min(32, M - r0);
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < nb * N; idx += blockDim.x) B[idx % nb + (idx / nb) * ldb] = A[r0 + idx % nb + (size_t)(idx / nb) * M];
+        __syncthreads();
+        if (mode == 0) cta_qr_append<false, 2>(R, ldr, B, ldb, nb, N);
+        if (mode == 1) cta_qr_append_wy<false>(R, ldr, B, ldb, nb, N, &wp);
+        if (mode == 2) cta_qr_append<true, 2>(R, ldr, B, ldb, nb, N);
+        if (mode == 3) cta_qr_append_wy<true>(R, ldr, B, ldb, nb, N, &wp);
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+        const int i = idx % N, c = idx / N;
+        Rout[idx] = i > c ? cmk(0.0, 0.0) : R[pk ? ridx<true>(i, c, ldr) : ridx<false>(i, c, ldr)];
+    }
+}
+extern "C" int devtest_append(int mode, const double* A, double* R, int M, int N, int threads) {
+    double2 *da, *dr;
+    cudaMalloc(&da, (size_t)M * N * 16);
+    cudaMalloc(&dr, (size_t)N * N * 16);
+    cudaMemcpy(da, A, (size_t)M * N * 16, cudaMemcpyHostToDevice);
+    const size_t relems = mode >= 2 ? (size_t)N * (N + 1) / 2 : (size_t)(N | 1) * N;
+    const size_t sm = (relems + (size_t)33 * N) * 16;
+    cudaFuncSetAttribute(k_devappend, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    k_devappend<<<1, threads, sm>>>(mode, da, dr, M, N);
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(R, dr, (size_t)N * N * 16, cudaMemcpyDeviceToHost);
+    cudaFree(da);
+    cudaFree(dr);
+    return e == cudaSuccess ? 0 : -2;
+}

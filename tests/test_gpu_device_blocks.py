@@ -172,3 +172,26 @@ def test_dmma_gemm(dev, nb, conj_s, strided):
         opS = opS.conj()
     ref = 0.5 * X @ opS
     assert np.abs(got - ref).max() <= 1e-14 * np.abs(ref).max() * 4
+
+
+@pytest.mark.parametrize("M,N", [(250, 125), (96, 64), (40, 27), (300, 125), (33, 125)])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+def test_qr_append_chunks(dev, M, N, mode):
+    """R of a tall A by 32-row chunks appended into a triangle (structured Householder; modes 1/3 the
+    blocked compact-WY form with DMMA trailing updates, 2/3 on the packed triangle): R^*R = A^*A."""
+    dev.devtest_append.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                   ctypes.c_int]
+    rng = np.random.default_rng(M * 7 + N + mode)
+    A = rng.normal(size=(M, N)) + 1j * rng.normal(size=(M, N))
+    A[:, 3] = 0.0  # a numerically zero column (HH_TINY path)
+    A[:, 5] = A[:, 4]  # exactly dependent columns
+    a = np.ascontiguousarray(A.T)  # column-major
+    R = np.empty((N, N), dtype=np.complex128)
+    assert dev.devtest_append(mode, a.ctypes.data, R.ctypes.data, M, N, 512) == 0
+    R = R.T.copy()  # column-major -> (N, N)
+    assert np.allclose(np.tril(R, -1), 0)
+    G0 = A.conj().T @ A
+    assert np.abs(R.conj().T @ R - G0).max() <= 1e-12 * np.abs(G0).max()
+    # the same R as numpy's Householder QR up to the diagonal phases
+    Rn = np.linalg.qr(A, mode="r")[: min(M, N)]
+    assert np.allclose(np.abs(np.diag(R))[: min(M, N)], np.abs(np.diag(Rn)), rtol=1e-9, atol=1e-9 * np.abs(Rn).max())

@@ -24,10 +24,10 @@ _GPU = {}
 CASES = [(n, 1) for n in SMALL + ["C2"]] + [(n, 0) for n in SMALL]
 
 
-def gpu_run(name, eps=None, mode="FROB_BLOCKREL", sym=1, ws=0, split=1, fuse=0, direct=64):
+def gpu_run(name, eps=None, mode="FROB_BLOCKREL", sym=1, ws=0, split=1, fuse=0, direct=64, wy=1):
     from paper_1809_04384_b200 import DH2
     from gpu_view import GpuView
-    key = (name, eps, mode, sym, ws, split, fuse, direct)
+    key = (name, eps, mode, sym, ws, split, fuse, direct, wy)
     if key not in _GPU:
         cfg = get_config(name)
         xyz, tri = mesh_for(cfg)
@@ -37,6 +37,7 @@ def gpu_run(name, eps=None, mode="FROB_BLOCKREL", sym=1, ws=0, split=1, fuse=0, 
         h.set_option("truncate_split", split)
         h.set_option("fuse_leaf_weights", fuse)
         h.set_option("fuse_direct_rows", direct)
+        h.set_option("qr_wy", wy)
         h.recompress(cfg["eps"] if eps is None else eps, mode)
         assert h.stats()["adjoint_symmetry"]["used"] == bool(sym)
         assert (h.stats()["truncate_ws_launches"] > 0) == bool(ws)
@@ -233,3 +234,19 @@ def test_storage_recomp_matches_oracle(name, sym):
             assert mine[f] == ref[f], (which, f, mine[f], ref[f])
         for f in ("kb_per_dof_basis", "kb_per_dof_matrix", "mean_rank"):
             assert mine[f] == pytest.approx(ref[f], rel=1e-13), (which, f)
+
+
+@pytest.mark.parametrize("name", ["P4", "P5", "P7"])
+def test_qr_append_column_by_column(name):
+    """k = 125: the column-by-column chunk appends (qr_wy = 0) instead of the blocked compact-WY ones
+    give the same ranks, singular values and matrix."""
+    h, g, rc = gpu_run(name, wy=0)
+    for side in ("row", "col"):
+        go, oo = getattr(g, side), getattr(rc, side)
+        assert go.rank == oo.rank
+        for key, so in oo.sigma.items():
+            n = min(len(go.sigma[key]), len(so))
+            assert np.abs(go.sigma[key][:n] - so[:n]).max(initial=0.0) <= 1e-12 * max(so[0] if len(so) else 0.0, 1e-300)
+    x = seeded_vector(rc.st.n, 1)
+    yo = ops.matvec(rc, x, "orig")
+    assert np.linalg.norm(h.matvec(x, 1) - ops.matvec(rc, x, "recomp")) <= 1e-10 * np.linalg.norm(yo)

@@ -1,0 +1,191 @@
+"""BASELINE configs[3..4] at FULL size on one GPU: C4 (sphere n = 131072, kappa = 64, m = 5, k = 125,
+leaf 64, eps = 1e-6) and C5 (cube n = 196608, kappa = 115), which only the memory-lean chunked plan
+holds.  Checked on seeded samples that the lazy oracle (oracle/lazy.py: the §3.2
+formulas on the dependency cone of each sampled item) computes one by one:
+  * per level, sampled row pairs: singular values (1e-12 sigma_1) and ranks;
+  * sampled direct basis weights: R^*R (1e-12 ||R||^2, G2) and block norms ||G_b|| (1e-12);
+  * per level, sampled blocks: the recompressed block G~_b = Q_tc S~_b Q'_sc^* densely, from both
+    factor sets (1e-10 ||G_b||_F per block, SURVEY §8(c) G5 restricted to the sample), and the
+    GPU bases' orthonormality;
+and by properties that hold at any size: the certified global bound (Pythagoras) and the
+antipodal symmetry E_row = E_col."""
+import numpy as np
+import pytest
+
+from synth import get_config, mesh_for
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", params=["C4", "C5"])
+def big(request):
+    from paper_1809_04384_b200 import DH2
+    from oracle.structure import DH2Structure
+    from oracle.lazy import LazyRecompression
+    cfg = get_config(request.param)
+    xyz, tri = mesh_for(cfg)
+    h = DH2(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"])
+    assert h.stats()["lean"]["on"], "C4/C5 exceed one GPU in the full plan: the lean plan must be chosen"
+    h.recompress(cfg["eps"])
+    st = DH2Structure(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"])
+    yield h, st, LazyRecompression(st, cfg["eps"]), cfg
+    h.close()
+
+
+def _sl(h, name, off, cnt, dtype):
+    return h.export("%s@%d:%d" % (name, int(off), int(cnt)), dtype)
+
+
+class _GpuFactors:
+    """Q/F (row pass; the column pass is the conjugate at -c), ranks, sigma read by slices."""
+
+    def __init__(self, h, st):
+        self.h, self.st = h, st
+        self.k = st.k
+        self.pairs = h.export("row_pairs", np.int64).reshape(-1, 3)
+        self.pid = {(int(t), int(c)): p for p, (_, t, c) in enumerate(self.pairs)}
+        self.rank = h.export("rank_row", np.int32)
+        self.Q_off = h.export("Q_off_row", np.int64)
+        self.rowsb = h.export("rowsb_row", np.int32)
+        self.child0 = h.export("child0_row", np.int32)
+        self.child1 = h.export("child1_row", np.int32)
+        self.bp_neg = h.export("bp_neg", np.int32)
+        bp = h.export("basis_pairs", np.int64).reshape(-1, 3)
+        self.bp_key = [(int(t), int(c)) for _, t, c in bp]
+        self.bp_id = {key: i for i, key in enumerate(self.bp_key)}
+        self._Q = {}
+
+    def neg(self, t, c):
+        return self.bp_key[self.bp_neg[self.bp_id[(t, c)]]]
+
+    def qhat(self, p):
+        kk, ld = int(self.rank[p]), int(self.rowsb[p])
+        if kk == 0:
+            return np.zeros((ld, 0), dtype=np.complex128)
+        return _sl(self.h, "Q_row", self.Q_off[p], ld * kk, np.complex128).reshape(kk, ld).T
+
+    def Q(self, t, c):
+        """dense new row basis Q_tc (#t x k_tc), expanded through the transfers F."""
+        key = (t, c)
+        if key not in self._Q:
+            p = self.pid[key]
+            ct = self.st.ct
+            if self.child0[p] < 0:
+                self._Q[key] = self.qhat(p)
+            else:
+                Qh = self.qhat(p)
+                k1 = int(self.rank[self.child0[p]])
+                parts = []
+                for i, ch in enumerate(ct.children[t]):
+                    _, tc, cc = self.pairs[self.child0[p] if i == 0 else self.child1[p]]
+                    F = Qh[:k1] if i == 0 else Qh[k1:]
+                    parts.append(self.Q(int(tc), int(cc)) @ F)
+                self._Q[key] = np.vstack(parts)
+        return self._Q[key]
+
+
+def _oracle_Q(lz, side, t, c):
+    st, ct = lz.st, lz.st.ct
+    tr = lz.truncate(side, t, c)
+    if ct.is_leaf(t):
+        return tr["Q"]
+    c2 = st.sd(int(ct.level[t]), c)
+    ch = [int(x) for x in ct.children[t]]
+    k1 = lz.truncate(side, ch[0], c2)["rank"]
+    Qh = tr["Q"]
+    return np.vstack([_oracle_Q(lz, side, ch[0], c2) @ Qh[:k1], _oracle_Q(lz, side, ch[1], c2) @ Qh[k1:]])
+
+
+def test_scale_sampled_pairs(big):
+    h, st, lz, cfg = big
+    pairs = h.export("row_pairs", np.int64).reshape(-1, 3)
+    lev_ptr = h.export("lev_ptr_row", np.int32)
+    sig_off, nsig = h.export("sig_off_row", np.int64), h.export("nsig_row", np.int32)
+    rank = h.export("rank_row", np.int32)
+    rng = np.random.default_rng(21)
+    checked = 0
+    for l in range(len(lev_ptr) - 1):
+        a, b = lev_ptr[l], lev_ptr[l + 1]
+        if b <= a:
+            continue
+        for p in rng.choice(np.arange(a, b), size=min(10, b - a), replace=False):
+            _, t, c = (int(v) for v in pairs[p])
+            tr = lz.truncate("row", t, c)
+            so, sg = tr["sigma"], _sl(h, "sigma_row", sig_off[p], nsig[p], np.float64)
+            n = min(len(so), len(sg))
+            assert np.abs(sg[:n] - so[:n]).max(initial=0.0) <= 1e-12 * so[0], (l, t, c)
+            assert np.all(so[n:] <= 1e-12 * so[0])
+            assert rank[p] == tr["rank"], (l, t, c)
+            checked += 1
+    assert checked >= 40
+
+
+def test_scale_sampled_weights(big):
+    h, st, lz, cfg = big
+    k = st.k
+    bp = h.export("basis_pairs", np.int64).reshape(-1, 3)
+    keep = np.nonzero(h.export("lean_keep", np.int8))[0]
+    R_off, R_rows = h.export("bp_R_off", np.int64), h.export("bp_R_rows", np.int32)
+    rng = np.random.default_rng(5)
+    for i in rng.choice(keep, size=40, replace=False):
+        _, t, c = (int(v) for v in bp[i])
+        r = int(R_rows[i])
+        Rg = _sl(h, "VR", R_off[i], r * k, np.complex128).reshape(k, r).T
+        Ro = lz.R(t, c)
+        G0 = Ro.conj().T @ Ro
+        assert np.abs(Rg.conj().T @ Rg - G0).max() <= 1e-12 * np.abs(G0).max(), (t, c)
+    g2 = h.export("normG2", np.float64)
+    for b in rng.choice(len(st.blocks), size=40, replace=False):
+        assert abs(np.sqrt(g2[b]) * lz.omega(int(b)) - 1.0) <= 1e-12
+
+
+def test_scale_sampled_blocks(big):
+    """Dense recompressed blocks G~_b = Q_tc S~_b Q'_sc^* from the GPU's exported factors and from the
+    lazy oracle; the column basis of the GPU is conj(Q_{s,-c}) (adjoint symmetry)."""
+    h, st, lz, cfg = big
+    g = _GpuFactors(h, st)
+    blocks = h.export("blocks", np.int64).reshape(-1, 3)
+    St_off, kb = h.export("blk_St_off", np.int64), h.export("kb_row", np.int32)
+    prow, pcol = h.export("blk_prow", np.int32), h.export("blk_pcol", np.int32)
+    kc = h.export("rank_col", np.int32)
+    g2 = h.export("normG2", np.float64)
+    ct = st.ct
+    lev = np.array([int(ct.level[int(t)]) for t in blocks[:, 0]])
+    rng = np.random.default_rng(33)
+    nchk = 0
+    for l in sorted(set(lev.tolist())):
+        idx = np.nonzero(lev == l)[0]
+        for b in rng.choice(idx, size=min(6 if l >= ct.depth - 1 else 3, len(idx)), replace=False):
+            t, s, c = (int(v) for v in blocks[b])
+            kt, ks, ld = int(g.rank[prow[b]]), int(kc[pcol[b]]), int(kb[prow[b]])
+            Stg = _sl(h, "St", St_off[b], ld * ks, np.complex128).reshape(ks, ld).T[:kt] if kt and ks else np.zeros((kt, ks))
+            Qt = g.Q(t, c)
+            Qs = g.Q(*g.neg(s, c)).conj()
+            Gg = Qt @ Stg @ Qs.conj().T
+            for Qx in (Qt, Qs):
+                assert np.abs(Qx.conj().T @ Qx - np.eye(Qx.shape[1])).max(initial=0.0) <= 1e-12
+            Ct = lz.truncate("row", t, c)["C"]
+            Cs = lz.truncate("col", s, c)["C"]
+            Go = _oracle_Q(lz, "row", t, c) @ (Ct @ lz.S(int(b)) @ Cs.conj().T) @ _oracle_Q(lz, "col", s, c).conj().T
+            assert np.linalg.norm(Gg - Go) <= 1e-10 * np.sqrt(g2[b]), (l, t, s, c)
+            nchk += 1
+    assert nchk >= 15
+
+
+def test_scale_certified_bound(big):
+    """sum_b w_b^2 (||G_b||^2 - ||S~_b||^2) <= E_row + E_col from the GPU factors; E_row = E_col."""
+    h, st, lz, cfg = big
+    s = h.stats()
+    g2, w = h.export("normG2", np.float64), h.export("omega", np.float64)
+    St_off, kb = h.export("blk_St_off", np.int64), h.export("kb_row", np.int32)
+    prow, pcol = h.export("blk_prow", np.int32), h.export("blk_pcol", np.int32)
+    kr, kc = h.export("rank_row", np.int32), h.export("rank_col", np.int32)
+    St = h.export("St", np.complex128)
+    err = 0.0
+    for b in range(len(g2)):
+        a, c, ld = int(kr[prow[b]]), int(kc[pcol[b]]), int(kb[prow[b]])
+        m = St[St_off[b]:St_off[b] + ld * c].reshape(c, ld)[:, :a] if a and c else np.zeros(0)
+        err += w[b] ** 2 * (g2[b] - np.sum(np.abs(m) ** 2))
+    assert err <= (s["E_row"] + s["E_col"]) * (1 + 1e-6) + 1e-12
+    assert abs(s["E_row"] - s["E_col"]) <= 1e-8 * s["E_row"]
+    assert s["lean"]["device_used_peak"] < 183e9
