@@ -263,7 +263,8 @@ __device__ inline void zero_lower(double2* A, int lda, int rows, int cols) {
 
 
 // Chunk append into the triangle: the blocked compact-WY form (chunks of <= 32 rows, option
-// "qr_wy", default on) or the column-by-column one.
+// "qr_wy"; measured 1.5-2x slower on C4: its panels are factorised by one warp while the others
+// wait, so the k-step critical path per chunk is not shorter) or the column-by-column one (default).
 template <bool PK, int E>
 __device__ __forceinline__ void qr_append(const PlanD& P, double2* R, int ldr, double2* B, int ldb, int nb, int k, WyPanel* wp) {
     if (E == 2 && P.qr_wy)

@@ -119,7 +119,8 @@ extern "C" int devtest_append(int mode, const double* A, double* R, int M, int N
     const size_t sm = (relems + (size_t)33 * N) * 16;
     cudaFuncSetAttribute(k_devappend, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     k_devappend<<<1, threads, sm>>>(mode, da, dr, M, N);
-    cudaError_t e = cudaDeviceSynchronize();
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
     cudaMemcpy(R, dr, (size_t)N * N * 16, cudaMemcpyDeviceToHost);
     cudaFree(da);
     cudaFree(dr);

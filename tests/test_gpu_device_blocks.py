@@ -179,6 +179,8 @@ def test_dmma_gemm(dev, nb, conj_s, strided):
 def test_qr_append_chunks(dev, M, N, mode):
     """R of a tall A by 32-row chunks appended into a triangle (structured Householder; modes 1/3 the
     blocked compact-WY form with DMMA trailing updates, 2/3 on the packed triangle): R^*R = A^*A."""
+    if mode < 2 and N > 100:
+        pytest.skip("the dense k x k triangle does not fit shared memory for k > 100 (the library packs it)")
     dev.devtest_append.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                    ctypes.c_int]
     rng = np.random.default_rng(M * 7 + N + mode)
