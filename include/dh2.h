@@ -45,8 +45,10 @@ enum {
     DH2_ECUDA = -3,     /* CUDA runtime error or no device */
     DH2_ENCCL = -4,     /* multi-GPU transport (NCCL) error or NCCL unavailable */
     DH2_ESTATE = -5,    /* call order: recompress before build, RECOMP matvec before recompress */
-    DH2_EMISMATCH = -6, /* reserved: ranks passed different arguments */
-    DH2_ENOTIMPL = -7   /* configuration outside what this build supports (e.g. m > 5, k > 125) */
+    DH2_EMISMATCH = -6, /* ranks of a multi-GPU context passed different arguments (parameter hash, all-reduced) */
+    DH2_ENOTIMPL = -7,  /* configuration outside what this build supports (e.g. m > 5, k > 125) */
+    DH2_ENUMERIC = -8   /* numerical failure: non-finite singular values, or a one-sided Jacobi SVD that did
+                           not converge in 60 sweeps (the factors of that recompression are not used) */
 };
 
 /* recompression error-control modes (reading Q12 of DESIGN.md) */

@@ -956,9 +956,41 @@ void truncate_level(Shard* C, PassH& X, bool row, int l, int p0, int np, int max
     cudaStream_t s = C->stream;
     const ClusterTree& T = C->st.ct;
     const int k = C->k, m = C->m;
+    const std::string cls = std::string(row ? "truncate_row@" : "truncate_col@") + std::to_string(l);
+    bool any_leaf = false, any_inner = false;
+    for (int p = p0; p < p0 + np; ++p) (X.child0[p] < 0 ? any_leaf : any_inner) = true;
+    if (any_leaf && any_inner) {
+        // a level mixing leaf and inner clusters (sizes straddling the leaf size): one launch per
+        // kind on pair lists, each sized by its own pairs
+        std::vector<int> lists[2];
+        int mr[2] = {0, 0}, mz[2] = {0, 0};
+        for (int p = p0; p < p0 + np; ++p) {
+            const int kind = X.child0[p] < 0 ? 0 : 1;
+            lists[kind].push_back(p);
+            mr[kind] = std::max(mr[kind], kind == 0 ? (int)T.size(C->bp_t[X.bp[p]]) : X.rank[X.child0[p]] + X.rank[X.child1[p]]);
+            mz[kind] = std::max(mz[kind], X.Z_rows[p]);
+        }
+        std::vector<int> both(lists[0]);
+        both.insert(both.end(), lists[1].begin(), lists[1].end());
+        CK(cudaStreamSynchronize(s));
+        C->d_plist.upload(both, s);
+        for (int kind = 0; kind < 2; ++kind) {
+            const int n = (int)lists[kind].size();
+            const TruncLaunch TL = plan_truncate(P, n, mr[kind], mz[kind], kind == 0, C->force_ws != 0);
+            if (TL.use_ws) {
+                const size_t need = (size_t)TL.grid * TL.ws_stride;
+                if (C->d_ws.n < need) {
+                    CK(cudaStreamSynchronize(s));
+                    C->d_ws.alloc(need);
+                }
+                ++C->ws_launches;
+            }
+            const int* pl = C->d_plist.p + (kind ? lists[0].size() : 0);
+            C->timed(cls, 1, [&] { launch_truncate(P, row, 0, n, TL, kind == 0, eps, mode, C->d_ws.p, s, pl); });
+        }
+    } else {
     const TruncLaunch TL = plan_truncate(P, np, maxrows, maxz, all_leaf, C->force_ws != 0);
     const bool split = C->split_trunc && all_leaf && maxrows <= 32 && !TL.use_ws;
-    const std::string cls = std::string(row ? "truncate_row@" : "truncate_col@") + std::to_string(l);
     if (split) {
         const size_t need = trunc_split_scratch_bytes(np);
         if (C->d_tscr.n < need) {
@@ -976,12 +1008,19 @@ void truncate_level(Shard* C, PassH& X, bool row, int l, int p0, int np, int max
         ++C->ws_launches;
     }
     if (!split) C->timed(cls, 1, [&] { launch_truncate(P, row, p0, np, TL, all_leaf, eps, mode, C->d_ws.p, s); });
+    }
     CK(cudaMemcpyAsync(X.rank.data() + p0, X.d_rank.p + p0, np * sizeof(int), cudaMemcpyDeviceToHost, s));
+    if ((int)C->sweeps_h.size() < np) C->sweeps_h.resize(np);
+    CK(cudaMemcpyAsync(C->sweeps_h.data(), X.d_sweeps.p + p0, np * sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     for (int p = p0; p < p0 + np; ++p)
         if (X.rank[p] < 0)
-            throw CudaError("non-finite singular values in the truncation of level " + std::to_string(l) + " (pair " +
-                            std::to_string(p) + "): non-finite input from an earlier phase");
+            throw NumericError("non-finite singular values in the truncation of level " + std::to_string(l) + " (pair " +
+                               std::to_string(p) + "): non-finite input from an earlier phase");
+    for (int i = 0; i < np; ++i)  // every Jacobi loop stops after 60 sweeps; reaching it means no convergence
+        if (C->sweeps_h[i] >= 60)
+            throw NumericError("one-sided Jacobi SVD did not converge in 60 sweeps (truncation of level " + std::to_string(l) +
+                               ", pair " + std::to_string(p0 + i) + ")");
     double fl = 0;
     for (int p = p0; p < p0 + np; ++p) {
         double rows = X.child0[p] < 0 ? (double)T.size(C->bp_t[X.bp[p]]) : X.rank[X.child0[p]] + X.rank[X.child1[p]];
@@ -1104,9 +1143,7 @@ void run_weights_truncate(Shard* C, double eps, int mode) {
             for (int p = p0; p < p0 + np; ++p)
                 if (X.child0[p] >= 0) maxrows = std::max(maxrows, X.rank[X.child0[p]] + X.rank[X.child1[p]]);
             bool all_leaf, any_leaf;
-            level_kind(l, all_leaf, any_leaf);
-            if (any_leaf && !all_leaf)  // median-split trees never mix leaves and inner clusters on a level
-                throw NotImpl("a tree level mixing leaf and non-leaf clusters is not supported by k_truncate");
+            level_kind(l, all_leaf, any_leaf);  // (mixed levels: one launch per kind, truncate_level)
             truncate_level(C, X, row, l, p0, np, maxrows, X.lev_max_zrows[l], all_leaf, fused[l] != 0, eps, mode);
         }
     }
@@ -1559,6 +1596,10 @@ int guarded(dh2_ctx* C, F&& f) {
         return fail(C, DH2_ENOTIMPL, e.what());
     } catch (const NoMem& e) {
         return fail(C, DH2_ENOMEM, e.what());
+    } catch (const NumericError& e) {
+        return fail(C, DH2_ENUMERIC, e.what());
+    } catch (const MismatchError& e) {
+        return fail(C, DH2_EMISMATCH, e.what());
     } catch (const std::bad_alloc& e) {
         return fail(C, DH2_ENOMEM, "host allocation failed");
     } catch (const std::exception& e) {
@@ -1742,6 +1783,30 @@ void finish_all(dh2_ctx* X) {
 
 void require_device(const dh2_ctx* X) { require_device(X->sh[0].get()); }
 
+uint64_t fnv1a(const void* data, size_t n, uint64_t h) {
+    const unsigned char* b = static_cast<const unsigned char*>(data);
+    for (size_t i = 0; i < n; ++i) {
+        h ^= b[i];
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+// DH2_EMISMATCH: the arguments' hash, min- and max-reduced over the ranks, must agree (NCCL mode;
+// the virtual mode runs every shard from the same call)
+void check_same_args(dh2_ctx* X, uint64_t h, const char* what) {
+    if (X->world == 1 || X->virt || !X->comm) return;
+    DevBuf<uint64_t> d;
+    d.alloc(2);
+    const uint64_t v[2] = {h, ~h};  // max of ~h = ~(min of h)
+    CK(cudaMemcpyAsync(d.p, v, sizeof(v), cudaMemcpyHostToDevice, X->stream));
+    NK(nccl().AllReduce(d.p, d.p, 2, ncclUint64, ncclMax, (ncclComm_t)X->comm, X->stream));
+    uint64_t r[2];
+    CK(cudaMemcpyAsync(r, d.p, sizeof(r), cudaMemcpyDeviceToHost, X->stream));
+    CK(cudaStreamSynchronize(X->stream));
+    if (r[0] != h || ~r[1] != h) throw MismatchError(std::string(what) + " differ between ranks");
+}
+
 void do_recompress(dh2_ctx* X, double eps, int mode) {
     if (X->sh.size() == 1 && X->sh[0]->lean.on && X->world == 1) {  // memory-lean chunked plan
         Shard* S = X->sh[0].get();
@@ -1883,6 +1948,8 @@ int dh2_build_interp(const dh2_mesh* mesh, const dh2_params* params, const dh2_d
             ncclUniqueId id;
             std::memcpy(&id, dist->nccl_uid, sizeof(id));
             ncclComm_t comm;
+            setenv("NCCL_DEBUG", "INFO", 0);  // communicator set-up in the log (rank count, transports), unless set
+            fprintf(stderr, "dh2: ncclCommInitRank rank %d of %d on device %d\n", X->rank, X->world, X->device);
             NK(api.CommInitRank(&comm, X->world, id, X->rank));
             X->comm = comm;
         }
@@ -1903,6 +1970,11 @@ int dh2_build_interp(const dh2_mesh* mesh, const dh2_params* params, const dh2_d
             run_setup(S.get());
         }
         finish_all(X.get());
+        // every rank must have passed the same mesh and parameters
+        uint64_t h = fnv1a(mesh->xyz, sizeof(double) * 3 * (size_t)mesh->nv, 1469598103934665603ull);
+        h = fnv1a(mesh->tri, sizeof(int64_t) * 3 * (size_t)mesh->nt, h);
+        const double pv[5] = {p.kappa, (double)p.m, (double)p.leaf_size, p.eta1, p.eta2};
+        check_same_args(X.get(), fnv1a(pv, sizeof(pv), h), "dh2_build_interp (mesh or parameters)");
     });
     if (rc != DH2_OK) return rc;
     *out = X.release();
@@ -1934,6 +2006,10 @@ int dh2_recompress(dh2_ctx* X, double eps, int32_t mode) {
             S->mode = mode;
         }
         X->exch_bytes = 0;
+        {
+            const double a[2] = {eps, (double)mode};
+            check_same_args(X, fnv1a(a, sizeof(a), 1469598103934665603ull), "dh2_recompress (eps or mode)");
+        }
         // a failure part-way leaves the factors inconsistent: RECOMP is unavailable until a
         // recompression completes
         for (auto& S : X->sh) S->recompressed = false;

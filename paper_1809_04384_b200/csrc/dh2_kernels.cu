@@ -701,22 +701,23 @@ __device__ inline void truncate_pair(const PlanD& P, const PassD& X, int p, doub
 
 template <bool LEAF>
 __global__ void __launch_bounds__(128, 5)
-    k_truncate(PlanD P, PassD X, int p0, int ldv, int ldb, bool append, double eps, int mode) {
+    k_truncate(PlanD P, PassD X, int p0, int ldv, int ldb, bool append, double eps, int mode, const int* plist) {
     extern __shared__ double2 smd[];
     __shared__ int flag, s_piv, s_rank;
     __shared__ double2 sh[2];
-    truncate_pair<LEAF>(P, X, p0 + blockIdx.x, smd, ldv, ldb, append, eps, mode, flag, s_piv, s_rank, sh);
+    const int p = plist ? plist[blockIdx.x] : p0 + blockIdx.x;
+    truncate_pair<LEAF>(P, X, p, smd, ldv, ldb, append, eps, mode, flag, s_piv, s_rank, sh);
 }
 
 template <bool LEAF>
 __global__ void __launch_bounds__(128, 4)
     k_truncate_ws(PlanD P, PassD X, int p0, int np, int ldv, int ldb, bool append, double eps, int mode, double2* ws,
-                  size_t ws_stride) {
+                  size_t ws_stride, const int* plist) {
     __shared__ int flag, s_piv, s_rank;
     __shared__ double2 sh[2];
     double2* base = ws + (size_t)blockIdx.x * ws_stride;
     for (int i = blockIdx.x; i < np; i += gridDim.x) {
-        truncate_pair<LEAF>(P, X, p0 + i, base, ldv, ldb, append, eps, mode, flag, s_piv, s_rank, sh);
+        truncate_pair<LEAF>(P, X, plist ? plist[i] : p0 + i, base, ldv, ldb, append, eps, mode, flag, s_piv, s_rank, sh);
         __syncthreads();
     }
 }
@@ -1049,18 +1050,18 @@ TruncLaunch plan_truncate(const PlanD& P, int np, int maxrowsM, int maxZrows, bo
 }
 
 void launch_truncate(const PlanD& P, bool row, int p0, int np, const TruncLaunch& L, bool leaf_level, double eps,
-                     int mode, double2* ws, cudaStream_t s) {
+                     int mode, double2* ws, cudaStream_t s, const int* plist) {
     if (!np) return;
     const PassD& X = row ? P.row : P.col;
     if (L.use_ws) {
         if (leaf_level)
-            k_truncate_ws<true><<<L.grid, 128, 0, s>>>(P, X, p0, np, L.ldv, L.ldb, L.append, eps, mode, ws, L.ws_stride);
+            k_truncate_ws<true><<<L.grid, 128, 0, s>>>(P, X, p0, np, L.ldv, L.ldb, L.append, eps, mode, ws, L.ws_stride, plist);
         else
-            k_truncate_ws<false><<<L.grid, 128, 0, s>>>(P, X, p0, np, L.ldv, L.ldb, L.append, eps, mode, ws, L.ws_stride);
+            k_truncate_ws<false><<<L.grid, 128, 0, s>>>(P, X, p0, np, L.ldv, L.ldb, L.append, eps, mode, ws, L.ws_stride, plist);
     } else if (leaf_level) {
-        k_truncate<true><<<np, 128, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, L.append, eps, mode);
+        k_truncate<true><<<np, 128, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, L.append, eps, mode, plist);
     } else {
-        k_truncate<false><<<np, 128, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, L.append, eps, mode);
+        k_truncate<false><<<np, 128, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, L.append, eps, mode, plist);
     }
 }
 

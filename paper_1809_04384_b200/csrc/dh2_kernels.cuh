@@ -108,8 +108,10 @@ struct TruncLaunch {
     size_t ws_stride = 0;     // workspace per CTA (double2 units); total grid * ws_stride
 };
 TruncLaunch plan_truncate(const PlanD& P, int np, int maxrowsM, int maxZrows, bool leaf_level, bool force_ws);
+// plist (optional): the pairs to truncate (np of them) instead of [p0, p0 + np) -- levels mixing
+// leaf and inner clusters are truncated in one launch per kind
 void launch_truncate(const PlanD& P, bool row, int p0, int np, const TruncLaunch& L, bool leaf_level, double eps,
-                     int mode, double2* ws, cudaStream_t s);
+                     int mode, double2* ws, cudaStream_t s, const int* plist = nullptr);
 // leaf levels with #t <= 32: pivoted QR per CTA, register-resident warp Jacobi, epilogue
 size_t trunc_split_scratch_bytes(int np);
 // fused: leaf total weights folded into the QR kernel (k_trunc_zqr, k <= 64; the level's Zhat is

@@ -513,7 +513,6 @@ void lean_chunk_weights_truncate(Shard* C, int g, double eps, int mode) {
             all_leaf = all_leaf && X.child0[p] < 0;
             any_leaf = any_leaf || X.child0[p] < 0;
         }
-        if (any_leaf && !all_leaf) throw NotImpl("a tree level mixing leaf and non-leaf clusters is not supported by k_truncate");
         int maxrows = 0, maxz = 0;
         int64_t cc = 0, qc = 0;
         for (int p = p0; p < p0 + np; ++p) {

@@ -2,6 +2,7 @@
 // error types, device buffers, per-pass host tables and the Shard itself.
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <map>
 #include <memory>
@@ -25,6 +26,12 @@ struct NotImpl : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
 struct NoMem : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct NumericError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct MismatchError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
 
@@ -266,6 +273,7 @@ struct Shard {
     std::vector<int64_t> blk_St_off;
     int64_t St_total = 0;
     PassH row, col;
+    std::vector<int> sweeps_h;  // Jacobi sweeps of the last truncated level (convergence check)
     LeanState lean;
     std::vector<int> lean_slot, lean_mirror;  // lean plan: S slot of each block in its chunk; chunk-local mirrors
     // device
@@ -276,7 +284,7 @@ struct Shard {
         d_blk_dir, d_blk_bprow, d_blk_bpcol, d_blk_prow, d_blk_pcol;
     std::vector<std::unique_ptr<DevBuf<int>>> d_lists;
     std::vector<const int*> d_leafV_list, d_basis_list, d_E_list, d_leafV_list_sym, d_basis_list_sym, d_E_list_sym;
-    DevBuf<int> d_blk_bpcs, d_blk_slot;
+    DevBuf<int> d_blk_bpcs, d_blk_slot, d_plist;
     DevBuf<double4> d_qp;
     DevBuf<GridD> d_grid;
     DevBuf<double2> d_VR, d_E, d_S, d_St, d_x, d_y, d_xp, d_yp, d_xh, d_yh;
@@ -313,6 +321,10 @@ struct Shard {
     bool debug_sync = std::getenv("DH2_DEBUG_SYNC") != nullptr;
     template <typename F>
     void timed(const std::string& cls, int nl, F&& f) {
+        struct Nvtx {  // one NVTX range per kernel class and level (visible to nsys / ncu --nvtx)
+            explicit Nvtx(const std::string& n) { nvtxRangePushA(n.c_str()); }
+            ~Nvtx() { nvtxRangePop(); }
+        } range(cls);
         if (profiling) {
             cudaEvent_t a = ev(), b = ev();
             CK(cudaEventRecord(a, stream));

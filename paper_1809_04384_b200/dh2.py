@@ -12,9 +12,10 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libdh2.so")
 
-DH2_OK, DH2_EINVAL, DH2_ENOMEM, DH2_ECUDA, DH2_ENCCL, DH2_ESTATE, DH2_EMISMATCH, DH2_ENOTIMPL = 0, -1, -2, -3, -4, -5, -6, -7
+DH2_OK, DH2_EINVAL, DH2_ENOMEM, DH2_ECUDA, DH2_ENCCL, DH2_ESTATE, DH2_EMISMATCH, DH2_ENOTIMPL, DH2_ENUMERIC = (
+    0, -1, -2, -3, -4, -5, -6, -7, -8)
 ERROR_NAMES = {-1: "DH2_EINVAL", -2: "DH2_ENOMEM", -3: "DH2_ECUDA", -4: "DH2_ENCCL", -5: "DH2_ESTATE",
-               -6: "DH2_EMISMATCH", -7: "DH2_ENOTIMPL"}
+               -6: "DH2_EMISMATCH", -7: "DH2_ENOTIMPL", -8: "DH2_ENUMERIC"}
 MODES = {"FROB_BLOCKREL": 0, "FROB_CLUSTERREL": 1, "SPEC_BLOCKREL": 2}
 DH2_ORIG, DH2_RECOMP = 0, 1
 DH2_HOST_PTRS, DH2_DEVICE_PTRS = 0, 1

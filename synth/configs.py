@@ -21,6 +21,16 @@ CONFIGS = {
     "P6": dict(mesh="cube", q=8, kappa=5.0, m=5, leaf=64, eta1=1.0, eta2=10.0, eps=1e-6),
     # three active levels of that shape: regression case of DESIGN reading N2 (numerically zero columns)
     "P7": dict(mesh="cube", q=16, kappa=14.0, m=5, leaf=64, eta1=1.0, eta2=10.0, eps=1e-6),
+    # an open sphere (every 37th triangle removed, n = 498) with leaf 15: tree levels mixing leaf and
+    # inner clusters (median splits of sizes that are no power-of-two multiple)
+    "P8": dict(mesh="sphere_cut", q=8, cut_every=37, cut_offset=5, kappa=4.0, m=3, leaf=15, eta1=1.0, eta2=10.0,
+               eps=1e-4),
+    # the PAPER's parameter setting (NEXT-3; eta1 = 10 for the directions, eta2 = 1 for
+    # admissibility, m = 4, leaf 32 in Table 3): many blocks per (t,c) (sigma up to 47 / 28), so Z^*
+    # stacks 1,000+ rows ("wide Z") -- P9 at desk scale (m = 3), P11 = the shape of Table 3's first
+    # row (sphere n = 8192, kappa = 16)
+    "P9": dict(mesh="sphere", q=16, kappa=4.0, m=3, leaf=16, eta1=10.0, eta2=1.0, eps=1e-4),
+    "P11": dict(mesh="sphere", q=32, kappa=16.0, m=4, leaf=32, eta1=10.0, eta2=1.0, eps=1e-4),
     # BASELINE.json configs
     "C1": dict(mesh="sphere", q=8, kappa=4.0, m=3, leaf=16, eta1=1.0, eta2=10.0, eps=1e-4),
     "C2": dict(mesh="sphere", q=32, kappa=16.0, m=4, leaf=32, eta1=1.0, eta2=10.0, eps=1e-4),

@@ -99,8 +99,18 @@ def cube_mesh(q):
     return np.array(pool.coords, dtype=np.float64), np.array(tris, dtype=np.int64)
 
 
+def cut_mesh(xyz, tri, every, offset):
+    """The mesh without the triangles i with i % every == offset (an open surface whose size is no
+    power-of-two multiple: median splits then leave clusters of sizes that straddle the leaf size,
+    so one tree level mixes leaf and inner clusters)."""
+    keep = np.arange(len(tri)) % every != offset
+    return xyz, np.ascontiguousarray(tri[keep])
+
+
 def mesh_for(cfg):
     """Mesh of a workload configuration (see synth.configs)."""
+    if cfg["mesh"] == "sphere_cut":
+        return cut_mesh(*sphere_mesh(cfg["q"]), cfg["cut_every"], cfg["cut_offset"])
     if cfg["mesh"] == "sphere":
         return sphere_mesh(cfg["q"])
     if cfg["mesh"] == "cube":

@@ -76,7 +76,7 @@ def _pairs(P):
     return np.array([(l, t, c) for l, lv in enumerate(P) for (t, c) in lv], dtype=np.int64).reshape(-1, 3)
 
 
-@pytest.mark.parametrize("name", ["P0", "P1", "P2", "P3", "C1", "C2"])
+@pytest.mark.parametrize("name", ["P0", "P1", "P2", "P3", "P8", "C1", "C2"])
 def test_structure_bit_identical_to_oracle(lib, name):
     cfg = get_config(name)
     h, xyz, tri = _structure_ctx(cfg)
@@ -113,7 +113,7 @@ def test_storage_orig_matches_oracle(lib):
         assert got[key] == ref[key], key
 
 
-@pytest.mark.parametrize("name", ["P0", "P1", "P2", "P3", "C1", "C2"])
+@pytest.mark.parametrize("name", ["P0", "P1", "P2", "P3", "P8", "C1", "C2"])
 def test_adjoint_symmetry_structure(name):
     """SURVEY NEXT-1 precondition, checked by the library on the host structure: every block
     has its antipodal mirror (s,t,-c) and every column pair (s,c) corresponds to the row pair

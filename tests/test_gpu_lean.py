@@ -72,7 +72,7 @@ def _st_blocks(h):
     return out
 
 
-@pytest.mark.parametrize("name,chunks", [("P1", 1), ("P1", 3), ("P2", 4), ("P4", 2), ("P6", 1), ("P7", 5), ("C1", 8),
+@pytest.mark.parametrize("name,chunks", [("P1", 1), ("P1", 3), ("P2", 4), ("P4", 2), ("P6", 1), ("P7", 5), ("P8", 3), ("C1", 8),
                                          ("C2", 1), ("C2", 16), ("C4s", 7)])
 def test_lean_bitwise_equal_to_full(name, chunks):
     hf, sf = _run(name, 0)

@@ -15,7 +15,7 @@ from conftest import oracle_run
 
 pytestmark = pytest.mark.gpu
 
-SMALL = ["P0", "P1", "P2", "P3", "P4", "P5", "P6", "P7", "C1"]
+SMALL = ["P0", "P1", "P2", "P3", "P4", "P5", "P6", "P7", "P8", "P9", "P11", "C1"]
 _GPU = {}
 
 

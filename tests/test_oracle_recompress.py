@@ -9,7 +9,7 @@ from oracle.recompress import select_rank, tail_sums
 
 from conftest import oracle_run
 
-CFGS = ["P0", "P1", "P3"]
+CFGS = ["P0", "P1", "P3", "P8", "P9"]
 
 
 def test_rank_rule_examples():
