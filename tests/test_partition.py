@@ -72,6 +72,13 @@ def test_virtual_partition(name, world):
             for b in range(world):
                 assert send[(kind, a, b)] == recv[(kind, b, a)]
     # independent recomputation of the items: blocks (t,s,c) with owner(t) != owner(s)
+    bp_neg = h.export("bp_neg", np.int32)
+    basis = h.export("basis_pairs", np.int64).reshape(-1, 3)
+    dirs, dir_off = h.export("dirs", np.float64).reshape(-1, 3), h.export("dir_off", np.int64)
+    for i in range(0, len(basis), 7):  # (t,-c) really is the antipodal direction
+        l, t, c = (int(v) for v in basis[i])
+        l2, t2, c2 = (int(v) for v in basis[bp_neg[i]])
+        assert (l2, t2) == (l, t) and np.array_equal(dirs[dir_off[l] + c2], -dirs[dir_off[l] + c])
     is_leaf = lambda t: not np.any((lev == lev[t] + 1) & (beg >= beg[t]) & (end <= end[t]))  # noqa: E731
     for a in range(world):
         for b in range(world):
@@ -79,7 +86,8 @@ def test_virtual_partition(name, world):
                 continue
             sel = blocks[(owner[blocks[:, 1]] == a) & (owner[blocks[:, 0]] == b)]
             xc = sorted({col_id[(int(s), int(c))] for t, s, c in sel})
-            xr = sorted({bp_id[(int(s), int(c))] for t, s, c in sel if not is_leaf(s) or end[s] - beg[s] > k})
+            # R of the row basis pair (s,-c): the column side is its conjugate (adjoint symmetry)
+            xr = sorted({int(bp_neg[bp_id[(int(s), int(c))]]) for t, s, c in sel if not is_leaf(s) or end[s] - beg[s] > k})
             assert send[("xC", a, b)] == xc
             assert send[("xR", a, b)] == xr
 
