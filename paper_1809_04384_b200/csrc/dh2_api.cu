@@ -686,7 +686,7 @@ void choose_plan(Shard* C) {
     const size_t need = plan_bytes(C);
     if (need + (size_t)256 * 1024 * 1024 <= freeb) return;
     const std::string full = "device memory plan needs " + std::to_string(need >> 20) + " MiB, free " + std::to_string(freeb >> 20) + " MiB";
-    if (!C->sym_ok || C->world > 1) throw NoMem(full + " (the memory-lean plan needs one shard and the adjoint symmetry)");
+    if (!C->sym_ok) throw NoMem(full + " (the memory-lean plan needs the adjoint symmetry)");
     const int ntop = (int)C->st.ct.levels[std::max(0, C->st.first_level)].size();
     for (int G = 1;; G *= 2) {  // (the estimate guesses the ranks: keep 15 % in reserve)
         lean_plan(C, G);
@@ -1808,15 +1808,30 @@ void check_same_args(dh2_ctx* X, uint64_t h, const char* what) {
 }
 
 void do_recompress(dh2_ctx* X, double eps, int mode) {
-    if (X->sh.size() == 1 && X->sh[0]->lean.on && X->world == 1) {  // memory-lean chunked plan
-        Shard* S = X->sh[0].get();
-        lean_recompress(S, eps, mode);
-        S->finish();
-        double v[3];
-        local_sums(S, v);
-        X->E_row = v[0];
-        X->E_col = v[1];
-        X->far2 = v[2];
+    if (X->sh[0]->lean.on) {  // memory-lean chunked plan (every shard of a context chooses alike)
+        for (auto& S : X->sh) lean_begin(S.get());
+        for (auto& S : X->sh) lean_basis(S.get());
+        exchange(X, X_R);  // R of the (s,-c) that other shards' blocks reference
+        for (auto& S : X->sh) lean_weights_truncate(S.get(), eps, mode);
+        exchange(X, X_RANK);
+        for (auto& S : X->sh) lean_columns(S.get());
+        // the compact C layout depends on the ranks: segment lists of X_C are rebuilt every time
+        for (auto it = X->segs.begin(); it != X->segs.end();)
+            it = std::get<0>(it->first) == (int)X_C ? X->segs.erase(it) : std::next(it);
+        exchange(X, X_C);
+        for (auto& S : X->sh) lean_project(S.get());
+        finish_all(X);
+        std::vector<double> sums(3, 0.0);
+        for (auto& S : X->sh) {
+            double v[3];
+            local_sums(S.get(), v);
+            for (int i = 0; i < 3; ++i) sums[i] += v[i];
+            lean_finish(S.get());
+        }
+        reduce_doubles(X, sums, false);
+        X->E_row = sums[0];
+        X->E_col = sums[1];
+        X->far2 = sums[2];
         return;
     }
     for (auto& S : X->sh) {
@@ -2113,11 +2128,12 @@ int dh2_set_option(dh2_ctx* X, const char* name, int64_t value) {
     if (nm == "lean_chunks") {  // > 0: re-lay the context out on the memory-lean chunked plan with that many chunks
         if (value < 1 || value > (1 << 20)) return fail(X, DH2_EINVAL, "lean_chunks must be >= 1");
         return guarded(X, [&] {
-            if (X->sh.size() != 1 || X->world != 1) throw NotImpl("the memory-lean plan runs on one shard");
-            Shard* S = X->sh[0].get();
+            if (X->world > 1 && !X->virt) throw NotImpl("lean_chunks on an NCCL context: the planner chooses per rank");
+            for (auto& Sp : X->sh) {
+            Shard* S = Sp.get();
             if (S->device == DH2_DEVICE_NONE) {  // structure-only context: the host plan alone (tests)
                 lean_plan(S, (int)value);
-                return;
+                continue;
             }
             if (!S->sym_ok || !S->sym_opt) throw NotImpl("the memory-lean plan needs adjoint_symmetry = 1");
             CK(cudaSetDevice(S->device));
@@ -2137,6 +2153,8 @@ int dh2_set_option(dh2_ctx* X, const char* name, int64_t value) {
             run_setup(S);
             S->finish();
             S->recompressed = false;
+            }
+            X->segs.clear();  // exchange segments refer to the previous layout
             X->recompressed = false;
         });
     }

@@ -545,6 +545,11 @@ __device__ inline int jacobi_rows_t(double2* R, int ldr, int nv, int len, double
         }
         if (tid == 0) *flag = 0;
         __syncthreads();
+        // absolute floor of the convergence test (DESIGN reading N3): |a_p^* a_q| <= 1e-28 sigma_1^2
+        // counts as orthogonal -- it moves no singular value >= 1e-14 sigma_1 by more than 3e-13 sigma_1
+        double mx = 0.0;
+        for (int p = 0; p < nv; ++p) mx = fmax(mx, nrm[p]);
+        const double floor2 = 1e-56 * mx * mx;
         for (int r = 0; r < nr; ++r) {
             for (int pi = gid; pi < np / 2; pi += ng) {
                 const int i1 = np - 1 - pi;
@@ -573,7 +578,7 @@ __device__ inline int jacobi_rows_t(double2* R, int ldr, int nv, int len, double
                 }
                 const double al = nrm[p], be = nrm[q];
                 const double g2 = cabs2(ga);
-                if (g2 > tol2 * (al * be) && al > 0.0 && be > 0.0) {
+                if (g2 > fmax(tol2 * (al * be), floor2) && al > 0.0 && be > 0.0) {
                     // rotation by the smaller angle theta with tan(2 theta) = 2|g|/(be - al), from
                     // two dependent rsqrt only: with d = be - al, r = sqrt(d^2 + 4|g|^2),
                     // c^2 = (1 + |d|/r)/2 and t = tan(theta) = sign(d) |g| / (r c^2)

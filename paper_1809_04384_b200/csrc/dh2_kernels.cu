@@ -360,6 +360,11 @@ void launch_basis(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStr
     if (P.k <= 64) {  // 64-row chunks, packed triangle
         const int ldb = odd_ld(64);
         k_basis<true, 4><<<nbps, 256, qr_chunk_smem(P, true, ldr, ldb, 6, any_qr), s>>>(P, bps, ldr, ldb);
+    } else if (!P.qr_wy && qr_chunk_smem(P, true, ldr, odd_ld(48), 6, any_qr) <= (size_t)P.smem_optin) {
+        // k = 125: 48-row chunks beside the packed triangle (224 KB): 6 instead of 8 appends of k
+        // reflector steps for a 250-row stack
+        const int ldb = odd_ld(48);
+        k_basis<true, 3><<<nbps, 512, qr_chunk_smem(P, true, ldr, ldb, 6, any_qr), s>>>(P, bps, ldr, ldb);
     } else {
         const int ldb = odd_ld(32);
         k_basis<true, 2><<<nbps, 512, qr_chunk_smem(P, true, ldr, ldb, 6, any_qr), s>>>(P, bps, ldr, ldb);
@@ -514,6 +519,9 @@ void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* m
     if (P.k <= 64) {  // 64-row chunks, packed triangle
         const int ldb = odd_ld(64);
         k_total_weights<true, 4><<<np, 256, qr_chunk_smem(P, true, ldr, ldb, 3), s>>>(P, X, row, p0, mirror, ldr, ldb);
+    } else if (!P.qr_wy && qr_chunk_smem(P, true, ldr, odd_ld(48), 3) <= (size_t)P.smem_optin) {
+        const int ldb = odd_ld(48);  // 48-row chunks (see launch_basis)
+        k_total_weights<true, 3><<<np, 512, qr_chunk_smem(P, true, ldr, ldb, 3), s>>>(P, X, row, p0, mirror, ldr, ldb);
     } else {
         const int ldb = odd_ld(32);
         k_total_weights<true, 2><<<np, 512, qr_chunk_smem(P, true, ldr, ldb, 3), s>>>(P, X, row, p0, mirror, ldr, ldb);
@@ -916,6 +924,11 @@ __global__ void __launch_bounds__(128, 3) k_jacobi_w32(PassD X, int p0, int np, 
     for (; sweep < 60 && ncol > 1; ++sweep) {
         nr = norms();
         bool any = false;
+        // absolute floor of the convergence test (DESIGN reading N3), as jacobi_rows_t
+        double mx = nr;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+        const double floor2 = 1e-56 * mx * mx;
 #pragma unroll 1
         for (int round = 0; round < 31; ++round) {
             // a conj(b) of the slot pairs (2q, 2q+1), this lane's element; pairs 0-7 and 8-15 are
@@ -941,7 +954,7 @@ __global__ void __launch_bounds__(128, 3) k_jacobi_w32(PassD X, int p0, int np, 
             const double g2 = cabs2(ga);
             double c = 1.0, sn = 0.0;
             double2 ec = cmk(1.0, 0.0);
-            if (g2 > tol2 * (al * be) && al > 0.0 && be > 0.0) {  // as jacobi_rows_t
+            if (g2 > fmax(tol2 * (al * be), floor2) && al > 0.0 && be > 0.0) {  // as jacobi_rows_t
                 const double ig = rsqrt(g2);
                 const double gm = g2 * ig;
                 const double dd = be - al;
@@ -1348,6 +1361,7 @@ cudaError_t configure_kernels() {
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     const void* ks[] = {(const void*)k_leafV<0>, (const void*)k_leafV<2>, (const void*)k_leafV<3>, (const void*)k_leafV<4>,
                         (const void*)k_leafV<5>, (const void*)k_basis<true, 4>, (const void*)k_basis<true, 2>,
+                        (const void*)k_basis<true, 3>, (const void*)k_total_weights<true, 3>,
                         (const void*)k_block_weights, (const void*)k_total_weights<true, 4>, (const void*)k_total_weights<true, 2>, (const void*)k_truncate<true>, (const void*)k_truncate<false>, (const void*)k_trunc_qr, (const void*)k_trunc_zqr,
                         (const void*)k_project};
     for (const void* f : ks) {

@@ -220,10 +220,14 @@ void lean_plan(Shard* C, int G) {
         Ln.keep[C->blk_bprow[b]] = 1;
         Ln.keep[C->blk_bpcs[b]] = 1;
         Ln.keepC[C->blk_prow[b]] = 1;
-        Ln.keepC[C->col2row[C->blk_pcol[b]]] = 1;
+        if (C->owner[C->blk_s[b]] == me) Ln.keepC[C->col2row[C->blk_pcol[b]]] = 1;
     }
-    for (int b = C->b_lo; b < C->b_hi; ++b)
-        if (C->owner[C->blk_s[b]] != me) throw NotImpl("lean plan with blocks across shards is not implemented");
+    // the own row pairs that other shards' blocks reference through their column side: C exported
+    for (int peer = 0; peer < C->world; ++peer)
+        for (int p : C->C_send[peer]) Ln.keepC[C->col2row[p]] = 1;
+    // (s,-c) of a block whose column cluster another shard owns: imported after phase b (R by QR,
+    // exchange X_R) or regenerated here (leaf with #s <= k: R = V); its C' is imported after the
+    // truncation into a slot of the C pool (lean_columns)
     auto r_by_qr = [&](int id) { return !T.is_leaf(C->bp_t[id]) || T.size(C->bp_t[id]) > k; };
     // VR layout: persistent slabs first, then per-chunk scratch (same offsets reused by every chunk)
     std::fill(C->bp_V_off.begin(), C->bp_V_off.end(), -1);
@@ -241,6 +245,9 @@ void lean_plan(Shard* C, int G) {
         }
     }
     Ln.VR_persist = off;
+    Ln.lvi.clear();
+    for (int id = 0; id < nbp; ++id)
+        if (Ln.keep[id] && !C->bp_own[id] && !r_by_qr(id)) Ln.lvi.push_back(id);
     Ln.qr_ptr.assign((size_t)G * (L + 1) + 1, 0);
     Ln.lvb_ptr.assign((size_t)G * (L + 1) + 1, 0);
     Ln.lvd_ptr.assign((size_t)G * (L + 1) + 1, 0);
@@ -409,6 +416,8 @@ void lean_basis(Shard* C) {
     cudaStream_t s = C->stream;
     const ClusterTree& T = C->st.ct;
     const int L = T.depth, k = C->k, m = C->m;
+    if (!Ln.lvi.empty())  // (s,-c) of other shards with R = V: regenerated from the replicated mesh
+        C->timed("setup_leafV", 1, [&] { launch_leafV(P, Ln.d_lvi.p, (int)Ln.lvi.size(), C->max_leaf, s); });
     for (int g = 0; g < Ln.G; ++g) {
         for (int l = L; l >= Ln.l0; --l) {
             const int gl = gl_of(C, g, l);
@@ -578,13 +587,25 @@ void lean_alias_columns(Shard* C) {
     cudaStream_t s = C->stream;
     const int np = (int)X.bp.size();
     std::vector<int> kb(np, 0), rowsb(np, 0);
+    std::vector<char> own(np, 0);
+    for (int l = 0; l < (int)X.own_lo.size(); ++l)
+        for (int p = X.own_lo[l]; p < X.own_hi[l]; ++p) own[p] = 1;
     for (int p = 0; p < np; ++p) {
         const int q = C->col2row[p];
-        X.C_off[p] = Ln.C_off_cur[q];
-        X.Q_off[p] = Ln.Q_off_cur[q];
-        kb[p] = Ln.kb_cur[q];
-        rowsb[p] = Ln.rowsb_cur[q];
+        X.C_off[p] = own[p] ? Ln.C_off_cur[q] : -1;
+        X.Q_off[p] = own[p] ? Ln.Q_off_cur[q] : -1;
+        kb[p] = own[p] ? Ln.kb_cur[q] : 0;
+        rowsb[p] = own[p] ? Ln.rowsb_cur[q] : 0;
     }
+    // C' of column pairs owned by other shards: compact slots (rank x k, ld rank) after the
+    // persistent C, filled by the exchange X_C (ranks imported by X_RANK)
+    for (int peer = 0; peer < C->world; ++peer)
+        for (int p : C->C_recv[peer]) {
+            X.C_off[p] = Ln.C_used;
+            kb[p] = X.rank[p];
+            Ln.C_used += (int64_t)X.rank[p] * C->k;
+        }
+    Ln.Cpool.ensure(0, (size_t)Ln.C_used * sizeof(double2));
     X.d_C_off.upload(X.C_off, s);
     X.d_Q_off.upload(X.Q_off, s);
     X.d_kb.upload(kb, s);
@@ -660,6 +681,7 @@ void lean_alloc(Shard* C) {
     Ln.d_qr.upload(Ln.qr, s);
     Ln.d_lvb.upload(Ln.lvb, s);
     Ln.d_lvd.upload(Ln.lvd, s);
+    Ln.d_lvi.upload(Ln.lvi, s);
     Ln.d_mirror.upload(C->lean_mirror, s);
     C->d_blk_slot.upload(C->lean_slot, s);
     P.blk_slot = C->d_blk_slot.p;
@@ -668,10 +690,12 @@ void lean_alloc(Shard* C) {
     CK(cudaStreamSynchronize(s));
 }
 
-void lean_recompress(Shard* C, double eps, int mode) {
+// Phases of the lean recompression; the context runs them shard by shard with the exchanges of
+// SURVEY §8(e) in between (dh2_api.cu do_recompress): lean_begin, lean_basis [X_R],
+// lean_weights_truncate [X_RANK], lean_columns [X_C], lean_project.
+void lean_begin(Shard* C) {
     LeanState& Ln = C->lean;
     PassH& X = C->row;
-    const int L = C->st.ct.depth;
     if (!(C->sym_ok && C->sym_opt)) throw NotImpl("the memory-lean plan needs adjoint_symmetry = 1");
     C->P.sym = 1;
     C->sym_used = true;
@@ -684,7 +708,12 @@ void lean_recompress(Shard* C, double eps, int mode) {
     // the Zhat offsets are the chunk-relative lean ones
     X.d_Z_off.upload(X.Z_off, C->stream);
     C->P.row.Z_off = X.d_Z_off.p;
-    lean_basis(C);
+}
+
+void lean_weights_truncate(Shard* C, double eps, int mode) {
+    LeanState& Ln = C->lean;
+    PassH& X = C->row;
+    const int L = C->st.ct.depth;
     X.rank.assign(X.bp.size(), 0);
     for (int g = 0; g < Ln.G; ++g) lean_chunk_weights_truncate(C, g, eps, mode);
     // column pass by the adjoint symmetry (ranks mirrored; factors read conjugated)
@@ -696,11 +725,24 @@ void lean_recompress(Shard* C, double eps, int mode) {
         C->timed("mirror_col", 1, [&] { launch_mirror_pass(C->P, C->d_col2row.p, p0, np, C->stream); });
         for (int p = p0; p < p0 + np; ++p) Y.rank[p] = X.rank[C->col2row[p]];
     }
+}
+
+void lean_columns(Shard* C) {
+    PassH& Y = C->col;
+    if (C->world > 1) {  // ranks of the imported column pairs (X_RANK) for their C' slots
+        CK(cudaStreamSynchronize(C->stream));
+        std::vector<int> all(Y.bp.size());
+        CK(cudaMemcpy(all.data(), Y.d_rank.p, all.size() * sizeof(int), cudaMemcpyDeviceToHost));
+        for (int peer = 0; peer < C->world; ++peer)
+            for (int p : C->C_recv[peer]) Y.rank[p] = all[p];
+    }
     lean_alias_columns(C);
-    lean_project(C);
+}
+
+void lean_finish(Shard* C) {
     size_t freeb = 0, totb = 0;
     cudaMemGetInfo(&freeb, &totb);
-    Ln.peak_bytes = std::max(Ln.peak_bytes, (double)(totb - freeb));
+    C->lean.peak_bytes = std::max(C->lean.peak_bytes, (double)(totb - freeb));
 }
 
 }  // namespace dh2

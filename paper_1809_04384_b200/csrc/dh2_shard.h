@@ -168,6 +168,7 @@ struct LeanState {
     std::vector<int> qr_ptr, qr;        // per (g,l): row basis pairs weighted by QR (phase b)
     std::vector<int> lvb_ptr, lvb;      // per (g,l): row leaf pairs whose V phase b needs
     std::vector<int> lvd_ptr, lvd;      // per (g,l): row leaf pairs whose V is regenerated for the truncation
+    std::vector<int> lvi;               // (s,-c) of other shards with R = V: regenerated from the mesh
     std::vector<char> keep;             // per basis pair: R (or V = R) persists after phase b
     std::vector<char> keepC;            // per row pair: C persists (projection)
     int64_t VR_persist = 0, VR_scratch = 0, E_total = 0, Z_scratch = 0, S_slots = 0;  // double2 units / slots
@@ -176,7 +177,7 @@ struct LeanState {
     std::vector<int64_t> C_off_cur, Q_off_cur;
     int64_t C_used = 0, Q_used = 0;     // persistent compact bytes in use (double2 units)
     VaPool Cpool, Qpool;                // C: regions 0 persistent, 1 bound scratch, 2/3 compact scratch; Q: 0, 1
-    DevBuf<int> d_blk, d_qr, d_lvb, d_lvd, d_mirror;
+    DevBuf<int> d_blk, d_qr, d_lvb, d_lvd, d_lvi, d_mirror;
     DevBuf<double2> d_Zs, d_Ss;
     DevBuf<int64_t> d_soff, d_doff;
     DevBuf<int> d_rows, d_cols, d_lds;
@@ -186,7 +187,8 @@ struct LeanState {
     void clear_plan() {
         on = false;
         G = l0 = 0;
-        for (auto* v : {&p_lo, &p_hi, &blk_ptr, &blk, &qr_ptr, &qr, &lvb_ptr, &lvb, &lvd_ptr, &lvd, &kb_cur, &rowsb_cur}) v->clear();
+        for (auto* v : {&p_lo, &p_hi, &blk_ptr, &blk, &qr_ptr, &qr, &lvb_ptr, &lvb, &lvd_ptr, &lvd, &lvi, &kb_cur, &rowsb_cur})
+            v->clear();
         keep.clear();
         keepC.clear();
         E_off.clear();
@@ -361,6 +363,11 @@ void truncate_level(Shard* C, PassH& X, bool row, int l, int p0, int np, int max
 void lean_plan(Shard* C, int G);
 double lean_bytes(const Shard* C);
 void lean_alloc(Shard* C);
-void lean_recompress(Shard* C, double eps, int mode);
+void lean_begin(Shard* C);
+void lean_basis(Shard* C);
+void lean_weights_truncate(Shard* C, double eps, int mode);
+void lean_columns(Shard* C);
+void lean_project(Shard* C);
+void lean_finish(Shard* C);
 
 }  // namespace dh2

@@ -124,3 +124,26 @@ def test_lean_state_errors():
         h.matvec(x, 0)  # ORIG needs V and S resident
     with pytest.raises(DH2Error):
         h.set_option("adjoint_symmetry", 0)
+
+
+@pytest.mark.parametrize("name,world,chunks", [("P2", 2, 3), ("P4", 2, 2), ("C1", 4, 2), ("C2", 4, 3), ("C4s", 2, 5)])
+def test_lean_sharded_bitwise_equal_to_full(name, world, chunks):
+    """The lean plan on every shard of the subtree partition (virtual mode: the shards run on this GPU
+    with device-to-device exchanges of R (s,-c), ranks and compact C'): the same matrix, bitwise."""
+    from paper_1809_04384_b200 import DH2
+    hf, sf = _run(name, 0)
+    cfg = get_config(name)
+    xyz, tri = mesh_for(cfg)
+    h = DH2(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"], world=world)
+    h.set_option("lean_chunks", chunks)
+    h.recompress(cfg["eps"])
+    s = h.stats()
+    assert s["lean"]["on"] and s["shards_here"] == world and s["exchange_bytes"] > 0
+    for key in ("E_row", "E_col", "far2"):
+        assert s[key] == pytest.approx(sf[key], rel=1e-14), key
+    assert np.array_equal(h.export("rank_row", np.int32), hf.export("rank_row", np.int32))
+    for seed in (1, 2):
+        x = seeded_vector(hf.n, seed)
+        assert np.array_equal(h.matvec(x, 1), hf.matvec(x, 1))
+    assert h.storage(1) == hf.storage(1)
+    h.close()

@@ -30,7 +30,10 @@ x = seeded_vector(h.n, 1)
 y = h.matvec(x, 1)
 t4 = time.time()
 s = h.stats()
+sw = h.export("sweeps_row", np.int32)
+lp = h.export("lev_ptr_row", np.int32)
+sweeps = {int(l): np.bincount(sw[lp[l]:lp[l + 1]]).tolist() for l in range(len(lp) - 1) if lp[l + 1] > lp[l]}
 ks = {k: round(v["ms"], 1) for k, v in sorted(s["kernels"].items(), key=lambda kv: -kv[1]["ms"])[:25]}
 print(json.dumps({"config": name, "build_s": t1 - t0, "matvec_s": t4 - t3, "lean": s["lean"], "device_bytes": s["device_bytes"],
                   "storage": h.storage(1), "E_row": s["E_row"], "far2": s["far2"], "ynorm": float(np.linalg.norm(y)),
-                  "kernels_ms_2runs": ks}), flush=True)
+                  "kernels_ms_2runs": ks, "jacobi_sweeps_hist_per_level": sweeps}), flush=True)
