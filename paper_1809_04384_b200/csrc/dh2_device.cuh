@@ -551,59 +551,81 @@ __device__ inline int jacobi_rows_t(double2* R, int ldr, int nv, int len, double
         for (int p = 0; p < nv; ++p) mx = fmax(mx, nrm[p]);
         const double floor2 = 1e-56 * mx * mx;
         for (int r = 0; r < nr; ++r) {
-            for (int pi = gid; pi < np / 2; pi += ng) {
-                const int i1 = np - 1 - pi;
-                int p = 0, q;
-                if (pi != 0) { p = pi - 1 + r; if (p >= nr) p -= nr; ++p; }
-                q = i1 - 1 + r; if (q >= nr) q -= nr; ++q;
-                if (p >= nv || q >= nv) continue;
-                double2* rp = R + p + gl * ldr;
-                double2* rq = R + q + gl * ldr;
-                double2 a[E], b[E];
-                double2 ga = cmk(0.0, 0.0);
+            // two pairs per iteration: independent dot products / rotations in flight
+            for (int pi0 = gid; pi0 < np / 2; pi0 += 2 * ng) {
+                int pp[2], qq[2];
+                bool act[2];
 #pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    if (gl + G * e < len) {
-                        a[e] = rp[e * st];
-                        b[e] = rq[e * st];
-                    } else {
-                        a[e] = cmk(0.0, 0.0);
-                        b[e] = cmk(0.0, 0.0);
-                    }
-                    cfma_bj(ga, a[e], b[e]);
+                for (int h = 0; h < 2; ++h) {
+                    const int pi = pi0 + h * ng;
+                    act[h] = pi < np / 2;
+                    const int i1 = np - 1 - pi;
+                    int p = 0, q;
+                    if (pi != 0) { p = pi - 1 + r; if (p >= nr) p -= nr; ++p; }
+                    q = i1 - 1 + r; if (q >= nr) q -= nr; ++q;
+                    act[h] = act[h] && p < nv && q < nv;
+                    pp[h] = act[h] ? p : 0;
+                    qq[h] = act[h] ? q : 0;
                 }
-                for (int o = G >> 1; o > 0; o >>= 1) {
-                    ga.x += __shfl_xor_sync(mask, ga.x, o);
-                    ga.y += __shfl_xor_sync(mask, ga.y, o);
-                }
-                const double al = nrm[p], be = nrm[q];
-                const double g2 = cabs2(ga);
-                if (g2 > fmax(tol2 * (al * be), floor2) && al > 0.0 && be > 0.0) {
-                    // rotation by the smaller angle theta with tan(2 theta) = 2|g|/(be - al), from
-                    // two dependent rsqrt only: with d = be - al, r = sqrt(d^2 + 4|g|^2),
-                    // c^2 = (1 + |d|/r)/2 and t = tan(theta) = sign(d) |g| / (r c^2)
-                    const double ig = rsqrt(g2);  // 1/|g| (independent chain)
-                    const double gm = g2 * ig;
-                    const double d = be - al;
-                    const double ir = rsqrt(fma(d, d, 4.0 * g2));
-                    const double c2 = fma(0.5 * fabs(d), ir, 0.5);
-                    const double ic = rsqrt(c2);
-                    const double c = c2 * ic;
-                    const double t = (d >= 0.0 ? gm : -gm) * ir * (ic * ic);
-                    const double sn = t * c;
-                    const double2 ec = cmk(ga.x * ig, ga.y * ig);
+                double2 a[2][E], b[2][E];
+                double2 ga[2] = {cmk(0.0, 0.0), cmk(0.0, 0.0)};
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const double2* rp = R + pp[h] + gl * ldr;
+                    const double2* rq = R + qq[h] + gl * ldr;
 #pragma unroll
                     for (int e = 0; e < E; ++e) {
-                        if (gl + G * e < len) {
-                            const double2 bb = cmul(ec, b[e]);
-                            rp[e * st] = cmk(c * a[e].x - sn * bb.x, c * a[e].y - sn * bb.y);
-                            rq[e * st] = cmk(sn * a[e].x + c * bb.x, sn * a[e].y + c * bb.y);
+                        if (act[h] && gl + G * e < len) {
+                            a[h][e] = rp[e * st];
+                            b[h][e] = rq[e * st];
+                        } else {
+                            a[h][e] = cmk(0.0, 0.0);
+                            b[h][e] = cmk(0.0, 0.0);
                         }
+                        cfma_bj(ga[h], a[h][e], b[h][e]);
                     }
-                    if (gl == 0) {
-                        nrm[p] = al - t * gm;
-                        nrm[q] = be + t * gm;
-                        *flag = 1;
+                }
+                for (int o = G >> 1; o > 0; o >>= 1) {
+                    ga[0].x += __shfl_xor_sync(mask, ga[0].x, o);
+                    ga[0].y += __shfl_xor_sync(mask, ga[0].y, o);
+                    ga[1].x += __shfl_xor_sync(mask, ga[1].x, o);
+                    ga[1].y += __shfl_xor_sync(mask, ga[1].y, o);
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (!act[h]) continue;
+                    const int p = pp[h], q = qq[h];
+                    const double al = nrm[p], be = nrm[q];
+                    const double g2 = cabs2(ga[h]);
+                    if (g2 > fmax(tol2 * (al * be), floor2) && al > 0.0 && be > 0.0) {
+                        // rotation by the smaller angle theta with tan(2 theta) = 2|g|/(be - al), from
+                        // two dependent rsqrt only: with d = be - al, r = sqrt(d^2 + 4|g|^2),
+                        // c^2 = (1 + |d|/r)/2 and t = tan(theta) = sign(d) |g| / (r c^2)
+                        const double ig = rsqrt(g2);  // 1/|g| (independent chain)
+                        const double gm = g2 * ig;
+                        const double d = be - al;
+                        const double ir = rsqrt(fma(d, d, 4.0 * g2));
+                        const double c2 = fma(0.5 * fabs(d), ir, 0.5);
+                        const double ic = rsqrt(c2);
+                        const double c = c2 * ic;
+                        const double t = (d >= 0.0 ? gm : -gm) * ir * (ic * ic);
+                        const double sn = t * c;
+                        const double2 ec = cmk(ga[h].x * ig, ga[h].y * ig);
+                        double2* rp = R + p + gl * ldr;
+                        double2* rq = R + q + gl * ldr;
+#pragma unroll
+                        for (int e = 0; e < E; ++e) {
+                            if (gl + G * e < len) {
+                                const double2 bb = cmul(ec, b[h][e]);
+                                rp[e * st] = cmk(c * a[h][e].x - sn * bb.x, c * a[h][e].y - sn * bb.y);
+                                rq[e * st] = cmk(sn * a[h][e].x + c * bb.x, sn * a[h][e].y + c * bb.y);
+                            }
+                        }
+                        if (gl == 0) {
+                            nrm[p] = al - t * gm;
+                            nrm[q] = be + t * gm;
+                            *flag = 1;
+                        }
                     }
                 }
             }
@@ -1033,24 +1055,39 @@ __host__ __device__ inline size_t r_elems(int k, int ldr) {
 // Annihilate the nb x k chunk B (nb <= 16 E) into the k x k upper-triangular smem factor R:
 // [R; B] = Q [R'; 0] by k structured Householder reflections, each touching row j of R and the
 // nb rows of B only (the rows of R below j are zero in column j).  Lane groups of 16 own one
-// column at a time, E rows of B per lane (rows gl + 16 e) plus row j of R on lane 0.  One
-// barrier per reflection: every warp forms the reflector itself; the new diagonal beta_j is
-// stored one step later (nobody reads R[j, j] during step j+1).
+// column at a time, E rows of B per lane (rows gl + 16 e) plus row j of R on lane 0, two columns
+// per iteration (independent reductions in flight).  One barrier per reflection: every warp forms
+// the reflector itself from ||B(:, j)||^2, which group 0 -- it updates column j during step j-1 --
+// publishes in shared memory (look-ahead: no reduction over B on the critical path); the new
+// diagonal beta_j is stored one step later (nobody reads R[j, j] during step j+1).
 template <bool PK, int E>
 __device__ inline void cta_qr_append(double2* R, int ldr, double2* B, int ldb, int nb, int k) {
     constexpr int G = 16;
+    __shared__ double s_col[2];  // ||B(:, j)||^2 of the next reflection (double-buffered by step parity)
     const int tid = threadIdx.x, lane = tid & 31;
     const int gl = tid & (G - 1), gid = tid / G, ng = blockDim.x / G;
     const unsigned mask = 0xffffu << (lane & 16);
+    __syncthreads();
+    auto col_norm = [&](int c) {  // 16-lane reduction of ||B(:, c)||^2 (group-uniform result)
+        double v = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+            if (gl + G * e < nb) v += cabs2(B[(size_t)c * ldb + gl + G * e]);
+#pragma unroll
+        for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
+        return v;
+    };
+    if (gid == 0 && k > 0) {
+        const double v = col_norm(0);
+        if (gl == 0) s_col[0] = v;
+    }
     __syncthreads();
     int prev = -1;
     double2 prev_beta = cmk(0.0, 0.0);
     for (int j = 0; j < k; ++j) {
         if (tid == 0 && prev >= 0) R[ridx<PK>(prev, prev, ldr)] = prev_beta;
         const double2* bj = B + j * ldb;
-        double s = 0.0;
-        for (int i = lane; i < nb; i += 32) s += cabs2(bj[i]);
-        s = warp_sum(s);
+        const double s = s_col[j & 1];
         const double2 alpha = R[ridx<PK>(j, j, ldr)];
         double tau = 0.0;
         double2 beta = alpha, u0 = cmk(0.0, 0.0);
@@ -1066,31 +1103,61 @@ __device__ inline void cta_qr_append(double2* R, int ldr, double2* B, int ldb, i
             double2 u[E];
 #pragma unroll
             for (int e = 0; e < E; ++e) u[e] = (gl + G * e < nb) ? bj[gl + G * e] : cmk(0.0, 0.0);
-            for (int c = j + 1 + gid; c < k; c += ng) {
+            for (int c = j + 1 + gid; c < k; c += 2 * ng) {
+                const int c2 = c + ng;
+                const bool two = c2 < k;
                 double2* bc = B + c * ldb;
-                double2 x[E];
-                double2 rj = cmk(0.0, 0.0);
-                double2 w = cmk(0.0, 0.0);
+                double2* bc2 = B + c2 * ldb;
+                double2 x[E], x2[E];
+                double2 rj = cmk(0.0, 0.0), rj2 = cmk(0.0, 0.0);
+                double2 w = cmk(0.0, 0.0), w2 = cmk(0.0, 0.0);
                 if (gl == 0) {
                     rj = R[ridx<PK>(j, c, ldr)];
                     cfma_cj(w, u0, rj);
+                    if (two) {
+                        rj2 = R[ridx<PK>(j, c2, ldr)];
+                        cfma_cj(w2, u0, rj2);
+                    }
                 }
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
-                    x[e] = (gl + G * e < nb) ? bc[gl + G * e] : cmk(0.0, 0.0);
+                    const bool ok = gl + G * e < nb;
+                    x[e] = ok ? bc[gl + G * e] : cmk(0.0, 0.0);
+                    x2[e] = (ok && two) ? bc2[gl + G * e] : cmk(0.0, 0.0);
                     cfma_cj(w, u[e], x[e]);
+                    cfma_cj(w2, u[e], x2[e]);
                 }
 #pragma unroll
                 for (int o = G >> 1; o > 0; o >>= 1) {
                     w.x += __shfl_xor_sync(mask, w.x, o);
                     w.y += __shfl_xor_sync(mask, w.y, o);
+                    w2.x += __shfl_xor_sync(mask, w2.x, o);
+                    w2.y += __shfl_xor_sync(mask, w2.y, o);
                 }
                 w = cscale(w, tau);
-                if (gl == 0) R[ridx<PK>(j, c, ldr)] = csub(rj, cmul(u0, w));
+                w2 = cscale(w2, tau);
+                if (gl == 0) {
+                    R[ridx<PK>(j, c, ldr)] = csub(rj, cmul(u0, w));
+                    if (two) R[ridx<PK>(j, c2, ldr)] = csub(rj2, cmul(u0, w2));
+                }
+                double vn = 0.0;  // ||B(:, j+1)||^2 after this reflection (group 0, column j + 1)
 #pragma unroll
                 for (int e = 0; e < E; ++e)
-                    if (gl + G * e < nb) bc[gl + G * e] = csub(x[e], cmul(u[e], w));
+                    if (gl + G * e < nb) {
+                        x[e] = csub(x[e], cmul(u[e], w));
+                        bc[gl + G * e] = x[e];
+                        vn += cabs2(x[e]);
+                        if (two) bc2[gl + G * e] = csub(x2[e], cmul(u[e], w2));
+                    }
+                if (c == j + 1) {  // only group 0 (gid == 0) meets column j + 1
+#pragma unroll
+                    for (int o = G >> 1; o > 0; o >>= 1) vn += __shfl_xor_sync(mask, vn, o);
+                    if (gl == 0) s_col[(j + 1) & 1] = vn;
+                }
             }
+        } else if (gid == 0 && j + 1 < k) {  // no reflection: column j + 1 unchanged, its norm read directly
+            const double v = col_norm(j + 1);
+            if (gl == 0) s_col[(j + 1) & 1] = v;
         }
         prev = j;
         prev_beta = beta;
@@ -1099,7 +1166,6 @@ __device__ inline void cta_qr_append(double2* R, int ldr, double2* B, int ldb, i
     if (tid == 0 && prev >= 0) R[ridx<PK>(prev, prev, ldr)] = prev_beta;
     __syncthreads();
 }
-
 
 // Blocked form of cta_qr_append (compact WY, panels of 8 columns): [R; B] = Q [R'; 0] with the same
 // structured reflectors H_j = I - tau_j u_j u_j^*, u_j = [u0_j e_j; b_j] (row j of R and the nb <= 32

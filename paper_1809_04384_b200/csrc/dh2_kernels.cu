@@ -708,7 +708,7 @@ __device__ inline void truncate_pair(const PlanD& P, const PassD& X, int p, doub
 }
 
 template <bool LEAF>
-__global__ void __launch_bounds__(128, 5)
+__global__ void __launch_bounds__(128, 4)
     k_truncate(PlanD P, PassD X, int p0, int ldv, int ldb, bool append, double eps, int mode, const int* plist) {
     extern __shared__ double2 smd[];
     __shared__ int flag, s_piv, s_rank;
@@ -718,7 +718,7 @@ __global__ void __launch_bounds__(128, 5)
 }
 
 template <bool LEAF>
-__global__ void __launch_bounds__(128, 4)
+__global__ void __launch_bounds__(128, 3)
     k_truncate_ws(PlanD P, PassD X, int p0, int np, int ldv, int ldb, bool append, double eps, int mode, double2* ws,
                   size_t ws_stride, const int* plist) {
     __shared__ int flag, s_piv, s_rank;
@@ -1053,7 +1053,7 @@ TruncLaunch plan_truncate(const PlanD& P, int np, int maxrowsM, int maxZrows, bo
     if (L.use_ws) {
         L.smem = 0;
         L.ws_stride = (bytes + sizeof(double2) - 1) / sizeof(double2);
-        L.grid = min(np, P.num_sms * 4);
+        L.grid = min(np, P.num_sms * 3);
     } else {
         L.smem = bytes;
         L.ws_stride = 0;

@@ -36,3 +36,19 @@ def oracle_run(name, eps=None, mode="FROB_BLOCKREL", **over):
 @pytest.fixture(scope="session")
 def oracle_cache():
     return oracle_run
+
+
+def release_gpu_contexts():
+    """Close the DH2 contexts other test modules cache (tests/test_gpu_parity.py _GPU,
+    tests/test_gpu_lean.py _RUNS), so that a full-size configuration finds the device memory free."""
+    import gc
+    for mod in list(sys.modules.values()):
+        for name in ("_GPU", "_RUNS"):
+            cache = getattr(mod, name, None)
+            if isinstance(cache, dict):
+                for v in cache.values():
+                    h = v[0] if isinstance(v, tuple) else v
+                    if hasattr(h, "close"):
+                        h.close()
+                cache.clear()
+    gc.collect()

@@ -22,6 +22,8 @@ def big(request):
     from paper_1809_04384_b200 import DH2
     from oracle.structure import DH2Structure
     from oracle.lazy import LazyRecompression
+    from conftest import release_gpu_contexts
+    release_gpu_contexts()
     cfg = get_config(request.param)
     xyz, tri = mesh_for(cfg)
     h = DH2(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"])
