@@ -875,9 +875,11 @@ void run_setup(Shard* C) {
     st.bytes += ent * 16;
 }
 
+// Householder QR (R only) of a complex M x N matrix, K = min(M, N): 4 x LAPACK's real count
+// 2(2MNK - (M+N)K^2 + 2K^3/3), i.e. 8(MN^2 - N^3/3) for M >= N (a complex multiply-add = 8 flops)
 inline double qr_flops(double M, double N) {
     double K = std::min(M, N);
-    return 8.0 * (M * N * K - (M + N) * K * K / 2.0 + K * K * K / 3.0);
+    return 16.0 * (M * N * K - (M + N) * K * K / 2.0 + K * K * K / 3.0);
 }
 
 // Column factors aliased to the conjugate row factors (adjoint symmetry) or in their own storage
@@ -947,11 +949,25 @@ void run_basis(Shard* C) {
 }  // namespace
 
 namespace dh2 {
+// Whether a leaf level folds its total weights into the truncation (dh2_set_option
+// "fuse_leaf_weights"): 1 = wherever a fused kernel applies -- the split path's k_trunc_zqr
+// (k <= 64, #t <= 32) or k_truncate_fused (#t <= 64, any k); 2 = only k_truncate_fused for k > 64
+// (C4/C5 leaves).
+bool fuse_leaf_level(const Shard* C, int leafrows, int maxz, int np) {
+    if (!C->fuse_leaf || C->force_ws) return false;
+    const PlanD& P = C->P;
+    if (C->fuse_leaf == 1 && C->split_trunc && P.k <= 64 && leafrows <= 32) {
+        const TruncLaunch TL = plan_truncate(P, np, leafrows, maxz, true, false);
+        return !TL.use_ws;
+    }
+    return (C->fuse_leaf == 1 || P.k > 64) && leafrows <= 64 && trunc_fused_smem(P, leafrows) <= (size_t)P.smem_optin;
+}
+
 // Truncation of the pairs [p0, p0 + np) of level l (all leaves or all inner pairs): kernel choice
 // (split warp-Jacobi path for leaves <= 32, shared-memory CTA per pair, or the global-workspace
 // persistent grid), rank read-back (sizes the next level) and the executed-flop model.
 void truncate_level(Shard* C, PassH& X, bool row, int l, int p0, int np, int maxrows, int maxz, bool all_leaf, bool fused,
-                    double eps, int mode) {
+                    double eps, int mode, const int* mirror) {
     const PlanD& P = C->P;
     cudaStream_t s = C->stream;
     const ClusterTree& T = C->st.ct;
@@ -990,16 +1006,18 @@ void truncate_level(Shard* C, PassH& X, bool row, int l, int p0, int np, int max
         }
     } else {
     const TruncLaunch TL = plan_truncate(P, np, maxrows, maxz, all_leaf, C->force_ws != 0);
-    const bool split = C->split_trunc && all_leaf && maxrows <= 32 && !TL.use_ws;
-    if (split) {
+    const bool split = C->split_trunc && all_leaf && maxrows <= 32 && !TL.use_ws && (!fused || P.k <= 64);
+    if (fused && !split) {  // leaf total weights folded into one CTA per pair (k_truncate_fused)
+        C->timed(cls, 1, [&] { launch_truncate_fused(P, row, p0, np, maxrows, eps, mode, mirror, s); });
+    } else if (split) {
         const size_t need = trunc_split_scratch_bytes(np);
         if (C->d_tscr.n < need) {
             CK(cudaStreamSynchronize(s));
             C->d_tscr.alloc(need);
         }
-        C->timed(cls, 3, [&] { launch_truncate_split(P, row, p0, np, TL, eps, mode, C->d_tscr.p, fused, C->fuse_direct, C->d_blk_mirror.p, s); });
+        C->timed(cls, 3, [&] { launch_truncate_split(P, row, p0, np, TL, eps, mode, C->d_tscr.p, fused, C->fuse_direct, mirror, s); });
     }
-    if (TL.use_ws) {
+    if (TL.use_ws && !fused) {
         const size_t need = (size_t)TL.grid * TL.ws_stride;
         if (C->d_ws.n < need) {
             CK(cudaStreamSynchronize(s));
@@ -1007,7 +1025,7 @@ void truncate_level(Shard* C, PassH& X, bool row, int l, int p0, int np, int max
         }
         ++C->ws_launches;
     }
-    if (!split) C->timed(cls, 1, [&] { launch_truncate(P, row, p0, np, TL, all_leaf, eps, mode, C->d_ws.p, s); });
+    if (!split && !fused) C->timed(cls, 1, [&] { launch_truncate(P, row, p0, np, TL, all_leaf, eps, mode, C->d_ws.p, s); });
     }
     CK(cudaMemcpyAsync(X.rank.data() + p0, X.d_rank.p + p0, np * sizeof(int), cudaMemcpyDeviceToHost, s));
     if ((int)C->sweeps_h.size() < np) C->sweeps_h.resize(np);
@@ -1111,9 +1129,7 @@ void run_weights_truncate(Shard* C, double eps, int mode) {
             const int np = X.own_hi[l] - X.own_lo[l];
             bool all_leaf, any_leaf;
             level_kind(l, all_leaf, any_leaf);
-            if (!np || !all_leaf || !C->fuse_leaf || !C->split_trunc || k > 64 || X.lev_max_leafrows[l] > 32) continue;
-            const TruncLaunch TL = plan_truncate(P, np, X.lev_max_leafrows[l], X.lev_max_zrows[l], true, C->force_ws != 0);
-            if (TL.use_ws) continue;
+            if (!np || !all_leaf || !fuse_leaf_level(C, X.lev_max_leafrows[l], X.lev_max_zrows[l], np)) continue;
             fused[l] = 1;
             C->fused_levels[side].push_back(l);
             for (int p = X.own_lo[l]; p < X.own_hi[l]; ++p) C->fused_append += X.total_rows[p] > C->fuse_direct;
@@ -1144,7 +1160,8 @@ void run_weights_truncate(Shard* C, double eps, int mode) {
                 if (X.child0[p] >= 0) maxrows = std::max(maxrows, X.rank[X.child0[p]] + X.rank[X.child1[p]]);
             bool all_leaf, any_leaf;
             level_kind(l, all_leaf, any_leaf);  // (mixed levels: one launch per kind, truncate_level)
-            truncate_level(C, X, row, l, p0, np, maxrows, X.lev_max_zrows[l], all_leaf, fused[l] != 0, eps, mode);
+            truncate_level(C, X, row, l, p0, np, maxrows, X.lev_max_zrows[l], all_leaf, fused[l] != 0, eps, mode,
+                           C->d_blk_mirror.p);
         }
     }
 }
@@ -2105,8 +2122,8 @@ int dh2_set_option(dh2_ctx* X, const char* name, int64_t value) {
         for (auto& S : X->sh) S->force_ws = (int)value;
         return DH2_OK;
     }
-    if (nm == "fuse_leaf_weights") {  // 1: leaf Zhat folded into the split QR (k_trunc_zqr), not stored
-        if (value != 0 && value != 1) return fail(X, DH2_EINVAL, "fuse_leaf_weights must be 0 or 1");
+    if (nm == "fuse_leaf_weights") {  // leaf Zhat folded into the truncation, never stored (fuse_leaf_level)
+        if (value < 0 || value > 2) return fail(X, DH2_EINVAL, "fuse_leaf_weights must be 0, 1 or 2");
         for (auto& S : X->sh) S->fuse_leaf = (int)value;
         return DH2_OK;
     }

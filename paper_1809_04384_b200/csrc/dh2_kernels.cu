@@ -888,6 +888,113 @@ __global__ void __launch_bounds__(256, 3) k_trunc_zqr(PlanD P, PassD X, bool row
     for (int j = threadIdx.x; j < 32; j += blockDim.x) sPiv[i * 32 + j] = j < rowsM ? piv[j] : 0;
 }
 
+// Leaf truncation with the leaf total weights folded in, for leaves of <= 64 triangles and any k
+// (C4/C5: k = 125, #t = 64 / 48): the rows of the stack whose R factor is Zhat_tc (P:1003-1036:
+// w_b R_sc S_b^*, Zhat_{t+c+} E_{tc+}^*) are streamed in chunks of 32, each chunk multiplied by
+// V_tc^* on the FP64 tensor cores and appended into a #t x #t triangle R0 (R0^* R0 = V Zhat^* Zhat V^*
+// = M M^*); then, in the same CTA, the pivoted QR of R0, the one-sided Jacobi and the epilogue of the
+// unfused truncation.  Zhat_tc (k columns) is never formed: the appends run on #t instead of k
+// columns, and the leaf level needs no Zhat storage.
+__global__ void __launch_bounds__(256, 1) k_truncate_fused(PlanD P, PassD X, bool row, int p0, const int* mirror, int ldv,
+                                                          double eps, int mode) {
+    extern __shared__ double2 smd[];
+    __shared__ int flag, s_piv, s_rank;
+    __shared__ double2 sh[2];
+    constexpr int CH = 32, LD = 33;
+    const int p = p0 + blockIdx.x;
+    const int k = P.k, m = P.m;
+    const int bp = X.bp[p];
+    const int rowsM = P.c_size[P.bp_t[bp]];
+    const double2* Vt = P.V + P.bp_V_off[bp];  // rowsM x k, ld rowsM
+    const int zr = X.Z_rows[p];
+    if (rowsM == 0 || zr == 0) {
+        if (threadIdx.x == 0) {
+            X.rank[p] = 0;
+            X.nsig[p] = 0;
+            X.disc[p] = 0.0;
+            X.sweeps[p] = 0;
+        }
+        return;
+    }
+    double2* B = smd;                         // CH x k stack chunk, ld LD
+    double2* Pm = B + (size_t)LD * k;         // CH x rowsM product chunk, ld LD
+    double2* R0 = Pm + (size_t)LD * ldv;      // rowsM x rowsM triangle, ld ldv
+    double2* Ef = R0 + (size_t)ldv * ldv;     // 3 m^2
+    double* nrm = reinterpret_cast<double*>(Ef + 3 * m * m);  // ldv
+    int* piv = reinterpret_cast<int*>(nrm + ldv);              // ldv
+    int* ord = piv + ldv;                                      // ldv
+    for (int idx = threadIdx.x; idx < ldv * rowsM; idx += blockDim.x) R0[idx] = cmk(0.0, 0.0);
+    int fill = 0, total = 0;
+    auto flush = [&]() {
+        __syncthreads();
+        dmma_abh<true>(B, LD, fill, Vt, rowsM, rowsM, k, Pm, LD);  // chunk V^*
+        cta_qr_append<false, 2>(R0, ldv, Pm, LD, fill, rowsM);
+        total += fill;
+        fill = 0;
+    };
+    for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) {
+        const int b = X.blk[ib];
+        const bool cj = row && P.sym;  // R_sc = conj R_{s,-c} (adjoint symmetry)
+        const int obp = row ? (cj ? P.blk_bpcs[b] : P.blk_bpcol[b]) : P.blk_bprow[b];
+        const int r = P.bp_R_rows[obp];
+        const double2* Ro = P.R + P.bp_R_off[obp];
+        const double w = P.omega[b];
+        const int mb = row ? b : mirror[b];
+        const double2* Sg = P.S + (size_t)P.blk_slot[mb >= 0 ? mb : b] * k * k;
+        const bool strided = !row && mb < 0;
+        for (int i0 = 0; i0 < r;) {
+            const int nb = min(CH - fill, r - i0);
+            __syncthreads();
+            chunk_gemm_S_dmma(Ro, r, i0, nb, Sg, row, strided, w, k, B + fill, LD, cj);
+            i0 += nb;
+            fill += nb;
+            if (fill == CH) flush();
+        }
+    }
+    for (int ip = X.par_ptr[p]; ip < X.par_ptr[p + 1]; ++ip) {
+        const int pp = X.par[ip];
+        const int ci = X.par_child[ip];
+        const int r = X.Z_rows[pp];
+        const double2* Zp = X.Z + X.Z_off[pp];
+        const double2* Eg = P.E + P.bp_E_off[X.bp[pp]] + ci * 3 * m * m;
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < 3 * m * m; idx += blockDim.x) Ef[idx] = Eg[idx];
+        for (int i0 = 0; i0 < r;) {
+            const int nb = min(CH - fill, r - i0);
+            double2* dst = B + fill;
+            __syncthreads();
+            for (int idx = threadIdx.x; idx < nb * k; idx += blockDim.x)
+                dst[idx % nb + (size_t)(idx / nb) * LD] = Zp[i0 + idx % nb + (size_t)(idx / nb) * r];
+            __syncthreads();
+            kron_apply(dst, LD, nb, m, Ef, true);  // Zhat_{t+c+} E_{tc+}^*
+            i0 += nb;
+            fill += nb;
+            if (fill == CH) flush();
+        }
+    }
+    if (fill > 0) flush();
+    // pivoted QR of R0 = that of M^* = Zhat V^* (same column norms), rank stop as the unfused path
+    const int ncol = qrcp_auto(R0, ldv, min(total, rowsM), rowsM, piv, nrm, sh, &s_piv, 1e-26);
+    zero_lower(R0, ldv, ncol, rowsM);
+    __syncthreads();
+    const int nsw = jacobi_rows_auto(R0, ldv, ncol, rowsM, nrm, &flag);
+    if (threadIdx.x == 0) X.sweeps[p] = nsw;
+    truncate_epilogue(X, p, k, R0, ldv, ncol, rowsM, piv, nrm, ord, Vt, rowsM, rowsM, eps, mode, s_rank);
+}
+
+size_t trunc_fused_smem(const PlanD& P, int maxrows) {
+    const int ldv = odd_ld(max(maxrows, 1));
+    return ((size_t)33 * P.k + (size_t)33 * ldv + (size_t)ldv * ldv + 3 * P.m * P.m) * sizeof(double2) +
+           (size_t)ldv * (sizeof(double) + 2 * sizeof(int));
+}
+
+void launch_truncate_fused(const PlanD& P, bool row, int p0, int np, int maxrows, double eps, int mode, const int* mirror,
+                           cudaStream_t s) {
+    if (!np) return;
+    const PassD& X = row ? P.row : P.col;
+    k_truncate_fused<<<np, 256, trunc_fused_smem(P, maxrows), s>>>(P, X, row, p0, mirror, odd_ld(max(maxrows, 1)), eps, mode);
+}
+
 size_t trunc_zqr_smem(const PlanD& P) {
     return ((size_t)33 * P.k + 2 * 33 * 32 + 3 * P.m * P.m) * sizeof(double2) + 64 * sizeof(double) + 32 * sizeof(int);
 }
@@ -1361,7 +1468,7 @@ cudaError_t configure_kernels() {
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     const void* ks[] = {(const void*)k_leafV<0>, (const void*)k_leafV<2>, (const void*)k_leafV<3>, (const void*)k_leafV<4>,
                         (const void*)k_leafV<5>, (const void*)k_basis<true, 4>, (const void*)k_basis<true, 2>,
-                        (const void*)k_basis<true, 3>, (const void*)k_total_weights<true, 3>,
+                        (const void*)k_basis<true, 3>, (const void*)k_total_weights<true, 3>, (const void*)k_truncate_fused,
                         (const void*)k_block_weights, (const void*)k_total_weights<true, 4>, (const void*)k_total_weights<true, 2>, (const void*)k_truncate<true>, (const void*)k_truncate<false>, (const void*)k_trunc_qr, (const void*)k_trunc_zqr,
                         (const void*)k_project};
     for (const void* f : ks) {

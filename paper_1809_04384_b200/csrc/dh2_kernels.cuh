@@ -119,6 +119,11 @@ size_t trunc_split_scratch_bytes(int np);
 // mirror as for launch_total_weights)
 void launch_truncate_split(const PlanD& P, bool row, int p0, int np, const TruncLaunch& L, double eps, int mode,
                            void* scratch, bool fused, int fuse_direct, const int* mirror, cudaStream_t s);
+// fused leaf total weights + truncation for leaves of <= 64 triangles, any k (one CTA per pair does
+// everything: stack x V^* appended into a #t x #t triangle, pivoted QR, Jacobi, epilogue)
+size_t trunc_fused_smem(const PlanD& P, int maxrows);
+void launch_truncate_fused(const PlanD& P, bool row, int p0, int np, int maxrows, double eps, int mode, const int* mirror,
+                           cudaStream_t s);
 void launch_mirror_pass(const PlanD& P, const int* col2row, int p0, int np, cudaStream_t s);
 void launch_project(const PlanD& P, int b0, int nb, int maxkrow, const int* mirror, cudaStream_t s,
                     const int* blist = nullptr);

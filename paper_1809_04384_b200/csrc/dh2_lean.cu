@@ -449,7 +449,7 @@ void lean_basis(Shard* C) {
                 }
                 if (rows > k) {
                     const double M = rows, N = k, K = std::min(M, N);
-                    fl += 8.0 * (M * N * K - (M + N) * K * K / 2.0 + K * K * K / 3.0);
+                    fl += 16.0 * (M * N * K - (M + N) * K * K / 2.0 + K * K * K / 3.0);  // as qr_flops (dh2_api.cu)
                 }
             }
             C->kstat[cls].flops += fl;
@@ -496,11 +496,27 @@ void lean_chunk_weights_truncate(Shard* C, int g, double eps, int mode) {
         }
         C->kstat["block_weights"].flops += fl;
     }
-    // total weights, top-down (Zhat of the chunk in the scratch slab)
+    // leaf levels whose total weights are folded into the truncation (fuse_leaf_weights)
+    std::vector<char> fused(L + 1, 0);
     for (int l = Ln.l0; l <= L; ++l) {
         const int gl = gl_of(C, g, l);
         const int p0 = Ln.p_lo[gl], np = Ln.p_hi[gl] - p0;
         if (!np) continue;
+        bool all_leaf = true;
+        int rows = 0, mz = 0;
+        for (int p = p0; p < p0 + np; ++p) {
+            all_leaf = all_leaf && X.child0[p] < 0;
+            rows = std::max(rows, (int)T.size(C->bp_t[X.bp[p]]));
+            mz = std::max(mz, X.Z_rows[p]);
+        }
+        fused[l] = all_leaf && fuse_leaf_level(C, rows, mz, np);
+        if (fused[l] && g == 0) C->fused_levels[0].push_back(l);
+    }
+    // total weights, top-down (Zhat of the chunk in the scratch slab)
+    for (int l = Ln.l0; l <= L; ++l) {
+        const int gl = gl_of(C, g, l);
+        const int p0 = Ln.p_lo[gl], np = Ln.p_hi[gl] - p0;
+        if (!np || fused[l]) continue;
         const std::string cls = "total_weights_row@" + std::to_string(l);
         C->timed(cls, 1, [&] { launch_total_weights(P, true, p0, np, Ln.d_mirror.p, s); });
         double fl = 0;
@@ -541,7 +557,7 @@ void lean_chunk_weights_truncate(Shard* C, int g, double eps, int mode) {
         upload_slice(X.d_rowsb, Ln.rowsb_cur, p0, np, s);
         upload_slice(X.d_C_off, Ln.C_off_cur, p0, np, s);
         upload_slice(X.d_Q_off, Ln.Q_off_cur, p0, np, s);
-        truncate_level(C, X, true, l, p0, np, maxrows, maxz, all_leaf, false, eps, mode);
+        truncate_level(C, X, true, l, p0, np, maxrows, maxz, all_leaf, fused[l] != 0, eps, mode, Ln.d_mirror.p);
         // compaction: Q/F -> persistent (ld = rows), C -> persistent (direct pairs) or the level's
         // compact scratch (read by the parent level only); ld = rank afterwards
         CopyList qlist, clist;
@@ -701,6 +717,7 @@ void lean_begin(Shard* C) {
     C->sym_used = true;
     C->fused_levels[0].clear();
     C->fused_levels[1].clear();
+    C->fused_append = 0;
     Ln.C_used = Ln.Q_used = 0;
     Ln.compact_items = 0;
     if (!Ln.d_Zs.p && Ln.Z_scratch) Ln.d_Zs.alloc(Ln.Z_scratch);

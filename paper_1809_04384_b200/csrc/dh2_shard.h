@@ -358,7 +358,8 @@ struct Shard {
 
 // truncation of one level's pairs (dh2_api.cu)
 void truncate_level(Shard* C, PassH& X, bool row, int l, int p0, int np, int maxrows, int maxz, bool all_leaf, bool fused,
-                    double eps, int mode);
+                    double eps, int mode, const int* mirror);
+bool fuse_leaf_level(const Shard* C, int leafrows, int maxz, int np);
 // memory-lean plan (dh2_lean.cu)
 void lean_plan(Shard* C, int G);
 double lean_bytes(const Shard* C);

@@ -18,13 +18,14 @@ pytestmark = pytest.mark.gpu
 _RUNS = {}
 
 
-def _run(name, chunks):
+def _run(name, chunks, fuse=0):
     from paper_1809_04384_b200 import DH2
-    key = (name, chunks)
+    key = (name, chunks, fuse)
     if key not in _RUNS:
         cfg = get_config(name)
         xyz, tri = mesh_for(cfg)
         h = DH2(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"])
+        h.set_option("fuse_leaf_weights", fuse)
         if chunks:
             h.set_option("lean_chunks", chunks)
         h.recompress(cfg["eps"])
@@ -72,11 +73,16 @@ def _st_blocks(h):
     return out
 
 
-@pytest.mark.parametrize("name,chunks", [("P1", 1), ("P1", 3), ("P2", 4), ("P4", 2), ("P6", 1), ("P7", 5), ("P8", 3), ("C1", 8),
-                                         ("C2", 1), ("C2", 16), ("C4s", 7)])
-def test_lean_bitwise_equal_to_full(name, chunks):
-    hf, sf = _run(name, 0)
-    hl, sl = _run(name, chunks)
+@pytest.mark.parametrize("name,chunks,fuse", [("P1", 1, 0), ("P1", 3, 0), ("P2", 4, 0), ("P4", 2, 0), ("P6", 1, 0),
+                                              ("P7", 5, 0), ("P8", 3, 0), ("C1", 8, 0), ("C2", 1, 0), ("C2", 16, 0),
+                                              ("C4s", 7, 0), ("C4s", 3, 2), ("P7", 2, 2), ("P2", 3, 1)])
+def test_lean_bitwise_equal_to_full(name, chunks, fuse):
+    """(fuse: dh2_set_option fuse_leaf_weights on both plans: the leaf total weights folded into the
+    truncation, leaf Zhat never formed)"""
+    hf, sf = _run(name, 0, fuse)
+    hl, sl = _run(name, chunks, fuse)
+    if fuse:
+        assert sl["fused_leaf_levels_row"] and sl["fused_leaf_levels_row"] == sf["fused_leaf_levels_row"]
     assert sl["lean"]["chunks"] >= 1
     for key in ("E_row", "E_col", "far2"):
         assert sl[key] == sf[key], key

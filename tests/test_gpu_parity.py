@@ -169,7 +169,8 @@ def test_G6_certified_sums(name, sym):
 
 @pytest.mark.parametrize("name,ws,split,fuse", [("P2", 1, 1, 0), ("P4", 1, 1, 0), ("P1", 0, 0, 0), ("P2", 0, 0, 0),
                                                ("C1", 0, 0, 0), ("P1", 0, 1, 1), ("P2", 0, 1, 1), ("P4", 0, 1, 1),
-                                               ("C1", 0, 1, 1), ("P2", 0, 1, 2), ("C1", 0, 1, 2)])
+                                               ("C1", 0, 1, 1), ("P2", 0, 1, 2), ("C1", 0, 1, 2),
+                                               ("P5", 0, 1, 3), ("P6", 0, 1, 3), ("P7", 0, 1, 3), ("P2", 0, 0, 1)])
 def test_truncate_paths(name, ws, split, fuse):
     """The other truncation kernels give the same ranks, singular values and matrix: the
     global-workspace persistent grid (used when the working set exceeds shared memory) and the
@@ -177,9 +178,12 @@ def test_truncate_paths(name, ws, split, fuse):
     kernels on leaf levels with #t <= 32), and the split path with the leaf total weights formed
     and stored (default) or folded into its QR kernel (fuse_leaf_weights = 1: stacks of <= 64 rows
     form M^* directly; fuse = 2 here: fuse_direct_rows = 0, every stack takes the QR-append mode)."""
-    h, g, rc = gpu_run(name, ws=ws, split=split, fuse=min(fuse, 1), direct=0 if fuse == 2 else 64)
+    # fuse = 3: fuse_leaf_weights = 2 (k = 125 leaves of <= 64 triangles: k_truncate_fused)
+    h, g, rc = gpu_run(name, ws=ws, split=split, fuse={0: 0, 1: 1, 2: 1, 3: 2}[fuse], direct=0 if fuse == 2 else 64)
     if fuse == 2:
         assert h.stats()["fused_append_pairs"] > 0
+    if fuse:
+        assert h.stats()["fused_leaf_levels_row"]
     for side in ("row", "col"):
         go, oo = getattr(g, side), getattr(rc, side)
         assert go.rank == oo.rank
