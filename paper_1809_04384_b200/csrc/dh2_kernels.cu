@@ -708,7 +708,7 @@ __device__ inline void truncate_pair(const PlanD& P, const PassD& X, int p, doub
 }
 
 template <bool LEAF>
-__global__ void __launch_bounds__(128, 4)
+__global__ void __launch_bounds__(512, 1)
     k_truncate(PlanD P, PassD X, int p0, int ldv, int ldb, bool append, double eps, int mode, const int* plist) {
     extern __shared__ double2 smd[];
     __shared__ int flag, s_piv, s_rank;
@@ -895,7 +895,7 @@ __global__ void __launch_bounds__(256, 3) k_trunc_zqr(PlanD P, PassD X, bool row
 // = M M^*); then, in the same CTA, the pivoted QR of R0, the one-sided Jacobi and the epilogue of the
 // unfused truncation.  Zhat_tc (k columns) is never formed: the appends run on #t instead of k
 // columns, and the leaf level needs no Zhat storage.
-__global__ void __launch_bounds__(256, 1) k_truncate_fused(PlanD P, PassD X, bool row, int p0, const int* mirror, int ldv,
+__global__ void __launch_bounds__(512, 1) k_truncate_fused(PlanD P, PassD X, bool row, int p0, const int* mirror, int ldv,
                                                           double eps, int mode) {
     extern __shared__ double2 smd[];
     __shared__ int flag, s_piv, s_rank;
@@ -992,7 +992,7 @@ void launch_truncate_fused(const PlanD& P, bool row, int p0, int np, int maxrows
                            cudaStream_t s) {
     if (!np) return;
     const PassD& X = row ? P.row : P.col;
-    k_truncate_fused<<<np, 256, trunc_fused_smem(P, maxrows), s>>>(P, X, row, p0, mirror, odd_ld(max(maxrows, 1)), eps, mode);
+    k_truncate_fused<<<np, 512, trunc_fused_smem(P, maxrows), s>>>(P, X, row, p0, mirror, odd_ld(max(maxrows, 1)), eps, mode);
 }
 
 size_t trunc_zqr_smem(const PlanD& P) {
@@ -1165,6 +1165,10 @@ TruncLaunch plan_truncate(const PlanD& P, int np, int maxrowsM, int maxZrows, bo
         L.smem = bytes;
         L.ws_stride = 0;
         L.grid = np;
+        // 4 warps per pair, more when shared memory holds fewer than 4 pairs per SM (C4/C5: 1-2):
+        // QRCP, Jacobi and the appends run their lane groups over more columns / pairs at once
+        const int c = ctas(bytes);
+        L.threads = c >= 4 ? 128 : c >= 2 ? 256 : 512;
     }
     return L;
 }
@@ -1179,9 +1183,9 @@ void launch_truncate(const PlanD& P, bool row, int p0, int np, const TruncLaunch
         else
             k_truncate_ws<false><<<L.grid, 128, 0, s>>>(P, X, p0, np, L.ldv, L.ldb, L.append, eps, mode, ws, L.ws_stride, plist);
     } else if (leaf_level) {
-        k_truncate<true><<<np, 128, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, L.append, eps, mode, plist);
+        k_truncate<true><<<np, L.threads, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, L.append, eps, mode, plist);
     } else {
-        k_truncate<false><<<np, 128, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, L.append, eps, mode, plist);
+        k_truncate<false><<<np, L.threads, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, L.append, eps, mode, plist);
     }
 }
 

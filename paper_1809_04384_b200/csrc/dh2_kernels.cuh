@@ -106,6 +106,7 @@ struct TruncLaunch {
     bool append = false;      // leaf level with zr > #t: M^* reduced to its R factor by streamed chunks
     size_t smem = 0;          // dynamic shared memory per CTA
     size_t ws_stride = 0;     // workspace per CTA (double2 units); total grid * ws_stride
+    int threads = 128;        // CTA size: more threads per pair when shared memory limits the CTAs per SM
 };
 TruncLaunch plan_truncate(const PlanD& P, int np, int maxrowsM, int maxZrows, bool leaf_level, bool force_ws);
 // plist (optional): the pairs to truncate (np of them) instead of [p0, p0 + np) -- levels mixing
