@@ -684,7 +684,7 @@ void choose_plan(Shard* C) {
         return;
     }
     const size_t need = plan_bytes(C);
-    if (need + (size_t)256 * 1024 * 1024 <= freeb) return;
+    if (!C->lean_required && need + (size_t)256 * 1024 * 1024 <= freeb) return;
     const std::string full = "device memory plan needs " + std::to_string(need >> 20) + " MiB, free " + std::to_string(freeb >> 20) + " MiB";
     if (!C->sym_ok) throw NoMem(full + " (the memory-lean plan needs the adjoint symmetry)");
     const int ntop = (int)C->st.ct.levels[std::max(0, C->st.first_level)].size();
@@ -1996,6 +1996,22 @@ int dh2_build_interp(const dh2_mesh* mesh, const dh2_params* params, const dh2_d
                 X->stream = S->own_stream;
             }
             S->stream = X->stream;  // all shards of a context issue on one stream
+        }
+        {
+            // every shard of a partition takes the same kind of plan (the exchanged C layouts differ):
+            // the lean one if any shard's full plan does not fit its GPU (virtual mode: all of them
+            // together on this GPU; NCCL: the maximum over the ranks)
+            size_t freeb = 0, totb = 0;
+            CK(cudaMemGetInfo(&freeb, &totb));
+            freeb += pool_reusable(X->device);
+            double need = 0.0;
+            for (auto& S : X->sh) need = X->virt ? need + plan_bytes(S.get()) : std::max(need, (double)plan_bytes(S.get()));
+            std::vector<double> v{need + (double)(256 << 20) > (double)freeb ? 1.0 : 0.0};
+            reduce_doubles(X.get(), v, true);
+            if (X->world > 1 && v[0] > 0.0)
+                for (auto& S : X->sh) S->lean_required = true;
+        }
+        for (auto& S : X->sh) {
             S->P.smem_optin = optin - 1024;  // margin for the kernels' static shared memory
             S->P.num_sms = nsm;
             upload_all(S.get(), mesh->xyz, mesh->nv, mesh->tri);

@@ -277,6 +277,7 @@ struct Shard {
     PassH row, col;
     std::vector<int> sweeps_h;  // Jacobi sweeps of the last truncated level (convergence check)
     LeanState lean;
+    bool lean_required = false;  // set by the context: the partition's shards all take the lean plan
     std::vector<int> lean_slot, lean_mirror;  // lean plan: S slot of each block in its chunk; chunk-local mirrors
     // device
     DevBuf<double> d_xyz, d_c_lo, d_c_hi, d_dirs, d_omega, d_normG2;
