@@ -1167,8 +1167,10 @@ TruncLaunch plan_truncate(const PlanD& P, int np, int maxrowsM, int maxZrows, bo
         L.grid = np;
         // 4 warps per pair, more when shared memory holds fewer than 4 pairs per SM (C4/C5: 1-2):
         // QRCP, Jacobi and the appends run their lane groups over more columns / pairs at once
+        // (measured: C4 leaves, append mode, 2 pairs per SM: 128 -> 256 threads -15 %; C5 leaves,
+        // direct mode, 2 pairs per SM: +18 %; one pair per SM (levels above the leaves): 512, -28 %)
         const int c = ctas(bytes);
-        L.threads = c >= 4 ? 128 : c >= 2 ? 256 : 512;
+        L.threads = (c >= 4 || (c >= 2 && !L.append)) ? 128 : c >= 2 ? 256 : 512;
     }
     return L;
 }
