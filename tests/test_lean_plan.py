@@ -137,3 +137,16 @@ def test_lean_plan_memory_estimates():
         h.set_option("lean_chunks", 32)
         est = h.stats()["device_bytes"]
         assert est < 160e9, (name, est)
+
+
+def test_lean_plan_partitioned_c4_fits_110gb_per_gpu():
+    """C4 on 8 GPUs: the full plan exceeds a B200 per shard, the lean plan of every
+    shard stays below 110 GB with 4 chunks (planner estimates; virtual structure-only context)."""
+    from paper_1809_04384_b200 import DH2
+    cfg = get_config("C4")
+    xyz, tri = mesh_for(cfg)
+    h = DH2(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"], device=-1, world=8)
+    assert min(h.stats()["shard_device_bytes"]) > 183e9
+    h.set_option("lean_chunks", 4)
+    per = h.stats()["shard_device_bytes"]
+    assert len(per) == 8 and max(per) < 110e9, per
