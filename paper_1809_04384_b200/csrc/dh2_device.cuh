@@ -1063,7 +1063,10 @@ __host__ __device__ inline size_t r_elems(int k, int ldr) {
 template <bool PK, int E>
 __device__ inline void cta_qr_append(double2* R, int ldr, double2* B, int ldb, int nb, int k) {
     constexpr int G = 16;
-    __shared__ double s_col[2];  // ||B(:, j)||^2 of the next reflection (double-buffered by step parity)
+    // reflector of the next step (double-buffered by step parity): tau, u0, beta, formed once by
+    // group 0 right after it applied the current reflector to column j + 1 (look-ahead)
+    __shared__ double2 s_u0[2], s_beta[2];
+    __shared__ double s_tau[2];
     const int tid = threadIdx.x, lane = tid & 31;
     const int gl = tid & (G - 1), gid = tid / G, ng = blockDim.x / G;
     const unsigned mask = 0xffffu << (lane & 16);
@@ -1077,17 +1080,8 @@ __device__ inline void cta_qr_append(double2* R, int ldr, double2* B, int ldb, i
         for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
         return v;
     };
-    if (gid == 0 && k > 0) {
-        const double v = col_norm(0);
-        if (gl == 0) s_col[0] = v;
-    }
-    __syncthreads();
-    int prev = -1;
-    double2 prev_beta = cmk(0.0, 0.0);
-    for (int j = 0; j < k; ++j) {
-        if (tid == 0 && prev >= 0) R[ridx<PK>(prev, prev, ldr)] = prev_beta;
-        const double2* bj = B + j * ldb;
-        const double s = s_col[j & 1];
+    // Householder reflector of column j from s = ||B(:, j)||^2 and alpha = R[j, j] (lane 0 of group 0)
+    auto publish = [&](int j, double s) {
         const double2 alpha = R[ridx<PK>(j, j, ldr)];
         double tau = 0.0;
         double2 beta = alpha, u0 = cmk(0.0, 0.0);
@@ -1099,6 +1093,20 @@ __device__ inline void cta_qr_append(double2* R, int ldr, double2* B, int ldb, i
             u0 = cscale(ph, aa + xn);
             tau = 1.0 / (xn * (xn + aa));
         }
+        s_tau[j & 1] = tau;
+        s_u0[j & 1] = u0;
+        s_beta[j & 1] = beta;
+    };
+    if (gid == 0 && k > 0) {
+        const double v = col_norm(0);
+        if (gl == 0) publish(0, v);
+    }
+    __syncthreads();
+    for (int j = 0; j < k; ++j) {
+        const double2* bj = B + j * ldb;
+        const double tau = s_tau[j & 1];
+        const double2 u0 = s_u0[j & 1];
+        if (tid == 0) R[ridx<PK>(j, j, ldr)] = s_beta[j & 1];  // (nobody reads R[j, j] after the publish)
         if (tau != 0.0) {
             double2 u[E];
 #pragma unroll
@@ -1149,22 +1157,18 @@ __device__ inline void cta_qr_append(double2* R, int ldr, double2* B, int ldb, i
                         vn += cabs2(x[e]);
                         if (two) bc2[gl + G * e] = csub(x2[e], cmul(u[e], w2));
                     }
-                if (c == j + 1) {  // only group 0 (gid == 0) meets column j + 1
+                if (c == j + 1) {  // only group 0 (gid == 0) meets column j + 1: next reflector now
 #pragma unroll
                     for (int o = G >> 1; o > 0; o >>= 1) vn += __shfl_xor_sync(mask, vn, o);
-                    if (gl == 0) s_col[(j + 1) & 1] = vn;
+                    if (gl == 0) publish(j + 1, vn);
                 }
             }
-        } else if (gid == 0 && j + 1 < k) {  // no reflection: column j + 1 unchanged, its norm read directly
+        } else if (gid == 0 && j + 1 < k) {  // no reflection: column j + 1 unchanged
             const double v = col_norm(j + 1);
-            if (gl == 0) s_col[(j + 1) & 1] = v;
+            if (gl == 0) publish(j + 1, v);
         }
-        prev = j;
-        prev_beta = beta;
         __syncthreads();
     }
-    if (tid == 0 && prev >= 0) R[ridx<PK>(prev, prev, ldr)] = prev_beta;
-    __syncthreads();
 }
 
 // Blocked form of cta_qr_append (compact WY, panels of 8 columns): [R; B] = Q [R'; 0] with the same
