@@ -1060,18 +1060,17 @@ __host__ __device__ inline size_t r_elems(int k, int ldr) {
 // the reflector itself from ||B(:, j)||^2, which group 0 -- it updates column j during step j-1 --
 // publishes in shared memory (look-ahead: no reduction over B on the critical path); the new
 // diagonal beta_j is stored one step later (nobody reads R[j, j] during step j+1).
-template <bool PK, int E>
+template <bool PK, int E, int G = 16>  // G lanes per column group (16 or 8), E rows per lane: nb <= G E
 __device__ inline void cta_qr_append(double2* R, int ldr, double2* B, int ldb, int nb, int k) {
-    constexpr int G = 16;
     // reflector of the next step (double-buffered by step parity): tau, u0, beta, formed once by
     // group 0 right after it applied the current reflector to column j + 1 (look-ahead)
     __shared__ double2 s_u0[2], s_beta[2];
     __shared__ double s_tau[2];
     const int tid = threadIdx.x, lane = tid & 31;
     const int gl = tid & (G - 1), gid = tid / G, ng = blockDim.x / G;
-    const unsigned mask = 0xffffu << (lane & 16);
+    const unsigned mask = ((1u << G) - 1u) << (lane & ~(G - 1));
     __syncthreads();
-    auto col_norm = [&](int c) {  // 16-lane reduction of ||B(:, c)||^2 (group-uniform result)
+    auto col_norm = [&](int c) {  // G-lane reduction of ||B(:, c)||^2 (group-uniform result)
         double v = 0.0;
 #pragma unroll
         for (int e = 0; e < E; ++e)

@@ -270,7 +270,7 @@ __device__ __forceinline__ void qr_append(const PlanD& P, double2* R, int ldr, d
     if (E == 2 && P.qr_wy)
         cta_qr_append_wy<PK>(R, ldr, B, ldb, nb, k, wp);
     else
-        cta_qr_append<PK, E>(R, ldr, B, ldb, nb, k);
+        cta_qr_append<PK, (E == 3 ? 6 : E), (E == 3 ? 8 : 16)>(R, ldr, B, ldb, nb, k);  // 48-row chunks: 8-lane groups
 }
 
 // Basis weights (Eq. 18; [BO10, Alg. 16] generalised to directions), one CTA per
@@ -375,7 +375,8 @@ void launch_basis(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStr
 // w_b = 1/||G_b||_F for the block-relative modes, 1 for FROB_CLUSTERREL.  CTA per block:
 // U = R_tc S_b on the FP64 tensor cores (S read coalesced through the mirror block), in chunks
 // of <= 64 rows of R_tc, then ||U R_sc^*||_F^2 with a fixed-order reduction.
-__global__ void __launch_bounds__(256, 3) k_block_weights(PlanD P, int b0, int mode, int ldu, int chunk, const int* mirror,
+template <int NT>  // 256 threads, 3 CTAs per SM (k <= 64) or 512 threads, one CTA per SM (k = 125)
+__global__ void __launch_bounds__(NT, NT == 512 ? 1 : 3) k_block_weights(PlanD P, int b0, int mode, int ldu, int chunk, const int* mirror,
                                                          const int* blist) {
     extern __shared__ double2 sm[];
     __shared__ double red[32];
@@ -410,10 +411,17 @@ __global__ void __launch_bounds__(256, 3) k_block_weights(PlanD P, int b0, int m
 
 void launch_block_weights(const PlanD& P, int b0, int nb, int mode, const int* mirror, cudaStream_t s, const int* blist) {
     if (!nb) return;
-    const int chunk = P.k <= 64 ? 64 : 32;
+    // k = 125: one CTA of 512 threads per SM with 64-row chunks of R_tc (2 instead of 4 passes over S_b
+    // and R_sc per block, and a working set of 148 blocks that stays in L2: the 32-row chunks at 3 CTAs
+    // per SM read 1.9 MB of DRAM per block, ncu r02)
+    const bool big = P.k > 64;
+    const int chunk = 64;
     const int ldu = odd_ld(chunk);
     size_t sm = (size_t)ldu * P.k * sizeof(double2);
-    k_block_weights<<<nb, 256, sm, s>>>(P, b0, mode, ldu, chunk, mirror, blist);
+    if (big)
+        k_block_weights<512><<<nb, 512, sm, s>>>(P, b0, mode, ldu, chunk, mirror, blist);
+    else
+        k_block_weights<256><<<nb, 256, sm, s>>>(P, b0, mode, ldu, chunk, mirror, blist);
 }
 
 // Total weights, one CTA per pair of one level (top-down):
@@ -1475,7 +1483,7 @@ cudaError_t configure_kernels() {
     const void* ks[] = {(const void*)k_leafV<0>, (const void*)k_leafV<2>, (const void*)k_leafV<3>, (const void*)k_leafV<4>,
                         (const void*)k_leafV<5>, (const void*)k_basis<true, 4>, (const void*)k_basis<true, 2>,
                         (const void*)k_basis<true, 3>, (const void*)k_total_weights<true, 3>, (const void*)k_truncate_fused,
-                        (const void*)k_block_weights, (const void*)k_total_weights<true, 4>, (const void*)k_total_weights<true, 2>, (const void*)k_truncate<true>, (const void*)k_truncate<false>, (const void*)k_trunc_qr, (const void*)k_trunc_zqr,
+                        (const void*)k_block_weights<256>, (const void*)k_block_weights<512>, (const void*)k_total_weights<true, 4>, (const void*)k_total_weights<true, 2>, (const void*)k_truncate<true>, (const void*)k_truncate<false>, (const void*)k_trunc_qr, (const void*)k_trunc_zqr,
                         (const void*)k_project};
     for (const void* f : ks) {
         if (e != cudaSuccess) break;

@@ -76,8 +76,8 @@ class _GpuFactors:
             if self.child0[p] < 0:
                 self._Q[key] = self.qhat(p)
             else:
-                Qh = self.qhat(p)
                 k1 = int(self.rank[self.child0[p]])
+                Qh = self.qhat(p)[:k1 + int(self.rank[self.child1[p]])]  # (full plan: ld = the rows bound)
                 parts = []
                 for i, ch in enumerate(ct.children[t]):
                     _, tc, cc = self.pairs[self.child0[p] if i == 0 else self.child1[p]]
