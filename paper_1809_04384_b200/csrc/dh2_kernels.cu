@@ -270,7 +270,7 @@ __device__ __forceinline__ void qr_append(const PlanD& P, double2* R, int ldr, d
     if (E == 2 && P.qr_wy)
         cta_qr_append_wy<PK>(R, ldr, B, ldb, nb, k, wp);
     else
-        cta_qr_append<PK, (E == 3 ? 6 : E), (E == 3 ? 8 : 16)>(R, ldr, B, ldb, nb, k);  // 48-row chunks: 8-lane groups
+        cta_qr_append<PK, E>(R, ldr, B, ldb, nb, k);  // (8-lane groups for the 48-row chunks: measured neutral)
 }
 
 // Basis weights (Eq. 18; [BO10, Alg. 16] generalised to directions), one CTA per
@@ -411,11 +411,10 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : 3) k_block_weights(PlanD P
 
 void launch_block_weights(const PlanD& P, int b0, int nb, int mode, const int* mirror, cudaStream_t s, const int* blist) {
     if (!nb) return;
-    // k = 125: one CTA of 512 threads per SM with 64-row chunks of R_tc (2 instead of 4 passes over S_b
-    // and R_sc per block, and a working set of 148 blocks that stays in L2: the 32-row chunks at 3 CTAs
-    // per SM read 1.9 MB of DRAM per block, ncu r02)
-    const bool big = P.k > 64;
-    const int chunk = 64;
+    // (k = 125: one 512-thread CTA per SM with 64-row chunks halves the DRAM re-reads of S_b and R_sc
+    // but measured 32 % slower on C4 than 3 CTAs per SM with 32-row chunks, which stays)
+    const bool big = false;
+    const int chunk = P.k <= 64 ? 64 : 32;
     const int ldu = odd_ld(chunk);
     size_t sm = (size_t)ldu * P.k * sizeof(double2);
     if (big)
