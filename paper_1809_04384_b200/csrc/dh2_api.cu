@@ -834,6 +834,7 @@ void upload_all(Shard* C, const double* xyz, int64_t nv, const int64_t* tri) {
     // set-up of the row basis pairs only when the column side can be read by conjugation
     P.sym = (C->sym_ok && C->sym_opt) ? 1 : 0;
     P.qr_wy = C->qr_wy_init;
+    P.qr_flag = C->qr_flag_init;
     if (C->lean.on) lean_alloc(C);
 }
 
@@ -2151,6 +2152,11 @@ int dh2_set_option(dh2_ctx* X, const char* name, int64_t value) {
     if (nm == "qr_wy") {  // 0: column-by-column chunk appends (A/B and tests)
         if (value != 0 && value != 1) return fail(X, DH2_EINVAL, "qr_wy must be 0 or 1");
         for (auto& S : X->sh) S->P.qr_wy = S->qr_wy_init = (int)value;
+        return DH2_OK;
+    }
+    if (nm == "qr_flag") {  // 0: one block barrier per reflection in the chunk appends (A/B and tests)
+        if (value != 0 && value != 1) return fail(X, DH2_EINVAL, "qr_flag must be 0 or 1");
+        for (auto& S : X->sh) S->P.qr_flag = S->qr_flag_init = (int)value;
         return DH2_OK;
     }
     if (nm == "truncate_split") {  // 0: the one-kernel truncation also for leaves <= 32 (tests)

@@ -2,6 +2,7 @@
 // Complex float64 is double2 (re, im); all matrices are column-major.
 #pragma once
 #include <cuda_runtime.h>
+#include <cuda/atomic>
 #include <stdint.h>
 
 namespace dh2 {
@@ -1168,6 +1169,123 @@ __device__ inline void cta_qr_append(double2* R, int ldr, double2* B, int ldb, i
         }
         __syncthreads();
     }
+}
+
+// Flag-synchronised form of cta_qr_append: the same reflections, but no block barrier per
+// reflection.  Warp w owns the columns c = w (mod #warps) for the whole chunk (its two 16-lane halves
+// take two columns at a time, E rows per lane); the owner of column j+1 applies reflection j to it
+// first, forms reflection j+1 and publishes it (tau, u0 in shared arrays indexed by the step, then a
+// release store of the step counter); every other warp only waits (acquire load) until reflection j+1
+// is published before applying it.  Warps run ahead or behind each other -- a reflection's data never
+// changes after its publication (column j is final once reflected, row j of R belongs to the column
+// owners), so the only synchronisation is producer -> consumers.  s_tau / s_u0 hold k entries.
+template <bool PK, int E>
+__device__ inline void cta_qr_append_flag(double2* R, int ldr, double2* B, int ldb, int nb, int k, double* s_tau,
+                                          double2* s_u0, int* s_step) {
+    constexpr int G = 16;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int gl = tid & (G - 1), half = lane >> 4;
+    const unsigned mask = 0xffffu << (lane & 16);
+    cuda::atomic_ref<int, cuda::thread_scope_block> step(*s_step);
+    auto reflector = [&](int j, double s) {  // lane 0 of the owner warp: publish reflection j
+        const double2 alpha = R[ridx<PK>(j, j, ldr)];
+        double tau = 0.0;
+        double2 beta = alpha, u0 = cmk(0.0, 0.0);
+        if (s > HH_TINY) {  // tiny columns are left as they are (1/(xn (xn + aa)) would overflow)
+            const double aa = sqrt(cabs2(alpha));
+            const double xn = sqrt(s + aa * aa);
+            const double2 ph = aa > 0.0 ? cscale(alpha, 1.0 / aa) : cmk(1.0, 0.0);
+            beta = cscale(ph, -xn);
+            u0 = cscale(ph, aa + xn);
+            tau = 1.0 / (xn * (xn + aa));
+        }
+        s_tau[j] = tau;
+        s_u0[j] = u0;
+        R[ridx<PK>(j, j, ldr)] = beta;  // nobody reads R[j, j] again
+        step.store(j, cuda::memory_order_release);
+    };
+    auto col_norm16 = [&](int c) {  // ||B(:, c)||^2 over one 16-lane half
+        double v = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+            if (gl + G * e < nb) v += cabs2(B[(size_t)c * ldb + gl + G * e]);
+#pragma unroll
+        for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
+        return v;
+    };
+    __syncthreads();
+    if (tid == 0) *s_step = -1;
+    __syncthreads();
+    if (warp == 0 && k > 0) {  // column 0 is owned by warp 0
+        const double v = col_norm16(0);  // (both halves compute it; lane 0 publishes)
+        if (lane == 0) reflector(0, v);
+    }
+    // own columns of this warp: c = warp + nw * i; in a step the two halves take two of them
+    for (int j = 0; j < k; ++j) {
+        // wait for reflection j (the owner of column j published it after reflection j-1)
+        if (lane == 0)
+            while (step.load(cuda::memory_order_acquire) < j) __nanosleep(20);
+        __syncwarp();
+        cuda::atomic_thread_fence(cuda::memory_order_acquire, cuda::thread_scope_block);
+        const double tau = s_tau[j];
+        if (tau == 0.0) {  // no reflection: the owner of column j + 1 publishes its reflector from the column
+            if (j + 1 < k && (j + 1) % nw == warp) {
+                const double v = col_norm16(j + 1);
+                if (lane == 0) reflector(j + 1, v);
+            }
+            continue;
+        }
+        const double2 u0 = s_u0[j];
+        const double2* bj = B + (size_t)j * ldb;
+        double2 u[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) u[e] = (gl + G * e < nb) ? bj[gl + G * e] : cmk(0.0, 0.0);
+        // this warp's columns > j, the column j+1 first (it feeds the next reflection)
+        int c0 = warp;
+        if (c0 <= j) c0 += ((j - c0) / nw + 1) * nw;
+        for (int cb = c0; cb < k; cb += 2 * nw) {
+            const int c = cb + half * nw;  // half 0: cb, half 1: cb + nw
+            const bool ok = c < k;
+            double2 x[E];
+            double2 rj = cmk(0.0, 0.0), w = cmk(0.0, 0.0);
+            if (ok && gl == 0) {
+                rj = R[ridx<PK>(j, c, ldr)];
+                cfma_cj(w, u0, rj);
+            }
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                x[e] = (ok && gl + G * e < nb) ? B[(size_t)c * ldb + gl + G * e] : cmk(0.0, 0.0);
+                cfma_cj(w, u[e], x[e]);
+            }
+#pragma unroll
+            for (int o = G >> 1; o > 0; o >>= 1) {
+                w.x += __shfl_xor_sync(mask, w.x, o);
+                w.y += __shfl_xor_sync(mask, w.y, o);
+            }
+            w = cscale(w, tau);
+            double vn = 0.0;
+            if (ok) {
+                if (gl == 0) R[ridx<PK>(j, c, ldr)] = csub(rj, cmul(u0, w));
+#pragma unroll
+                for (int e = 0; e < E; ++e)
+                    if (gl + G * e < nb) {
+                        x[e] = csub(x[e], cmul(u[e], w));
+                        B[(size_t)c * ldb + gl + G * e] = x[e];
+                        vn += cabs2(x[e]);
+                    }
+            }
+            if (cb == c0 && c0 == j + 1) {  // column j+1 is this warp's (half 0): form reflection j+1
+#pragma unroll
+                for (int o = G >> 1; o > 0; o >>= 1) vn += __shfl_xor_sync(mask, vn, o);
+                __syncwarp();  // (the half-0 lanes wrote column j+1 and row j of R)
+                if (lane == 0) {
+                    cuda::atomic_thread_fence(cuda::memory_order_release, cuda::thread_scope_block);
+                    reflector(j + 1, vn);
+                }
+            }
+        }
+    }
+    __syncthreads();
 }
 
 // Blocked form of cta_qr_append (compact WY, panels of 8 columns): [R; B] = Q [R'; 0] with the same

@@ -267,8 +267,13 @@ __device__ inline void zero_lower(double2* A, int lda, int rows, int cols) {
 // wait, so the k-step critical path per chunk is not shorter) or the column-by-column one (default).
 template <bool PK, int E>
 __device__ __forceinline__ void qr_append(const PlanD& P, double2* R, int ldr, double2* B, int ldb, int nb, int k, WyPanel* wp) {
+    __shared__ double s_tau[MMAX * MMAX * MMAX];
+    __shared__ double2 s_u0[MMAX * MMAX * MMAX];
+    __shared__ int s_step;
     if (E == 2 && P.qr_wy)
         cta_qr_append_wy<PK>(R, ldr, B, ldb, nb, k, wp);
+    else if (P.qr_flag)
+        cta_qr_append_flag<PK, E>(R, ldr, B, ldb, nb, k, s_tau, s_u0, &s_step);
     else
         cta_qr_append<PK, E>(R, ldr, B, ldb, nb, k);  // (8-lane groups for the 48-row chunks: measured neutral)
 }

@@ -260,6 +260,7 @@ struct Shard {
     bool sym_ok = false;     // structure admits it (checked in build_tables)
     int sym_opt = 1;         // dh2_set_option("adjoint_symmetry")
     int force_ws = 0;        // dh2_set_option("truncate_workspace")
+    int qr_flag_init = 0;    // initial value of PlanD::qr_flag
     int qr_wy_init = 0;      // initial value of PlanD::qr_wy (blocked WY appends measured slower on C4: 0) (dh2_set_option("qr_wy") sets the plan directly)
     int split_trunc = 1;     // dh2_set_option("truncate_split"): warp-register Jacobi for leaves <= 32
     int fuse_leaf = 0;       // dh2_set_option("fuse_leaf_weights"): leaf Zhat folded into the split QR

@@ -88,7 +88,10 @@ extern "C" int devtest_gemm(const double* X, const double* S, double* out, int n
 __global__ void k_devappend(int mode, const double2* A, double2* Rout, int M, int N) {
     extern __shared__ double2 smem[];
     __shared__ WyPanel wp;
-    const bool pk = mode >= 2;
+    __shared__ double s_tau[128];
+    __shared__ double2 s_u0[128];
+    __shared__ int s_step;
+    const bool pk = mode == 2 || mode == 3 || mode == 5;
     const int ldr = N | 1, ldb = 33;
     double2* R = smem;
     const size_t relems = pk ? (size_t)N * (N + 1) / 2 : (size_t)ldr * N;
@@ -103,6 +106,8 @@ __global__ void k_devappend(int mode, const double2* A, double2* Rout, int M, in
         if (mode == 1) cta_qr_append_wy<false>(R, ldr, B, ldb, nb, N, &wp);
         if (mode == 2) cta_qr_append<true, 2>(R, ldr, B, ldb, nb, N);
         if (mode == 3) cta_qr_append_wy<true>(R, ldr, B, ldb, nb, N, &wp);
+        if (mode == 4) cta_qr_append_flag<false, 2>(R, ldr, B, ldb, nb, N, s_tau, s_u0, &s_step);
+        if (mode == 5) cta_qr_append_flag<true, 2>(R, ldr, B, ldb, nb, N, s_tau, s_u0, &s_step);
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
@@ -115,7 +120,8 @@ extern "C" int devtest_append(int mode, const double* A, double* R, int M, int N
     cudaMalloc(&da, (size_t)M * N * 16);
     cudaMalloc(&dr, (size_t)N * N * 16);
     cudaMemcpy(da, A, (size_t)M * N * 16, cudaMemcpyHostToDevice);
-    const size_t relems = mode >= 2 ? (size_t)N * (N + 1) / 2 : (size_t)(N | 1) * N;
+    const bool pk = mode == 2 || mode == 3 || mode == 5;
+    const size_t relems = pk ? (size_t)N * (N + 1) / 2 : (size_t)(N | 1) * N;
     const size_t sm = (relems + (size_t)33 * N) * 16;
     cudaFuncSetAttribute(k_devappend, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     k_devappend<<<1, threads, sm>>>(mode, da, dr, M, N);

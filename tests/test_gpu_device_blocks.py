@@ -175,11 +175,12 @@ def test_dmma_gemm(dev, nb, conj_s, strided):
 
 
 @pytest.mark.parametrize("M,N", [(250, 125), (96, 64), (40, 27), (300, 125), (33, 125)])
-@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4, 5])
 def test_qr_append_chunks(dev, M, N, mode):
     """R of a tall A by 32-row chunks appended into a triangle (structured Householder; modes 1/3 the
-    blocked compact-WY form with DMMA trailing updates, 2/3 on the packed triangle): R^*R = A^*A."""
-    if mode < 2 and N > 100:
+    blocked compact-WY form with DMMA trailing updates, 4/5 flag-synchronised without block barriers,
+    2/3/5 on the packed triangle): R^*R = A^*A."""
+    if mode in (0, 1, 4) and N > 100:
         pytest.skip("the dense k x k triangle does not fit shared memory for k > 100 (the library packs it)")
     dev.devtest_append.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                    ctypes.c_int]

@@ -24,7 +24,7 @@ _GPU = {}
 CASES = [(n, 1) for n in SMALL + ["C2"]] + [(n, 0) for n in SMALL]
 
 
-def gpu_run(name, eps=None, mode="FROB_BLOCKREL", sym=1, ws=0, split=1, fuse=0, direct=64, wy=1):
+def gpu_run(name, eps=None, mode="FROB_BLOCKREL", sym=1, ws=0, split=1, fuse=0, direct=64, wy=0):
     from paper_1809_04384_b200 import DH2
     from gpu_view import GpuView
     key = (name, eps, mode, sym, ws, split, fuse, direct, wy)
@@ -37,7 +37,8 @@ def gpu_run(name, eps=None, mode="FROB_BLOCKREL", sym=1, ws=0, split=1, fuse=0, 
         h.set_option("truncate_split", split)
         h.set_option("fuse_leaf_weights", fuse)
         h.set_option("fuse_direct_rows", direct)
-        h.set_option("qr_wy", wy)
+        h.set_option("qr_wy", 1 if wy == 1 else 0)
+        h.set_option("qr_flag", 1 if wy == 2 else 0)
         h.recompress(cfg["eps"] if eps is None else eps, mode)
         assert h.stats()["adjoint_symmetry"]["used"] == bool(sym)
         assert (h.stats()["truncate_ws_launches"] > 0) == bool(ws)
@@ -240,11 +241,12 @@ def test_storage_recomp_matches_oracle(name, sym):
             assert mine[f] == pytest.approx(ref[f], rel=1e-13), (which, f)
 
 
-@pytest.mark.parametrize("name", ["P4", "P5", "P7"])
-def test_qr_append_column_by_column(name):
-    """k = 125: the column-by-column chunk appends (qr_wy = 0) instead of the blocked compact-WY ones
-    give the same ranks, singular values and matrix."""
-    h, g, rc = gpu_run(name, wy=0)
+@pytest.mark.parametrize("name,wy", [("P4", 1), ("P5", 1), ("P7", 1), ("P4", 2), ("P5", 2), ("C1", 2), ("P2", 2), ("P7", 2)])
+def test_qr_append_column_by_column(name, wy):
+    """The chunk appends in their other forms give the same ranks, singular values and matrix:
+    wy = 1 blocked compact-WY (qr_wy = 1), wy = 2 flag-synchronised
+    (dh2_set_option qr_flag = 1)."""
+    h, g, rc = gpu_run(name, wy=wy)
     for side in ("row", "col"):
         go, oo = getattr(g, side), getattr(rc, side)
         assert go.rank == oo.rank
