@@ -1179,13 +1179,13 @@ __device__ inline void cta_qr_append(double2* R, int ldr, double2* B, int ldb, i
 // is published before applying it.  Warps run ahead or behind each other -- a reflection's data never
 // changes after its publication (column j is final once reflected, row j of R belongs to the column
 // owners), so the only synchronisation is producer -> consumers.  s_tau / s_u0 hold k entries.
-template <bool PK, int E>
+template <bool PK, int E, int G = 8>  // G lanes per column (32/G columns per warp at once), E rows per lane: nb <= G E
 __device__ inline void cta_qr_append_flag(double2* R, int ldr, double2* B, int ldb, int nb, int k, double* s_tau,
                                           double2* s_u0, int* s_step) {
-    constexpr int G = 16;
+    constexpr int NQ = 32 / G;  // column slots per warp
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-    const int gl = tid & (G - 1), half = lane >> 4;
-    const unsigned mask = 0xffffu << (lane & 16);
+    const int gl = tid & (G - 1), half = lane / G;
+    const unsigned mask = ((1u << G) - 1u) << (lane & ~(G - 1));
     cuda::atomic_ref<int, cuda::thread_scope_block> step(*s_step);
     auto reflector = [&](int j, double s) {  // lane 0 of the owner warp: publish reflection j
         const double2 alpha = R[ridx<PK>(j, j, ldr)];
@@ -1204,7 +1204,7 @@ __device__ inline void cta_qr_append_flag(double2* R, int ldr, double2* B, int l
         R[ridx<PK>(j, j, ldr)] = beta;  // nobody reads R[j, j] again
         step.store(j, cuda::memory_order_release);
     };
-    auto col_norm16 = [&](int c) {  // ||B(:, c)||^2 over one 16-lane half
+    auto col_norm16 = [&](int c) {  // ||B(:, c)||^2 over one G-lane slot
         double v = 0.0;
 #pragma unroll
         for (int e = 0; e < E; ++e)
@@ -1243,8 +1243,8 @@ __device__ inline void cta_qr_append_flag(double2* R, int ldr, double2* B, int l
         // this warp's columns > j, the column j+1 first (it feeds the next reflection)
         int c0 = warp;
         if (c0 <= j) c0 += ((j - c0) / nw + 1) * nw;
-        for (int cb = c0; cb < k; cb += 2 * nw) {
-            const int c = cb + half * nw;  // half 0: cb, half 1: cb + nw
+        for (int cb = c0; cb < k; cb += NQ * nw) {
+            const int c = cb + half * nw;  // slot q takes column cb + q nw
             const bool ok = c < k;
             double2 x[E];
             double2 rj = cmk(0.0, 0.0), w = cmk(0.0, 0.0);

@@ -273,7 +273,7 @@ __device__ __forceinline__ void qr_append(const PlanD& P, double2* R, int ldr, d
     if (E == 2 && P.qr_wy)
         cta_qr_append_wy<PK>(R, ldr, B, ldb, nb, k, wp);
     else if (P.qr_flag)
-        cta_qr_append_flag<PK, E>(R, ldr, B, ldb, nb, k, s_tau, s_u0, &s_step);
+        cta_qr_append_flag<PK, 2 * E, 8>(R, ldr, B, ldb, nb, k, s_tau, s_u0, &s_step);  // (nb <= 16 E = 8 (2E))
     else
         cta_qr_append<PK, E>(R, ldr, B, ldb, nb, k);  // (8-lane groups for the 48-row chunks: measured neutral)
 }

@@ -106,8 +106,8 @@ __global__ void k_devappend(int mode, const double2* A, double2* Rout, int M, in
         if (mode == 1) cta_qr_append_wy<false>(R, ldr, B, ldb, nb, N, &wp);
         if (mode == 2) cta_qr_append<true, 2>(R, ldr, B, ldb, nb, N);
         if (mode == 3) cta_qr_append_wy<true>(R, ldr, B, ldb, nb, N, &wp);
-        if (mode == 4) cta_qr_append_flag<false, 2>(R, ldr, B, ldb, nb, N, s_tau, s_u0, &s_step);
-        if (mode == 5) cta_qr_append_flag<true, 2>(R, ldr, B, ldb, nb, N, s_tau, s_u0, &s_step);
+        if (mode == 4) cta_qr_append_flag<false, 4, 8>(R, ldr, B, ldb, nb, N, s_tau, s_u0, &s_step);
+        if (mode == 5) cta_qr_append_flag<true, 4, 8>(R, ldr, B, ldb, nb, N, s_tau, s_u0, &s_step);
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
