@@ -137,6 +137,11 @@ int dh2_setup_device(dh2_ctx* ctx);
  * from the interpolation matrix). */
 int dh2_recompress(dh2_ctx* ctx, double eps, int32_t mode);
 
+/* Far-field matrix-vector product y = G_far x of the ORIG or RECOMP matrix: the admissible blocks
+ * only -- the nearfield (inadmissible leaves, singular Galerkin quadrature) is not
+ * assembled by this build, so y is NOT G x of the full Galerkin matrix (dh2_storage's
+ * nearfield_bytes counts what it would occupy).  ORIG needs V and S resident: DH2_ENOTIMPL on the
+ * memory-lean plan (dh2_get_stats "lean"). */
 /* Far-field matrix-vector product y = G_far x of the ORIG or RECOMP matrix.
  * x, y: n complex (2n float64) in original triangle order; host pointers
  * (flags = DH2_HOST_PTRS, copied through the context's stream) or device

@@ -147,6 +147,7 @@ class DH2:
         self._check(self.lib.dh2_recompress(self.h, float(eps), MODES[mode] if isinstance(mode, str) else int(mode)))
 
     def matvec(self, x, which=DH2_RECOMP):
+        """y = G_far x: the far field only (admissible blocks); the nearfield is not assembled."""
         x = np.ascontiguousarray(x, dtype=np.complex128)
         if x.shape != (self.n,):
             raise ValueError("x must have shape (n,)")

@@ -221,3 +221,29 @@ def test_scale_hutchinson_global_error(big):
     est = np.mean([np.linalg.norm(h.matvec(x, 0) - h.matvec(x, 1)) ** 2
                    for x in (seeded_vector(h.n, seed) for seed in range(1, 9))]) * 1.5
     assert exact > 0 and 0.5 * exact <= est <= 2.0 * exact, (est, exact)
+
+
+def test_scale_sampled_coupling_norms(big):
+    """Per level 25 more seeded blocks: ||S~_b||_F = ||G~_b||_F (Q, Q' orthonormal) against the lazy
+    oracle's, to 1e-10 ||G_b||_F (unitarily invariant: no expansion of the bases needed)."""
+    h, st, lz, cfg = big
+    blocks = h.export("blocks", np.int64).reshape(-1, 3)
+    St_off, kb = h.export("blk_St_off", np.int64), h.export("kb_row", np.int32)
+    prow, pcol = h.export("blk_prow", np.int32), h.export("blk_pcol", np.int32)
+    kr, kc = h.export("rank_row", np.int32), h.export("rank_col", np.int32)
+    g2 = h.export("normG2", np.float64)
+    ct = st.ct
+    lev = np.array([int(ct.level[int(t)]) for t in blocks[:, 0]])
+    rng = np.random.default_rng(44)
+    n = 0
+    for l in sorted(set(lev.tolist())):
+        idx = np.nonzero(lev == l)[0]
+        for b in rng.choice(idx, size=min(25, len(idx)), replace=False):
+            t, s, c = (int(v) for v in blocks[b])
+            a, cc, ld = int(kr[prow[b]]), int(kc[pcol[b]]), int(kb[prow[b]])
+            Stg = _sl(h, "St", St_off[b], ld * cc, np.complex128).reshape(cc, ld)[:, :a] if a and cc else np.zeros(0)
+            Ct, Cs = lz.truncate("row", t, c)["C"], lz.truncate("col", s, c)["C"]
+            no = np.linalg.norm(Ct @ lz.S(int(b)) @ Cs.conj().T)
+            assert abs(np.linalg.norm(Stg) - no) <= 1e-10 * np.sqrt(g2[b]), (l, t, s, c)
+            n += 1
+    assert n >= 100
