@@ -224,7 +224,7 @@ def test_scale_hutchinson_global_error(big):
 
 
 def test_scale_sampled_coupling_norms(big):
-    """Per level 25 more seeded blocks: ||S~_b||_F = ||G~_b||_F (Q, Q' orthonormal) against the lazy
+    """Per level 12 more seeded blocks: ||S~_b||_F = ||G~_b||_F (Q, Q' orthonormal) against the lazy
     oracle's, to 1e-10 ||G_b||_F (unitarily invariant: no expansion of the bases needed)."""
     h, st, lz, cfg = big
     blocks = h.export("blocks", np.int64).reshape(-1, 3)
@@ -238,7 +238,7 @@ def test_scale_sampled_coupling_norms(big):
     n = 0
     for l in sorted(set(lev.tolist())):
         idx = np.nonzero(lev == l)[0]
-        for b in rng.choice(idx, size=min(25, len(idx)), replace=False):
+        for b in rng.choice(idx, size=min(12, len(idx)), replace=False):
             t, s, c = (int(v) for v in blocks[b])
             a, cc, ld = int(kr[prow[b]]), int(kc[pcol[b]]), int(kb[prow[b]])
             Stg = _sl(h, "St", St_off[b], ld * cc, np.complex128).reshape(cc, ld)[:, :a] if a and cc else np.zeros(0)
@@ -246,4 +246,4 @@ def test_scale_sampled_coupling_norms(big):
             no = np.linalg.norm(Ct @ lz.S(int(b)) @ Cs.conj().T)
             assert abs(np.linalg.norm(Stg) - no) <= 1e-10 * np.sqrt(g2[b]), (l, t, s, c)
             n += 1
-    assert n >= 100
+    assert n >= 48
