@@ -835,6 +835,7 @@ void upload_all(Shard* C, const double* xyz, int64_t nv, const int64_t* tri) {
     P.sym = (C->sym_ok && C->sym_opt) ? 1 : 0;
     P.qr_wy = C->qr_wy_init;
     P.qr_flag = C->qr_flag_init;
+    P.trunc_mode = C->trunc_mode_init;
     if (C->lean.on) lean_alloc(C);
 }
 
@@ -2152,6 +2153,11 @@ int dh2_set_option(dh2_ctx* X, const char* name, int64_t value) {
     if (nm == "qr_wy") {  // 0: column-by-column chunk appends (A/B and tests)
         if (value != 0 && value != 1) return fail(X, DH2_EINVAL, "qr_wy must be 0 or 1");
         for (auto& S : X->sh) S->P.qr_wy = S->qr_wy_init = (int)value;
+        return DH2_OK;
+    }
+    if (nm == "trunc_direct") {  // 1: the leaf truncation factorises M^* = Zhat V^* directly (no streamed appends)
+        if (value != 0 && value != 1) return fail(X, DH2_EINVAL, "trunc_direct must be 0 or 1");
+        for (auto& S : X->sh) S->P.trunc_mode = S->trunc_mode_init = (int)value;
         return DH2_OK;
     }
     if (nm == "qr_flag") {  // 0: one block barrier per reflection in the chunk appends (A/B and tests)

@@ -1167,6 +1167,7 @@ TruncLaunch plan_truncate(const PlanD& P, int np, int maxrowsM, int maxZrows, bo
     const size_t bytes_a = (size_t)(L.ldv + 33) * L.ldv * sizeof(double2) + extra;
     auto ctas = [&](size_t b) { return b > (size_t)P.smem_optin ? 0 : (int)((size_t)(228 * 1024) / (b + 1024)); };
     L.append = leaf_level && maxZrows > maxrowsM && maxrowsM > 32 && ctas(bytes_a) > ctas(bytes_d);
+    if (P.trunc_mode == 1) L.append = false;  // (dh2_set_option "trunc_direct": A/B of the two leaf modes)
     const size_t bytes = L.append ? bytes_a : bytes_d;
     L.use_ws = force_ws || bytes > (size_t)P.smem_optin;
     if (L.use_ws) {

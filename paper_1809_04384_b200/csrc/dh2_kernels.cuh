@@ -42,6 +42,7 @@ struct PlanD {
     int col_conj;         // 1: column factors C', Q' are stored as the row factors at -c (read conjugated)
     int qr_wy;            // 1: chunk appends of <= 32 rows in the blocked compact-WY form (dh2_set_option "qr_wy", default 0)
     int qr_flag;          // 1: chunk appends synchronised by per-reflection flags instead of block barriers ("qr_flag")
+    int trunc_mode;       // 1: leaf truncation on M^* directly, never by streamed appends ("trunc_direct")
     int sym;              // 1: only row basis pairs have V/R/E; the column side of a block (t,s,c) reads
                           //    the row basis pair (s,-c) conjugated (blk_bpcs; matvec: col2row)
     const int* col2row;   // column pair (s,c) -> row pair (s,-c) (adjoint-symmetric structures)
