@@ -5,7 +5,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB = os.path.join(HERE, "libdh2.so")
-SOURCES = ["csrc/dh2_kernels.cu", "csrc/dh2_api.cu", "csrc/dh2_lean.cu", "csrc/dh2_host.cpp"]
+SOURCES = ["csrc/dh2_kernels.cu", "csrc/dh2_api.cu", "csrc/dh2_lean.cu", "csrc/dh2_cq.cu", "csrc/dh2_host.cpp"]
 HEADERS = ["csrc/dh2_device.cuh", "csrc/dh2_kernels.cuh", "csrc/dh2_host.h", "csrc/dh2_shard.h", "../include/dh2.h"]
 
 NVCC_FLAGS = [

@@ -666,6 +666,7 @@ size_t plan_bytes(const Shard* C) {
             b += (size_t)((X == &C->col && C->sym_ok ? 0 : X->Z_total) + X->C_total + X->C_extra + X->Q_total) * 16 +
                  (size_t)X->sig_total * 8;
     b += (size_t)C->n * 7 * 32 + (size_t)C->nclusters * sizeof(GridD);
+    b += cq_scratch_bytes_bound(C->k);
     return b;
 }
 
@@ -836,6 +837,14 @@ void upload_all(Shard* C, const double* xyz, int64_t nv, const int64_t* tri) {
     P.qr_wy = C->qr_wy_init;
     P.qr_flag = C->qr_flag_init;
     P.trunc_mode = C->trunc_mode_init;
+    P.qr_cq = C->qr_cq_init;
+    P.qr_cq_tw = C->qr_cq_tw_init;
+    if (P.k > 64 && P.k <= 128) {
+        C->d_cq.alloc(cq_scratch_elems(P));
+        P.cq_scr = C->d_cq.p;
+    } else {
+        P.cq_scr = nullptr;
+    }
     if (C->lean.on) lean_alloc(C);
 }
 
@@ -2153,6 +2162,16 @@ int dh2_set_option(dh2_ctx* X, const char* name, int64_t value) {
     if (nm == "qr_wy") {  // 0: column-by-column chunk appends (A/B and tests)
         if (value != 0 && value != 1) return fail(X, DH2_EINVAL, "qr_wy must be 0 or 1");
         for (auto& S : X->sh) S->P.qr_wy = S->qr_wy_init = (int)value;
+        return DH2_OK;
+    }
+    if (nm == "qr_cq" || nm == "qr_cq_tw") {  // 0: k > 64 basis (total) weights by the CTA-cooperative appends
+        if (value < 0 || value > 2) return fail(X, DH2_EINVAL, nm + " must be 0, 1 or 2 (variant)");
+        for (auto& S : X->sh) {
+            if (nm == "qr_cq")
+                S->P.qr_cq = S->qr_cq_init = (int)value;
+            else
+                S->P.qr_cq_tw = S->qr_cq_tw_init = (int)value;
+        }
         return DH2_OK;
     }
     if (nm == "trunc_direct") {  // 1: the leaf truncation factorises M^* = Zhat V^* directly (no streamed appends)

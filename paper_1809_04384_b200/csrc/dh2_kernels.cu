@@ -360,6 +360,7 @@ static size_t qr_chunk_smem(const PlanD& P, bool pk, int ldr, int ldb, int nE, b
 
 void launch_basis(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStream_t s) {
     if (!nbps) return;
+    if (P.k > 64 && P.k <= 128 && P.qr_cq && P.cq_scr) return launch_basis_cq(P, bps, nbps, s);
     const bool any_qr = maxrows > P.k;
     const int ldr = odd_ld(P.k);
     if (P.k <= 64) {  // 64-row chunks, packed triangle
@@ -526,6 +527,7 @@ __global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, const int* m
 
 void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* mirror, cudaStream_t s) {
     if (!np) return;
+    if (P.k > 64 && P.k <= 128 && P.qr_cq_tw && P.cq_scr) return launch_total_weights_cq(P, row, p0, np, mirror, s);
     const int ldr = odd_ld(P.k);
     const PassD& X = row ? P.row : P.col;
     if (P.k <= 64) {  // 64-row chunks, packed triangle

@@ -325,6 +325,7 @@ double lean_bytes(const Shard* C) {
     const int L = T.depth;
     double b = 16.0 * ((double)C->VR_total + Ln.E_total + Ln.Z_scratch + Ln.S_slots * (double)k * k);
     b += 8.0 * X.sig_total + (double)C->n * 7 * 32 + (double)C->nclusters * sizeof(GridD);
+    b += (double)cq_scratch_bytes_bound(k);
     b += 16.0 * (double)k * (X.bp.size() + C->col.bp.size()) + 16.0 * 4 * C->n;  // matvec xh, yh, x, y
     const double r_est = std::max(8.0, k / 8.0);  // ranks measured on C4q/C5q: mean 11-20 at k = 125
     double cb = 0, qb = 0, comp = 0, st = 0;
