@@ -1018,7 +1018,15 @@ void truncate_level(Shard* C, PassH& X, bool row, int l, int p0, int np, int max
     } else {
     const TruncLaunch TL = plan_truncate(P, np, maxrows, maxz, all_leaf, C->force_ws != 0);
     const bool split = C->split_trunc && all_leaf && maxrows <= 32 && !TL.use_ws && (!fused || P.k <= 64);
-    if (fused && !split) {  // leaf total weights folded into one CTA per pair (k_truncate_fused)
+    const bool split64 = C->split_trunc64 && all_leaf && maxrows > 32 && maxrows <= 64 && !TL.use_ws && !TL.append && !fused;
+    if (split64) {
+        const size_t need = trunc_split64_scratch_bytes(np);
+        if (C->d_tscr.n < need) {
+            CK(cudaStreamSynchronize(s));
+            C->d_tscr.alloc(need);
+        }
+        C->timed(cls, 2, [&] { launch_truncate_split64(P, row, p0, np, TL, eps, mode, C->d_tscr.p, s); });
+    } else if (fused && !split) {  // leaf total weights folded into one CTA per pair (k_truncate_fused)
         C->timed(cls, 1, [&] { launch_truncate_fused(P, row, p0, np, maxrows, eps, mode, mirror, s); });
     } else if (split) {
         const size_t need = trunc_split_scratch_bytes(np);
@@ -1036,7 +1044,7 @@ void truncate_level(Shard* C, PassH& X, bool row, int l, int p0, int np, int max
         }
         ++C->ws_launches;
     }
-    if (!split && !fused) C->timed(cls, 1, [&] { launch_truncate(P, row, p0, np, TL, all_leaf, eps, mode, C->d_ws.p, s); });
+    if (!split && !split64 && !fused) C->timed(cls, 1, [&] { launch_truncate(P, row, p0, np, TL, all_leaf, eps, mode, C->d_ws.p, s); });
     }
     CK(cudaMemcpyAsync(X.rank.data() + p0, X.d_rank.p + p0, np * sizeof(int), cudaMemcpyDeviceToHost, s));
     if ((int)C->sweeps_h.size() < np) C->sweeps_h.resize(np);
@@ -2162,6 +2170,11 @@ int dh2_set_option(dh2_ctx* X, const char* name, int64_t value) {
     if (nm == "qr_wy") {  // 0: column-by-column chunk appends (A/B and tests)
         if (value != 0 && value != 1) return fail(X, DH2_EINVAL, "qr_wy must be 0 or 1");
         for (auto& S : X->sh) S->P.qr_wy = S->qr_wy_init = (int)value;
+        return DH2_OK;
+    }
+    if (nm == "truncate_split64") {  // 0: leaves of 33..64 truncated by one kernel (k_truncate)
+        if (value != 0 && value != 1) return fail(X, DH2_EINVAL, "truncate_split64 must be 0 or 1");
+        for (auto& S : X->sh) S->split_trunc64 = (int)value;
         return DH2_OK;
     }
     if (nm == "qr_cq" || nm == "qr_cq_tw") {  // 0: k > 64 basis (total) weights by the CTA-cooperative appends

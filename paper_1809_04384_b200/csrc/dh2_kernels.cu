@@ -1140,6 +1140,89 @@ __global__ void __launch_bounds__(128) k_trunc_epi(PlanD P, PassD X, int p0, con
     truncate_epilogue(X, p, P.k, B, 33, ncol, rowsM, piv, nrm, ord, Vt, rowsM, rowsM, eps, mode, s_rank);
 }
 
+// ------------------------------------------------------------------ leaf truncation, wide split path
+// Leaves of 33..64 triangles (C4/C5: 64): the one-sided Jacobi is half of the leaf truncation and
+// the direct prologue (M^* = Zhat V^*, up to 125 x 64 in shared memory) allows one CTA per SM, so
+// the Jacobi rounds (one block barrier each) run one pair per SM.  Split: (1) k_trunc_qr64, the
+// prologue and pivoted QR exactly as k_truncate (one CTA per SM), R (ncol x rowsM) and the pivot
+// order to a scratch slab; (2) k_trunc_jepi64, Jacobi on the rows of R and the epilogue with R
+// alone in shared memory (66 KB: three pairs per SM).  Same device functions, same results.
+constexpr int T64 = 64;
+__global__ void __launch_bounds__(512, 1) k_trunc_qr64(PlanD P, PassD X, int p0, int ldv, int ldb, double2* sR, int* sPiv,
+                                                      int* sMeta) {
+    extern __shared__ double2 smd[];
+    __shared__ int s_piv;
+    __shared__ double2 sh[2];
+    const int i = blockIdx.x, p = p0 + i;
+    double2* B;
+    double* nrm;
+    int *piv, *ord;
+    int rowsM, ldvt, ldB;
+    const double2* Vt;
+    const int ncol = truncate_prologue<true>(P, X, p, smd, ldv, ldb, false, B, ldB, nrm, piv, ord, rowsM, Vt, ldvt, s_piv, sh);
+    if (threadIdx.x == 0) {
+        sMeta[2 * i] = ncol;  // -1: empty pair, already recorded
+        sMeta[2 * i + 1] = rowsM;
+    }
+    if (ncol < 0) return;
+    double2* R = sR + (size_t)i * T64 * T64;  // column-major, ld 64
+    for (int idx = threadIdx.x; idx < ncol * rowsM; idx += blockDim.x) {
+        const int r = idx % ncol, j = idx / ncol;
+        R[r + (size_t)j * T64] = B[r + (size_t)j * ldB];
+    }
+    for (int j = threadIdx.x; j < rowsM; j += blockDim.x) sPiv[i * T64 + j] = piv[j];
+}
+
+__global__ void __launch_bounds__(128, 3) k_trunc_jepi64(PlanD P, PassD X, int p0, const double2* sR, const int* sPiv,
+                                                        const int* sMeta, double eps, int mode) {
+    constexpr int LD = T64 + 1;
+    extern __shared__ double2 smd[];
+    __shared__ double nrm[T64];
+    __shared__ int piv[T64], ord[T64];
+    __shared__ int flag, s_rank;
+    const int i = blockIdx.x, p = p0 + i;
+    const int ncol = sMeta[2 * i], rowsM = sMeta[2 * i + 1];
+    if (ncol < 0) return;
+    double2* B = smd;
+    const double2* R = sR + (size_t)i * T64 * T64;
+    for (int idx = threadIdx.x; idx < ncol * rowsM; idx += blockDim.x) {
+        const int r = idx % ncol, j = idx / ncol;
+        B[r + (size_t)j * LD] = R[r + (size_t)j * T64];
+    }
+    for (int j = threadIdx.x; j < rowsM; j += blockDim.x) piv[j] = sPiv[i * T64 + j];
+    __syncthreads();
+    const int nsw = jacobi_rows_auto(B, LD, ncol, rowsM, nrm, &flag);
+    if (threadIdx.x == 0) X.sweeps[p] = nsw;
+    const int bp = X.bp[p];
+    const double2* Vt = P.V + P.bp_V_off[bp];
+    truncate_epilogue(X, p, P.k, B, LD, ncol, rowsM, piv, nrm, ord, Vt, rowsM, rowsM, eps, mode, s_rank);
+}
+
+size_t trunc_split64_scratch_bytes(int np) {
+    return (size_t)np * (T64 * T64 * sizeof(double2) + T64 * sizeof(int) + 2 * sizeof(int));
+}
+
+void launch_truncate_split64(const PlanD& P, bool row, int p0, int np, const TruncLaunch& L, double eps, int mode,
+                             void* scratch, cudaStream_t s) {
+    if (!np) return;
+    const PassD& X = row ? P.row : P.col;
+    double2* sR = reinterpret_cast<double2*>(scratch);
+    int* sPiv = reinterpret_cast<int*>(sR + (size_t)np * T64 * T64);
+    int* sMeta = sPiv + (size_t)np * T64;
+    static size_t attr_qr = 0, attr_j = 0;
+    const size_t smj = (size_t)(T64 + 1) * T64 * sizeof(double2);
+    if (L.smem > attr_qr) {
+        cudaFuncSetAttribute(k_trunc_qr64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+        attr_qr = L.smem;
+    }
+    if (smj > attr_j) {
+        cudaFuncSetAttribute(k_trunc_jepi64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smj);
+        attr_j = smj;
+    }
+    k_trunc_qr64<<<np, 512, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, sR, sPiv, sMeta);
+    k_trunc_jepi64<<<np, 128, smj, s>>>(P, X, p0, sR, sPiv, sMeta, eps, mode);
+}
+
 size_t trunc_split_scratch_bytes(int np) { return (size_t)np * (1024 * sizeof(double2) + 32 * sizeof(double) + 34 * sizeof(int)); }
 
 void launch_truncate_split(const PlanD& P, bool row, int p0, int np, const TruncLaunch& L, double eps, int mode,

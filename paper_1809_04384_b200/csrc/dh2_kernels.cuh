@@ -125,6 +125,11 @@ void launch_truncate(const PlanD& P, bool row, int p0, int np, const TruncLaunch
                      int mode, double2* ws, cudaStream_t s, const int* plist = nullptr);
 // leaf levels with #t <= 32: pivoted QR per CTA, register-resident warp Jacobi, epilogue
 size_t trunc_split_scratch_bytes(int np);
+// leaf levels with 32 < #t <= 64 (C4/C5): prologue + pivoted QR (one CTA per SM), then Jacobi +
+// epilogue with R alone in shared memory (three pairs per SM)
+size_t trunc_split64_scratch_bytes(int np);
+void launch_truncate_split64(const PlanD& P, bool row, int p0, int np, const TruncLaunch& L, double eps, int mode,
+                             void* scratch, cudaStream_t s);
 // fused: leaf total weights folded into the QR kernel (k_trunc_zqr, k <= 64; the level's Zhat is
 // not formed; stacks of <= fuse_direct rows form M^* directly, taller ones are QR-appended;
 // mirror as for launch_total_weights)

@@ -267,6 +267,7 @@ struct Shard {
     DevBuf<double2> d_cq;    // their scratch triangles
     int trunc_mode_init = 1; // initial value of PlanD::trunc_mode (direct: measured -3 % C4, -16 % C5 leaves)
     int qr_wy_init = 0;      // initial value of PlanD::qr_wy (blocked WY appends measured slower on C4: 0) (dh2_set_option("qr_wy") sets the plan directly)
+    int split_trunc64 = 1;   // dh2_set_option("truncate_split64"): leaves of 33..64 as QR kernel + Jacobi/epilogue kernel
     int split_trunc = 1;     // dh2_set_option("truncate_split"): warp-register Jacobi for leaves <= 32
     int fuse_leaf = 0;       // dh2_set_option("fuse_leaf_weights"): leaf Zhat folded into the split QR
     std::vector<int> fused_levels[2];  // levels of the last recompress whose Zhat was fused (row, col)

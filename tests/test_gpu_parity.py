@@ -263,3 +263,25 @@ def test_qr_append_column_by_column(name, wy):
     x = seeded_vector(rc.st.n, 1)
     yo = ops.matvec(rc, x, "orig")
     assert np.linalg.norm(h.matvec(x, 1) - ops.matvec(rc, x, "recomp")) <= 1e-10 * np.linalg.norm(yo)
+
+
+@pytest.mark.parametrize("name", ["P6", "P7", "C4s", "C5s"])
+def test_truncate_split64_bitwise(name):
+    """Leaves of 33..64 triangles (leaf 64 at k = 125): the split path (pivoted QR kernel, then the
+    Jacobi + epilogue kernel at three pairs per SM; default) runs the same device functions on the
+    same data as the single truncation kernel (dh2_set_option truncate_split64 = 0), so ranks,
+    singular values and the recompressed matvec are bitwise equal."""
+    from paper_1809_04384_b200 import DH2
+    cfg = get_config(name)
+    xyz, tri = mesh_for(cfg)
+    out = []
+    for v in (1, 0):
+        h = DH2(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"])
+        h.set_option("truncate_split64", v)
+        h.recompress(cfg["eps"])
+        x = seeded_vector(h.n, 3)
+        out.append((h.export("rank_row", np.int32), h.export("sigma_row", np.float64), h.matvec(x, 1)))
+        h.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
+    assert np.array_equal(out[0][2], out[1][2])
