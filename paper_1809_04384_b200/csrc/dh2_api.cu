@@ -838,7 +838,9 @@ void upload_all(Shard* C, const double* xyz, int64_t nv, const int64_t* tri) {
     P.qr_flag = C->qr_flag_init;
     P.trunc_mode = C->trunc_mode_init;
     P.qr_cq = C->qr_cq_init;
+    P.t64_threads = C->t64_threads_init;
     P.qr_cq_tw = C->qr_cq_tw_init;
+    P.qr_cq_tw_leaf = C->qr_cq_tw_leaf_init;
     if (P.k > 64 && P.k <= 128) {
         C->d_cq.alloc(cq_scratch_elems(P));
         P.cq_scr = C->d_cq.p;
@@ -1157,7 +1159,10 @@ void run_weights_truncate(Shard* C, double eps, int mode) {
         for (int l = 0; l <= L; ++l) {
             int p0 = X.own_lo[l], np = X.own_hi[l] - p0;
             if (!np || fused[l]) continue;
-            C->timed(std::string(row ? "total_weights_row@" : "total_weights_col@") + std::to_string(l), 1, [&] { launch_total_weights(P, row, p0, np, C->d_blk_mirror.p, s); });
+            bool all_leaf, any_leaf;
+            level_kind(l, all_leaf, any_leaf);
+            C->timed(std::string(row ? "total_weights_row@" : "total_weights_col@") + std::to_string(l), 1,
+                     [&] { launch_total_weights(P, row, p0, np, C->d_blk_mirror.p, s, all_leaf); });
             double fl = 0;
             for (int p = p0; p < p0 + np; ++p) {
                 for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) {
@@ -2172,18 +2177,25 @@ int dh2_set_option(dh2_ctx* X, const char* name, int64_t value) {
         for (auto& S : X->sh) S->P.qr_wy = S->qr_wy_init = (int)value;
         return DH2_OK;
     }
+    if (nm == "trunc64_threads") {
+        if (value != 64 && value != 128 && value != 256) return fail(X, DH2_EINVAL, "trunc64_threads must be 64, 128 or 256");
+        for (auto& S : X->sh) S->P.t64_threads = S->t64_threads_init = (int)value;
+        return DH2_OK;
+    }
     if (nm == "truncate_split64") {  // 0: leaves of 33..64 truncated by one kernel (k_truncate)
         if (value != 0 && value != 1) return fail(X, DH2_EINVAL, "truncate_split64 must be 0 or 1");
         for (auto& S : X->sh) S->split_trunc64 = (int)value;
         return DH2_OK;
     }
-    if (nm == "qr_cq" || nm == "qr_cq_tw") {  // 0: k > 64 basis (total) weights by the CTA-cooperative appends
-        if (value < 0 || value > 2) return fail(X, DH2_EINVAL, nm + " must be 0, 1 or 2 (variant)");
+    if (nm == "qr_cq" || nm == "qr_cq_tw" || nm == "qr_cq_tw_leaf") {  // 0: k > 64 basis (total) weights by the CTA-cooperative appends
+        if (value < 0 || value > 3) return fail(X, DH2_EINVAL, nm + " must be 0..3 (variant)");
         for (auto& S : X->sh) {
             if (nm == "qr_cq")
                 S->P.qr_cq = S->qr_cq_init = (int)value;
-            else
+            else if (nm == "qr_cq_tw")
                 S->P.qr_cq_tw = S->qr_cq_tw_init = (int)value;
+            else
+                S->P.qr_cq_tw_leaf = S->qr_cq_tw_leaf_init = (int)value;
         }
         return DH2_OK;
     }

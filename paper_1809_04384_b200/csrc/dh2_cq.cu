@@ -296,10 +296,39 @@ __global__ void __launch_bounds__(128 / NC, CTAS) k_basis_cq(PlanD P, const int*
     }
 }
 
+// Chunk rows of the total weights by thread-column FP64 FMAs (qr_cq_tw = 3): thread c forms column c
+// of the NB-row chunk w X~ S~ directly in its registers, X~ = the staged rows of R_sc (shared,
+// broadcast reads; conjugated when stored conjugated), S~(mu, c) = S_b[c, mu] (or S_b[mu, c] when
+// strided), conjugated for the row pass -- one coalesced 16-byte load per mu per thread, NB
+// independent accumulators.  X~ S~ with an odd number of conjugations is accumulated as
+// x conj(s); conj_x is applied to the sum: sum conj(x) s = conj(sum x conj(s)).
+template <int NB, bool XCS>
+__device__ __forceinline__ void cq_gemm_cols(double2 (&b)[NB], const double2* Xs, int ldx, const double2* Sg, bool strided,
+                                             int k) {
+    const int c = threadIdx.x;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) b[i] = cmk(0.0, 0.0);
+    if (c >= k) return;
+    const double2* sp = strided ? Sg + (size_t)c * k : Sg + c;
+    const size_t ss = strided ? 1 : (size_t)k;
+#pragma unroll 2
+    for (int mu = 0; mu < k; ++mu) {
+        const double2 sv = sp[(size_t)mu * ss];
+        const double2* xr = Xs + (size_t)mu * ldx;
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            if (XCS)
+                cfma_bj(b[i], xr[i], sv);
+            else
+                cfma(b[i], xr[i], sv);
+        }
+    }
+}
+
 // Total weights, persistent grid (see k_total_weights: the rows of Z_tc^* are w_b R_sc S_b^*
 // (row pass; column pass w_b R_tc S_b) for the blocks of the pair, then Zhat_{t+c+} E_{tc+}^* for
 // its parents; Zhat_tc = R of their QR, or the rows themselves when there are <= k of them).
-template <int NB, int NC, int CTAS>
+template <int NB, int NC, int CTAS, bool TCOL>
 __global__ void __launch_bounds__(128 / NC, CTAS) k_total_weights_cq(PlanD P, PassD X, bool row, int p0, int np,
                                                                          const int* mirror, double2* scr) {
     extern __shared__ double2 sm[];
@@ -347,6 +376,36 @@ __global__ void __launch_bounds__(128 / NC, CTAS) k_total_weights_cq(PlanD P, Pa
             const int mb = row ? bb : mirror[bb];
             const double2* Sg = P.S + (size_t)P.blk_slot[mb >= 0 ? mb : bb] * k * k;
             const bool strided = !row && mb < 0;
+            if (qr && TCOL) {
+                // chunks of one block only (the last one zero-padded: zero rows change no norm or dot
+                // product), formed in the registers by cq_gemm_cols and appended at once
+                if (fill > 0) {  // (rows of an earlier source pending)
+                    __syncthreads();
+                    cq_load<NB, NC>(b, Bs, LDB, fill, k);
+                    cq_append<NB, NC>(b, Rs, k, first, sh);
+                    first = false;
+                    fill = 0;
+                }
+                const bool xcs = row != cj;  // S conjugated XOR X stored conjugated
+                for (int i0 = 0; i0 < r; i0 += NB) {
+                    const int nb = min(NB, r - i0);
+                    __syncthreads();
+                    stage_rows(Bs, LDB, Ro, r, i0, nb, k);
+                    for (int idx = threadIdx.x; idx < (NB - nb) * k; idx += blockDim.x)
+                        Bs[nb + idx % (NB - nb) + (size_t)(idx / (NB - nb)) * LDB] = cmk(0.0, 0.0);
+                    cp_async_wait_all();
+                    __syncthreads();
+                    if (xcs)
+                        cq_gemm_cols<NB, true>(b[0], Bs, LDB, Sg, strided, k);
+                    else
+                        cq_gemm_cols<NB, false>(b[0], Bs, LDB, Sg, strided, k);
+#pragma unroll
+                    for (int i = 0; i < NB; ++i) b[0][i] = cj ? cmk(w * b[0][i].x, -w * b[0][i].y) : cscale(b[0][i], w);
+                    cq_append<NB, NC>(b, Rs, k, first, sh);
+                    first = false;
+                }
+                continue;
+            }
             for (int i0 = 0; i0 < r;) {
                 const int nb = qr ? min(NB - fill, r - i0) : min(NB, r - i0);
                 double2* dst = qr ? Bs + fill : Zg + cur;
@@ -391,10 +450,12 @@ __global__ void __launch_bounds__(128 / NC, CTAS) k_total_weights_cq(PlanD P, Pa
 
 // Variants (dh2_set_option "qr_cq" for the basis weights, "qr_cq_tw" for the total weights):
 // 1 = NB 16 rows at 4 CTAs per SM (128 registers; default), 2 = NB 24 at 3 (168 registers).
-// Measured on C4 (k = 125): basis weights 3.1 s (cta_qr_append) -> 1.8 s (1) / 2.14 s (2: the
-// 128-row stacks of the level above the leaves fill 6 chunks of 24 = 144 rows); total weights
-// 2.2 s -> 2.26 s (1) / 2.26 s (2): their chunk formation (DMMA rows w_b R_sc S_b^* with 4 warps,
-// S_b re-read per chunk) outweighs the faster appends, so qr_cq_tw stays off by default.
+// 3 = total weights with thread-column chunk rows (cq_gemm_cols).  Measured on C4 (k = 125):
+// basis weights 3.1 s (cta_qr_append) -> 1.8 s (1) / 2.14 s (2: the 128-row stacks of the level
+// above the leaves fill 6 chunks of 24 = 144 rows); total weights: the CTA-cooperative kernel
+// stays above the leaves (its 48-row DMMA chunks read S_b three times per 125-row block; the
+// thread-column rows of 16-row chunks eight times: +9 %), variant 3 runs the leaf levels (blocks
+// of 64-row leaf weights: C4 1.36 -> 1.24 s, C5 1.91 -> 1.81 s).
 // Microbenchmark (tools/cq_bench.cu, k = 125, appends only): 2: 9.96 TF/s, 1: 9.07, NB 32 at 2 CTAs
 // 8.58, NB 8 at 4 CTAs 6.57; two columns per thread (t, 127 - t) at NB 8 / 8 CTAs: 6.3.
 constexpr int CQ_MAX_CTAS = 8;
@@ -416,16 +477,16 @@ static void cq_basis(const PlanD& P, const int* bps, int nbps, cudaStream_t s) {
     k_basis_cq<NB, NC, CTAS><<<grid, 128 / NC, cq_smem(P, NB, 6), s>>>(P, bps, nbps, P.cq_scr);
 }
 
-template <int NB, int NC, int CTAS>
+template <int NB, int NC, int CTAS, bool TCOL>
 static void cq_total(const PlanD& P, const PassD& X, bool row, int p0, int np, const int* mirror, cudaStream_t s) {
     static_assert(CTAS <= CQ_MAX_CTAS, "scratch");
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_total_weights_cq<NB, NC, CTAS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        cudaFuncSetAttribute(k_total_weights_cq<NB, NC, CTAS, TCOL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
         attr = true;
     }
     const int grid = std::min(np, P.num_sms * CTAS);
-    k_total_weights_cq<NB, NC, CTAS><<<grid, 128 / NC, cq_smem(P, NB, 3), s>>>(P, X, row, p0, np, mirror, P.cq_scr);
+    k_total_weights_cq<NB, NC, CTAS, TCOL><<<grid, 128 / NC, cq_smem(P, NB, 3), s>>>(P, X, row, p0, np, mirror, P.cq_scr);
 }
 
 void launch_basis_cq(const PlanD& P, const int* bps, int nbps, cudaStream_t s) {
@@ -436,12 +497,13 @@ void launch_basis_cq(const PlanD& P, const int* bps, int nbps, cudaStream_t s) {
     }
 }
 
-void launch_total_weights_cq(const PlanD& P, bool row, int p0, int np, const int* mirror, cudaStream_t s) {
+void launch_total_weights_cq(const PlanD& P, bool row, int p0, int np, const int* mirror, cudaStream_t s, int variant) {
     if (!np) return;
     const PassD& X = row ? P.row : P.col;
-    switch (P.qr_cq_tw) {
-        case 2: cq_total<24, 1, 3>(P, X, row, p0, np, mirror, s); break;
-        default: cq_total<16, 1, 4>(P, X, row, p0, np, mirror, s); break;
+    switch (variant) {
+        case 2: cq_total<24, 1, 3, false>(P, X, row, p0, np, mirror, s); break;
+        case 3: cq_total<16, 1, 4, true>(P, X, row, p0, np, mirror, s); break;
+        default: cq_total<16, 1, 4, false>(P, X, row, p0, np, mirror, s); break;
     }
 }
 

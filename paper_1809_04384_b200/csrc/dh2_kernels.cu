@@ -525,9 +525,10 @@ __global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, const int* m
     }
 }
 
-void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* mirror, cudaStream_t s) {
+void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* mirror, cudaStream_t s, bool leaf_level) {
     if (!np) return;
-    if (P.k > 64 && P.k <= 128 && P.qr_cq_tw && P.cq_scr) return launch_total_weights_cq(P, row, p0, np, mirror, s);
+    const int v = leaf_level && P.qr_cq_tw_leaf ? P.qr_cq_tw_leaf : P.qr_cq_tw;
+    if (P.k > 64 && P.k <= 128 && v && P.cq_scr) return launch_total_weights_cq(P, row, p0, np, mirror, s, v);
     const int ldr = odd_ld(P.k);
     const PassD& X = row ? P.row : P.col;
     if (P.k <= 64) {  // 64-row chunks, packed triangle
@@ -1173,8 +1174,10 @@ __global__ void __launch_bounds__(512, 1) k_trunc_qr64(PlanD P, PassD X, int p0,
     for (int j = threadIdx.x; j < rowsM; j += blockDim.x) sPiv[i * T64 + j] = piv[j];
 }
 
-__global__ void __launch_bounds__(128, 3) k_trunc_jepi64(PlanD P, PassD X, int p0, const double2* sR, const int* sPiv,
-                                                        const int* sMeta, double eps, int mode) {
+template <int NT>
+__global__ void __launch_bounds__(NT, NT == 64 ? 3 : NT == 128 ? 3 : 2) k_trunc_jepi64(PlanD P, PassD X, int p0, const double2* sR,
+                                                                                   const int* sPiv, const int* sMeta, double eps,
+                                                                                   int mode) {
     constexpr int LD = T64 + 1;
     extern __shared__ double2 smd[];
     __shared__ double nrm[T64];
@@ -1209,18 +1212,27 @@ void launch_truncate_split64(const PlanD& P, bool row, int p0, int np, const Tru
     double2* sR = reinterpret_cast<double2*>(scratch);
     int* sPiv = reinterpret_cast<int*>(sR + (size_t)np * T64 * T64);
     int* sMeta = sPiv + (size_t)np * T64;
-    static size_t attr_qr = 0, attr_j = 0;
+    static size_t attr_qr = 0;
+    static bool attr_j = false;
     const size_t smj = (size_t)(T64 + 1) * T64 * sizeof(double2);
     if (L.smem > attr_qr) {
         cudaFuncSetAttribute(k_trunc_qr64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
         attr_qr = L.smem;
     }
-    if (smj > attr_j) {
-        cudaFuncSetAttribute(k_trunc_jepi64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smj);
-        attr_j = smj;
+    if (!attr_j) {
+        cudaFuncSetAttribute(k_trunc_jepi64<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smj);
+        cudaFuncSetAttribute(k_trunc_jepi64<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smj);
+        cudaFuncSetAttribute(k_trunc_jepi64<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smj);
+        attr_j = true;
     }
     k_trunc_qr64<<<np, 512, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, sR, sPiv, sMeta);
-    k_trunc_jepi64<<<np, 128, smj, s>>>(P, X, p0, sR, sPiv, sMeta, eps, mode);
+    // Jacobi + epilogue threads (dh2_set_option "trunc64_threads")
+    if (P.t64_threads == 64)
+        k_trunc_jepi64<64><<<np, 64, smj, s>>>(P, X, p0, sR, sPiv, sMeta, eps, mode);
+    else if (P.t64_threads == 256)
+        k_trunc_jepi64<256><<<np, 256, smj, s>>>(P, X, p0, sR, sPiv, sMeta, eps, mode);
+    else
+        k_trunc_jepi64<128><<<np, 128, smj, s>>>(P, X, p0, sR, sPiv, sMeta, eps, mode);
 }
 
 size_t trunc_split_scratch_bytes(int np) { return (size_t)np * (1024 * sizeof(double2) + 32 * sizeof(double) + 34 * sizeof(int)); }

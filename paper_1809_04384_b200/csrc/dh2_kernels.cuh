@@ -45,7 +45,9 @@ struct PlanD {
     int trunc_mode;       // 1: leaf truncation on M^* directly, never by streamed appends ("trunc_direct")
     int qr_cq;            // != 0: k > 64 basis weights by column-per-thread appends (dh2_cq.cu; "qr_cq" = variant)
     int qr_cq_tw;         // != 0: the same for the total weights ("qr_cq_tw")
+    int qr_cq_tw_leaf;    // variant at leaf levels ("qr_cq_tw_leaf", default 3: thread-column chunk rows)
     double2* cq_scr;      // their scratch triangles (cq_scratch_elems), null when unused
+    int t64_threads;      // threads of the Jacobi + epilogue kernel of the wide split leaf truncation ("trunc64_threads")
     int sym;              // 1: only row basis pairs have V/R/E; the column side of a block (t,s,c) reads
                           //    the row basis pair (s,-c) conjugated (blk_bpcs; matvec: col2row)
     const int* col2row;   // column pair (s,c) -> row pair (s,-c) (adjoint-symmetric structures)
@@ -104,12 +106,13 @@ void launch_S(const PlanD& P, int b0, int nb, cudaStream_t s, const int* blist =
 void launch_basis(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStream_t s);
 void launch_block_weights(const PlanD& P, int b0, int nb, int mode, const int* mirror, cudaStream_t s,
                           const int* blist = nullptr);
-void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* mirror, cudaStream_t s);
+// leaf_level: every pair of the launch is a leaf (k > 64: the thread-column form, qr_cq_tw_leaf)
+void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* mirror, cudaStream_t s, bool leaf_level = false);
 // column-per-thread chunk appends (k in (64, 128]; dh2_cq.cu), persistent grid on P.cq_scr
 size_t cq_scratch_elems(const PlanD& P);
 inline size_t cq_scratch_bytes_bound(int k) { return k > 64 ? (size_t)160 * 8 * k * 128 * 16 : 0; }
 void launch_basis_cq(const PlanD& P, const int* bps, int nbps, cudaStream_t s);
-void launch_total_weights_cq(const PlanD& P, bool row, int p0, int np, const int* mirror, cudaStream_t s);
+void launch_total_weights_cq(const PlanD& P, bool row, int p0, int np, const int* mirror, cudaStream_t s, int variant);
 struct TruncLaunch {
     int ldv = 1, ldb = 1, grid = 0;
     bool use_ws = false;      // working set in a global workspace (persistent grid) instead of smem

@@ -519,7 +519,9 @@ void lean_chunk_weights_truncate(Shard* C, int g, double eps, int mode) {
         const int p0 = Ln.p_lo[gl], np = Ln.p_hi[gl] - p0;
         if (!np || fused[l]) continue;
         const std::string cls = "total_weights_row@" + std::to_string(l);
-        C->timed(cls, 1, [&] { launch_total_weights(P, true, p0, np, Ln.d_mirror.p, s); });
+        bool all_leaf = true;
+        for (int p = p0; p < p0 + np; ++p) all_leaf = all_leaf && X.child0[p] < 0;
+        C->timed(cls, 1, [&] { launch_total_weights(P, true, p0, np, Ln.d_mirror.p, s, all_leaf); });
         double fl = 0;
         for (int p = p0; p < p0 + np; ++p) {
             for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) fl += 8.0 * C->bp_R_rows[C->blk_bpcs[X.blk[ib]]] * (double)k * k;

@@ -40,8 +40,9 @@ def gpu_run(name, eps=None, mode="FROB_BLOCKREL", sym=1, ws=0, split=1, fuse=0, 
         h.set_option("qr_wy", 1 if wy == 1 else 0)
         h.set_option("qr_flag", 1 if wy == 2 else 0)
         # k > 64: the other append forms replace the column-per-thread ones (dh2_cq.cu)
-        h.set_option("qr_cq", 1 if wy in (0, 4) else 0)
-        h.set_option("qr_cq_tw", 1 if wy == 4 else 0)
+        h.set_option("qr_cq", 1 if wy in (0, 4, 5) else 0)
+        h.set_option("qr_cq_tw", {4: 1, 5: 3}.get(wy, 0))
+        h.set_option("qr_cq_tw_leaf", 3 if wy in (0, 5) else 1 if wy == 4 else 0)
         h.recompress(cfg["eps"] if eps is None else eps, mode)
         assert h.stats()["adjoint_symmetry"]["used"] == bool(sym)
         assert (h.stats()["truncate_ws_launches"] > 0) == bool(ws)
@@ -246,13 +247,14 @@ def test_storage_recomp_matches_oracle(name, sym):
 
 @pytest.mark.parametrize("name,wy", [("P4", 1), ("P5", 1), ("P7", 1), ("P4", 2), ("P5", 2), ("C1", 2), ("P2", 2), ("P7", 2),
                                      ("P4", 3), ("P5", 3), ("P6", 3), ("P7", 3), ("P4", 4), ("P5", 4), ("P6", 4),
-                                     ("P7", 4)])
+                                     ("P7", 4), ("P4", 5), ("P5", 5), ("P6", 5), ("P7", 5)])
 def test_qr_append_column_by_column(name, wy):
     """The chunk appends in their other forms give the same ranks, singular values and matrix:
     wy = 1 blocked compact-WY (qr_wy = 1), wy = 2 flag-synchronised
     (dh2_set_option qr_flag = 1), wy = 3 the CTA-cooperative column-by-column form
     (qr_cq = 0; k = 125 runs the column-per-thread basis-weight appends of dh2_cq.cu by default),
-    wy = 4 the column-per-thread total weights too (qr_cq_tw = 1)."""
+    wy = 4 the column-per-thread total weights too (qr_cq_tw = 1), wy = 5 with their chunk rows
+    formed by thread-column FMAs (qr_cq_tw = 3)."""
     h, g, rc = gpu_run(name, wy=wy)
     for side in ("row", "col"):
         go, oo = getattr(g, side), getattr(rc, side)
