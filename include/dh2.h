@@ -181,6 +181,15 @@ int dh2_set_stream(dh2_ctx* ctx, void* cuda_stream);
  *     "fused_leaf_levels_row/col"; export "Z" is not defined on those levels).
  *   "fuse_direct_rows" (0..64, default 64): fused stacks up to this height form M^* directly,
  *     taller ones are reduced by Householder appends (stats "fused_append_pairs").
+ *   "truncate_split64" (0 | 1, default 1): leaf levels with 32 < #t <= 64 truncate in two kernels
+ *     (prologue + pivoted QR; one-sided Jacobi + epilogue at three pairs per SM); bitwise equal.
+ *   "truncate_split64_inner" (0 | 1, default 1): the same for inner levels (k > 64, <= 64 rows).
+ *   "trunc64_threads" (64 | 128 | 256, default 128): threads of that Jacobi + epilogue kernel.
+ *   "qr_cq" (0..2, default 1): k > 64 basis weights by column-per-thread Householder appends
+ *     (thread c holds column c of a 16-row (1) or 24-row (2) chunk in registers); 0: CTA-cooperative.
+ *   "qr_cq_tw" (0..3, default 0), "qr_cq_tw_leaf" (0..3, default 3): the same for the total
+ *     weights above / at the leaf levels (3: chunk rows formed by thread-column FMAs).
+ *   Further A/B switches (qr_wy, qr_flag, trunc_direct, lean_chunks) are listed in DESIGN.md §8.
  *   All variants give the same ranks, singular values and matrices up to rounding (tests).
  * Errors: DH2_EINVAL for an unknown name or value. */
 int dh2_set_option(dh2_ctx* ctx, const char* name, int64_t value);

@@ -841,7 +841,9 @@ void upload_all(Shard* C, const double* xyz, int64_t nv, const int64_t* tri) {
     P.t64_threads = C->t64_threads_init;
     P.qr_cq_tw = C->qr_cq_tw_init;
     P.qr_cq_tw_leaf = C->qr_cq_tw_leaf_init;
-    if (P.k > 64 && P.k <= 128) {
+    P.qr_cq64 = C->qr_cq64_init;
+    P.qr_cq64_tw = C->qr_cq64_tw_init;
+    if (P.k <= 128) {
         C->d_cq.alloc(cq_scratch_elems(P));
         P.cq_scr = C->d_cq.p;
     } else {
@@ -1020,14 +1022,17 @@ void truncate_level(Shard* C, PassH& X, bool row, int l, int p0, int np, int max
     } else {
     const TruncLaunch TL = plan_truncate(P, np, maxrows, maxz, all_leaf, C->force_ws != 0);
     const bool split = C->split_trunc && all_leaf && maxrows <= 32 && !TL.use_ws && (!fused || P.k <= 64);
-    const bool split64 = C->split_trunc64 && all_leaf && maxrows > 32 && maxrows <= 64 && !TL.use_ws && !TL.append && !fused;
+    // leaves of 33..64 (C4/C5) and, with k > 64, inner levels of k1 + k2 <= 64 rows: QR kernel, then
+    // Jacobi + epilogue at three pairs per SM
+    const bool split64 = C->split_trunc64 && !TL.use_ws && !TL.append && !fused && maxrows <= 64 &&
+                         ((all_leaf && maxrows > 32) || (!all_leaf && P.k > 64 && C->split_trunc64_inner));
     if (split64) {
-        const size_t need = trunc_split64_scratch_bytes(np);
+        const size_t need = trunc_split64_scratch_bytes(np, all_leaf, P.k);
         if (C->d_tscr.n < need) {
             CK(cudaStreamSynchronize(s));
             C->d_tscr.alloc(need);
         }
-        C->timed(cls, 2, [&] { launch_truncate_split64(P, row, p0, np, TL, eps, mode, C->d_tscr.p, s); });
+        C->timed(cls, 2, [&] { launch_truncate_split64(P, row, p0, np, TL, all_leaf, eps, mode, C->d_tscr.p, s); });
     } else if (fused && !split) {  // leaf total weights folded into one CTA per pair (k_truncate_fused)
         C->timed(cls, 1, [&] { launch_truncate_fused(P, row, p0, np, maxrows, eps, mode, mirror, s); });
     } else if (split) {
@@ -2187,6 +2192,21 @@ int dh2_set_option(dh2_ctx* X, const char* name, int64_t value) {
         for (auto& S : X->sh) S->split_trunc64 = (int)value;
         return DH2_OK;
     }
+    if (nm == "truncate_split64_inner") {  // 0: inner levels (k > 64, <= 64 rows) truncated by one kernel
+        if (value != 0 && value != 1) return fail(X, DH2_EINVAL, "truncate_split64_inner must be 0 or 1");
+        for (auto& S : X->sh) S->split_trunc64_inner = (int)value;
+        return DH2_OK;
+    }
+    if (nm == "qr_cq64" || nm == "qr_cq64_tw") {  // k <= 64: 0 CTA-cooperative, 1 (3: rows by thread-column FMAs) column-per-thread
+        if (value != 0 && value != 1 && value != 3) return fail(X, DH2_EINVAL, nm + " must be 0, 1 or 3");
+        for (auto& S : X->sh) {
+            if (nm == "qr_cq64")
+                S->P.qr_cq64 = S->qr_cq64_init = (int)value;
+            else
+                S->P.qr_cq64_tw = S->qr_cq64_tw_init = (int)value;
+        }
+        return DH2_OK;
+    }
     if (nm == "qr_cq" || nm == "qr_cq_tw" || nm == "qr_cq_tw_leaf") {  // 0: k > 64 basis (total) weights by the CTA-cooperative appends
         if (value < 0 || value > 3) return fail(X, DH2_EINVAL, nm + " must be 0..3 (variant)");
         for (auto& S : X->sh) {
@@ -2308,7 +2328,8 @@ int dh2_get_stats(const dh2_ctx* C, char* buf, int64_t* len) {
           << ", \"Z_scratch_bytes\": " << 16.0 * Ln.Z_scratch << ", \"S_slots\": " << Ln.S_slots
           << ", \"C_pool_mapped\": " << Ln.Cpool.mapped_bytes() << ", \"Q_pool_mapped\": " << Ln.Qpool.mapped_bytes()
           << ", \"C_compact_bytes\": " << 16.0 * Ln.C_used << ", \"Q_compact_bytes\": " << 16.0 * Ln.Q_used
-          << ", \"compact_items\": " << Ln.compact_items << ", \"device_used_peak\": " << Ln.peak_bytes << "}";
+          << ", \"compact_items\": " << Ln.compact_items << ", \"device_used_peak\": " << Ln.peak_bytes
+          << ", \"plan_bytes\": " << (Ln.on ? lean_bytes(S0) : 0.0) << "}";
     }
     for (int side = 0; side < 2; ++side) {
         o << (side ? ", \"fused_leaf_levels_col\": [" : ", \"fused_leaf_levels_row\": [");

@@ -228,8 +228,8 @@ __device__ inline void cq_store(const double2* Rs, double2* out, int rows, int k
 // Basis weights, persistent grid, one pair per CTA at a time (see k_basis for the algorithm:
 // leaf with #t > k: R of QR(V_tc); non-leaf: R of QR([R_{t1c1} E_{t1c}; R_{t2c2} E_{t2c}]); a
 // stack of <= k rows is the weight itself).
-template <int NB, int NC, int CTAS>
-__global__ void __launch_bounds__(128 / NC, CTAS) k_basis_cq(PlanD P, const int* bps, int nbps, double2* scr) {
+template <int NB, int NC, int CTAS, int NT = 128 / NC>
+__global__ void __launch_bounds__(NT, CTAS) k_basis_cq(PlanD P, const int* bps, int nbps, double2* scr) {
     extern __shared__ double2 sm[];
     __shared__ CqRefl<NB> sh;
     constexpr int LDB = NB + 1;
@@ -328,8 +328,8 @@ __device__ __forceinline__ void cq_gemm_cols(double2 (&b)[NB], const double2* Xs
 // Total weights, persistent grid (see k_total_weights: the rows of Z_tc^* are w_b R_sc S_b^*
 // (row pass; column pass w_b R_tc S_b) for the blocks of the pair, then Zhat_{t+c+} E_{tc+}^* for
 // its parents; Zhat_tc = R of their QR, or the rows themselves when there are <= k of them).
-template <int NB, int NC, int CTAS, bool TCOL>
-__global__ void __launch_bounds__(128 / NC, CTAS) k_total_weights_cq(PlanD P, PassD X, bool row, int p0, int np,
+template <int NB, int NC, int CTAS, bool TCOL, int NT = 128 / NC>
+__global__ void __launch_bounds__(NT, CTAS) k_total_weights_cq(PlanD P, PassD X, bool row, int p0, int np,
                                                                          const int* mirror, double2* scr) {
     extern __shared__ double2 sm[];
     __shared__ CqRefl<NB> sh;
@@ -465,32 +465,36 @@ static size_t cq_smem(const PlanD& P, int NB, int nE) {
     return ((size_t)(NB + 1) * P.k + (size_t)nE * P.m * P.m) * sizeof(double2);
 }
 
-template <int NB, int NC, int CTAS>
+template <int NB, int NC, int CTAS, int NT = 128 / NC>
 static void cq_basis(const PlanD& P, const int* bps, int nbps, cudaStream_t s) {
     static_assert(CTAS <= CQ_MAX_CTAS, "scratch");
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_basis_cq<NB, NC, CTAS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        cudaFuncSetAttribute(k_basis_cq<NB, NC, CTAS, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
         attr = true;
     }
     const int grid = std::min(nbps, P.num_sms * CTAS);
-    k_basis_cq<NB, NC, CTAS><<<grid, 128 / NC, cq_smem(P, NB, 6), s>>>(P, bps, nbps, P.cq_scr);
+    k_basis_cq<NB, NC, CTAS, NT><<<grid, NT, cq_smem(P, NB, 6), s>>>(P, bps, nbps, P.cq_scr);
 }
 
-template <int NB, int NC, int CTAS, bool TCOL>
+template <int NB, int NC, int CTAS, bool TCOL, int NT = 128 / NC>
 static void cq_total(const PlanD& P, const PassD& X, bool row, int p0, int np, const int* mirror, cudaStream_t s) {
     static_assert(CTAS <= CQ_MAX_CTAS, "scratch");
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_total_weights_cq<NB, NC, CTAS, TCOL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        cudaFuncSetAttribute(k_total_weights_cq<NB, NC, CTAS, TCOL, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
         attr = true;
     }
     const int grid = std::min(np, P.num_sms * CTAS);
-    k_total_weights_cq<NB, NC, CTAS, TCOL><<<grid, 128 / NC, cq_smem(P, NB, 3), s>>>(P, X, row, p0, np, mirror, P.cq_scr);
+    k_total_weights_cq<NB, NC, CTAS, TCOL, NT><<<grid, NT, cq_smem(P, NB, 3), s>>>(P, X, row, p0, np, mirror, P.cq_scr);
 }
 
 void launch_basis_cq(const PlanD& P, const int* bps, int nbps, cudaStream_t s) {
     if (!nbps) return;
+    if (P.k <= 64) {  // (k = 64: 64 threads, one column each, 8 pairs per SM)
+        cq_basis<16, 1, 8, 64>(P, bps, nbps, s);
+        return;
+    }
     switch (P.qr_cq) {
         case 2: cq_basis<24, 1, 3>(P, bps, nbps, s); break;
         default: cq_basis<16, 1, 4>(P, bps, nbps, s); break;
@@ -500,6 +504,13 @@ void launch_basis_cq(const PlanD& P, const int* bps, int nbps, cudaStream_t s) {
 void launch_total_weights_cq(const PlanD& P, bool row, int p0, int np, const int* mirror, cudaStream_t s, int variant) {
     if (!np) return;
     const PassD& X = row ? P.row : P.col;
+    if (P.k <= 64) {
+        if (variant == 3)
+            cq_total<16, 1, 8, true, 64>(P, X, row, p0, np, mirror, s);
+        else
+            cq_total<16, 1, 8, false, 64>(P, X, row, p0, np, mirror, s);
+        return;
+    }
     switch (variant) {
         case 2: cq_total<24, 1, 3, false>(P, X, row, p0, np, mirror, s); break;
         case 3: cq_total<16, 1, 4, true>(P, X, row, p0, np, mirror, s); break;

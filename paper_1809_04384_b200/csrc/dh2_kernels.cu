@@ -360,7 +360,7 @@ static size_t qr_chunk_smem(const PlanD& P, bool pk, int ldr, int ldb, int nE, b
 
 void launch_basis(const PlanD& P, const int* bps, int nbps, int maxrows, cudaStream_t s) {
     if (!nbps) return;
-    if (P.k > 64 && P.k <= 128 && P.qr_cq && P.cq_scr) return launch_basis_cq(P, bps, nbps, s);
+    if (P.k <= 128 && (P.k > 64 ? P.qr_cq : P.qr_cq64) && P.cq_scr) return launch_basis_cq(P, bps, nbps, s);
     const bool any_qr = maxrows > P.k;
     const int ldr = odd_ld(P.k);
     if (P.k <= 64) {  // 64-row chunks, packed triangle
@@ -528,7 +528,8 @@ __global__ void k_total_weights(PlanD P, PassD X, bool row, int p0, const int* m
 void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* mirror, cudaStream_t s, bool leaf_level) {
     if (!np) return;
     const int v = leaf_level && P.qr_cq_tw_leaf ? P.qr_cq_tw_leaf : P.qr_cq_tw;
-    if (P.k > 64 && P.k <= 128 && v && P.cq_scr) return launch_total_weights_cq(P, row, p0, np, mirror, s, v);
+    if (P.k <= 128 && (P.k > 64 ? v : P.qr_cq64_tw) && P.cq_scr)
+        return launch_total_weights_cq(P, row, p0, np, mirror, s, P.k > 64 ? v : P.qr_cq64_tw);
     const int ldr = odd_ld(P.k);
     const PassD& X = row ? P.row : P.col;
     if (P.k <= 64) {  // 64-row chunks, packed triangle
@@ -1149,8 +1150,12 @@ __global__ void __launch_bounds__(128) k_trunc_epi(PlanD P, PassD X, int p0, con
 // order to a scratch slab; (2) k_trunc_jepi64, Jacobi on the rows of R and the epilogue with R
 // alone in shared memory (66 KB: three pairs per SM).  Same device functions, same results.
 constexpr int T64 = 64;
+// LEAF = false (levels above the leaves with rowsM = k1 + k2 <= 64): Vhat = [C_{t1c1} E_{t1c};
+// C_{t2c2} E_{t2c}] (rowsM x k, built by the prologue in shared memory) also goes to the scratch
+// (sV, ld 64) for the epilogue's C = Qhat^* Vhat.
+template <bool LEAF>
 __global__ void __launch_bounds__(512, 1) k_trunc_qr64(PlanD P, PassD X, int p0, int ldv, int ldb, double2* sR, int* sPiv,
-                                                      int* sMeta) {
+                                                      int* sMeta, double2* sV) {
     extern __shared__ double2 smd[];
     __shared__ int s_piv;
     __shared__ double2 sh[2];
@@ -1160,7 +1165,7 @@ __global__ void __launch_bounds__(512, 1) k_trunc_qr64(PlanD P, PassD X, int p0,
     int *piv, *ord;
     int rowsM, ldvt, ldB;
     const double2* Vt;
-    const int ncol = truncate_prologue<true>(P, X, p, smd, ldv, ldb, false, B, ldB, nrm, piv, ord, rowsM, Vt, ldvt, s_piv, sh);
+    const int ncol = truncate_prologue<LEAF>(P, X, p, smd, ldv, ldb, false, B, ldB, nrm, piv, ord, rowsM, Vt, ldvt, s_piv, sh);
     if (threadIdx.x == 0) {
         sMeta[2 * i] = ncol;  // -1: empty pair, already recorded
         sMeta[2 * i + 1] = rowsM;
@@ -1172,12 +1177,19 @@ __global__ void __launch_bounds__(512, 1) k_trunc_qr64(PlanD P, PassD X, int p0,
         R[r + (size_t)j * T64] = B[r + (size_t)j * ldB];
     }
     for (int j = threadIdx.x; j < rowsM; j += blockDim.x) sPiv[i * T64 + j] = piv[j];
+    if (!LEAF) {
+        double2* V = sV + (size_t)i * T64 * P.k;
+        for (int idx = threadIdx.x; idx < rowsM * P.k; idx += blockDim.x) {
+            const int r = idx % rowsM, nu = idx / rowsM;
+            V[r + (size_t)nu * T64] = Vt[r + (size_t)nu * ldvt];
+        }
+    }
 }
 
-template <int NT>
+template <int NT, bool LEAF>
 __global__ void __launch_bounds__(NT, NT == 64 ? 3 : NT == 128 ? 3 : 2) k_trunc_jepi64(PlanD P, PassD X, int p0, const double2* sR,
                                                                                    const int* sPiv, const int* sMeta, double eps,
-                                                                                   int mode) {
+                                                                                   int mode, const double2* sV) {
     constexpr int LD = T64 + 1;
     extern __shared__ double2 smd[];
     __shared__ double nrm[T64];
@@ -1196,43 +1208,59 @@ __global__ void __launch_bounds__(NT, NT == 64 ? 3 : NT == 128 ? 3 : 2) k_trunc_
     __syncthreads();
     const int nsw = jacobi_rows_auto(B, LD, ncol, rowsM, nrm, &flag);
     if (threadIdx.x == 0) X.sweeps[p] = nsw;
-    const int bp = X.bp[p];
-    const double2* Vt = P.V + P.bp_V_off[bp];
-    truncate_epilogue(X, p, P.k, B, LD, ncol, rowsM, piv, nrm, ord, Vt, rowsM, rowsM, eps, mode, s_rank);
+    if (LEAF) {
+        const double2* Vt = P.V + P.bp_V_off[X.bp[p]];
+        truncate_epilogue(X, p, P.k, B, LD, ncol, rowsM, piv, nrm, ord, Vt, rowsM, rowsM, eps, mode, s_rank);
+    } else {
+        const double2* Vt = sV + (size_t)i * T64 * P.k;
+        truncate_epilogue(X, p, P.k, B, LD, ncol, rowsM, piv, nrm, ord, Vt, T64, X.rowsb[p], eps, mode, s_rank);
+    }
 }
 
-size_t trunc_split64_scratch_bytes(int np) {
-    return (size_t)np * (T64 * T64 * sizeof(double2) + T64 * sizeof(int) + 2 * sizeof(int));
+size_t trunc_split64_scratch_bytes(int np, bool leaf, int k) {
+    return (size_t)np * (T64 * T64 * sizeof(double2) + T64 * sizeof(int) + 2 * sizeof(int) +
+                         (leaf ? 0 : (size_t)T64 * k * sizeof(double2))) + 16;
 }
 
-void launch_truncate_split64(const PlanD& P, bool row, int p0, int np, const TruncLaunch& L, double eps, int mode,
-                             void* scratch, cudaStream_t s) {
-    if (!np) return;
-    const PassD& X = row ? P.row : P.col;
+template <bool LEAF>
+static void split64_launch(const PlanD& P, const PassD& X, int p0, int np, const TruncLaunch& L, double eps, int mode,
+                           void* scratch, cudaStream_t s) {
     double2* sR = reinterpret_cast<double2*>(scratch);
     int* sPiv = reinterpret_cast<int*>(sR + (size_t)np * T64 * T64);
     int* sMeta = sPiv + (size_t)np * T64;
+    const uintptr_t vend = reinterpret_cast<uintptr_t>(sMeta + 2 * (size_t)np);
+    double2* sV = reinterpret_cast<double2*>((vend + 15) & ~(uintptr_t)15);  // (16-byte aligned)
     static size_t attr_qr = 0;
     static bool attr_j = false;
     const size_t smj = (size_t)(T64 + 1) * T64 * sizeof(double2);
     if (L.smem > attr_qr) {
-        cudaFuncSetAttribute(k_trunc_qr64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+        cudaFuncSetAttribute(k_trunc_qr64<LEAF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
         attr_qr = L.smem;
     }
     if (!attr_j) {
-        cudaFuncSetAttribute(k_trunc_jepi64<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smj);
-        cudaFuncSetAttribute(k_trunc_jepi64<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smj);
-        cudaFuncSetAttribute(k_trunc_jepi64<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smj);
+        cudaFuncSetAttribute(k_trunc_jepi64<64, LEAF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smj);
+        cudaFuncSetAttribute(k_trunc_jepi64<128, LEAF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smj);
+        cudaFuncSetAttribute(k_trunc_jepi64<256, LEAF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smj);
         attr_j = true;
     }
-    k_trunc_qr64<<<np, 512, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, sR, sPiv, sMeta);
+    k_trunc_qr64<LEAF><<<np, 512, L.smem, s>>>(P, X, p0, L.ldv, L.ldb, sR, sPiv, sMeta, sV);
     // Jacobi + epilogue threads (dh2_set_option "trunc64_threads")
     if (P.t64_threads == 64)
-        k_trunc_jepi64<64><<<np, 64, smj, s>>>(P, X, p0, sR, sPiv, sMeta, eps, mode);
+        k_trunc_jepi64<64, LEAF><<<np, 64, smj, s>>>(P, X, p0, sR, sPiv, sMeta, eps, mode, sV);
     else if (P.t64_threads == 256)
-        k_trunc_jepi64<256><<<np, 256, smj, s>>>(P, X, p0, sR, sPiv, sMeta, eps, mode);
+        k_trunc_jepi64<256, LEAF><<<np, 256, smj, s>>>(P, X, p0, sR, sPiv, sMeta, eps, mode, sV);
     else
-        k_trunc_jepi64<128><<<np, 128, smj, s>>>(P, X, p0, sR, sPiv, sMeta, eps, mode);
+        k_trunc_jepi64<128, LEAF><<<np, 128, smj, s>>>(P, X, p0, sR, sPiv, sMeta, eps, mode, sV);
+}
+
+void launch_truncate_split64(const PlanD& P, bool row, int p0, int np, const TruncLaunch& L, bool leaf_level, double eps,
+                             int mode, void* scratch, cudaStream_t s) {
+    if (!np) return;
+    const PassD& X = row ? P.row : P.col;
+    if (leaf_level)
+        split64_launch<true>(P, X, p0, np, L, eps, mode, scratch, s);
+    else
+        split64_launch<false>(P, X, p0, np, L, eps, mode, scratch, s);
 }
 
 size_t trunc_split_scratch_bytes(int np) { return (size_t)np * (1024 * sizeof(double2) + 32 * sizeof(double) + 34 * sizeof(int)); }

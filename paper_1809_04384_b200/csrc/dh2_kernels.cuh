@@ -46,6 +46,7 @@ struct PlanD {
     int qr_cq;            // != 0: k > 64 basis weights by column-per-thread appends (dh2_cq.cu; "qr_cq" = variant)
     int qr_cq_tw;         // != 0: the same for the total weights ("qr_cq_tw")
     int qr_cq_tw_leaf;    // variant at leaf levels ("qr_cq_tw_leaf", default 3: thread-column chunk rows)
+    int qr_cq64, qr_cq64_tw;  // k <= 64: the column-per-thread basis / total weights ("qr_cq64", "qr_cq64_tw": 0, 1, 3)
     double2* cq_scr;      // their scratch triangles (cq_scratch_elems), null when unused
     int t64_threads;      // threads of the Jacobi + epilogue kernel of the wide split leaf truncation ("trunc64_threads")
     int sym;              // 1: only row basis pairs have V/R/E; the column side of a block (t,s,c) reads
@@ -110,7 +111,7 @@ void launch_block_weights(const PlanD& P, int b0, int nb, int mode, const int* m
 void launch_total_weights(const PlanD& P, bool row, int p0, int np, const int* mirror, cudaStream_t s, bool leaf_level = false);
 // column-per-thread chunk appends (k in (64, 128]; dh2_cq.cu), persistent grid on P.cq_scr
 size_t cq_scratch_elems(const PlanD& P);
-inline size_t cq_scratch_bytes_bound(int k) { return k > 64 ? (size_t)160 * 8 * k * 128 * 16 : 0; }
+inline size_t cq_scratch_bytes_bound(int k) { return k <= 128 ? (size_t)160 * 8 * k * 128 * 16 : 0; }
 void launch_basis_cq(const PlanD& P, const int* bps, int nbps, cudaStream_t s);
 void launch_total_weights_cq(const PlanD& P, bool row, int p0, int np, const int* mirror, cudaStream_t s, int variant);
 struct TruncLaunch {
@@ -130,9 +131,10 @@ void launch_truncate(const PlanD& P, bool row, int p0, int np, const TruncLaunch
 size_t trunc_split_scratch_bytes(int np);
 // leaf levels with 32 < #t <= 64 (C4/C5): prologue + pivoted QR (one CTA per SM), then Jacobi +
 // epilogue with R alone in shared memory (three pairs per SM)
-size_t trunc_split64_scratch_bytes(int np);
-void launch_truncate_split64(const PlanD& P, bool row, int p0, int np, const TruncLaunch& L, double eps, int mode,
-                             void* scratch, cudaStream_t s);
+// (levels above the leaves with k1 + k2 <= 64 rows: the same split, Vhat kept in the scratch)
+size_t trunc_split64_scratch_bytes(int np, bool leaf, int k);
+void launch_truncate_split64(const PlanD& P, bool row, int p0, int np, const TruncLaunch& L, bool leaf_level, double eps,
+                             int mode, void* scratch, cudaStream_t s);
 // fused: leaf total weights folded into the QR kernel (k_trunc_zqr, k <= 64; the level's Zhat is
 // not formed; stacks of <= fuse_direct rows form M^* directly, taller ones are QR-appended;
 // mirror as for launch_total_weights)

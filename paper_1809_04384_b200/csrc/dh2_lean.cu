@@ -346,6 +346,15 @@ double lean_bytes(const Shard* C) {
         comp += r * (X.child0[p] < 0 ? (double)T.size(t) : 2.0 * r) + (Ln.keepC.size() && Ln.keepC[p] ? r * k : 0.0);
     }
     for (int b2 = C->b_lo; b2 < C->b_hi; ++b2) st += r_est * r_est;
+    // scratch of the wide split truncation (k_trunc_qr64 -> k_trunc_jepi64) for the largest
+    // chunk-level launch (bounded by its inner-level form, which also keeps Vhat)
+    int npmax = 0;
+    for (int g = 0; g < Ln.G; ++g)
+        for (int l = 0; l <= L; ++l) {
+            const int gl = g * (L + 1) + l;
+            npmax = std::max(npmax, Ln.p_hi[gl] - Ln.p_lo[gl]);
+        }
+    b += (double)trunc_split64_scratch_bytes(npmax, false, k);
     return b + 16.0 * (cb * 1.5 + qb + comp + st);
 }
 

@@ -263,13 +263,15 @@ struct Shard {
     int qr_flag_init = 0;    // initial value of PlanD::qr_flag
     int qr_cq_init = 1;      // initial value of PlanD::qr_cq (column-per-thread basis-weight appends for k > 64:
                              // variant 1 = 16-row chunks, measured C4 basis -43 %)
+    int qr_cq64_init = 1, qr_cq64_tw_init = 0;  // k <= 64 column-per-thread appends (basis: C3 -3 %, C2 -15 %; total weights +10 %)
     int qr_cq_tw_leaf_init = 3;  // PlanD::qr_cq_tw_leaf (thread-column total weights at leaf levels: C4 -9 %)
     int qr_cq_tw_init = 0;   // initial value of PlanD::qr_cq_tw (total weights: measured slower above the leaves, 0)
     DevBuf<double2> d_cq;    // their scratch triangles
     int trunc_mode_init = 1; // initial value of PlanD::trunc_mode (direct: measured -3 % C4, -16 % C5 leaves)
     int qr_wy_init = 0;      // initial value of PlanD::qr_wy (blocked WY appends measured slower on C4: 0) (dh2_set_option("qr_wy") sets the plan directly)
     int t64_threads_init = 128;  // PlanD::t64_threads
-    int split_trunc64 = 1;   // dh2_set_option("truncate_split64"): leaves of 33..64 as QR kernel + Jacobi/epilogue kernel
+    int split_trunc64 = 1;
+    int split_trunc64_inner = 1;  // dh2_set_option("truncate_split64_inner")   // dh2_set_option("truncate_split64"): leaves of 33..64 as QR kernel + Jacobi/epilogue kernel
     int split_trunc = 1;     // dh2_set_option("truncate_split"): warp-register Jacobi for leaves <= 32
     int fuse_leaf = 0;       // dh2_set_option("fuse_leaf_weights"): leaf Zhat folded into the split QR
     std::vector<int> fused_levels[2];  // levels of the last recompress whose Zhat was fused (row, col)

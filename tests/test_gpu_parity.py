@@ -43,6 +43,8 @@ def gpu_run(name, eps=None, mode="FROB_BLOCKREL", sym=1, ws=0, split=1, fuse=0, 
         h.set_option("qr_cq", 1 if wy in (0, 4, 5) else 0)
         h.set_option("qr_cq_tw", {4: 1, 5: 3}.get(wy, 0))
         h.set_option("qr_cq_tw_leaf", 3 if wy in (0, 5) else 1 if wy == 4 else 0)
+        h.set_option("qr_cq64", 0 if wy in (1, 2, 3) else 1)  # k <= 64 column-per-thread basis appends (default)
+        h.set_option("qr_cq64_tw", {6: 1, 7: 3}.get(wy, 0))
         h.recompress(cfg["eps"] if eps is None else eps, mode)
         assert h.stats()["adjoint_symmetry"]["used"] == bool(sym)
         assert (h.stats()["truncate_ws_launches"] > 0) == bool(ws)
@@ -247,14 +249,16 @@ def test_storage_recomp_matches_oracle(name, sym):
 
 @pytest.mark.parametrize("name,wy", [("P4", 1), ("P5", 1), ("P7", 1), ("P4", 2), ("P5", 2), ("C1", 2), ("P2", 2), ("P7", 2),
                                      ("P4", 3), ("P5", 3), ("P6", 3), ("P7", 3), ("P4", 4), ("P5", 4), ("P6", 4),
-                                     ("P7", 4), ("P4", 5), ("P5", 5), ("P6", 5), ("P7", 5)])
+                                     ("P7", 4), ("P4", 5), ("P5", 5), ("P6", 5), ("P7", 5),
+                                     ("C1", 6), ("C2", 6), ("P2", 6), ("P3", 6), ("C1", 7), ("C2", 7), ("P2", 7), ("P3", 7)])
 def test_qr_append_column_by_column(name, wy):
     """The chunk appends in their other forms give the same ranks, singular values and matrix:
     wy = 1 blocked compact-WY (qr_wy = 1), wy = 2 flag-synchronised
     (dh2_set_option qr_flag = 1), wy = 3 the CTA-cooperative column-by-column form
     (qr_cq = 0; k = 125 runs the column-per-thread basis-weight appends of dh2_cq.cu by default),
     wy = 4 the column-per-thread total weights too (qr_cq_tw = 1), wy = 5 with their chunk rows
-    formed by thread-column FMAs (qr_cq_tw = 3)."""
+    formed by thread-column FMAs (qr_cq_tw = 3); wy = 6 / 7 the same at k <= 64 (qr_cq64,
+    qr_cq64_tw = 1 / 3)."""
     h, g, rc = gpu_run(name, wy=wy)
     for side in ("row", "col"):
         go, oo = getattr(g, side), getattr(rc, side)
@@ -267,11 +271,12 @@ def test_qr_append_column_by_column(name, wy):
     assert np.linalg.norm(h.matvec(x, 1) - ops.matvec(rc, x, "recomp")) <= 1e-10 * np.linalg.norm(yo)
 
 
-@pytest.mark.parametrize("name", ["P6", "P7", "C4s", "C5s"])
+@pytest.mark.parametrize("name", ["P4", "P5", "P6", "P7", "C4s", "C5s"])
 def test_truncate_split64_bitwise(name):
-    """Leaves of 33..64 triangles (leaf 64 at k = 125): the split path (pivoted QR kernel, then the
-    Jacobi + epilogue kernel at three pairs per SM; default) runs the same device functions on the
-    same data as the single truncation kernel (dh2_set_option truncate_split64 = 0), so ranks,
+    """Leaves of 33..64 triangles (leaf 64 at k = 125) and, at k = 125, inner levels of <= 64 rows:
+    the split path (pivoted QR kernel, then the Jacobi + epilogue kernel at three pairs per SM,
+    Vhat kept in the scratch for inner levels; default) runs the same device functions on the same
+    data as the single truncation kernel (dh2_set_option truncate_split64(_inner) = 0), so ranks,
     singular values and the recompressed matvec are bitwise equal."""
     from paper_1809_04384_b200 import DH2
     cfg = get_config(name)
@@ -280,6 +285,7 @@ def test_truncate_split64_bitwise(name):
     for v in (1, 0):
         h = DH2(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"])
         h.set_option("truncate_split64", v)
+        h.set_option("truncate_split64_inner", v)
         h.recompress(cfg["eps"])
         x = seeded_vector(h.n, 3)
         out.append((h.export("rank_row", np.int32), h.export("sigma_row", np.float64), h.matvec(x, 1)))
