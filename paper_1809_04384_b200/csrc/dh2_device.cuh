@@ -1041,6 +1041,45 @@ __device__ inline double dmma_abh(const double2* A, int lda, int na, const doubl
     return part;
 }
 
+// C = A B^H as dmma_abh<true>, register-blocked: a warp task is an 8-row tile times 4 column
+// tiles (32 columns), so each A fragment is loaded once for four DMMA chains (A re-read per 32
+// instead of per 8 columns; four independent accumulations in flight).
+__device__ inline void dmma_abh4(const double2* A, int lda, int na, const double2* Bm, int ldbm, int nbm, int k, double2* out,
+                                 int ldo) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int nrt = (na + 7) >> 3, ncq = (nbm + 31) >> 5;
+    const int ar = lane >> 2, ac = lane & 3;
+    for (int task = warp; task < nrt * ncq; task += nw) {
+        const int rt = task % nrt, cq = task / nrt;
+        const int row = rt * 8 + ar;
+        const bool rok = row < na;
+        ZTile t[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) t[q] = ZTile{0.0, 0.0, 0.0, 0.0};
+        const double2* ap = A + row;
+#pragma unroll 2
+        for (int mu = 0; mu < k; mu += 4) {
+            const int mm = mu + ac;
+            const bool mok = mm < k;
+            const double2 a = (rok && mok) ? ap[(size_t)mm * lda] : cmk(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int col = (cq * 4 + q) * 8 + ar;
+                const double2 b = (mok && col < nbm) ? cconj(Bm[col + (size_t)mm * ldbm]) : cmk(0.0, 0.0);
+                ztile_mma(t[q], a, b);
+            }
+        }
+        if (rok) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int oc = (cq * 4 + q) * 8 + 2 * ac;
+                if (oc < nbm) out[row + (size_t)oc * ldo] = cmk(t[q].r0, t[q].i0);
+                if (oc + 1 < nbm) out[row + (size_t)(oc + 1) * ldo] = cmk(t[q].r1, t[q].i1);
+            }
+        }
+    }
+}
+
 // Upper-triangular k x k factor R in shared memory: dense column-major (ld ldr) or packed by
 // columns (R[i, c] at i + c(c+1)/2, 8 k(k+1) bytes; used when the dense square does not fit,
 // e.g. k = 125: 126 KB packed instead of 250 KB).

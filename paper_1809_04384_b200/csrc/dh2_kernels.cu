@@ -622,7 +622,7 @@ __device__ inline int truncate_prologue(const PlanD& P, const PassD& X, int p, d
         Mq = min(zr, rowsM);
     } else {
         // B = M^* = Zhat Vt^*  (zr x rowsM) on the FP64 tensor cores
-        dmma_abh<true>(Z, zr, zr, Vt, ldvt, rowsM, k, B, ldb);
+        dmma_abh4(Z, zr, zr, Vt, ldvt, rowsM, k, B, ldb);  // (register-blocked: 8 x 32 per warp task)
     }
     // pivoted QR, stopped once the trailing block has ||R22||_F <= 1e-13 max_j ||M^*(:, j)|| <=
     // 1e-13 sigma_1: every singular value dropped with it is below the parity tolerance
