@@ -839,6 +839,7 @@ void upload_all(Shard* C, const double* xyz, int64_t nv, const int64_t* tri) {
     P.trunc_mode = C->trunc_mode_init;
     P.qr_cq = C->qr_cq_init;
     P.t64_threads = C->t64_threads_init;
+    P.bw_variant = C->bw_variant_init;
     P.qr_cq_tw = C->qr_cq_tw_init;
     P.qr_cq_tw_leaf = C->qr_cq_tw_leaf_init;
     P.qr_cq64 = C->qr_cq64_init;
@@ -2180,6 +2181,11 @@ int dh2_set_option(dh2_ctx* X, const char* name, int64_t value) {
     if (nm == "qr_wy") {  // 0: column-by-column chunk appends (A/B and tests)
         if (value != 0 && value != 1) return fail(X, DH2_EINVAL, "qr_wy must be 0 or 1");
         for (auto& S : X->sh) S->P.qr_wy = S->qr_wy_init = (int)value;
+        return DH2_OK;
+    }
+    if (nm == "bw_variant") {  // block weights at k > 64: 1 = unrolled loads + register-blocked norm GEMM
+        if (value != 0 && value != 1) return fail(X, DH2_EINVAL, nm + " must be 0 or 1");
+        for (auto& S : X->sh) S->P.bw_variant = S->bw_variant_init = (int)value;
         return DH2_OK;
     }
     if (nm == "trunc64_threads") {

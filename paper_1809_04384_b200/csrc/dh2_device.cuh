@@ -1080,6 +1080,43 @@ __device__ inline void dmma_abh4(const double2* A, int lda, int na, const double
     }
 }
 
+// ||A B^H||_F^2 share of this thread (as dmma_abh<false, BCONJ>), register-blocked as dmma_abh4
+template <bool BCONJ>
+__device__ inline double dmma_abh4_norm(const double2* A, int lda, int na, const double2* Bm, int ldbm, int nbm, int k) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int nrt = (na + 7) >> 3, ncq = (nbm + 31) >> 5;
+    const int ar = lane >> 2, ac = lane & 3;
+    double part = 0.0;
+    for (int task = warp; task < nrt * ncq; task += nw) {
+        const int rt = task % nrt, cq = task / nrt;
+        const int row = rt * 8 + ar;
+        const bool rok = row < na;
+        ZTile t[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) t[q] = ZTile{0.0, 0.0, 0.0, 0.0};
+        const double2* ap = A + row;
+#pragma unroll 2
+        for (int mu = 0; mu < k; mu += 4) {
+            const int mm = mu + ac;
+            const bool mok = mm < k;
+            const double2 a = (rok && mok) ? ap[(size_t)mm * lda] : cmk(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int col = (cq * 4 + q) * 8 + ar;
+                double2 b = cmk(0.0, 0.0);
+                if (mok && col < nbm) {
+                    b = Bm[col + (size_t)mm * ldbm];
+                    if (!BCONJ) b = cconj(b);
+                }
+                ztile_mma(t[q], a, b);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) part += (t[q].r0 * t[q].r0 + t[q].i0 * t[q].i0) + (t[q].r1 * t[q].r1 + t[q].i1 * t[q].i1);
+    }
+    return part;
+}
+
 // Upper-triangular k x k factor R in shared memory: dense column-major (ld ldr) or packed by
 // columns (R[i, c] at i + c(c+1)/2, 8 k(k+1) bytes; used when the dense square does not fit,
 // e.g. k = 125: 126 KB packed instead of 250 KB).

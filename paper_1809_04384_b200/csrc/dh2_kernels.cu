@@ -398,6 +398,12 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : 3) k_block_weights(PlanD P
     for (int i0 = 0; i0 < rt; i0 += chunk) {
         const int nb = min(chunk, rt - i0);
         if (i0) __syncthreads();
+        if (P.bw_variant && k > 64) {  // (4 k-steps of loads in flight; the norm GEMM register-blocked 8 x 32: C4 -5 %, C2 +27 %)
+            chunk_gemm_S_dmma<true>(Rt, rt, i0, nb, Sg, false, mb < 0, 1.0, k, U, ldu);
+            __syncthreads();
+            part += P.sym ? dmma_abh4_norm<true>(U, ldu, nb, Rs, rs, rs, k) : dmma_abh4_norm<false>(U, ldu, nb, Rs, rs, rs, k);
+            continue;
+        }
         chunk_gemm_S_dmma(Rt, rt, i0, nb, Sg, false, mb < 0, 1.0, k, U, ldu);
         __syncthreads();
         // ||U R_sc^*||_F^2 on the FP64 tensor cores (sym: R_sc^* = (conj R_{s,-c})^* = R_{s,-c}^T)
