@@ -254,6 +254,8 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-nearfield", dest="nearfield", action="store_false",
+                    help="skip the (untimed-in-value) nearfield assembly + matvec measurement")
     ap.add_argument("--sample-frac", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shards", type=int, default=1, help="virtual shards on one GPU (single process)")
@@ -396,6 +398,32 @@ def main():
                     "tflops": (v["flops"] / (v["ms"] * 1e-3) / 1e12) if v["ms"] > 0 else 0.0}
               for cls, v in sorted(kern.items())}
 
+    # NEXT-4 (not part of `value`): nearfield assembly (Sauter-Schwab / Duffy-Gauss, FP64 ALU bound)
+    # and the nearfield matvec (every stored coefficient read once, HBM bound), timed by the library's
+    # CUDA events on the bench stream
+    near = None
+    if args.nearfield:
+        try:
+            h.set_profiling(True)
+            k0 = h.stats()["kernels"]
+            h.nearfield_assemble()
+            for _ in range(3):
+                h.matvec_device(x.data_ptr(), y.data_ptr(), 1, add_near=True)
+            torch.cuda.synchronize()
+            s2 = h.stats()
+            h.set_profiling(False)
+            kd = lambda c, f: s2["kernels"].get(c, {}).get(f, 0.0) - k0.get(c, {}).get(f, 0.0)  # noqa: E731
+            nf = s2["nearfield"]
+            a_ms, m_ms = kd("nearfield", "ms"), kd("matvec_near", "ms") / 3
+            gbps = 16.0 * nf["values"] / (m_ms * 1e-3) / 1e9 if m_ms > 0 else 0.0
+            near = {"assemble_ms": a_ms, "blocks": nf["blocks"], "values": nf["values"],
+                    "touching_entries": nf["touching_entries"], "kernel_evals": nf["kernel_evals"],
+                    "gevals_per_s": nf["kernel_evals"] / (a_ms * 1e-3) / 1e9 if a_ms > 0 else 0.0,
+                    "matvec_near_ms": m_ms, "matvec_near_GBps": gbps, "matvec_near_frac_of_hbm": gbps / hbm,
+                    "note": "NEXT-4, outside the timed step; nq_singular 5, nq_regular 3 (P:1486-1492)"}
+        except Exception as e:  # (e.g. device memory on the largest configs)
+            near = {"unavailable": str(e).splitlines()[0]}
+
     # end-to-end through the C ABI with host buffers
     e2e = None
     if args.e2e_steps > 0:
@@ -453,7 +481,7 @@ def main():
                 "seconds_per_step": ms * 1e-3,
                 "roofline": roof, "cpu_baseline": cpu, "clocks": clocks, "e2e": e2e, "gpu_launches": launches,
                 "exchange_bytes_per_step": s1.get("exchange_bytes"),
-                "phases": phases,
+                "phases": phases, "nearfield": near,
                 "launch_detail_ms_per_step": {c: round(v["ms"] / args.steps, 4) for c, v in sorted(detail.items())}}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -11,8 +11,8 @@
  * (Eq. 4, Eq. 10/11, Def. 2.7); dh2_recompress
  * replaces the interpolation bases by orthogonal, nested, adaptively truncated
  * ones (§3.2) and projects the couplings.  The
- * nearfield (inadmissible leaves) is out of scope: it is untouched by the
- * recompression and is only counted in dh2_storage.
+ * nearfield (inadmissible leaves) is untouched by the recompression; it is assembled on
+ * request by dh2_nearfield_assemble (NEXT-4) and added by dh2_matvec(DH2_ADD_NEAR).
  *
  * Conventions (all functions):
  *   - return int: 0 = DH2_OK, < 0 = error code below; no C++ exception crosses the ABI;
@@ -62,7 +62,7 @@ enum {
 enum { DH2_ORIG = 0, DH2_RECOMP = 1 };
 
 /* matvec flags */
-enum { DH2_HOST_PTRS = 0, DH2_DEVICE_PTRS = 1 };
+enum { DH2_HOST_PTRS = 0, DH2_DEVICE_PTRS = 1, DH2_ADD_NEAR = 2 /* y += N x (assembled nearfield) */ };
 
 typedef struct dh2_ctx dh2_ctx; /* opaque; owns all device memory */
 
@@ -137,16 +137,28 @@ int dh2_setup_device(dh2_ctx* ctx);
  * from the interpolation matrix). */
 int dh2_recompress(dh2_ctx* ctx, double eps, int32_t mode);
 
-/* Far-field matrix-vector product y = G_far x of the ORIG or RECOMP matrix: the admissible blocks
- * only -- the nearfield (inadmissible leaves, singular Galerkin quadrature) is not
- * assembled by this build, so y is NOT G x of the full Galerkin matrix (dh2_storage's
- * nearfield_bytes counts what it would occupy).  ORIG needs V and S resident: DH2_ENOTIMPL on the
- * memory-lean plan (dh2_get_stats "lean"). */
-/* Far-field matrix-vector product y = G_far x of the ORIG or RECOMP matrix.
+/* Matrix-vector product y = G_far x of the ORIG or RECOMP matrix (the admissible blocks), plus
+ * the nearfield N x with DH2_ADD_NEAR.  ORIG needs V and S resident: DH2_ENOTIMPL on the
+ * memory-lean plan (dh2_get_stats "lean").
  * x, y: n complex (2n float64) in original triangle order; host pointers
  * (flags = DH2_HOST_PTRS, copied through the context's stream) or device
- * pointers (DH2_DEVICE_PTRS, no copies).  Nearfield is not included. */
+ * pointers (DH2_DEVICE_PTRS, no copies).  Without DH2_ADD_NEAR the result is the far field
+ * only; with DH2_ADD_NEAR (after dh2_nearfield_assemble) it is the whole Galerkin product
+ * G x = G_far x + N x.  DH2_ESTATE if DH2_ADD_NEAR is set before the nearfield is assembled. */
 int dh2_matvec(dh2_ctx* ctx, int32_t which, const double* x, double* y, int32_t flags);
+
+/* Nearfield assembly (NEXT-4; Section 5): every inadmissible leaf (t, s) of
+ * the block tree (export "near", sorted by (t, s)) is stored as a dense #t x #s block, column-major,
+ * rows and columns in cluster order, entries the Galerkin integrals
+ *     g_ij = int_{tau_i} int_{tau_j} exp(i kappa |x-y|) / (4 pi |x-y|) dy dx
+ * of the piecewise-constant basis: Sauter-Erichsen-Schwab quadrature of order nq_singular (paper:
+ * 5) on [0,1]^4 for identical, edge- and vertex-adjacent triangles, Gauss quadrature with the Duffy
+ * transformation of order nq_regular (paper: 3) per axis otherwise.  Orders in 1..8 (DH2_EINVAL
+ * otherwise).  Device memory: 16 B per coefficient (dh2_storage's nearfield_bytes), owned by ctx;
+ * a second call re-assembles.  Shards assemble the blocks of the row leaves they own.  Exports:
+ * "near_values" (complex, the blocks concatenated in "near" order), "near_off" (int64 entry offset
+ * per block).  Collective with world > 1. */
+int dh2_nearfield_assemble(dh2_ctx* ctx, int32_t nq_singular, int32_t nq_regular);
 
 /* Storage report, 16 B per complex coefficient, 1 KB = 1024 B.
  * basis = leaf matrices + transfers of the row and the column basis;

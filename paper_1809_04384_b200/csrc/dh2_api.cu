@@ -627,6 +627,8 @@ void upload_pass(Shard* C, PassH& X, PassD& D, bool alloc_Z) {
             X.d_Q.alloc(X.Q_total);
         }
         X.d_sigma.alloc(X.sig_total);
+        // slots past a pair's nsig (pivoted-QR rank stop, N1) are never written: zero, not pool garbage
+        if (X.sig_total) CK(cudaMemsetAsync(X.d_sigma.p, 0, X.sig_total * sizeof(double), s));
     }
     D.npairs = (int)np;
     D.bp = X.d_bp.p;
@@ -919,7 +921,10 @@ void set_col_alias(Shard* C, bool alias) {
         X.sig_off = X.sig_off_own;
         if (!X.d_C.p && X.C_total) X.d_C.alloc(X.C_total);
         if (!X.d_Q.p && X.Q_total) X.d_Q.alloc(X.Q_total);
-        if (!X.d_sigma.p && X.sig_total) X.d_sigma.alloc(X.sig_total);
+        if (!X.d_sigma.p && X.sig_total) {
+            X.d_sigma.alloc(X.sig_total);
+            CK(cudaMemsetAsync(X.d_sigma.p, 0, X.sig_total * sizeof(double), s));
+        }
         P.col.C = X.d_C.p;
         P.col.Q = X.d_Q.p;
         P.col.sigma = X.d_sigma.p;
@@ -1463,6 +1468,12 @@ void export_shard(const Shard* C, const char* name, void* buf, int64_t* nbytes) 
                 tmp64.push_back(b.second);
             }
             it = hv(tmp64);
+        } else if (nm == "near_values") {  // this shard's assembled nearfield blocks (dh2_nearfield_assemble)
+            if (!C->near.on) throw StateError("near_values before dh2_nearfield_assemble");
+            it = {C->near.d_val.p, (size_t)C->near.values * sizeof(double2), true, sizeof(double2)};
+        } else if (nm == "near_off") {
+            if (!C->near.on) throw StateError("near_off before dh2_nearfield_assemble");
+            it = hv(C->near.off);
         } else if (nm == "row_pairs") it = pairs_arr(S.row_pairs);
         else if (nm == "col_pairs") it = pairs_arr(S.col_pairs);
         else if (nm == "basis_pairs") it = pairs_arr(S.basis_pairs);
@@ -1918,12 +1929,18 @@ void do_recompress(dh2_ctx* X, double eps, int mode) {
     X->far2 = sums[2];
 }
 
-void do_matvec(dh2_ctx* X, bool recomp, const double2* x, double2* y) {
+void do_matvec(dh2_ctx* X, bool recomp, const double2* x, double2* y, bool add_near) {
     if (!recomp && X->sh[0]->lean.on)
         throw NotImpl("ORIG matvec on the memory-lean plan (V and S are not resident)");
+    if (add_near)
+        for (auto& S : X->sh)
+            if (!S->near.on) throw StateError("DH2_ADD_NEAR before dh2_nearfield_assemble");
     for (auto& S : X->sh) run_mv_forward(S.get(), recomp, x);
     exchange(X, X_XH);  // xh'_sc of column pairs referenced across shards
-    for (auto& S : X->sh) run_mv_rest(S.get(), recomp);
+    for (auto& S : X->sh) {
+        run_mv_rest(S.get(), recomp);
+        if (add_near) near_matvec(S.get());  // own rows, x_p holds all of x on every shard
+    }
     gather_y(X);
     run_mv_out(X->sh[0].get(), y);
     if (!X->virt)
@@ -2108,12 +2125,23 @@ int dh2_matvec(dh2_ctx* X, int32_t which, const double* x, double* y, int32_t fl
         Shard* S0 = X->sh[0].get();
         const size_t nb = (size_t)S0->n * sizeof(double2);
         if (flags & DH2_DEVICE_PTRS) {
-            do_matvec(X, which == DH2_RECOMP, reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y));
+            do_matvec(X, which == DH2_RECOMP, reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y),
+                      flags & DH2_ADD_NEAR);
         } else {
             CK(cudaMemcpyAsync(S0->d_x.p, x, nb, cudaMemcpyHostToDevice, X->stream));
-            do_matvec(X, which == DH2_RECOMP, S0->d_x.p, S0->d_y.p);
+            do_matvec(X, which == DH2_RECOMP, S0->d_x.p, S0->d_y.p, flags & DH2_ADD_NEAR);
             CK(cudaMemcpyAsync(y, S0->d_y.p, nb, cudaMemcpyDeviceToHost, X->stream));
         }
+        finish_all(X);
+    });
+}
+
+int dh2_nearfield_assemble(dh2_ctx* X, int32_t nq_singular, int32_t nq_regular) {
+    if (!X) return fail(nullptr, DH2_EINVAL, "null context");
+    return guarded(X, [&] {
+        require_device(X);
+        CK(cudaSetDevice(X->device));
+        for (auto& S : X->sh) near_assemble(S.get(), nq_singular, nq_regular);
         finish_all(X);
     });
 }
@@ -2336,6 +2364,17 @@ int dh2_get_stats(const dh2_ctx* C, char* buf, int64_t* len) {
           << ", \"C_compact_bytes\": " << 16.0 * Ln.C_used << ", \"Q_compact_bytes\": " << 16.0 * Ln.Q_used
           << ", \"compact_items\": " << Ln.compact_items << ", \"device_used_peak\": " << Ln.peak_bytes
           << ", \"plan_bytes\": " << (Ln.on ? lean_bytes(S0) : 0.0) << "}";
+    }
+    {
+        int64_t nb = 0, nv = 0, ns = 0;
+        double ne = 0;
+        bool on = true;
+        for (auto& sh : C->sh)
+            nb += sh->near.nblk, nv += sh->near.values, ns += sh->near.nsing, ne += sh->near.evals, on = on && sh->near.on;
+        o << ", \"nearfield\": {\"assembled\": " << (on ? "true" : "false") << ", \"blocks\": " << nb
+          << ", \"values\": " << nv << ", \"touching_entries\": " << ns << ", \"kernel_evals\": " << ne
+          << ", \"nq_singular\": " << S0->near.nq_sing
+          << ", \"nq_regular\": " << S0->near.nq_reg << "}";
     }
     for (int side = 0; side < 2; ++side) {
         o << (side ? ", \"fused_leaf_levels_col\": [" : ", \"fused_leaf_levels_row\": [");

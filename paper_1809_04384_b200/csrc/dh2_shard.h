@@ -304,6 +304,21 @@ struct Shard {
     DevBuf<GridD> d_grid;
     DevBuf<double2> d_VR, d_E, d_S, d_St, d_x, d_y, d_xp, d_yp, d_xh, d_yh;
     PlanD P{};
+    // nearfield (NEXT-4, dh2_near.cu): this shard's inadmissible leaves (t owned), dense #t x #s
+    // column-major in cluster order, assembled by dh2_nearfield_assemble
+    struct NearH {
+        bool on = false;
+        int nq_sing = 0, nq_reg = 0;
+        int nblk = 0, ngroups = 0;     // own blocks, distinct row leaves
+        int64_t nsing = 0, values = 0;  // touching entries, stored coefficients
+        double evals = 0;               // kernel evaluations of the last assembly
+        std::vector<int> t, s;          // per own block
+        std::vector<int64_t> off;       // entry offset per own block
+        DevBuf<int> d_t, d_s, d_gptr;   // d_gptr: blocks of row group g = [gptr[g], gptr[g+1])
+        DevBuf<int64_t> d_off;
+        DevBuf<double4> d_pts;          // n x nq_reg^2 Duffy-Gauss points (x, y, z, w 2|tau|), cluster order
+        DevBuf<double2> d_val;
+    } near;
     // stats
     std::map<std::string, KStat> kstat;
     std::vector<std::tuple<std::string, cudaEvent_t, cudaEvent_t>> pending;
@@ -373,6 +388,9 @@ struct Shard {
 void truncate_level(Shard* C, PassH& X, bool row, int l, int p0, int np, int maxrows, int maxz, bool all_leaf, bool fused,
                     double eps, int mode, const int* mirror);
 bool fuse_leaf_level(const Shard* C, int leafrows, int maxz, int np);
+// nearfield, NEXT-4 (dh2_near.cu)
+void near_assemble(Shard* C, int nq_sing, int nq_reg);
+void near_matvec(Shard* C);
 // memory-lean plan (dh2_lean.cu)
 void lean_plan(Shard* C, int G);
 double lean_bytes(const Shard* C);

@@ -18,10 +18,10 @@ ERROR_NAMES = {-1: "DH2_EINVAL", -2: "DH2_ENOMEM", -3: "DH2_ECUDA", -4: "DH2_ENC
                -6: "DH2_EMISMATCH", -7: "DH2_ENOTIMPL", -8: "DH2_ENUMERIC"}
 MODES = {"FROB_BLOCKREL": 0, "FROB_CLUSTERREL": 1, "SPEC_BLOCKREL": 2}
 DH2_ORIG, DH2_RECOMP = 0, 1
-DH2_HOST_PTRS, DH2_DEVICE_PTRS = 0, 1
+DH2_HOST_PTRS, DH2_DEVICE_PTRS, DH2_ADD_NEAR = 0, 1, 2
 
 # every symbol include/dh2.h declares
-EXPORTED = ["dh2_build_interp", "dh2_setup_device", "dh2_recompress", "dh2_matvec", "dh2_storage",
+EXPORTED = ["dh2_build_interp", "dh2_setup_device", "dh2_recompress", "dh2_matvec", "dh2_nearfield_assemble", "dh2_storage",
             "dh2_set_stream", "dh2_set_option", "dh2_set_profiling", "dh2_get_stats", "dh2_export", "dh2_export_shard",
             "dh2_nccl_unique_id", "dh2_destroy", "dh2_last_error"]
 
@@ -71,6 +71,7 @@ def load_library(path=LIB_PATH):
     lib.dh2_setup_device.argtypes = [vp]
     lib.dh2_recompress.argtypes = [vp, ctypes.c_double, ctypes.c_int32]
     lib.dh2_matvec.argtypes = [vp, ctypes.c_int32, vp, vp, ctypes.c_int32]
+    lib.dh2_nearfield_assemble.argtypes = [vp, ctypes.c_int32, ctypes.c_int32]
     lib.dh2_storage.argtypes = [vp, ctypes.c_int32, P(dh2_storage_report)]
     lib.dh2_set_stream.argtypes = [vp, vp]
     lib.dh2_set_profiling.argtypes = [vp, ctypes.c_int32]
@@ -146,18 +147,25 @@ class DH2:
     def recompress(self, eps, mode="FROB_BLOCKREL"):
         self._check(self.lib.dh2_recompress(self.h, float(eps), MODES[mode] if isinstance(mode, str) else int(mode)))
 
-    def matvec(self, x, which=DH2_RECOMP):
-        """y = G_far x: the far field only (admissible blocks); the nearfield is not assembled."""
+    def matvec(self, x, which=DH2_RECOMP, add_near=False):
+        """y = G_far x (admissible blocks); with add_near, y = G x = G_far x + N x (the nearfield
+        of nearfield_assemble)."""
         x = np.ascontiguousarray(x, dtype=np.complex128)
         if x.shape != (self.n,):
             raise ValueError("x must have shape (n,)")
         y = np.empty_like(x)
-        self._check(self.lib.dh2_matvec(self.h, which, x.ctypes.data, y.ctypes.data, DH2_HOST_PTRS))
+        self._check(self.lib.dh2_matvec(self.h, which, x.ctypes.data, y.ctypes.data,
+                                        DH2_HOST_PTRS | (DH2_ADD_NEAR if add_near else 0)))
         return y
 
-    def matvec_device(self, x_ptr, y_ptr, which=DH2_RECOMP):
+    def matvec_device(self, x_ptr, y_ptr, which=DH2_RECOMP, add_near=False):
         """x_ptr, y_ptr: device pointers to n complex128 values (e.g. torch tensor data_ptr())."""
-        self._check(self.lib.dh2_matvec(self.h, which, ctypes.c_void_p(x_ptr), ctypes.c_void_p(y_ptr), DH2_DEVICE_PTRS))
+        self._check(self.lib.dh2_matvec(self.h, which, ctypes.c_void_p(x_ptr), ctypes.c_void_p(y_ptr),
+                                        DH2_DEVICE_PTRS | (DH2_ADD_NEAR if add_near else 0)))
+
+    def nearfield_assemble(self, nq_singular=5, nq_regular=3):
+        """Assemble the nearfield blocks on the device (NEXT-4; the paper's orders by default)."""
+        self._check(self.lib.dh2_nearfield_assemble(self.h, int(nq_singular), int(nq_regular)))
 
     def storage(self, which=DH2_RECOMP):
         rep = dh2_storage_report()

@@ -288,8 +288,14 @@ def test_truncate_split64_bitwise(name):
         h.set_option("truncate_split64_inner", v)
         h.recompress(cfg["eps"])
         x = seeded_vector(h.n, 3)
-        out.append((h.export("rank_row", np.int32), h.export("sigma_row", np.float64), h.matvec(x, 1)))
+        # sigma slots past a pair's nsig are not results (pivoted-QR rank stop N1): masked
+        sig, nsig, off = h.export("sigma_row", np.float64), h.export("nsig_row", np.int32), h.export("sig_off_row", np.int64)
+        mask = np.zeros(len(sig), dtype=bool)
+        for o, c in zip(off, nsig):
+            mask[o:o + c] = True
+        out.append((h.export("rank_row", np.int32), sig[mask], h.matvec(x, 1), nsig))
         h.close()
     assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][3], out[1][3])
     assert np.array_equal(out[0][1], out[1][1])
     assert np.array_equal(out[0][2], out[1][2])
