@@ -1867,18 +1867,33 @@ void check_same_args(dh2_ctx* X, uint64_t h, const char* what) {
 
 void do_recompress(dh2_ctx* X, double eps, int mode) {
     if (X->sh[0]->lean.on) {  // memory-lean chunked plan (every shard of a context chooses alike)
+        // host wall clock per phase (issue + the phase's own synchronisations; stats "lean_wall_ms")
+        auto& W = X->sh[0]->lean_wall_ms;
+        W.assign(6, 0.0);
+        auto tw = std::chrono::steady_clock::now();
+        auto mark = [&](int i) {
+            auto now = std::chrono::steady_clock::now();
+            W[i] += std::chrono::duration<double, std::milli>(now - tw).count();
+            tw = now;
+        };
         for (auto& S : X->sh) lean_begin(S.get());
+        mark(0);
         for (auto& S : X->sh) lean_basis(S.get());
         exchange(X, X_R);  // R of the (s,-c) that other shards' blocks reference
+        mark(1);
         for (auto& S : X->sh) lean_weights_truncate(S.get(), eps, mode);
         exchange(X, X_RANK);
+        mark(2);
         for (auto& S : X->sh) lean_columns(S.get());
         // the compact C layout depends on the ranks: segment lists of X_C are rebuilt every time
         for (auto it = X->segs.begin(); it != X->segs.end();)
             it = std::get<0>(it->first) == (int)X_C ? X->segs.erase(it) : std::next(it);
         exchange(X, X_C);
+        mark(3);
         for (auto& S : X->sh) lean_project(S.get());
+        mark(4);
         finish_all(X);
+        mark(5);
         std::vector<double> sums(3, 0.0);
         for (auto& S : X->sh) {
             double v[3];
@@ -2363,7 +2378,11 @@ int dh2_get_stats(const dh2_ctx* C, char* buf, int64_t* len) {
           << ", \"C_pool_mapped\": " << Ln.Cpool.mapped_bytes() << ", \"Q_pool_mapped\": " << Ln.Qpool.mapped_bytes()
           << ", \"C_compact_bytes\": " << 16.0 * Ln.C_used << ", \"Q_compact_bytes\": " << 16.0 * Ln.Q_used
           << ", \"compact_items\": " << Ln.compact_items << ", \"device_used_peak\": " << Ln.peak_bytes
-          << ", \"plan_bytes\": " << (Ln.on ? lean_bytes(S0) : 0.0) << "}";
+          << ", \"plan_bytes\": " << (Ln.on ? lean_bytes(S0) : 0.0) << ", \"wall_ms\": {";
+        static const char* wn[6] = {"begin", "basis", "weights_truncate", "columns", "project", "finish"};
+        for (size_t i = 0; i < S0->lean_wall_ms.size() && i < 6; ++i)
+            o << (i ? ", " : "") << "\"" << wn[i] << "\": " << S0->lean_wall_ms[i];
+        o << "}}";
     }
     {
         int64_t nb = 0, nv = 0, ns = 0;

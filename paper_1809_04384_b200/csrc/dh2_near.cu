@@ -186,9 +186,13 @@ __device__ __forceinline__ double ss_region(int cas, int r, double xi, double e1
     return xi * xi * xi * e2;
 }
 
-__global__ void __launch_bounds__(256) k_near_singular(const double* __restrict__ xyz, const int64_t* __restrict__ tri,
-                                                       const SingItem* __restrict__ items, int64_t nitems, int nq,
-                                                       double kappa, double2* __restrict__ val) {
+// NQ: the singular order as a compile-time constant (the point index decomposes by constant
+// divisions); a generic-order instance (NQ = 0) serves the other orders.
+template <int NQ>
+__global__ void __launch_bounds__(256, 3) k_near_singular(const double* __restrict__ xyz, const int64_t* __restrict__ tri,
+                                                          const SingItem* __restrict__ items, int64_t nitems, int nq_rt,
+                                                          double kappa, double2* __restrict__ val) {
+    const int nq = NQ ? NQ : nq_rt;
     const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= nitems) return;
@@ -197,15 +201,15 @@ __global__ void __launch_bounds__(256) k_near_singular(const double* __restrict_
     const Tri X = make_tri(xyz, tri, it.i, (it.code >> 2) & 3, (it.code >> 4) & 3, (it.code >> 6) & 3);
     const Tri Y = make_tri(xyz, tri, it.j, (it.code >> 8) & 3, (it.code >> 10) & 3, (it.code >> 12) & 3);
     const int nreg = cas == 0 ? 6 : cas == 1 ? 5 : 2;
-    const int q4 = nq * nq * nq * nq, total = nreg * q4;
+    const int q3 = nq * nq * nq, q4 = q3 * nq;
     double2 acc = make_double2(0.0, 0.0);
-    for (int p = lane; p < total; p += 32) {
-        const int r = p / q4, q = p % q4;
-        const int a = q / (nq * nq * nq), b = (q / (nq * nq)) % nq, c = (q / nq) % nq, d = q % nq;
-        double u1, u2, v1, v2;
-        const double wr = ss_region(cas, r, c_gx[a], c_gx[b], c_gx[c], c_gx[d], u1, u2, v1, v2);
-        acc_g(acc, chi(X, u1, u2), chi(Y, v1, v2), wr * c_gw[a] * c_gw[b] * c_gw[c] * c_gw[d], kappa);
-    }
+    for (int r = 0; r < nreg; ++r)  // (region uniform across the warp)
+        for (int q = lane; q < q4; q += 32) {
+            const int a = q / q3, b = (q / (nq * nq)) % nq, c = (q / nq) % nq, d = q % nq;
+            double u1, u2, v1, v2;
+            const double wr = ss_region(cas, r, c_gx[a], c_gx[b], c_gx[c], c_gx[d], u1, u2, v1, v2);
+            acc_g(acc, chi(X, u1, u2), chi(Y, v1, v2), wr * (c_gw[a] * c_gw[b]) * (c_gw[c] * c_gw[d]), kappa);
+        }
     for (int o = 16; o; o >>= 1) {
         acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
         acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
@@ -218,17 +222,20 @@ __global__ void __launch_bounds__(256) k_near_singular(const double* __restrict_
 }
 
 // y_p[t] += sum over the row group's blocks N_b x_p[s] (cluster order); one CTA per row leaf,
-// 64 rows x 4 column slices per pass, reduction of the slices in shared memory.
+// R rows x 256/R column slices per pass (R = 32 when every leaf has <= 32 triangles), reduction of
+// the slices in shared memory.
+template <int R>
 __global__ void __launch_bounds__(256) k_mv_near(const int64_t* __restrict__ c_begin, const int* __restrict__ c_size,
                                                  const int* __restrict__ gptr, const int* __restrict__ bt,
                                                  const int* __restrict__ bs, const int64_t* __restrict__ off,
                                                  const double2* __restrict__ val, const double2* __restrict__ xp,
                                                  double2* __restrict__ yp) {
-    __shared__ double2 red[4][64];
+    constexpr int NS = 256 / R;
+    __shared__ double2 red[NS][R];
     const int g0 = gptr[blockIdx.x], g1 = gptr[blockIdx.x + 1];
     const int t = bt[g0], nt = c_size[t];
-    const int lr = threadIdx.x & 63, sl = threadIdx.x >> 6;
-    for (int a0 = 0; a0 < nt; a0 += 64) {
+    const int lr = threadIdx.x % R, sl = threadIdx.x / R;
+    for (int a0 = 0; a0 < nt; a0 += R) {
         const int a = a0 + lr;
         double2 acc = make_double2(0.0, 0.0);
         if (a < nt)
@@ -236,7 +243,7 @@ __global__ void __launch_bounds__(256) k_mv_near(const int64_t* __restrict__ c_b
                 const int s = bs[b], ns = c_size[s];
                 const double2* N = val + off[b];
                 const double2* x = xp + c_begin[s];
-                for (int c = sl; c < ns; c += 4) {
+                for (int c = sl; c < ns; c += NS) {
                     const double2 v = __ldg(N + (int64_t)c * nt + a), xv = __ldg(x + c);
                     acc.x += v.x * xv.x - v.y * xv.y;
                     acc.y += v.x * xv.y + v.y * xv.x;
@@ -246,7 +253,7 @@ __global__ void __launch_bounds__(256) k_mv_near(const int64_t* __restrict__ c_b
         __syncthreads();
         if (sl == 0 && a < nt) {
             double2 y = yp[c_begin[t] + a];
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < NS; ++k) {
                 y.x += red[k][lr].x;
                 y.y += red[k][lr].y;
             }
@@ -271,6 +278,7 @@ void near_assemble(Shard* C, int nq_sing, int nq_reg) {
     // own blocks (row leaf t owned by this shard), in the structure's (t, s) order
     N.t.clear();
     N.s.clear();
+    N.max_rows = 0;
     N.off.clear();
     std::vector<int> gptr;
     int64_t acc = 0;
@@ -280,6 +288,7 @@ void near_assemble(Shard* C, int nq_sing, int nq_reg) {
         if (N.t.empty() || N.t.back() != t) gptr.push_back((int)N.t.size());
         N.t.push_back(t);
         N.s.push_back(sc);
+        N.max_rows = std::max(N.max_rows, (int)T.size(t));
         N.off.push_back(acc);
         acc += T.size(t) * T.size(sc);
     }
@@ -393,8 +402,11 @@ void near_assemble(Shard* C, int nq_sing, int nq_reg) {
         });
     if (N.nsing)
         C->timed("nearfield", 1, [&] {
-            k_near_singular<<<(unsigned)((N.nsing * 32 + 255) / 256), 256, 0, s>>>(P.xyz, P.tri, d_items.p, N.nsing, nq_sing,
-                                                                                 P.kappa, N.d_val.p);
+            const unsigned grid = (unsigned)((N.nsing * 32 + 255) / 256);
+            if (nq_sing == 5)
+                k_near_singular<5><<<grid, 256, 0, s>>>(P.xyz, P.tri, d_items.p, N.nsing, nq_sing, P.kappa, N.d_val.p);
+            else
+                k_near_singular<0><<<grid, 256, 0, s>>>(P.xyz, P.tri, d_items.p, N.nsing, nq_sing, P.kappa, N.d_val.p);
         });
     CK(cudaStreamSynchronize(s));
     N.d_pts.free();
@@ -406,8 +418,12 @@ void near_matvec(Shard* C) {
     if (!N.on || !N.ngroups) return;
     C->kstat["matvec_near"].bytes += 16.0 * (double)N.values;  // every coefficient read once
     C->timed("matvec_near", 1, [&] {
-        k_mv_near<<<N.ngroups, 256, 0, C->stream>>>(C->d_c_begin.p, C->d_c_size.p, N.d_gptr.p, N.d_t.p, N.d_s.p, N.d_off.p,
-                                                   N.d_val.p, C->d_xp.p, C->d_yp.p);
+        if (N.max_rows <= 32)
+            k_mv_near<32><<<N.ngroups, 256, 0, C->stream>>>(C->d_c_begin.p, C->d_c_size.p, N.d_gptr.p, N.d_t.p, N.d_s.p,
+                                                           N.d_off.p, N.d_val.p, C->d_xp.p, C->d_yp.p);
+        else
+            k_mv_near<64><<<N.ngroups, 256, 0, C->stream>>>(C->d_c_begin.p, C->d_c_size.p, N.d_gptr.p, N.d_t.p, N.d_s.p,
+                                                           N.d_off.p, N.d_val.p, C->d_xp.p, C->d_yp.p);
     });
 }
 

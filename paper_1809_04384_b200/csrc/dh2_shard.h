@@ -310,6 +310,7 @@ struct Shard {
         bool on = false;
         int nq_sing = 0, nq_reg = 0;
         int nblk = 0, ngroups = 0;     // own blocks, distinct row leaves
+        int max_rows = 0;               // largest row leaf
         int64_t nsing = 0, values = 0;  // touching entries, stored coefficients
         double evals = 0;               // kernel evaluations of the last assembly
         std::vector<int> t, s;          // per own block
@@ -325,6 +326,7 @@ struct Shard {
     std::vector<cudaEvent_t> ev_pool;
     int64_t launches_total = 0;
     double host_build_ms = 0.0, host_tables_ms = 0.0;
+    std::vector<double> lean_wall_ms;  // host wall clock per lean recompression phase (last call)
     double tab_ms[6] = {0, 0, 0, 0, 0, 0};  // build_tables: basis pairs, blocks, passes, mirror, symmetry, exchange
     double E_row = 0, E_col = 0, far2 = 0;
 
