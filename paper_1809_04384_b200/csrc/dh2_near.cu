@@ -94,11 +94,14 @@ __device__ __forceinline__ void acc_g(double2& acc, double3 x, double3 y, double
 }
 
 // Regular entries of the own blocks: one CTA per block, one thread per entry (column-major).
+// Q2 = n_q^2 at compile time (9: the paper's order 3, loops unrolled), 0 = run-time q2.
+template <int Q2>
 __global__ void __launch_bounds__(256) k_near_regular(const double4* __restrict__ pts, const int64_t* __restrict__ tri,
                                                       const int64_t* __restrict__ perm, const int64_t* __restrict__ c_begin,
                                                       const int* __restrict__ c_size, const int* __restrict__ bt,
-                                                      const int* __restrict__ bs, const int64_t* __restrict__ off, int q2,
+                                                      const int* __restrict__ bs, const int64_t* __restrict__ off, int q2_rt,
                                                       double kappa, double2* __restrict__ val) {
+    const int q2 = Q2 ? Q2 : q2_rt;
     const int b = blockIdx.x, t = bt[b], s = bs[b];
     const int nt = c_size[t], ns = c_size[s];
     const int64_t bt0 = c_begin[t], bs0 = c_begin[s];
@@ -116,10 +119,12 @@ __global__ void __launch_bounds__(256) k_near_regular(const double4* __restrict_
         const double4* X = pts + pi * q2;
         const double4* Y = pts + pj * q2;
         double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 1
         for (int p = 0; p < q2; ++p) {
             const double4 xp = X[p];
             double2 row = make_double2(0.0, 0.0);
-            for (int q = 0; q < q2; ++q) {
+#pragma unroll
+            for (int q = 0; q < (Q2 ? Q2 : q2); ++q) {
                 const double4 yq = Y[q];
                 acc_g(row, make_double3(xp.x, xp.y, xp.z), make_double3(yq.x, yq.y, yq.z), yq.w, kappa);
             }
@@ -193,6 +198,14 @@ __global__ void __launch_bounds__(256, 3) k_near_singular(const double* __restri
                                                           const SingItem* __restrict__ items, int64_t nitems, int nq_rt,
                                                           double kappa, double2* __restrict__ val) {
     const int nq = NQ ? NQ : nq_rt;
+    // the rule in shared memory: lanes index it at different points (constant memory would
+    // serialise the divergent addresses)
+    __shared__ double sgx[NQ_MAX], sgw[NQ_MAX];
+    if (threadIdx.x < NQ_MAX) {
+        sgx[threadIdx.x] = c_gx[threadIdx.x];
+        sgw[threadIdx.x] = c_gw[threadIdx.x];
+    }
+    __syncthreads();
     const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= nitems) return;
@@ -207,8 +220,8 @@ __global__ void __launch_bounds__(256, 3) k_near_singular(const double* __restri
         for (int q = lane; q < q4; q += 32) {
             const int a = q / q3, b = (q / (nq * nq)) % nq, c = (q / nq) % nq, d = q % nq;
             double u1, u2, v1, v2;
-            const double wr = ss_region(cas, r, c_gx[a], c_gx[b], c_gx[c], c_gx[d], u1, u2, v1, v2);
-            acc_g(acc, chi(X, u1, u2), chi(Y, v1, v2), wr * (c_gw[a] * c_gw[b]) * (c_gw[c] * c_gw[d]), kappa);
+            const double wr = ss_region(cas, r, sgx[a], sgx[b], sgx[c], sgx[d], u1, u2, v1, v2);
+            acc_g(acc, chi(X, u1, u2), chi(Y, v1, v2), wr * (sgw[a] * sgw[b]) * (sgw[c] * sgw[d]), kappa);
         }
     for (int o = 16; o; o >>= 1) {
         acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
@@ -397,8 +410,12 @@ void near_assemble(Shard* C, int nq_sing, int nq_reg) {
     });
     if (N.nblk)
         C->timed("nearfield", 1, [&] {
-            k_near_regular<<<N.nblk, 256, 0, s>>>(N.d_pts.p, P.tri, P.perm, C->d_c_begin.p, C->d_c_size.p, N.d_t.p, N.d_s.p,
-                                                  N.d_off.p, q2, P.kappa, N.d_val.p);
+            if (q2 == 9)
+                k_near_regular<9><<<N.nblk, 256, 0, s>>>(N.d_pts.p, P.tri, P.perm, C->d_c_begin.p, C->d_c_size.p, N.d_t.p,
+                                                         N.d_s.p, N.d_off.p, q2, P.kappa, N.d_val.p);
+            else
+                k_near_regular<0><<<N.nblk, 256, 0, s>>>(N.d_pts.p, P.tri, P.perm, C->d_c_begin.p, C->d_c_size.p, N.d_t.p,
+                                                         N.d_s.p, N.d_off.p, q2, P.kappa, N.d_val.p);
         });
     if (N.nsing)
         C->timed("nearfield", 1, [&] {

@@ -110,3 +110,26 @@ def test_near_block_matches_entrywise():
         for b in (0, 5, len(cols) - 1):
             i, j = rows[a], cols[b]
             assert abs(B[a, b] - nf.entry(xyz[tri[i]], xyz[tri[j]], tri[i], tri[j], cfg["kappa"])) <= 1e-15 * abs(B).max()
+
+
+def test_near_and_far_blocks_partition_the_matrix():
+    """L+ and L- tile I x I exactly once (Def. 2.5, P:414-452), so G = G_far + N has every entry once;
+    every touching pair of triangles lies in L- (the boxes of touching triangles intersect)."""
+    from synth import get_config, mesh_for
+    from oracle.structure import DH2Structure
+    for name in ("P1", "P3"):
+        cfg = get_config(name)
+        xyz, tri = mesh_for(cfg)
+        st = DH2Structure(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"])
+        ct, n = st.ct, len(tri)
+        cover = np.zeros((n, n), dtype=np.int32)
+        rng = lambda t: ct.perm[ct.begin[t]: ct.begin[t] + ct.size(t)]  # noqa: E731
+        for t, s, _c in st.blocks:
+            cover[np.ix_(rng(int(t)), rng(int(s)))] += 1
+        near = np.zeros((n, n), dtype=bool)
+        for t, s in st.near:
+            cover[np.ix_(rng(int(t)), rng(int(s)))] += 1
+            near[np.ix_(rng(int(t)), rng(int(s)))] = True
+        assert (cover == 1).all()
+        touch = (tri[:, None, :, None] == tri[None, :, None, :]).any(axis=(2, 3))
+        assert near[touch].all()
