@@ -201,6 +201,8 @@ int dh2_set_stream(dh2_ctx* ctx, void* cuda_stream);
  *     (thread c holds column c of a 16-row (1) or 24-row (2) chunk in registers); 0: CTA-cooperative.
  *   "qr_cq_tw" (0..3, default 0), "qr_cq_tw_leaf" (0..3, default 3): the same for the total
  *     weights above / at the leaf levels (3: chunk rows formed by thread-column FMAs).
+ *   "near_tma" (0 | 1, default 1): nearfield matvec streams the blocks N_b through a ring of
+ *     shared-memory stages filled by cp.async.bulk (TMA) on mbarriers; 0: direct global loads.
  *   Further A/B switches (qr_wy, qr_flag, trunc_direct, lean_chunks) are listed in DESIGN.md §8.
  *   All variants give the same ranks, singular values and matrices up to rounding (tests).
  * Errors: DH2_EINVAL for an unknown name or value. */

@@ -2226,6 +2226,11 @@ int dh2_set_option(dh2_ctx* X, const char* name, int64_t value) {
         for (auto& S : X->sh) S->P.qr_wy = S->qr_wy_init = (int)value;
         return DH2_OK;
     }
+    if (nm == "near_tma") {  // nearfield matvec: 1 = TMA bulk-copy ring (default), 0 = direct global loads (A/B)
+        if (value != 0 && value != 1) return fail(X, DH2_EINVAL, nm + " must be 0 or 1");
+        for (auto& S : X->sh) S->near_tma = (int)value;
+        return DH2_OK;
+    }
     if (nm == "bw_variant") {  // block weights at k > 64: 1 = unrolled loads + register-blocked norm GEMM
         if (value != 0 && value != 1) return fail(X, DH2_EINVAL, nm + " must be 0 or 1");
         for (auto& S : X->sh) S->P.bw_variant = S->bw_variant_init = (int)value;

@@ -102,14 +102,16 @@ __device__ inline void leafV_out(double2* V, int nt, const double2* ph, const do
                 ly[j] = Lq[MM + j];
             }
             const double lz = Lq[2 * MM + jz];
+            const double pzx = p.x * lz, pzy = p.y * lz;  // p L_z, then (p L_z) L_y: 2 FMAs per entry
 #pragma unroll
-            for (int b = 0; b < MM; ++b)
+            for (int b = 0; b < MM; ++b) {
+                const double qx = pzx * ly[b], qy = pzy * ly[b];
 #pragma unroll
                 for (int a = 0; a < MM; ++a) {
-                    const double l = lx[a] * ly[b] * lz;
-                    acc[b][a].x = fma(p.x, l, acc[b][a].x);
-                    acc[b][a].y = fma(p.y, l, acc[b][a].y);
+                    acc[b][a].x = fma(qx, lx[a], acc[b][a].x);
+                    acc[b][a].y = fma(qy, lx[a], acc[b][a].y);
                 }
+            }
         }
 #pragma unroll
         for (int b = 0; b < MM; ++b)

@@ -276,6 +276,109 @@ __global__ void __launch_bounds__(256) k_mv_near(const int64_t* __restrict__ c_b
     }
 }
 
+
+// TMA form of the nearfield matvec: the row group's blocks N_b (contiguous, column-major, 16-byte
+// aligned) are streamed through a ring of NEAR_ST shared-memory stages by 1-D bulk copies
+// (cp.async.bulk, completion on an mbarrier per stage), NEAR_CE coefficients (16 KB) per stage, issued
+// NEAR_ST - 1 chunks ahead by thread 0; the 256 threads multiply from shared memory (R rows x 256/R
+// column slices).  One __syncthreads per chunk hands the consumed stage back to the producer.
+constexpr int NEAR_ST = 4, NEAR_CE = 1024;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, int n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@p bra D;\nbra W;\nD:\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(b))
+                 : "memory");
+}
+
+struct NearCursor {  // walks the chunks (block b, first column c0) of a row group in order
+    int b, c0;
+    __device__ __forceinline__ void next(int cw, int ns) {
+        c0 += cw;
+        if (c0 >= ns) {
+            c0 = 0;
+            ++b;
+        }
+    }
+};
+
+template <int R>
+__global__ void __launch_bounds__(256) k_mv_near_tma(const int64_t* __restrict__ c_begin, const int* __restrict__ c_size,
+                                                     const int* __restrict__ gptr, const int* __restrict__ bt,
+                                                     const int* __restrict__ bs, const int64_t* __restrict__ off,
+                                                     const double2* __restrict__ val, const double2* __restrict__ xp,
+                                                     double2* __restrict__ yp) {
+    constexpr int NS = 256 / R;
+    extern __shared__ __align__(128) unsigned char near_smem[];
+    double2* ring = reinterpret_cast<double2*>(near_smem);                          // NEAR_ST x NEAR_CE
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)NEAR_ST * NEAR_CE);  // NEAR_ST barriers
+    __shared__ double2 red[NS][R];
+    const int g0 = gptr[blockIdx.x], g1 = gptr[blockIdx.x + 1];
+    const int t = bt[g0], nt = c_size[t];  // nt <= R (checked by the host)
+    const int cwmax = NEAR_CE / nt;        // columns per chunk
+    const int lr = threadIdx.x % R, sl = threadIdx.x / R;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NEAR_ST; ++i) mbar_init(full + i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    NearCursor pc{g0, 0};  // producer (thread 0 only)
+    int issued = 0;
+    auto issue = [&]() {
+        if (pc.b >= g1) return;
+        const int ns = c_size[bs[pc.b]];
+        const int cw = min(cwmax, ns - pc.c0);
+        const int st = issued % NEAR_ST;
+        bulk_g2s(ring + (size_t)st * NEAR_CE, val + off[pc.b] + (int64_t)pc.c0 * nt, (uint32_t)(cw * nt) * 16u, full + st);
+        ++issued;
+        pc.next(cw, ns);
+    };
+    if (threadIdx.x == 0)
+        for (int i = 0; i < NEAR_ST - 1; ++i) issue();
+    double2 acc = make_double2(0.0, 0.0);
+    NearCursor cc{g0, 0};
+    for (int i = 0; cc.b < g1; ++i) {
+        if (threadIdx.x == 0) issue();  // into the stage consumed in iteration i - 1
+        const int s = bs[cc.b], ns = c_size[s];
+        const int cw = min(cwmax, ns - cc.c0);
+        const int st = i % NEAR_ST;
+        mbar_wait(full + st, (uint32_t)(i / NEAR_ST) & 1u);
+        if (lr < nt) {
+            const double2* N = ring + (size_t)st * NEAR_CE;
+            const double2* x = xp + c_begin[s] + cc.c0;
+#pragma unroll 4
+            for (int c = sl; c < cw; c += NS) {
+                const double2 v = N[c * nt + lr], xv = __ldg(x + c);
+                acc.x += v.x * xv.x - v.y * xv.y;
+                acc.y += v.x * xv.y + v.y * xv.x;
+            }
+        }
+        cc.next(cw, ns);
+        __syncthreads();
+    }
+    red[sl][lr] = acc;
+    __syncthreads();
+    if (sl == 0 && lr < nt) {
+        double2 y = yp[c_begin[t] + lr];
+        for (int k = 0; k < NS; ++k) {
+            y.x += red[k][lr].x;
+            y.y += red[k][lr].y;
+        }
+        yp[c_begin[t] + lr] = y;
+    }
+}
+
 }  // namespace
 
 void near_assemble(Shard* C, int nq_sing, int nq_reg) {
@@ -328,6 +431,7 @@ void near_assemble(Shard* C, int nq_sing, int nq_reg) {
     std::vector<SingItem> items;
     std::vector<int64_t> nb;
     int64_t expected = 0;
+    std::vector<char> seen(n, 0);
     for (int b = 0; b < N.nblk; ++b) {
         const int t = N.t[b], sc = N.s[b];
         const int64_t t0 = T.begin[t], nt = T.size(t), s0 = T.begin[sc], ns = T.size(sc);
@@ -338,7 +442,10 @@ void near_assemble(Shard* C, int nq_sing, int nq_reg) {
                 for (int64_t q = vptr[tri[3 * i + k]]; q < vptr[tri[3 * i + k] + 1]; ++q) nb.push_back(vtri[q]);
             std::sort(nb.begin(), nb.end());
             nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
-            if (b == 0 || N.t[b - 1] != t) expected += (int64_t)nb.size();
+            if (!seen[i]) {  // once per row triangle: with mixed levels a row lies in several row clusters
+                seen[i] = 1;
+                expected += (int64_t)nb.size();
+            }
             for (int64_t j : nb) {
                 const int64_t pj = ipos[j];
                 if (pj < s0 || pj >= s0 + ns) continue;
@@ -435,7 +542,18 @@ void near_matvec(Shard* C) {
     if (!N.on || !N.ngroups) return;
     C->kstat["matvec_near"].bytes += 16.0 * (double)N.values;  // every coefficient read once
     C->timed("matvec_near", 1, [&] {
-        if (N.max_rows <= 32)
+        constexpr size_t smem = (size_t)NEAR_ST * NEAR_CE * sizeof(double2) + NEAR_ST * sizeof(uint64_t);
+        if (C->near_tma && N.max_rows <= 64) {
+            if (N.max_rows <= 32) {
+                CK(cudaFuncSetAttribute(k_mv_near_tma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                k_mv_near_tma<32><<<N.ngroups, 256, smem, C->stream>>>(C->d_c_begin.p, C->d_c_size.p, N.d_gptr.p, N.d_t.p,
+                                                                       N.d_s.p, N.d_off.p, N.d_val.p, C->d_xp.p, C->d_yp.p);
+            } else {
+                CK(cudaFuncSetAttribute(k_mv_near_tma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                k_mv_near_tma<64><<<N.ngroups, 256, smem, C->stream>>>(C->d_c_begin.p, C->d_c_size.p, N.d_gptr.p, N.d_t.p,
+                                                                       N.d_s.p, N.d_off.p, N.d_val.p, C->d_xp.p, C->d_yp.p);
+            }
+        } else if (N.max_rows <= 32)
             k_mv_near<32><<<N.ngroups, 256, 0, C->stream>>>(C->d_c_begin.p, C->d_c_size.p, N.d_gptr.p, N.d_t.p, N.d_s.p,
                                                            N.d_off.p, N.d_val.p, C->d_xp.p, C->d_yp.p);
         else

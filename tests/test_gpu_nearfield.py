@@ -156,3 +156,28 @@ def test_full_size_sampled(name):
     assert st["kernels"]["nearfield"]["launches"] >= 3 and st["nearfield"]["assembled"]
     assert st["nearfield"]["touching_entries"] > h.n
     h.close()
+
+
+@pytest.mark.parametrize("name", ["P1", "P8", "C1", "P6", "P7"])
+def test_near_matvec_tma_and_direct(name):
+    """Both forms of the nearfield matvec (option near_tma: 1 = blocks streamed through shared memory
+    by cp.async.bulk stages, 0 = direct global loads) against the oracle's N x; leaves of 8, 15 (ragged,
+    cut mesh), 16 and 64 triangles, i.e. both row widths of the kernel and chunks that end inside a
+    stage.  The two forms sum each row in a different order: equal to rounding, not bitwise."""
+    h, cfg, xyz, tri = near_run(name)
+    st = DH2Structure(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"])
+    blocks = nf.nearfield_blocks(st, xyz, tri, cfg["kappa"])
+    for seed in (1, 2):
+        x = seeded_vector(h.n, seed)
+        yn = nf.near_matvec(st, blocks, x)
+        far = h.matvec(x, 0)
+        got = {}
+        for tma in (1, 0):
+            h.set_option("near_tma", tma)
+            got[tma] = h.matvec(x, 0, add_near=True) - far
+            assert np.linalg.norm(got[tma] - yn) <= 1e-12 * np.linalg.norm(yn)
+        assert np.linalg.norm(got[1] - got[0]) <= 1e-13 * np.linalg.norm(yn)
+    h.set_option("near_tma", 1)
+    from paper_1809_04384_b200.dh2 import DH2Error
+    with pytest.raises(DH2Error, match="DH2_EINVAL"):
+        h.set_option("near_tma", 2)
