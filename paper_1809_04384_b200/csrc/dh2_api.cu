@@ -842,6 +842,7 @@ void upload_all(Shard* C, const double* xyz, int64_t nv, const int64_t* tri) {
     P.qr_cq = C->qr_cq_init;
     P.t64_threads = C->t64_threads_init;
     P.bw_variant = C->bw_variant_init;
+    P.mv_fwd_warp = C->mv_fwd_warp_init;
     P.qr_cq_tw = C->qr_cq_tw_init;
     P.qr_cq_tw_leaf = C->qr_cq_tw_leaf_init;
     P.qr_cq64 = C->qr_cq64_init;
@@ -2229,6 +2230,11 @@ int dh2_set_option(dh2_ctx* X, const char* name, int64_t value) {
     if (nm == "near_tma") {  // nearfield matvec: 1 = TMA bulk-copy ring (default), 0 = direct global loads (A/B)
         if (value != 0 && value != 1) return fail(X, DH2_EINVAL, nm + " must be 0 or 1");
         for (auto& S : X->sh) S->near_tma = (int)value;
+        return DH2_OK;
+    }
+    if (nm == "mv_forward_warp") {  // matvec, leaf forward transform: 1 = warp per coefficient (default), 0 = thread per coefficient
+        if (value < 0 || value > 2) return fail(X, DH2_EINVAL, nm + " must be 0, 1 or 2");
+        for (auto& S : X->sh) S->P.mv_fwd_warp = S->mv_fwd_warp_init = (int)value;
         return DH2_OK;
     }
     if (nm == "bw_variant") {  // block weights at k > 64: 1 = unrolled loads + register-blocked norm GEMM

@@ -1396,15 +1396,52 @@ void launch_project(const PlanD& P, int b0, int nb, int maxkrow, const int* mirr
 // ============================================================== matvec (far field)
 // Forward transformation on the column basis: xh_sc = B_sc^* x|_s, nested through the
 // transfers (V, E for ORIG; Q', F' for RECOMP).  Coefficients stored with stride k.
-__global__ void k_mv_forward(PlanD P, bool recomp, int p0, const double2* xp, double2* xh) {
+__global__ void k_mv_forward(PlanD P, bool recomp, int p0, int pend, int wpp, const double2* xp, double2* xh) {
     const PassD& X = P.col;
-    const int p = p0 + blockIdx.x, k = P.k, m = P.m;
+    // wpp: one warp per pair and blockDim / 32 pairs per CTA (RECOMP, small ranks), else one CTA per pair
+    const int lane = threadIdx.x & 31;
+    const int p = p0 + (wpp ? blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5) : blockIdx.x), k = P.k, m = P.m;
+    if (p >= pend) return;
+    const int tid = wpp ? lane : threadIdx.x, nth = wpp ? 32 : blockDim.x;
     // sym: V_sc and E of the column pair are the conjugates of those of the row pair (s,-c)
     const bool vcj = !recomp && P.sym;
     const int bp = vcj ? P.row.bp[P.col2row[p]] : X.bp[p];
     const bool leaf = X.child0[p] < 0;
     const int kout = recomp ? X.rank[p] : k;
-    for (int a = threadIdx.x; a < kout; a += blockDim.x) {
+    if (leaf && P.mv_fwd_warp) {
+        // a warp per output coefficient (two at a time): lanes over the rows of the leaf (coalesced reads
+        // of the column B(:, a); a thread per coefficient, as below, reads with stride nt and leaves
+        // most lanes idle at small ranks), shuffle reduction in a fixed order
+        const int w = wpp ? 0 : threadIdx.x >> 5, nw = wpp ? 1 : blockDim.x >> 5;
+        const int t = P.bp_t[bp];
+        const int nt = P.c_size[t];
+        const double2* x = xp + P.c_begin[t];
+        const double2* B = recomp ? (X.Q + X.Q_off[p]) : (P.V + P.bp_V_off[bp]);
+        const bool plain = (recomp && P.col_conj) || vcj;
+        for (int a = w; a < kout; a += 2 * nw) {
+            const int a2 = a + nw;
+            const bool two = a2 < kout;
+            double2 acc = cmk(0.0, 0.0), acc2 = cmk(0.0, 0.0);
+            for (int i = lane; i < nt; i += 32) {
+                const double2 xv = x[i], b1 = B[i + (size_t)a * nt], b2 = two ? B[i + (size_t)a2 * nt] : cmk(0.0, 0.0);
+                if (plain) {
+                    cfma(acc, b1, xv);
+                    cfma(acc2, b2, xv);
+                } else {
+                    cfma_cj(acc, b1, xv);
+                    cfma_cj(acc2, b2, xv);
+                }
+            }
+            acc = warp_sum2(acc);
+            acc2 = warp_sum2(acc2);
+            if (lane == 0) {
+                xh[(size_t)p * k + a] = acc;
+                if (two) xh[(size_t)p * k + a2] = acc2;
+            }
+        }
+        return;
+    }
+    for (int a = tid; a < kout; a += nth) {
         double2 acc = cmk(0.0, 0.0);
         if (leaf) {
             const int t = P.bp_t[bp];
@@ -1450,11 +1487,14 @@ __global__ void k_mv_forward(PlanD P, bool recomp, int p0, const double2* xp, do
 }
 
 // Coupling: yh_tc = sum_{b=(t,s,c)} S_b xh_sc (ORIG) or S~_b xh'_sc (RECOMP).
-__global__ void k_mv_couple(PlanD P, bool recomp, int p0, const double2* xh, double2* yh) {
+// gsz threads per pair, blockDim / gsz pairs per CTA (RECOMP ranks are ~10-20: 16 lanes per pair keep
+// the lanes busy and cut the CTA count by 8; each coefficient is summed by one thread in the same order).
+__global__ void k_mv_couple(PlanD P, bool recomp, int p0, int pend, int gsz, const double2* xh, double2* yh) {
     const PassD& X = P.row;
-    const int p = p0 + blockIdx.x, k = P.k;
+    const int p = p0 + blockIdx.x * (blockDim.x / gsz) + threadIdx.x / gsz, k = P.k;
+    if (p >= pend) return;
     const int kout = recomp ? X.rank[p] : k;
-    for (int a = threadIdx.x; a < kout; a += blockDim.x) {
+    for (int a = threadIdx.x % gsz; a < kout; a += gsz) {
         double2 acc = cmk(0.0, 0.0);
         for (int ib = X.blk_ptr[p]; ib < X.blk_ptr[p + 1]; ++ib) {
             const int b = X.blk[ib];
@@ -1476,11 +1516,12 @@ __global__ void k_mv_couple(PlanD P, bool recomp, int p0, const double2* xh, dou
 
 // Backward transformation (top-down): yh_{t'c'} += T yh_{tc} for every parent (t,c) with
 // sd(c) = c'; T = E_{t'c} (ORIG) or F_{t'c} (RECOMP).
-__global__ void k_mv_backward(PlanD P, bool recomp, int p0, double2* yh) {
+__global__ void k_mv_backward(PlanD P, bool recomp, int p0, int pend, int gsz, double2* yh) {
     const PassD& X = P.row;
-    const int p = p0 + blockIdx.x, k = P.k, m = P.m;
+    const int p = p0 + blockIdx.x * (blockDim.x / gsz) + threadIdx.x / gsz, k = P.k, m = P.m;
+    if (p >= pend) return;
     const int kout = recomp ? X.rank[p] : k;
-    for (int a = threadIdx.x; a < kout; a += blockDim.x) {
+    for (int a = threadIdx.x % gsz; a < kout; a += gsz) {
         double2 acc = yh[(size_t)p * k + a];
         for (int ip = X.par_ptr[p]; ip < X.par_ptr[p + 1]; ++ip) {
             const int pp = X.par[ip];
@@ -1556,13 +1597,25 @@ __global__ void k_permute(const int64_t* perm, const double2* in, double2* out, 
 }
 
 void launch_mv_forward(const PlanD& P, bool recomp, int p0, int np, const double2* xp, double2* xh, cudaStream_t s) {
-    if (np) k_mv_forward<<<np, 64, 0, s>>>(P, recomp, p0, xp, xh);
+    if (!np) return;
+    if (recomp && P.mv_fwd_warp == 2)
+        k_mv_forward<<<(np + 3) / 4, 128, 0, s>>>(P, recomp, p0, p0 + np, 1, xp, xh);
+    else
+        k_mv_forward<<<np, 64, 0, s>>>(P, recomp, p0, p0 + np, 0, xp, xh);
 }
 void launch_mv_couple(const PlanD& P, bool recomp, int p0, int np, const double2* xh, double2* yh, cudaStream_t s) {
-    if (np) k_mv_couple<<<np, 64, 0, s>>>(P, recomp, p0, xh, yh);
+    if (!np) return;
+    if (recomp && P.mv_fwd_warp)
+        k_mv_couple<<<(np + 7) / 8, 128, 0, s>>>(P, recomp, p0, p0 + np, 16, xh, yh);
+    else
+        k_mv_couple<<<np, 64, 0, s>>>(P, recomp, p0, p0 + np, 64, xh, yh);
 }
 void launch_mv_backward(const PlanD& P, bool recomp, int p0, int np, double2* yh, cudaStream_t s) {
-    if (np) k_mv_backward<<<np, 64, 0, s>>>(P, recomp, p0, yh);
+    if (!np) return;
+    if (recomp && P.mv_fwd_warp)
+        k_mv_backward<<<(np + 7) / 8, 128, 0, s>>>(P, recomp, p0, p0 + np, 16, yh);
+    else
+        k_mv_backward<<<np, 64, 0, s>>>(P, recomp, p0, p0 + np, 64, yh);
 }
 void launch_mv_leaf_out(const PlanD& P, bool recomp, const int* lc, const int* lc_ptr, int g0, int nlc, const double2* yh,
                         double2* yp, cudaStream_t s) {

@@ -48,6 +48,7 @@ struct PlanD {
     int qr_cq_tw_leaf;    // variant at leaf levels ("qr_cq_tw_leaf", default 3: thread-column chunk rows)
     int qr_cq64, qr_cq64_tw;  // k <= 64: the column-per-thread basis / total weights ("qr_cq64", "qr_cq64_tw": 0, 1, 3)
     double2* cq_scr;      // their scratch triangles (cq_scratch_elems), null when unused
+    int mv_fwd_warp;      // leaf forward transform of the matvec: 1 = one warp per coefficient, coalesced ("mv_forward_warp")
     int bw_variant;       // block weights at k > 64: 1 = unrolled S loads + register-blocked norm GEMM ("bw_variant")
     int t64_threads;      // threads of the Jacobi + epilogue kernel of the wide split leaf truncation ("trunc64_threads")
     int sym;              // 1: only row basis pairs have V/R/E; the column side of a block (t,s,c) reads

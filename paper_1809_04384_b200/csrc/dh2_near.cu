@@ -239,13 +239,13 @@ __global__ void __launch_bounds__(256, 3) k_near_singular(const double* __restri
 // the slices in shared memory.
 template <int R>
 __global__ void __launch_bounds__(256) k_mv_near(const int64_t* __restrict__ c_begin, const int* __restrict__ c_size,
-                                                 const int* __restrict__ gptr, const int* __restrict__ bt,
+                                                 const int* __restrict__ gord, const int* __restrict__ gptr, const int* __restrict__ bt,
                                                  const int* __restrict__ bs, const int64_t* __restrict__ off,
                                                  const double2* __restrict__ val, const double2* __restrict__ xp,
                                                  double2* __restrict__ yp) {
     constexpr int NS = 256 / R;
     __shared__ double2 red[NS][R];
-    const int g0 = gptr[blockIdx.x], g1 = gptr[blockIdx.x + 1];
+    const int g0 = gptr[gord[blockIdx.x]], g1 = gptr[gord[blockIdx.x] + 1];
     const int t = bt[g0], nt = c_size[t];
     const int lr = threadIdx.x % R, sl = threadIdx.x / R;
     for (int a0 = 0; a0 < nt; a0 += R) {
@@ -314,7 +314,7 @@ struct NearCursor {  // walks the chunks (block b, first column c0) of a row gro
 
 template <int R>
 __global__ void __launch_bounds__(256) k_mv_near_tma(const int64_t* __restrict__ c_begin, const int* __restrict__ c_size,
-                                                     const int* __restrict__ gptr, const int* __restrict__ bt,
+                                                     const int* __restrict__ gord, const int* __restrict__ gptr, const int* __restrict__ bt,
                                                      const int* __restrict__ bs, const int64_t* __restrict__ off,
                                                      const double2* __restrict__ val, const double2* __restrict__ xp,
                                                      double2* __restrict__ yp) {
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(256) k_mv_near_tma(const int64_t* __restrict__
     double2* ring = reinterpret_cast<double2*>(near_smem);                          // NEAR_ST x NEAR_CE
     uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)NEAR_ST * NEAR_CE);  // NEAR_ST barriers
     __shared__ double2 red[NS][R];
-    const int g0 = gptr[blockIdx.x], g1 = gptr[blockIdx.x + 1];
+    const int g0 = gptr[gord[blockIdx.x]], g1 = gptr[gord[blockIdx.x] + 1];
     const int t = bt[g0], nt = c_size[t];  // nt <= R (checked by the host)
     const int cwmax = NEAR_CE / nt;        // columns per chunk
     const int lr = threadIdx.x % R, sl = threadIdx.x / R;
@@ -505,6 +505,17 @@ void near_assemble(Shard* C, int nq_sing, int nq_reg) {
     N.d_s.upload(N.s, s);
     N.d_off.upload(N.off, s);
     N.d_gptr.upload(gptr, s);
+    {   // with mixed levels a row triangle lies in row clusters of several levels (a cluster and a descendant
+        // leaf): the matvec adds one level per launch, in level order, so that no two CTAs update the same rows
+        std::vector<int> gord(N.ngroups);
+        for (int g = 0; g < N.ngroups; ++g) gord[g] = g;
+        std::stable_sort(gord.begin(), gord.end(),
+                         [&](int a, int b) { return T.level[N.t[gptr[a]]] < T.level[N.t[gptr[b]]]; });
+        N.glev_ptr.assign(1, 0);
+        for (int i = 1; i <= N.ngroups; ++i)
+            if (i == N.ngroups || T.level[N.t[gptr[gord[i]]]] != T.level[N.t[gptr[gord[i - 1]]]]) N.glev_ptr.push_back(i);
+        N.d_gord.upload(gord, s);
+    }
     N.d_val.alloc((size_t)std::max<int64_t>(N.values, 1));
     const int q2 = nq_reg * nq_reg;
     N.d_pts.alloc((size_t)n * q2);
@@ -541,24 +552,30 @@ void near_matvec(Shard* C) {
     auto& N = C->near;
     if (!N.on || !N.ngroups) return;
     C->kstat["matvec_near"].bytes += 16.0 * (double)N.values;  // every coefficient read once
-    C->timed("matvec_near", 1, [&] {
-        constexpr size_t smem = (size_t)NEAR_ST * NEAR_CE * sizeof(double2) + NEAR_ST * sizeof(uint64_t);
-        if (C->near_tma && N.max_rows <= 64) {
-            if (N.max_rows <= 32) {
-                CK(cudaFuncSetAttribute(k_mv_near_tma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                k_mv_near_tma<32><<<N.ngroups, 256, smem, C->stream>>>(C->d_c_begin.p, C->d_c_size.p, N.d_gptr.p, N.d_t.p,
-                                                                       N.d_s.p, N.d_off.p, N.d_val.p, C->d_xp.p, C->d_yp.p);
-            } else {
-                CK(cudaFuncSetAttribute(k_mv_near_tma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                k_mv_near_tma<64><<<N.ngroups, 256, smem, C->stream>>>(C->d_c_begin.p, C->d_c_size.p, N.d_gptr.p, N.d_t.p,
-                                                                       N.d_s.p, N.d_off.p, N.d_val.p, C->d_xp.p, C->d_yp.p);
-            }
-        } else if (N.max_rows <= 32)
-            k_mv_near<32><<<N.ngroups, 256, 0, C->stream>>>(C->d_c_begin.p, C->d_c_size.p, N.d_gptr.p, N.d_t.p, N.d_s.p,
-                                                           N.d_off.p, N.d_val.p, C->d_xp.p, C->d_yp.p);
-        else
-            k_mv_near<64><<<N.ngroups, 256, 0, C->stream>>>(C->d_c_begin.p, C->d_c_size.p, N.d_gptr.p, N.d_t.p, N.d_s.p,
-                                                           N.d_off.p, N.d_val.p, C->d_xp.p, C->d_yp.p);
+    constexpr size_t smem = (size_t)NEAR_ST * NEAR_CE * sizeof(double2) + NEAR_ST * sizeof(uint64_t);
+    const bool tma = C->near_tma && N.max_rows <= 64;
+    if (tma) {
+        CK(cudaFuncSetAttribute(k_mv_near_tma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k_mv_near_tma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    }
+    const int nlev = (int)N.glev_ptr.size() - 1;
+    C->timed("matvec_near", nlev, [&] {
+        for (int i = 0; i < nlev; ++i) {  // one launch per tree level of the row clusters (one, unless levels are mixed)
+            const int* gord = N.d_gord.p + N.glev_ptr[i];
+            const int ng = N.glev_ptr[i + 1] - N.glev_ptr[i];
+            if (tma && N.max_rows <= 32)
+                k_mv_near_tma<32><<<ng, 256, smem, C->stream>>>(C->d_c_begin.p, C->d_c_size.p, gord, N.d_gptr.p, N.d_t.p, N.d_s.p,
+                                                                N.d_off.p, N.d_val.p, C->d_xp.p, C->d_yp.p);
+            else if (tma)
+                k_mv_near_tma<64><<<ng, 256, smem, C->stream>>>(C->d_c_begin.p, C->d_c_size.p, gord, N.d_gptr.p, N.d_t.p, N.d_s.p,
+                                                                N.d_off.p, N.d_val.p, C->d_xp.p, C->d_yp.p);
+            else if (N.max_rows <= 32)
+                k_mv_near<32><<<ng, 256, 0, C->stream>>>(C->d_c_begin.p, C->d_c_size.p, gord, N.d_gptr.p, N.d_t.p, N.d_s.p,
+                                                         N.d_off.p, N.d_val.p, C->d_xp.p, C->d_yp.p);
+            else
+                k_mv_near<64><<<ng, 256, 0, C->stream>>>(C->d_c_begin.p, C->d_c_size.p, gord, N.d_gptr.p, N.d_t.p, N.d_s.p,
+                                                         N.d_off.p, N.d_val.p, C->d_xp.p, C->d_yp.p);
+        }
     });
 }
 

@@ -270,6 +270,7 @@ struct Shard {
     int trunc_mode_init = 1; // initial value of PlanD::trunc_mode (direct: measured -3 % C4, -16 % C5 leaves)
     int qr_wy_init = 0;      // initial value of PlanD::qr_wy (blocked WY appends measured slower on C4: 0) (dh2_set_option("qr_wy") sets the plan directly)
     int near_tma = 1;         // dh2_set_option("near_tma"): nearfield matvec streams N_b by cp.async.bulk (TMA) stages
+    int mv_fwd_warp_init = 1; // PlanD::mv_fwd_warp
     int bw_variant_init = 1;  // PlanD::bw_variant (k > 64 only: C4 block weights -5 %)
     int t64_threads_init = 128;  // PlanD::t64_threads
     int split_trunc64 = 1;
@@ -317,6 +318,8 @@ struct Shard {
         std::vector<int> t, s;          // per own block
         std::vector<int64_t> off;       // entry offset per own block
         DevBuf<int> d_t, d_s, d_gptr;   // d_gptr: blocks of row group g = [gptr[g], gptr[g+1])
+        DevBuf<int> d_gord;             // row groups ordered by the tree level of their row cluster
+        std::vector<int> glev_ptr;      // d_gord[glev_ptr[i] .. glev_ptr[i+1]): one level (disjoint rows: one launch)
         DevBuf<int64_t> d_off;
         DevBuf<double4> d_pts;          // n x nq_reg^2 Duffy-Gauss points (x, y, z, w 2|tau|), cluster order
         DevBuf<double2> d_val;

@@ -51,7 +51,7 @@ def _check_block(cfg, xyz, tri, st, t, s, got):
     assert err <= 1e-12, (t, s, err)
 
 
-@pytest.mark.parametrize("name", ["P1", "P3", "C1"])
+@pytest.mark.parametrize("name", ["P1", "P3", "C1", "P8"])
 def test_nearfield_blocks_all(name):
     h, cfg, xyz, tri = near_run(name)
     st = DH2Structure(xyz, tri, cfg["kappa"], cfg["m"], cfg["leaf"], cfg["eta1"], cfg["eta2"])

@@ -144,6 +144,29 @@ def test_G4_matvec(name, sym):
         assert np.linalg.norm(yrg - yr) <= 1e-10 * ref
 
 
+@pytest.mark.parametrize("name,sym", [("P1", 1), ("P8", 1), ("P6", 1), ("P6", 0), ("P3", 0), ("C2", 1)])
+def test_G4_matvec_variants(name, sym):
+    """The matvec's launch shapes (option mv_forward_warp: 0 = a thread per coefficient and a CTA per
+    pair everywhere, 1 = a warp per coefficient in the leaf forward transform and 16 lanes per pair in
+    the coupling and backward steps, 2 = also a warp per pair in the forward transform) against the
+    oracle, ORIG and RECOMP, on leaves of 8, 15 (mixed levels), 16, 32 and 64 triangles."""
+    h, g, rc = gpu_run(name, sym=sym)
+    x = seeded_vector(rc.st.n, 4)
+    yo = ops.matvec(rc, x, "orig")
+    yr = ops.matvec(rc, x, "recomp")
+    ref = np.linalg.norm(yo)
+    got = {}
+    try:
+        for v in (0, 1, 2):
+            h.set_option("mv_forward_warp", v)
+            assert np.linalg.norm(h.matvec(x, 0) - yo) <= 1e-12 * ref
+            got[v] = h.matvec(x, 1)
+            assert np.linalg.norm(got[v] - yr) <= 1e-10 * ref
+        assert np.linalg.norm(got[1] - got[0]) <= 1e-13 * ref and np.linalg.norm(got[2] - got[0]) <= 1e-13 * ref
+    finally:
+        h.set_option("mv_forward_warp", 1)
+
+
 @pytest.mark.parametrize("name,sym", [c for c in CASES if c[0] in SMALL] + [("C2", 1)])
 def test_G5_dense_blocks(name, sym):
     """Every block densely expanded from both factor sets:
