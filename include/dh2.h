@@ -203,8 +203,10 @@ int dh2_set_stream(dh2_ctx* ctx, void* cuda_stream);
  *     weights above / at the leaf levels (3: chunk rows formed by thread-column FMAs).
  *   "near_tma" (0 | 1, default 1): nearfield matvec streams the blocks N_b through a ring of
  *     shared-memory stages filled by cp.async.bulk (TMA) on mbarriers; 0: direct global loads.
- *   "mv_forward_warp" (0 | 1, default 1): leaf forward transform of the matvec with one warp per
- *     coefficient (coalesced column reads, shuffle reduction); 0: one thread per coefficient.
+ *   "mv_forward_warp" (0 | 1 | 2, default 2): launch shapes of the far-field matvec.  1: leaf forward
+ *     transform with one warp per coefficient (coalesced column reads, shuffle reduction), coupling
+ *     and backward steps with 16 lanes per pair (RECOMP); 2: also one warp per pair, four pairs per
+ *     CTA, in the forward transform (RECOMP); 0: a thread per coefficient and a CTA per pair.
  *   Further A/B switches (qr_wy, qr_flag, trunc_direct, lean_chunks) are listed in DESIGN.md §8.
  *   All variants give the same ranks, singular values and matrices up to rounding (tests).
  * Errors: DH2_EINVAL for an unknown name or value. */

@@ -270,7 +270,7 @@ struct Shard {
     int trunc_mode_init = 1; // initial value of PlanD::trunc_mode (direct: measured -3 % C4, -16 % C5 leaves)
     int qr_wy_init = 0;      // initial value of PlanD::qr_wy (blocked WY appends measured slower on C4: 0) (dh2_set_option("qr_wy") sets the plan directly)
     int near_tma = 1;         // dh2_set_option("near_tma"): nearfield matvec streams N_b by cp.async.bulk (TMA) stages
-    int mv_fwd_warp_init = 1; // PlanD::mv_fwd_warp
+    int mv_fwd_warp_init = 2; // PlanD::mv_fwd_warp (measured C4 matvec 12.0 / 7.7 / 6.6 ms for 0 / 1 / 2)
     int bw_variant_init = 1;  // PlanD::bw_variant (k > 64 only: C4 block weights -5 %)
     int t64_threads_init = 128;  // PlanD::t64_threads
     int split_trunc64 = 1;

@@ -164,7 +164,7 @@ def test_G4_matvec_variants(name, sym):
             assert np.linalg.norm(got[v] - yr) <= 1e-10 * ref
         assert np.linalg.norm(got[1] - got[0]) <= 1e-13 * ref and np.linalg.norm(got[2] - got[0]) <= 1e-13 * ref
     finally:
-        h.set_option("mv_forward_warp", 1)
+        h.set_option("mv_forward_warp", 2)
 
 
 @pytest.mark.parametrize("name,sym", [c for c in CASES if c[0] in SMALL] + [("C2", 1)])
